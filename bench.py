@@ -1,0 +1,581 @@
+#!/usr/bin/env python
+"""bench.py — DOT/GEMV/GER achieved HBM GB/s and % of the B200 roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload G1] [--no-suite] [--no-cpu-baseline]
+
+Multi-GPU runs are launched one process per GPU by torchrun (RANK /
+LOCAL_RANK / WORLD_SIZE from the environment, NCCL over NVLink).
+
+Headline workload (``--workload``, default G1 = BASELINE.json configs[1],
+GEMV fp32 row-major 8192 x 8192): a STEP is one pass of the hot path over one
+batch — one c += A x over an 8192 x 8192 row block.  At N GPUs every rank
+owns its own 8192-row block of an (8192 N) x 8192 matrix with x replicated
+(weak scaling; row blocks need no collective).
+
+* ``value``     whole-job GB/s = algorithmic bytes of all ranks x K / the
+                max over ranks of the summed per-step CUDA-event time, inputs
+                resident in HBM, L2 flushed between steps (512 MiB write,
+                outside the events).
+* ``e2e``       the same metric through the public host-buffer API
+                (cabl_host_gemv_f32 via cabl.gemv_row_major on pinned CPU
+                tensors): H2D of A, x, c + kernel + D2H of c every step.
+* ``roofline``  the dominant (only) kernel: algorithmic bytes per launch /
+                mean launch time vs MEASURED_PEAKS.json hbm_gbs; traffic =
+                DRAM bytes per launch from the committed ncu capture.
+* ``cpu_baseline`` the compiled, UNMODIFIED reference (oracle/_ref,
+                kind "reference") — its threaded gemv_row_major with every
+                host core — on a bounded sample of the same workload.
+* ``suite``     every BASELINE config at this N (device GB/s, % of peak).
+
+``--impl reference`` times the reference's own CPU implementation of the
+path on this box's host cores (rank 0 only) and prints the same line shape.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FALLBACK_HBM_GBS = 6650.0
+FLUSH_BYTES = 512 << 20
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def traffic_for(kernel_key: str):
+    """DRAM bytes per launch for a kernel from the committed ncu summary."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None, None
+    d = json.loads(p.read_text())
+    e = d.get(kernel_key)
+    if not e:
+        return None, None
+    return e.get("dram_bytes_per_launch"), e.get("source")
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons through NVML while running."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.ok = False
+        self.samples: list[int] = []
+        self.reasons: set[str] = set()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- setup
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Ctx:
+    def __init__(self, world, rank, local, dev):
+        self.world, self.rank, self.local, self.dev = world, rank, local, dev
+
+    def barrier(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier(device_ids=[self.local])
+
+    def max(self, v: float) -> float:
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=self.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+def make_inputs(w, rows: tuple[int, int], dev, layout=None):
+    """Seeded device inputs for this rank's shard of workload w."""
+    import torch
+
+    import paper_2108_02025_b200 as cb
+    from paper_2108_02025_b200 import workloads as WL
+    fill = cb.fill_normal if w.dist == "normal" else cb.fill_uniform
+    r0, r1 = rows
+    if w.op == "dot":
+        n = r1 - r0
+        x = fill(torch.empty(n, dtype=w.dtype, device=dev), WL.SEED, WL.STREAM_X, r0)
+        y = fill(torch.empty(n, dtype=w.dtype, device=dev), WL.SEED, WL.STREAM_Y, r0)
+        return {"x": x, "y": y, "out": torch.empty(1, dtype=w.dtype, device=dev)}
+    m = r1 - r0
+    if w.op.startswith("gemv"):
+        lay = cb.Layout.RowMajor if w.op == "gemv-row" else cb.Layout.ColMajor
+        A = torch.empty(m * w.n, dtype=w.dtype, device=dev)
+        if lay == cb.Layout.RowMajor:
+            fill(A, WL.SEED, WL.STREAM_A, r0 * w.n)
+        else:
+            fill(A, WL.SEED, WL.STREAM_A, 0)
+        x = fill(torch.empty(w.n, dtype=w.dtype, device=dev), WL.SEED, WL.STREAM_X, 0)
+        c = fill(torch.empty(m, dtype=w.dtype, device=dev), WL.SEED, WL.STREAM_C, r0)
+        return {"A": cb.DenseMatrix.wrap(A, m, w.n, lay), "x": x, "c": c}
+    C = fill(torch.empty(m * w.n, dtype=w.dtype, device=dev), WL.SEED, WL.STREAM_CC, r0 * w.n)
+    x = fill(torch.empty(m, dtype=w.dtype, device=dev), WL.SEED, WL.STREAM_X, r0)
+    y = fill(torch.empty(w.n, dtype=w.dtype, device=dev), WL.SEED, WL.STREAM_Y, 0)
+    return {"C": cb.DenseMatrix.wrap(C, m, w.n, cb.Layout.RowMajor), "x": x, "y": y}
+
+
+def step_fn(w, ins, policy, ctx, sharded_dot: bool):
+    import paper_2108_02025_b200 as cb
+    from paper_2108_02025_b200 import shard
+    if w.op == "dot":
+        if sharded_dot and ctx.world > 1:
+            import torch
+            gathered = torch.empty(ctx.world, dtype=w.dtype, device=ctx.dev)
+            return (lambda: shard.sharded_dot(ins["x"], ins["y"], 0.0, ins["out"], policy,
+                                              gathered=gathered)), 3
+        return (lambda: cb.dot_into(ins["x"], ins["y"], 0.0, ins["out"], policy)), 1
+    if w.op == "gemv-row":
+        return (lambda: cb.gemv_row_major(ins["A"], ins["x"], ins["c"], policy)), 1
+    if w.op == "gemv-col":
+        return (lambda: cb.gemv_col_major(ins["A"], ins["x"], ins["c"], policy)), 1
+    return (lambda: cb.ger(ins["x"], ins["y"], ins["C"], policy)), 1
+
+
+def time_steps(fn, steps, warmup, ctx, flush, sampler=None):
+    """Per-step CUDA-event times (ms) on the launching stream, L2 flushed
+    between steps outside the events; barrier + synchronize on both sides."""
+    import torch
+    for _ in range(warmup):
+        flush.zero_()
+        fn()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ctx.barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__enter__()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        flush.zero_()
+        starts[k].record()
+        fn()
+        ends[k].record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    if sampler:
+        sampler.__exit__()
+    ctx.barrier()
+    return [s.elapsed_time(e) for s, e in zip(starts, ends)], wall
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_reference_sample(w, max_bytes=1 << 30, reps=5, threads=None):
+    """Time the compiled reference (oracle/_ref) on a bounded sample of w."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2108_02025_b200 import workloads as WL
+    cores = threads or os.cpu_count() or 1
+    kind = "reference" if O.ref_available() else "port"
+    npdt = np.float32 if w.dtype_name == "f32" else np.float64
+    s = np.dtype(npdt).itemsize
+    gen = (lambda n, st, off=0: O.gen_normal_f64(n, WL.SEED, st, off)) if w.dist == "normal" \
+        else (lambda n, st, off=0: O.gen_uniform(n, npdt, WL.SEED, st, off))
+    if w.op == "dot":
+        n = min(w.n, max_bytes // (2 * s))
+        m = 0
+        x, y = gen(n, WL.STREAM_X), gen(n, WL.STREAM_Y)
+        alg = 2 * n * s
+        sample = f"dot {w.dtype_name} n={n}"
+    else:
+        m, n = w.m, w.n
+        if m * n * s > max_bytes:
+            if w.op == "gemv-col" and m > n:
+                m = max(1, max_bytes // (n * s))
+            elif w.op == "gemv-col":
+                n = max(1, max_bytes // (m * s))
+            else:
+                m = max(1, max_bytes // (n * s))
+        if w.op.startswith("gemv"):
+            A, x, c = gen(m * n, WL.STREAM_A), gen(n, WL.STREAM_X), gen(m, WL.STREAM_C)
+            alg = m * n * s + n * s + 2 * m * s
+        else:
+            A, x, c = gen(m * n, WL.STREAM_CC), gen(m, WL.STREAM_X), gen(n, WL.STREAM_Y)
+            alg = 2 * m * n * s + m * s + n * s
+        sample = f"{w.op} {w.dtype_name} {m}x{n}"
+    times = []
+    if kind == "reference":
+        if w.op == "dot":
+            sess = O.RefSession("dot", npdt, 0, 0, n, None, x, y, 0.0, cores=cores)
+        elif w.op == "ger":
+            sess = O.RefSession("ger", npdt, 0, m, n, A, x, c, cores=cores)
+        else:
+            sess = O.RefSession(w.op, npdt, 0 if w.op == "gemv-row" else 1, m, n, A, x, c,
+                                cores=cores)
+        times = O.time_ref(sess, use_ref=False, threads=cores, reps=reps)
+        sess.close()
+        used = cores
+    else:  # restated oracle, single thread
+        used = 1
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            if w.op == "dot":
+                O.dot_ref(x, y, 0.0)
+            elif w.op == "ger":
+                O.ger_ref(x, c, A, 0)
+            else:
+                O.gemv_ref(A, 0 if w.op == "gemv-row" else 1, x, c)
+            times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": round(alg / t / 1e9, 3), "unit": "GB/s", "cores": used, "kind": kind,
+            "sample": f"{sample}, median of {reps} after 1 warm-up"
+                      + (", reference threaded path (ExecPolicy threads=%d)" % used
+                         if kind == "reference" else ", restated oracle (1 thread)"),
+            "median_s": t}
+
+
+# ------------------------------------------------------------ our arm
+def run_ours(args, ctx):
+    import torch
+
+    import paper_2108_02025_b200 as cb
+    from paper_2108_02025_b200 import workloads as WL
+    peak, peak_src = peaks()
+    policy = cb.default_policy(1)
+    w = WL.WORKLOADS[args.workload]
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=ctx.dev)
+
+    # ---- headline: weak scaling, every rank its own full-size block
+    span = w.n if w.op == "dot" else w.m
+    rows = (ctx.rank * span, (ctx.rank + 1) * span)
+    ins = make_inputs(w, rows, ctx.dev)
+    fn, launches_per_step = step_fn(w, ins, policy, ctx, sharded_dot=False)
+    sampler = ClockSampler(ctx.local)
+    times, wall = time_steps(fn, args.steps, args.warmup, ctx, flush, sampler)
+    t_rank = sum(times) / 1000.0
+    t_max = ctx.max(t_rank)
+    bytes_rank = w.alg_bytes(1)
+    value = ctx.world * bytes_rank * args.steps / t_max / 1e9
+    mean_launch_s = t_rank / args.steps
+    achieved = bytes_rank / mean_launch_s / 1e9
+    traffic, traffic_src = traffic_for(f"{w.id}")
+    clocks = sampler.summary()
+
+    # ---- e2e through the host-buffer public API (pinned host tensors)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(w, ins, policy, ctx, args)
+
+    del ins
+    torch.cuda.empty_cache()
+
+    # ---- CPU baseline (rank 0, N=1)
+    cpu = None
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(w)
+            cpu.pop("median_s", None)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "error": str(e)}
+
+    # ---- suite of all BASELINE configs at this N
+    suite = None
+    if not args.no_suite:
+        suite = run_suite(args, ctx, flush, policy, peak)
+
+    if ctx.rank != 0:
+        return
+    line = {
+        "metric": "DOT/GEMV/GER achieved HBM GB/s & % of B200 roofline at 1/2/4/8 GPUs",
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": ctx.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(t_max / args.steps * 1e3, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": w.dtype_name,
+        "data": "synthetic: seeded SplitMix64 U[-1,1) (seed 42), generated on device",
+        "config": {
+            "workload": f"{w.id}: {w.desc}",
+            "m_per_gpu": w.m, "n": w.n, "layout": "row-major",
+            "parallelism": f"row blocks over {ctx.world} GPU(s), x replicated, no collective",
+            "l2": "flushed between steps (512 MiB write outside the timed events)",
+            "alg_bytes_per_step_per_gpu": bytes_rank,
+        },
+        "roofline": {
+            "bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "peak_source": peak_src,
+            "traffic": traffic, "traffic_source": traffic_src,
+            "kernel": "gemv_rm_vec_kernel" if w.op == "gemv-row" else w.op,
+            "mean_launch_us": round(mean_launch_s * 1e6, 3),
+        },
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+        "wall_s_timed_region": round(wall, 4),
+        "suite": suite,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(w, ins, policy, ctx, args):
+    import torch
+
+    import paper_2108_02025_b200 as cb
+    steps = max(1, min(args.steps, args.e2e_steps))
+    if w.op == "dot":
+        hx, hy = ins["x"].cpu().pin_memory(), ins["y"].cpu().pin_memory()
+        fn = lambda: cb.dot(hx, hy, 0.0, policy)  # noqa: E731
+        h2d = (hx.numel() + hy.numel()) * w.s
+        d2h = w.s
+    elif w.op.startswith("gemv"):
+        A = ins["A"]
+        hA = cb.DenseMatrix.wrap(A.data.cpu().pin_memory(), A.rows(), A.cols(), A.layout())
+        hx, hc = ins["x"].cpu().pin_memory(), ins["c"].cpu().pin_memory()
+        f = cb.gemv_row_major if w.op == "gemv-row" else cb.gemv_col_major
+        fn = lambda: f(hA, hx, hc, policy)  # noqa: E731
+        h2d = (hA.size() + hx.numel() + hc.numel()) * w.s
+        d2h = hc.numel() * w.s
+    else:
+        Cm = ins["C"]
+        hC = cb.DenseMatrix.wrap(Cm.data.cpu().pin_memory(), Cm.rows(), Cm.cols(), Cm.layout())
+        hx, hy = ins["x"].cpu().pin_memory(), ins["y"].cpu().pin_memory()
+        fn = lambda: cb.ger(hx, hy, hC, policy)  # noqa: E731
+        h2d = (hC.size() + hx.numel() + hy.numel()) * w.s
+        d2h = hC.size() * w.s
+    for _ in range(min(3, args.warmup)):
+        fn()
+    ctx.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        fn()
+    t = time.perf_counter() - t0
+    t_max = ctx.max(t)
+    return {"value": round(ctx.world * w.alg_bytes(1) * steps / t_max / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "ms_per_step": round(t_max / steps * 1e3, 4),
+            "api": "cabl.{dot,gemv_*,ger} on pinned CPU tensors -> cabl_host_* (C ABI)"}
+
+
+def run_suite(args, ctx, flush, policy, peak):
+    """Every BASELINE config at this N.  N=1: all seven on one GPU.  N>1: the
+    configs BASELINE shards (R1, G4 row blocks; D2 chunks + all-gather),
+    strong scaling (fixed total problem)."""
+    import torch
+
+    from paper_2108_02025_b200 import workloads as WL
+    ids = list(WL.WORKLOADS) if ctx.world == 1 else ["R1", "G4", "D2"]
+    out = {}
+    steps = max(3, min(args.steps, args.suite_steps))
+    for wid in ids:
+        w = WL.WORKLOADS[wid]
+        total = w.n if w.op == "dot" else w.m
+        b, e = (0, total) if ctx.world == 1 else WL.Workload.shard_rows(w, ctx.rank, ctx.world)
+        try:
+            ins = make_inputs(w, (b, e), ctx.dev)
+            if w.op == "dot":
+                import dataclasses
+                wl = dataclasses.replace(w, n=e - b)
+            else:
+                import dataclasses
+                wl = dataclasses.replace(w, m=e - b)
+            fn, lps = step_fn(wl, ins, policy, ctx, sharded_dot=True)
+            times, _ = time_steps(fn, steps, args.warmup, ctx, flush)
+            t_max = ctx.max(sum(times) / 1000.0)
+            alg = w.alg_bytes(ctx.world)
+            gbs = alg * steps / t_max / 1e9
+            out[wid] = {"desc": w.desc, "gbs": round(gbs, 2),
+                        "frac_of_peak": round(gbs / (peak * ctx.world), 4),
+                        "us_per_step": round(t_max / steps * 1e6, 3),
+                        "gflops": round(w.flops() * steps / t_max / 1e9, 2),
+                        "alg_bytes": alg, "launches_per_step": lps,
+                        "scaling": "strong" if ctx.world > 1 else None}
+            del ins
+        except torch.cuda.OutOfMemoryError as ex:
+            out[wid] = {"error": f"OOM: {ex}"}
+        torch.cuda.empty_cache()
+    return out
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args, ctx):
+    """The reference's own CPU implementation (compiled oracle/_ref; the
+    restated oracle only if the reference build is absent) on all host cores,
+    same workload/metric as our arm.  Rank 0 only."""
+    if ctx.rank != 0:
+        return
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2108_02025_b200 import workloads as WL
+    w = WL.WORKLOADS[args.workload]
+    cores = os.cpu_count() or 1
+    kind = "reference" if O.ref_available() else "port"
+    npdt = np.float32 if w.dtype_name == "f32" else np.float64
+    gen = lambda n, st: O.gen_uniform(n, npdt, WL.SEED, st)  # noqa: E731
+    if w.op == "dot":
+        x, y = gen(w.n, WL.STREAM_X), gen(w.n, WL.STREAM_Y)
+        sess = O.RefSession("dot", npdt, 0, 0, w.n, None, x, y, 0.0, cores=cores) \
+            if kind == "reference" else None
+    elif w.op.startswith("gemv"):
+        A, x, c = gen(w.m * w.n, WL.STREAM_A), gen(w.n, WL.STREAM_X), gen(w.m, WL.STREAM_C)
+        sess = O.RefSession(w.op, npdt, 0 if w.op == "gemv-row" else 1, w.m, w.n, A, x, c,
+                            cores=cores) if kind == "reference" else None
+    else:
+        A, x, c = gen(w.m * w.n, WL.STREAM_CC), gen(w.m, WL.STREAM_X), gen(w.n, WL.STREAM_Y)
+        sess = O.RefSession("ger", npdt, 0, w.m, w.n, A, x, c, cores=cores) \
+            if kind == "reference" else None
+
+    def one():
+        if sess is not None:
+            sess.run(False, cores)
+        elif w.op == "dot":
+            O.dot_ref(x, y, 0.0)
+        elif w.op == "ger":
+            O.ger_ref(x, c, A, 0)
+        else:
+            O.gemv_ref(A, 0, x, c)
+
+    # each step is one full pass over the workload; bound the step count so
+    # the run stays within a few minutes
+    for _ in range(max(1, min(args.warmup, 3))):
+        one()
+    t_probe = time.perf_counter()
+    one()
+    per = time.perf_counter() - t_probe
+    steps = max(1, min(args.steps, int(120.0 / max(per, 1e-6))))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    t = time.perf_counter() - t0
+    value = w.alg_bytes(1) * steps / t / 1e9
+    used = cores if kind == "reference" else 1
+    line = {
+        "metric": "DOT/GEMV/GER achieved HBM GB/s & % of B200 roofline at 1/2/4/8 GPUs",
+        "impl": "reference",
+        "value": round(value, 3), "unit": "GB/s", "n_gpus": ctx.world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": round(t / steps * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": w.dtype_name,
+        "data": "synthetic: seeded SplitMix64 U[-1,1) (seed 42), generated on the host",
+        "config": {"workload": f"{w.id}: {w.desc}", "m_per_gpu": w.m, "n": w.n,
+                   "layout": "row-major", "parallelism": "CPU threads (reference ThreadPool)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": used, "kind": kind,
+                         "sample": f"full {w.id} workload per step; "
+                                   f"{'cabl::' + w.op.replace('-', '_') if kind == 'reference' else 'restated oracle'}"
+                                   f" with ExecPolicy threads={used}"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="G1")
+    ap.add_argument("--no-suite", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--suite-steps", type=int, default=30)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("bench.py: --warmup must be >= 3", file=sys.stderr)
+        args.warmup = 3
+
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        ctx = Ctx(world, rank, local, None)
+        run_reference(args, ctx)
+        return
+
+    import torch
+    if not torch.cuda.is_available():
+        print(json.dumps({"error": "no CUDA device; libcabl_cuda has no CPU path"}))
+        sys.exit(2)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = Ctx(world, rank, local, dev)
+    try:
+        run_ours(args, ctx)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,173 @@
+/*
+ * cabl_cuda.h — the C ABI of the B200-native DOT / GEMV / GER library
+ * (libcabl_cuda.so, built from paper_2108_02025_b200/csrc/).
+ *
+ * This is the drop-in boundary for the hot path of the reference library
+ * `cabl` (arXiv 2108.02025).  The reference is a header-only C++20 template
+ * library; its four hot-path entry points are
+ *
+ *   T    cabl::dot(const Vector<T>& x, const Vector<T>& y, T alpha0, const ExecPolicy&)
+ *            reference proj/include/cabl/kernels.hpp:134-164
+ *   void cabl::gemv_col_major(const DenseMatrix<T>& A, const Vector<T>& x, Vector<T>& c,
+ *                             const ExecPolicy&)      kernels.hpp:187-224
+ *   void cabl::gemv_row_major(same signature)          kernels.hpp:230-257
+ *   void cabl::ger(const Vector<T>& x, const Vector<T>& y, DenseMatrix<T>& C,
+ *                  const ExecPolicy&)                  kernels.hpp:277-313
+ *
+ * The drop-in header include/cabl/kernels.hpp keeps those signatures and
+ * forwards here.  Every symbol below is plain C: raw pointers, sizes, an int
+ * status and an opaque stream (a cudaStream_t passed as void*; NULL means
+ * the legacy default stream).  There is no CPU fallback: when no CUDA device
+ * is usable every compute entry point returns CABL_ECUDA.
+ *
+ * Device entry points (`cabl_cuda_*`) take DEVICE pointers and only enqueue
+ * work on `stream`.  Host entry points (`cabl_host_*`) take HOST pointers
+ * (pinned or pageable), stage through device memory on `stream`, and return
+ * after the result is back on the host — they are what the C++ drop-in
+ * overloads on cabl::Vector / cabl::DenseMatrix call.
+ *
+ * Semantics are the reference's: pure accumulate (alpha0 + x.y, c += A x,
+ * C += x (x) y), no scaling, no strides (reference SPEC.md:292,304).
+ * Zero-size operands are no-ops; DOT of empty vectors returns alpha0.
+ * Results are bitwise reproducible run to run for fixed inputs and device.
+ */
+#ifndef CABL_CUDA_H
+#define CABL_CUDA_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CABL_API __attribute__((visibility("default")))
+#else
+#define CABL_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  CABL_EINVAL mirrors the reference's std::invalid_argument
+ * (kernels.hpp:59-61); the message is available from cabl_last_error(). */
+enum {
+    CABL_OK = 0,
+    CABL_EINVAL = 1,
+    CABL_ECUDA = 2,
+    CABL_ENOMEM = 3
+};
+
+/* Storage order of a dense matrix — reference dense.hpp:9, element (i,j) at
+ * j + i*cols (row-major) or i + j*rows (col-major), dense.hpp:54-56. */
+enum { CABL_ROW_MAJOR = 0, CABL_COL_MAJOR = 1 };
+
+/* Execution-path probe — reference KernelVariant / ExecProbe, kernels.hpp:40-55.
+ * Numbering matches the reference enum order. */
+enum {
+    CABL_VARIANT_NONE = 0,
+    CABL_VARIANT_DOT_SMALL = 1,
+    CABL_VARIANT_DOT_BLOCKED = 2,
+    CABL_VARIANT_GEMV_COL_BLOCKED = 3,
+    CABL_VARIANT_GEMV_ROW = 4,
+    CABL_VARIANT_GER = 5
+};
+
+typedef struct cabl_probe {
+    int variant;           /* CABL_VARIANT_* */
+    unsigned threads_used; /* CTAs launched on the main pass (1 for the ordered small path) */
+} cabl_probe;
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+CABL_API const char* cabl_last_error(void);
+/* ABI version (major*100 + minor). */
+CABL_API int cabl_abi_version(void);
+/* Number of usable CUDA devices (0 when none; never a CPU fallback). */
+CABL_API int cabl_device_count(void);
+
+/* ---------------------------------------------------------------- DOT ---
+ * *out = alpha0 + sum_p x[p]*y[p]   (device scalar; alpha0 is added last,
+ * as reference kernels.hpp:142,163 do).
+ * n <= small_cutoff runs the single-CTA path (reference dot_small,
+ * kernels.hpp:140-143); otherwise the bandwidth path over the whole GPU.
+ * `probe` may be NULL.  Replaces cabl::dot<float|double>, kernels.hpp:134. */
+CABL_API int cabl_cuda_dot_f32(const float* x, const float* y, uint64_t n, float alpha0, float* out,
+                      uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_cuda_dot_f64(const double* x, const double* y, uint64_t n, double alpha0,
+                      double* out, uint64_t small_cutoff, cabl_probe* probe, void* stream);
+
+/* Deterministic, rank-ordered combine of `count` partial dot products (one per
+ * shard / GPU): *out = ((p[0] + p[1]) + ...) + alpha0, summed left to right in
+ * index order like the reference combines thread partials (kernels.hpp:160-163).
+ * Used by the multi-GPU DOT after the partials are all-gathered. */
+CABL_API int cabl_cuda_combine_partials_f32(const float* partials, uint32_t count, float alpha0,
+                                   float* out, void* stream);
+CABL_API int cabl_cuda_combine_partials_f64(const double* partials, uint32_t count, double alpha0,
+                                   double* out, void* stream);
+
+/* --------------------------------------------------------------- GEMV ---
+ * c[0..m) += A x, A is m x n.  `small_cutoff`: when m*n + m + n <= cutoff the
+ * call runs the ordered single-CTA path, which reproduces the compiled
+ * reference gemv_ref / gemv_row_major bit for bit (reference kernels.hpp:238-243).
+ * Replaces cabl::gemv_row_major (kernels.hpp:230) and cabl::gemv_col_major
+ * (kernels.hpp:187); the layout is part of the symbol, as the reference
+ * rejects the other layout (kernels.hpp:190,233). c must not alias x. */
+CABL_API int cabl_cuda_gemv_rm_f32(const float* A, uint64_t m, uint64_t n, const float* x, float* c,
+                          uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_cuda_gemv_rm_f64(const double* A, uint64_t m, uint64_t n, const double* x, double* c,
+                          uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_cuda_gemv_cm_f32(const float* A, uint64_t m, uint64_t n, const float* x, float* c,
+                          uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_cuda_gemv_cm_f64(const double* A, uint64_t m, uint64_t n, const double* x, double* c,
+                          uint64_t small_cutoff, cabl_probe* probe, void* stream);
+
+/* ---------------------------------------------------------------- GER ---
+ * C(i,j) = fma(x[i], y[j], C(i,j)) for i < m, j < n — exactly one fused
+ * multiply-add per element, bitwise equal to the reference ger_ref / ger
+ * (kernels.hpp:264-313).  x has m entries, y has n; C must not alias x or y.
+ * Replaces cabl::ger (kernels.hpp:277): _rm = RowMajor branch (:300-310),
+ * _cm = ColMajor branch (:290-299). */
+CABL_API int cabl_cuda_ger_rm_f32(const float* x, const float* y, float* C, uint64_t m, uint64_t n,
+                         uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_cuda_ger_rm_f64(const double* x, const double* y, double* C, uint64_t m, uint64_t n,
+                         uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_cuda_ger_cm_f32(const float* x, const float* y, float* C, uint64_t m, uint64_t n,
+                         uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_cuda_ger_cm_f64(const double* x, const double* y, double* C, uint64_t m, uint64_t n,
+                         uint64_t small_cutoff, cabl_probe* probe, void* stream);
+
+/* ------------------------------------------------- host-buffer entry points
+ * Same operations on HOST buffers (what the C++ drop-in overloads on
+ * cabl::Vector / cabl::DenseMatrix call): H2D copy of the operands, the
+ * device kernel, D2H copy of the result, then a stream synchronize.  `layout`
+ * is CABL_ROW_MAJOR / CABL_COL_MAJOR.  Temporaries come from a library-owned
+ * stream-ordered device pool (never freed mid-call, thread-safe). */
+CABL_API int cabl_host_dot_f32(const float* x, const float* y, uint64_t n, float alpha0, float* result,
+                      uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_host_dot_f64(const double* x, const double* y, uint64_t n, double alpha0,
+                      double* result, uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_host_gemv_f32(const float* A, int layout, uint64_t m, uint64_t n, const float* x,
+                       float* c, uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_host_gemv_f64(const double* A, int layout, uint64_t m, uint64_t n, const double* x,
+                       double* c, uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_host_ger_f32(const float* x, const float* y, float* C, int layout, uint64_t m,
+                      uint64_t n, uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_host_ger_f64(const double* x, const double* y, double* C, int layout, uint64_t m,
+                      uint64_t n, uint64_t small_cutoff, cabl_probe* probe, void* stream);
+
+/* ------------------------------------------------------ seeded inputs ---
+ * Counter-based SplitMix64 generator, bit-identical to the host oracle's
+ * (oracle/cabl_oracle.c): out[i] = U[-1,1) of counter (offset + i) in
+ * (seed, stream_id).  The normal variant is Box-Muller on counters
+ * (2(offset+i), 2(offset+i)+1).  Stand-in for the reference's seeded
+ * mt19937_64 fills (reference bench.hpp:68-71), which are sequential and
+ * cannot be reproduced on a GPU. */
+CABL_API int cabl_cuda_fill_uniform_f32(float* out, uint64_t n, uint64_t seed, uint64_t stream_id,
+                               uint64_t offset, void* stream);
+CABL_API int cabl_cuda_fill_uniform_f64(double* out, uint64_t n, uint64_t seed, uint64_t stream_id,
+                               uint64_t offset, void* stream);
+CABL_API int cabl_cuda_fill_normal_f64(double* out, uint64_t n, uint64_t seed, uint64_t stream_id,
+                              uint64_t offset, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CABL_CUDA_H */

@@ -1,0 +1,460 @@
+// extern "C" boundary of libcabl_cuda.so — see include/cabl_cuda.h.
+//
+// Responsibilities: argument validation with the reference's messages
+// (proj/include/cabl/kernels.hpp:59-64 and the `require` call sites), the
+// small-problem dispatch rule (kernels.hpp:140, :240-241, :286-287), the
+// execution-path probe (kernels.hpp:40-55), per-(device, stream) scratch for
+// the kernels' cross-CTA combines, host-buffer staging, and the mapping of
+// CUDA errors to status codes with a thread-local message.  No CPU fallback:
+// without a usable device every compute entry point returns CABL_ECUDA.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <tuple>
+
+#include "cabl_cuda.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace cabl_dev;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    cudaGetLastError(); // clear sticky-free errors so the next call starts clean
+    return fail(CABL_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CABL_TRY_CUDA(expr, where)                                                            \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where);                                   \
+    } while (0)
+
+int current_device(int* dev) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(CABL_ECUDA,
+                    "no CUDA device available (libcabl_cuda has no CPU fallback)");
+    }
+    CABL_TRY_CUDA(cudaGetDevice(dev), "cudaGetDevice");
+    return CABL_OK;
+}
+
+// ---------------------------------------------------------------- scratch
+struct WsKey {
+    int device;
+    cudaStream_t stream;
+    std::thread::id tid; // only for the per-thread default stream
+    bool operator<(const WsKey& o) const {
+        return std::tie(device, stream, tid) < std::tie(o.device, o.stream, o.tid);
+    }
+};
+
+struct WsEntry {
+    Workspace ws;
+    std::mutex mu; // serialises growth; launches on one stream are ordered anyway
+};
+
+std::mutex g_ws_mu;
+std::map<WsKey, WsEntry*>& ws_map() {
+    static auto* m = new std::map<WsKey, WsEntry*>(); // leaked on purpose: no teardown order issues
+    return *m;
+}
+
+int get_workspace(int device, cudaStream_t s, const WorkspaceNeed& need, Workspace* out) {
+    if (need.counters == 0 && need.scratch_bytes == 0) {
+        *out = Workspace{};
+        return CABL_OK;
+    }
+    WsKey key{device, s, s == cudaStreamPerThread ? std::this_thread::get_id() : std::thread::id()};
+    WsEntry* ent;
+    {
+        std::lock_guard<std::mutex> lk(g_ws_mu);
+        auto& m = ws_map();
+        auto it = m.find(key);
+        if (it == m.end()) it = m.emplace(key, new WsEntry()).first;
+        ent = it->second;
+    }
+    std::lock_guard<std::mutex> lk(ent->mu);
+    Workspace& ws = ent->ws;
+    if (need.counters > ws.n_counters) {
+        size_t cnt = need.counters < 1024 ? 1024 : need.counters * 2;
+        void* p = nullptr;
+        CABL_TRY_CUDA(cudaMallocAsync(&p, cnt * sizeof(unsigned), s), "workspace counters");
+        CABL_TRY_CUDA(cudaMemsetAsync(p, 0, cnt * sizeof(unsigned), s), "workspace memset");
+        if (ws.counters) cudaFreeAsync(ws.counters, s);
+        ws.counters = static_cast<unsigned*>(p);
+        ws.n_counters = cnt;
+    }
+    if (need.scratch_bytes > ws.scratch_bytes) {
+        size_t bytes = need.scratch_bytes < (1u << 20) ? (1u << 20) : need.scratch_bytes * 2;
+        void* p = nullptr;
+        CABL_TRY_CUDA(cudaMallocAsync(&p, bytes, s), "workspace scratch");
+        if (ws.scratch) cudaFreeAsync(ws.scratch, s);
+        ws.scratch = p;
+        ws.scratch_bytes = bytes;
+    }
+    *out = ws;
+    return CABL_OK;
+}
+
+void set_probe(cabl_probe* p, int variant, unsigned ctas) {
+    if (p) {
+        p->variant = variant;
+        p->threads_used = ctas < 1 ? 1u : ctas;
+    }
+}
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+template <typename T> const char* tname();
+template <> const char* tname<float>() { return "f32"; }
+template <> const char* tname<double>() { return "f64"; }
+
+// ------------------------------------------------------------------- DOT
+template <typename T>
+int dot_impl(const T* x, const T* y, uint64_t n, T alpha0, T* out, uint64_t cutoff,
+             cabl_probe* probe, void* stream) {
+    if (!out) return fail(CABL_EINVAL, "dot: out must not be null");
+    if (n > 0 && (!x || !y)) return fail(CABL_EINVAL, "dot: x and y must not be null");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    const bool small = n <= cutoff; // reference kernels.hpp:140
+    cudaStream_t s = as_stream(stream);
+    Workspace ws;
+    if (int rc = get_workspace(dev, s, dot_need<T>(n, small), &ws)) return rc;
+    LaunchInfo info;
+    CABL_TRY_CUDA(dot_launch<T>(x, y, n, alpha0, out, small, ws, s, &info), "dot kernel");
+    set_probe(probe, small ? CABL_VARIANT_DOT_SMALL : CABL_VARIANT_DOT_BLOCKED, info.ctas);
+    return CABL_OK;
+}
+
+template <typename T>
+int combine_impl(const T* p, uint32_t count, T alpha0, T* out, void* stream) {
+    if (!out || (count > 0 && !p)) return fail(CABL_EINVAL, "combine: null pointer");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    CABL_TRY_CUDA(combine_partials_launch<T>(p, count, alpha0, out, as_stream(stream)),
+                  "combine kernel");
+    return CABL_OK;
+}
+
+// ------------------------------------------------------------------ GEMV
+template <typename T>
+int gemv_impl(const T* A, int layout, uint64_t m, uint64_t n, const T* x, T* c,
+              uint64_t cutoff, cabl_probe* probe, void* stream) {
+    if (m > 0 && n > 0 && (!A || !x || !c))
+        return fail(CABL_EINVAL, "gemv: A, x and c must not be null");
+    if (c != nullptr && static_cast<const void*>(c) == static_cast<const void*>(x))
+        return fail(CABL_EINVAL, "gemv: c must not alias x"); // kernels.hpp:176,193,236
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    const int variant = layout == CABL_ROW_MAJOR ? CABL_VARIANT_GEMV_ROW
+                                                 : CABL_VARIANT_GEMV_COL_BLOCKED;
+    const uint64_t touched = m * n + m + n; // kernels.hpp:240
+    cudaStream_t s = as_stream(stream);
+    LaunchInfo info;
+    if (touched <= cutoff) {
+        CABL_TRY_CUDA(gemv_ordered_launch<T>(A, layout, m, n, x, c, s, &info), "gemv kernel");
+    } else if (layout == CABL_ROW_MAJOR) {
+        Workspace ws;
+        if (int rc = get_workspace(dev, s, gemv_rm_need<T>(A, x, m, n), &ws)) return rc;
+        CABL_TRY_CUDA(gemv_rm_launch<T>(A, m, n, x, c, ws, s, &info), "gemv_rm kernel");
+    } else {
+        Workspace ws;
+        if (int rc = get_workspace(dev, s, gemv_cm_need<T>(A, x, m, n), &ws)) return rc;
+        CABL_TRY_CUDA(gemv_cm_launch<T>(A, m, n, x, c, ws, s, &info), "gemv_cm kernel");
+    }
+    set_probe(probe, variant, info.ctas);
+    return CABL_OK;
+}
+
+// ------------------------------------------------------------------- GER
+template <typename T>
+int ger_impl(const T* x, const T* y, T* C, int layout, uint64_t m, uint64_t n, uint64_t cutoff,
+             cabl_probe* probe, void* stream) {
+    if (m > 0 && n > 0 && (!x || !y || !C))
+        return fail(CABL_EINVAL, "ger: x, y and C must not be null");
+    if (C != nullptr && (static_cast<const void*>(C) == static_cast<const void*>(x) ||
+                         static_cast<const void*>(C) == static_cast<const void*>(y)))
+        return fail(CABL_EINVAL, "ger: C must not alias x or y"); // kernels.hpp:281-282
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    const uint64_t touched = m * n + m + n; // kernels.hpp:285-287
+    const bool small = touched <= cutoff;
+    LaunchInfo info;
+    cudaStream_t s = as_stream(stream);
+    if (layout == CABL_ROW_MAJOR)
+        CABL_TRY_CUDA(ger_launch<T>(x, y, C, m, n, small, s, &info), "ger kernel");
+    else
+        CABL_TRY_CUDA(ger_launch<T>(y, x, C, n, m, small, s, &info), "ger kernel");
+    set_probe(probe, CABL_VARIANT_GER, info.ctas);
+    return CABL_OK;
+}
+
+// ---------------------------------------------------- host-buffer staging
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+int dev_alloc(DevBuf& b, size_t bytes, cudaStream_t s) {
+    b.s = s;
+    if (bytes == 0) bytes = 32;
+    CABL_TRY_CUDA(cudaMallocAsync(&b.p, bytes, s), "staging alloc");
+    return CABL_OK;
+}
+
+void keep_pool_warm(int dev) {
+    // Stream-ordered frees return memory to the device pool; keep it there
+    // instead of releasing it at every synchronize.
+    static std::once_flag flags[64];
+    if (dev < 0 || dev >= 64) return;
+    std::call_once(flags[dev], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ULL;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
+int h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
+    if (bytes) CABL_TRY_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s), "H2D copy");
+    return CABL_OK;
+}
+int d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
+    if (bytes) CABL_TRY_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s), "D2H copy");
+    return CABL_OK;
+}
+
+template <typename T>
+int host_dot(const T* x, const T* y, uint64_t n, T alpha0, T* result, uint64_t cutoff,
+             cabl_probe* probe, void* stream) {
+    if (!result) return fail(CABL_EINVAL, "dot: result must not be null");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    keep_pool_warm(dev);
+    cudaStream_t s = as_stream(stream);
+    {
+        DevBuf dx, dy, dout;
+        if (int rc = dev_alloc(dx, n * sizeof(T), s)) return rc;
+        if (int rc = dev_alloc(dy, n * sizeof(T), s)) return rc;
+        if (int rc = dev_alloc(dout, sizeof(T), s)) return rc;
+        if (int rc = h2d(dx.p, x, n * sizeof(T), s)) return rc;
+        if (int rc = h2d(dy.p, y, n * sizeof(T), s)) return rc;
+        if (int rc = dot_impl<T>(static_cast<T*>(dx.p), static_cast<T*>(dy.p), n, alpha0,
+                                 static_cast<T*>(dout.p), cutoff, probe, stream))
+            return rc;
+        if (int rc = d2h(result, dout.p, sizeof(T), s)) return rc;
+    }
+    CABL_TRY_CUDA(cudaStreamSynchronize(s), "dot sync");
+    return CABL_OK;
+}
+
+template <typename T>
+int host_gemv(const T* A, int layout, uint64_t m, uint64_t n, const T* x, T* c, uint64_t cutoff,
+              cabl_probe* probe, void* stream) {
+    if (layout != CABL_ROW_MAJOR && layout != CABL_COL_MAJOR)
+        return fail(CABL_EINVAL, "gemv: bad layout");
+    if (c != nullptr && static_cast<const void*>(c) == static_cast<const void*>(x))
+        return fail(CABL_EINVAL, "gemv: c must not alias x");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    keep_pool_warm(dev);
+    cudaStream_t s = as_stream(stream);
+    {
+        DevBuf dA, dx, dc;
+        if (int rc = dev_alloc(dA, m * n * sizeof(T), s)) return rc;
+        if (int rc = dev_alloc(dx, n * sizeof(T), s)) return rc;
+        if (int rc = dev_alloc(dc, m * sizeof(T), s)) return rc;
+        if (int rc = h2d(dA.p, A, m * n * sizeof(T), s)) return rc;
+        if (int rc = h2d(dx.p, x, n * sizeof(T), s)) return rc;
+        if (int rc = h2d(dc.p, c, m * sizeof(T), s)) return rc;
+        if (int rc = gemv_impl<T>(static_cast<T*>(dA.p), layout, m, n, static_cast<T*>(dx.p),
+                                  static_cast<T*>(dc.p), cutoff, probe, stream))
+            return rc;
+        if (int rc = d2h(c, dc.p, m * sizeof(T), s)) return rc;
+    }
+    CABL_TRY_CUDA(cudaStreamSynchronize(s), "gemv sync");
+    return CABL_OK;
+}
+
+template <typename T>
+int host_ger(const T* x, const T* y, T* C, int layout, uint64_t m, uint64_t n, uint64_t cutoff,
+             cabl_probe* probe, void* stream) {
+    if (layout != CABL_ROW_MAJOR && layout != CABL_COL_MAJOR)
+        return fail(CABL_EINVAL, "ger: bad layout");
+    if (C != nullptr && (static_cast<const void*>(C) == static_cast<const void*>(x) ||
+                         static_cast<const void*>(C) == static_cast<const void*>(y)))
+        return fail(CABL_EINVAL, "ger: C must not alias x or y");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    keep_pool_warm(dev);
+    cudaStream_t s = as_stream(stream);
+    {
+        DevBuf dx, dy, dC;
+        if (int rc = dev_alloc(dx, m * sizeof(T), s)) return rc;
+        if (int rc = dev_alloc(dy, n * sizeof(T), s)) return rc;
+        if (int rc = dev_alloc(dC, m * n * sizeof(T), s)) return rc;
+        if (int rc = h2d(dx.p, x, m * sizeof(T), s)) return rc;
+        if (int rc = h2d(dy.p, y, n * sizeof(T), s)) return rc;
+        if (int rc = h2d(dC.p, C, m * n * sizeof(T), s)) return rc;
+        if (int rc = ger_impl<T>(static_cast<T*>(dx.p), static_cast<T*>(dy.p),
+                                 static_cast<T*>(dC.p), layout, m, n, cutoff, probe, stream))
+            return rc;
+        if (int rc = d2h(C, dC.p, m * n * sizeof(T), s)) return rc;
+    }
+    CABL_TRY_CUDA(cudaStreamSynchronize(s), "ger sync");
+    return CABL_OK;
+}
+
+} // namespace
+
+namespace cabl_dev {
+int sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (v == 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+            v = 148;
+        cache[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+} // namespace cabl_dev
+
+extern "C" {
+
+const char* cabl_last_error(void) { return g_err.c_str(); }
+int cabl_abi_version(void) { return 100; }
+int cabl_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
+
+int cabl_cuda_dot_f32(const float* x, const float* y, uint64_t n, float alpha0, float* out,
+                      uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return dot_impl<float>(x, y, n, alpha0, out, small_cutoff, probe, stream);
+}
+int cabl_cuda_dot_f64(const double* x, const double* y, uint64_t n, double alpha0,
+                      double* out, uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return dot_impl<double>(x, y, n, alpha0, out, small_cutoff, probe, stream);
+}
+int cabl_cuda_combine_partials_f32(const float* p, uint32_t count, float alpha0, float* out,
+                                   void* stream) {
+    return combine_impl<float>(p, count, alpha0, out, stream);
+}
+int cabl_cuda_combine_partials_f64(const double* p, uint32_t count, double alpha0,
+                                   double* out, void* stream) {
+    return combine_impl<double>(p, count, alpha0, out, stream);
+}
+
+int cabl_cuda_gemv_rm_f32(const float* A, uint64_t m, uint64_t n, const float* x, float* c,
+                          uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return gemv_impl<float>(A, CABL_ROW_MAJOR, m, n, x, c, small_cutoff, probe, stream);
+}
+int cabl_cuda_gemv_rm_f64(const double* A, uint64_t m, uint64_t n, const double* x, double* c,
+                          uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return gemv_impl<double>(A, CABL_ROW_MAJOR, m, n, x, c, small_cutoff, probe, stream);
+}
+int cabl_cuda_gemv_cm_f32(const float* A, uint64_t m, uint64_t n, const float* x, float* c,
+                          uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return gemv_impl<float>(A, CABL_COL_MAJOR, m, n, x, c, small_cutoff, probe, stream);
+}
+int cabl_cuda_gemv_cm_f64(const double* A, uint64_t m, uint64_t n, const double* x, double* c,
+                          uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return gemv_impl<double>(A, CABL_COL_MAJOR, m, n, x, c, small_cutoff, probe, stream);
+}
+
+int cabl_cuda_ger_rm_f32(const float* x, const float* y, float* C, uint64_t m, uint64_t n,
+                         uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return ger_impl<float>(x, y, C, CABL_ROW_MAJOR, m, n, small_cutoff, probe, stream);
+}
+int cabl_cuda_ger_rm_f64(const double* x, const double* y, double* C, uint64_t m, uint64_t n,
+                         uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return ger_impl<double>(x, y, C, CABL_ROW_MAJOR, m, n, small_cutoff, probe, stream);
+}
+int cabl_cuda_ger_cm_f32(const float* x, const float* y, float* C, uint64_t m, uint64_t n,
+                         uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return ger_impl<float>(x, y, C, CABL_COL_MAJOR, m, n, small_cutoff, probe, stream);
+}
+int cabl_cuda_ger_cm_f64(const double* x, const double* y, double* C, uint64_t m, uint64_t n,
+                         uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return ger_impl<double>(x, y, C, CABL_COL_MAJOR, m, n, small_cutoff, probe, stream);
+}
+
+int cabl_host_dot_f32(const float* x, const float* y, uint64_t n, float alpha0, float* result,
+                      uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return host_dot<float>(x, y, n, alpha0, result, small_cutoff, probe, stream);
+}
+int cabl_host_dot_f64(const double* x, const double* y, uint64_t n, double alpha0,
+                      double* result, uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return host_dot<double>(x, y, n, alpha0, result, small_cutoff, probe, stream);
+}
+int cabl_host_gemv_f32(const float* A, int layout, uint64_t m, uint64_t n, const float* x,
+                       float* c, uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return host_gemv<float>(A, layout, m, n, x, c, small_cutoff, probe, stream);
+}
+int cabl_host_gemv_f64(const double* A, int layout, uint64_t m, uint64_t n, const double* x,
+                       double* c, uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return host_gemv<double>(A, layout, m, n, x, c, small_cutoff, probe, stream);
+}
+int cabl_host_ger_f32(const float* x, const float* y, float* C, int layout, uint64_t m,
+                      uint64_t n, uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return host_ger<float>(x, y, C, layout, m, n, small_cutoff, probe, stream);
+}
+int cabl_host_ger_f64(const double* x, const double* y, double* C, int layout, uint64_t m,
+                      uint64_t n, uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return host_ger<double>(x, y, C, layout, m, n, small_cutoff, probe, stream);
+}
+
+int cabl_cuda_fill_uniform_f32(float* out, uint64_t n, uint64_t seed, uint64_t stream_id,
+                               uint64_t offset, void* stream) {
+    if (n > 0 && !out) return fail(CABL_EINVAL, "fill: out must not be null");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    CABL_TRY_CUDA(fill_uniform_f32(out, n, seed, stream_id, offset, as_stream(stream)), "fill");
+    return CABL_OK;
+}
+int cabl_cuda_fill_uniform_f64(double* out, uint64_t n, uint64_t seed, uint64_t stream_id,
+                               uint64_t offset, void* stream) {
+    if (n > 0 && !out) return fail(CABL_EINVAL, "fill: out must not be null");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    CABL_TRY_CUDA(fill_uniform_f64(out, n, seed, stream_id, offset, as_stream(stream)), "fill");
+    return CABL_OK;
+}
+int cabl_cuda_fill_normal_f64(double* out, uint64_t n, uint64_t seed, uint64_t stream_id,
+                              uint64_t offset, void* stream) {
+    if (n > 0 && !out) return fail(CABL_EINVAL, "fill: out must not be null");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    CABL_TRY_CUDA(fill_normal_f64(out, n, seed, stream_id, offset, as_stream(stream)), "fill");
+    return CABL_OK;
+}
+
+} // extern "C"

@@ -1,0 +1,156 @@
+// Shared device helpers for the B200 (sm_100a) DOT / GEMV / GER kernels.
+//
+// Every kernel here is HBM-bound (<= 0.5 flop/byte); the
+// levers are the bytes in flight per SM, the LSU instruction count and load
+// balance across the 148 SMs — not tensor cores.  sm_100a has 256-bit global
+// loads/stores (SASS LDG.E.256 / STG.E.256), so a "vector" below is 32 bytes:
+// 8 floats or 4 doubles per lane per instruction, half the LSU issue of
+// float4/double2.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cabl_dev {
+
+constexpr int kWarp = 32;
+
+// 32-byte vector of T.
+template <typename T> struct Vec;
+template <> struct alignas(32) Vec<float> {
+    static constexpr int N = 8;
+    float v[8];
+};
+template <> struct alignas(32) Vec<double> {
+    static constexpr int N = 4;
+    double v[4];
+};
+
+// ---- 256-bit loads -------------------------------------------------------
+// Streaming read-only operand (A, x/y of DOT): non-coherent path, no L1
+// allocation, and a 256 B L2 prefetch hint so each DRAM burst is a full
+// 256 B.  Only for data no thread writes during the kernel.
+__device__ __forceinline__ Vec<float> ld_stream(const Vec<float>* p) {
+    Vec<float> r;
+    asm volatile(
+        "ld.global.nc.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+          "=f"(r.v[6]), "=f"(r.v[7])
+        : "l"(p));
+    return r;
+}
+__device__ __forceinline__ Vec<double> ld_stream(const Vec<double>* p) {
+    Vec<double> r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+                 : "l"(p));
+    return r;
+}
+
+// Reused read-only operand (x of GEMV, y of GER): cached in L1.
+__device__ __forceinline__ Vec<float> ld_reuse(const Vec<float>* p) {
+    Vec<float> r;
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                   "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ Vec<double> ld_reuse(const Vec<double>* p) {
+    Vec<double> r;
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+                 : "l"(p));
+    return r;
+}
+
+// Read-modify-write operand (C of GER): coherent load, no L1 allocation.
+__device__ __forceinline__ Vec<float> ld_rmw(const Vec<float>* p) {
+    Vec<float> r;
+    asm volatile("ld.global.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                   "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ Vec<double> ld_rmw(const Vec<double>* p) {
+    Vec<double> r;
+    asm volatile("ld.global.L1::no_allocate.L2::256B.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+
+__device__ __forceinline__ void st_stream(Vec<float>* p, const Vec<float>& r) {
+    asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+                 "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]),
+                 "f"(r.v[6]), "f"(r.v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void st_stream(Vec<double>* p, const Vec<double>& r) {
+    asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r.v[0]),
+                 "d"(r.v[1]), "d"(r.v[2]), "d"(r.v[3])
+                 : "memory");
+}
+
+// ---- arithmetic with the rounding spelled out ------------------------------
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+// acc + a.b over one 32-byte vector, one FMA chain in element order.
+template <typename T>
+__device__ __forceinline__ T dot_vec(const Vec<T>& a, const Vec<T>& b, T acc) {
+#pragma unroll
+    for (int k = 0; k < Vec<T>::N; ++k) acc = fma_rn(a.v[k], b.v[k], acc);
+    return acc;
+}
+
+// Fixed butterfly: every lane ends with the same, order-fixed sum.
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = add_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Order-fixed block sum (blockDim.x multiple of 32, <= 1024); result valid in
+// every thread.  `red` must hold 32 T.  Contains two __syncthreads().
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    T t = lane < nw ? red[lane] : T(0);
+    t = warp_sum(t);
+    __syncthreads();
+    return t;
+}
+
+// L1-bypassing loads for data another CTA produced in this kernel.
+__device__ __forceinline__ float ld_cg(const float* p) { return __ldcg(p); }
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// Balanced static partition of `total` units over `parts`: part w owns
+// [begin(w), begin(w+1)).  owner(u) inverts it.
+struct Partition {
+    uint64_t total, parts, q, r;
+    __host__ __device__ Partition(uint64_t total_, uint64_t parts_)
+        : total(total_), parts(parts_), q(total_ / parts_), r(total_ % parts_) {}
+    __host__ __device__ uint64_t begin(uint64_t w) const { return w * q + (w < r ? w : r); }
+    __host__ __device__ uint64_t owner(uint64_t u) const {
+        const uint64_t big = r * (q + 1);
+        return u < big ? u / (q + 1) : r + (u - big) / q;
+    }
+};
+
+inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
+
+} // namespace cabl_dev

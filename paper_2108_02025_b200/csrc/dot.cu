@@ -1,0 +1,158 @@
+// DOT: *out = alpha0 + sum_p x[p]*y[p]  — B200 re-design of reference
+// cabl::dot (proj/include/cabl/kernels.hpp:134-164).
+//
+// One launch, no host round trip:
+//   * grid = min(tiles, 148 * CTAS_PER_SM) CTAs (one wave, all resident);
+//     CTAs stride over tiles of BLOCK*U 32-byte vectors, every thread keeps
+//     2*U 256-bit loads in flight and accumulates with FMA in registers;
+//   * fixed butterfly warp sums, fixed-order CTA sum -> partials[cta];
+//   * the last CTA to arrive (atomic ticket) sums the partials in a fixed
+//     order, adds alpha0 LAST (as the reference does, kernels.hpp:142,163)
+//     and resets the ticket for the next launch on this stream.
+// The element -> thread mapping depends only on n and the grid, so the result
+// is bitwise reproducible run to run (reference kernels.hpp:9-13).
+//
+// Algorithmic bytes per launch: 2 * n * sizeof(T).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cabl_dev {
+
+namespace {
+
+constexpr int kDotBlock = 256;
+constexpr int kDotUnroll = 2;
+constexpr int kDotCtasPerSm = 4;
+
+template <typename T, int BLOCK, int U>
+__global__ void __launch_bounds__(BLOCK)
+    dot_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t n, int vec_ok,
+               T alpha0, T* __restrict__ out, T* __restrict__ partials,
+               unsigned* __restrict__ ticket) {
+    __shared__ T red[32];
+    __shared__ bool am_last;
+    constexpr int V = Vec<T>::N;
+    const int tid = threadIdx.x;
+
+    T acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = T(0);
+
+    uint64_t done = 0; // elements covered by the vector loop
+    if (vec_ok) {
+        const uint64_t nvec = n / V;
+        const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
+        const Vec<T>* Y = reinterpret_cast<const Vec<T>*>(y);
+        const uint64_t per_iter = uint64_t(BLOCK) * U;
+        const uint64_t stride = uint64_t(gridDim.x) * per_iter;
+        for (uint64_t base = uint64_t(blockIdx.x) * per_iter; base < nvec; base += stride) {
+            Vec<T> xv[U], yv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t i = base + uint64_t(u) * BLOCK + tid;
+                if (i < nvec) {
+                    xv[u] = ld_stream(X + i);
+                    yv[u] = ld_stream(Y + i);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < V; ++k) xv[u].v[k] = yv[u].v[k] = T(0);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u] = dot_vec(xv[u], yv[u], acc[u]);
+        }
+        done = nvec * V;
+    }
+    // Scalar remainder (unaligned operands, or the < V trailing elements).
+    {
+        const uint64_t gt = uint64_t(blockIdx.x) * BLOCK + tid;
+        const uint64_t gs = uint64_t(gridDim.x) * BLOCK;
+        for (uint64_t i = done + gt; i < n; i += gs) acc[0] = fma_rn(x[i], y[i], acc[0]);
+    }
+
+    T s = acc[0];
+#pragma unroll
+    for (int u = 1; u < U; ++u) s = add_rn(s, acc[u]);
+    const T cta_total = block_sum(s, red);
+
+    if (gridDim.x == 1) {
+        if (tid == 0) *out = add_rn(cta_total, alpha0);
+        return;
+    }
+    if (tid == 0) {
+        partials[blockIdx.x] = cta_total;
+        __threadfence();
+        const unsigned t = atomicAdd(ticket, 1u);
+        am_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    T v = T(0);
+    for (unsigned i = tid; i < gridDim.x; i += BLOCK) v = add_rn(v, ld_cg(partials + i));
+    const T total = block_sum(v, red);
+    if (tid == 0) {
+        *out = add_rn(total, alpha0);
+        *ticket = 0u; // ready for the next launch on this stream
+    }
+}
+
+template <typename T>
+__global__ void combine_kernel(const T* __restrict__ p, uint32_t count, T alpha0,
+                               T* __restrict__ out) {
+    // Reference kernels.hpp:160-163: total{} += partials[c] in index order,
+    // then + alpha0.
+    T total = T(0);
+    for (uint32_t i = 0; i < count; ++i) total = add_rn(total, p[i]);
+    *out = add_rn(total, alpha0);
+}
+
+template <typename T> unsigned dot_grid(uint64_t n, bool small) {
+    if (small) return 1;
+    constexpr int V = Vec<T>::N;
+    const uint64_t tiles = (n / V + uint64_t(kDotBlock) * kDotUnroll - 1) /
+                           (uint64_t(kDotBlock) * kDotUnroll);
+    const uint64_t cap = uint64_t(sm_count()) * kDotCtasPerSm;
+    uint64_t g = tiles < cap ? tiles : cap;
+    return g < 1 ? 1u : unsigned(g);
+}
+
+} // namespace
+
+template <typename T> WorkspaceNeed dot_need(uint64_t n, bool small) {
+    WorkspaceNeed w;
+    w.counters = 1;
+    w.scratch_bytes = size_t(dot_grid<T>(n, small)) * sizeof(T);
+    return w;
+}
+
+template <typename T>
+cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, bool small,
+                       const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
+    const unsigned grid = dot_grid<T>(n, small);
+    const int vec_ok = aligned32(x) && aligned32(y);
+    dot_kernel<T, kDotBlock, kDotUnroll><<<grid, kDotBlock, 0, s>>>(
+        x, y, n, vec_ok, alpha0, out, static_cast<T*>(ws.scratch), ws.counters);
+    if (info) info->ctas = grid;
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t combine_partials_launch(const T* p, uint32_t count, T alpha0, T* out,
+                                    cudaStream_t s) {
+    combine_kernel<T><<<1, 1, 0, s>>>(p, count, alpha0, out);
+    return cudaGetLastError();
+}
+
+template WorkspaceNeed dot_need<float>(uint64_t, bool);
+template WorkspaceNeed dot_need<double>(uint64_t, bool);
+template cudaError_t dot_launch<float>(const float*, const float*, uint64_t, float, float*, bool,
+                                       const Workspace&, cudaStream_t, LaunchInfo*);
+template cudaError_t dot_launch<double>(const double*, const double*, uint64_t, double, double*,
+                                        bool, const Workspace&, cudaStream_t, LaunchInfo*);
+template cudaError_t combine_partials_launch<float>(const float*, uint32_t, float, float*,
+                                                    cudaStream_t);
+template cudaError_t combine_partials_launch<double>(const double*, uint32_t, double, double*,
+                                                     cudaStream_t);
+
+} // namespace cabl_dev

@@ -1,0 +1,222 @@
+// Row-major GEMV: c += A x, A is m x n row-major — B200 re-design of reference
+// cabl::gemv_row_major (proj/include/cabl/kernels.hpp:230-257).
+//
+// The reference hands whole rows to CPU threads.  On B200 a whole-row split
+// leaves the 148 SMs unevenly loaded whenever m is not a large multiple of
+// the warp count (8192 rows over 2368 warps is 3.46 rows/warp: 16% of the
+// machine idles at the end).  Instead the work is cut into UNITS of
+// R rows x SEG warp-vectors (one warp-vector = 32 lanes x 32 bytes), units
+// are ordered (row group, column segment), and every warp of a single-wave
+// grid owns a contiguous, balanced range of units (±1 unit).
+//
+//   * a warp keeps R*SEG + SEG 256-bit loads in flight per lane per unit
+//     (A streamed with L1::no_allocate, x through L1 — it is re-read by every
+//     row group, R rows share each x load);
+//   * per row, lanes accumulate with FMA, then a fixed butterfly sums lanes;
+//   * a row group entirely inside one warp's range is finished by that warp:
+//     c[i] = c[i] + sum;
+//   * a row group split across warps (only at range boundaries — at most one
+//     per warp) leaves one partial per touching warp in a slot; the last warp
+//     to arrive (atomic ticket) adds the partials in warp order, then to c,
+//     and resets the ticket.
+// Every per-element order is a function of (m, n, grid) only: bitwise
+// reproducible run to run.
+//
+// Unaligned operands or n % (32/sizeof(T)) != 0 take a scalar warp-per-row
+// kernel (same ordering guarantees).
+//
+// Algorithmic bytes per launch: m*n*s + n*s + 2*m*s.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cabl_dev {
+
+namespace {
+
+constexpr int kRmBlock = 256;
+constexpr int kRmCtasPerSm = 2;
+constexpr int kRmRows = 2; // R
+constexpr int kRmSeg = 2;  // SEG warp-vectors per unit
+
+struct RmGeom {
+    uint64_t nvec_row; // 32-byte vectors per row
+    uint64_t nwv;      // warp-vectors per row
+    uint64_t S;        // segments per row group
+    uint64_t G;        // row groups
+    uint64_t warps;    // warps that own units
+};
+
+template <typename T, int R, int SEG>
+__global__ void __launch_bounds__(kRmBlock, kRmCtasPerSm)
+    gemv_rm_vec_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
+                       uint64_t m, uint64_t n, RmGeom geo, T* __restrict__ slots,
+                       unsigned* __restrict__ tickets) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (gw >= geo.warps) return;
+    const Partition part(geo.G * geo.S, geo.warps);
+    const uint64_t u0 = part.begin(gw), u1 = part.begin(gw + 1);
+    const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
+    const uint64_t first_group = u0 / geo.S;
+
+    uint64_t u = u0;
+    while (u < u1) {
+        const uint64_t g = u / geo.S;
+        const uint64_t s_begin = u - g * geo.S;
+        const uint64_t s_end = (geo.S - s_begin < u1 - u) ? geo.S : s_begin + (u1 - u);
+        const uint64_t row0 = g * R;
+        const int rows = (m - row0 < uint64_t(R)) ? int(m - row0) : R;
+        const Vec<T>* Arow[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            Arow[r] = reinterpret_cast<const Vec<T>*>(A + (row0 + (r < rows ? r : 0)) * n);
+
+        T acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = T(0);
+
+        for (uint64_t s = s_begin; s < s_end; ++s) {
+            Vec<T> xv[SEG];
+            Vec<T> av[SEG][R];
+#pragma unroll
+            for (int k = 0; k < SEG; ++k) {
+                const uint64_t cv = (s * SEG + k) * kWarp + lane; // vector column
+                if (cv < geo.nvec_row) {
+                    xv[k] = ld_reuse(X + cv);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        if (r < rows) av[k][r] = ld_stream(Arow[r] + cv);
+                        else
+#pragma unroll
+                            for (int e = 0; e < Vec<T>::N; ++e) av[k][r].v[e] = T(0);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < Vec<T>::N; ++e) xv[k].v[e] = T(0);
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+#pragma unroll
+                        for (int e = 0; e < Vec<T>::N; ++e) av[k][r].v[e] = T(0);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < SEG; ++k)
+#pragma unroll
+                for (int r = 0; r < R; ++r) acc[r] = dot_vec(av[k][r], xv[k], acc[r]);
+        }
+
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = warp_sum(acc[r]);
+
+        if (s_begin == 0 && s_end == geo.S) {
+            // whole row group owned by this warp
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (lane == r && r < rows) c[row0 + r] = add_rn(c[row0 + r], acc[r]);
+        } else {
+            // split row group: deposit, then last arriver combines in warp order
+            const int which = (g == first_group) ? 0 : 1;
+            T* my_slot = slots + (gw * 2 + which) * R;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (lane == r) my_slot[r] = acc[r];
+            __threadfence();
+            __syncwarp();
+            const uint64_t wf = part.owner(g * geo.S);
+            const uint64_t wl = part.owner(g * geo.S + geo.S - 1);
+            unsigned arrived = 0;
+            if (lane == 0) arrived = atomicAdd(tickets + wf, 1u);
+            arrived = __shfl_sync(0xffffffffu, arrived, 0);
+            if (arrived == unsigned(wl - wf)) {
+                __threadfence();
+                if (lane < rows) {
+                    T total = T(0);
+                    for (uint64_t w = wf; w <= wl; ++w) {
+                        const int wh = (g == part.begin(w) / geo.S) ? 0 : 1;
+                        total = add_rn(total, ld_cg(slots + (w * 2 + wh) * R + lane));
+                    }
+                    c[row0 + lane] = add_rn(c[row0 + lane], total);
+                }
+                if (lane == 0) tickets[wf] = 0u;
+            }
+        }
+        u += s_end - s_begin;
+    }
+}
+
+// Generic path: one warp per row (balanced row ranges), scalar coalesced loads.
+template <typename T>
+__global__ void __launch_bounds__(kRmBlock)
+    gemv_rm_scalar_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
+                          uint64_t m, uint64_t n, uint64_t warps) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (gw >= warps) return;
+    const Partition part(m, warps);
+    for (uint64_t i = part.begin(gw); i < part.begin(gw + 1); ++i) {
+        const T* row = A + i * n;
+        T acc = T(0);
+        for (uint64_t j = lane; j < n; j += kWarp) acc = fma_rn(row[j], x[j], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) c[i] = add_rn(c[i], acc);
+    }
+}
+
+template <typename T> bool rm_vec_ok(const T* A, const T* x, uint64_t n) {
+    return aligned32(A) && aligned32(x) && (n % Vec<T>::N == 0);
+}
+
+template <typename T> RmGeom rm_geom(uint64_t m, uint64_t n) {
+    RmGeom g;
+    g.nvec_row = n / Vec<T>::N;
+    g.nwv = (g.nvec_row + kWarp - 1) / kWarp;
+    g.S = (g.nwv + kRmSeg - 1) / kRmSeg;
+    if (g.S == 0) g.S = 1;
+    g.G = (m + kRmRows - 1) / kRmRows;
+    const uint64_t max_warps = uint64_t(sm_count()) * kRmCtasPerSm * (kRmBlock / kWarp);
+    const uint64_t units = g.G * g.S;
+    g.warps = units < max_warps ? units : max_warps;
+    return g;
+}
+
+} // namespace
+
+template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n) {
+    WorkspaceNeed w;
+    if (m == 0 || n == 0 || !rm_vec_ok(A, x, n)) return w;
+    const RmGeom g = rm_geom<T>(m, n);
+    w.counters = g.warps;
+    w.scratch_bytes = g.warps * 2 * kRmRows * sizeof(T);
+    return w;
+}
+
+template <typename T>
+cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
+                           const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
+    if (info) info->ctas = 0;
+    if (m == 0 || n == 0) return cudaSuccess; // c += 0
+    if (rm_vec_ok(A, x, n)) {
+        const RmGeom g = rm_geom<T>(m, n);
+        const unsigned grid = unsigned((g.warps * kWarp + kRmBlock - 1) / kRmBlock);
+        gemv_rm_vec_kernel<T, kRmRows, kRmSeg><<<grid, kRmBlock, 0, s>>>(
+            A, x, c, m, n, g, static_cast<T*>(ws.scratch), ws.counters);
+        if (info) info->ctas = grid;
+    } else {
+        const uint64_t max_warps = uint64_t(sm_count()) * 8 * (kRmBlock / kWarp);
+        const uint64_t warps = m < max_warps ? m : max_warps;
+        const unsigned grid = unsigned((warps * kWarp + kRmBlock - 1) / kRmBlock);
+        gemv_rm_scalar_kernel<T><<<grid, kRmBlock, 0, s>>>(A, x, c, m, n, warps);
+        if (info) info->ctas = grid;
+    }
+    return cudaGetLastError();
+}
+
+template WorkspaceNeed gemv_rm_need<float>(const float*, const float*, uint64_t, uint64_t);
+template WorkspaceNeed gemv_rm_need<double>(const double*, const double*, uint64_t, uint64_t);
+template cudaError_t gemv_rm_launch<float>(const float*, uint64_t, uint64_t, const float*,
+                                           float*, const Workspace&, cudaStream_t, LaunchInfo*);
+template cudaError_t gemv_rm_launch<double>(const double*, uint64_t, uint64_t, const double*,
+                                            double*, const Workspace&, cudaStream_t,
+                                            LaunchInfo*);
+
+} // namespace cabl_dev

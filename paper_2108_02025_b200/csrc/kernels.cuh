@@ -1,0 +1,76 @@
+// Internal launcher interface between the C ABI (capi.cu) and the kernels.
+// Not installed; the public boundary is include/cabl_cuda.h.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cabl_dev {
+
+// Per-(device, stream) scratch owned by the C ABI.  `counters` are zero on
+// entry and every kernel that uses them leaves them zero on exit (the
+// last-arriving CTA resets what it used), so the workspace is reusable by the
+// next launch on the same stream without a memset.
+struct Workspace {
+    unsigned* counters = nullptr;
+    size_t n_counters = 0;
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+};
+
+struct WorkspaceNeed {
+    size_t counters = 0;
+    size_t scratch_bytes = 0;
+};
+
+struct LaunchInfo {
+    unsigned ctas = 0; // CTAs of the main pass (probe threads_used)
+};
+
+int sm_count(); // of the current device (cached per device)
+
+// ---- DOT (dot.cu) ----
+template <typename T> WorkspaceNeed dot_need(uint64_t n, bool small);
+template <typename T>
+cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, bool small,
+                       const Workspace& ws, cudaStream_t s, LaunchInfo* info);
+template <typename T>
+cudaError_t combine_partials_launch(const T* p, uint32_t count, T alpha0, T* out,
+                                    cudaStream_t s);
+
+// ---- GEMV row-major (gemv_rm.cu) ----
+template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n);
+template <typename T>
+cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
+                           const Workspace& ws, cudaStream_t s, LaunchInfo* info);
+
+// ---- GEMV col-major (gemv_cm.cu) ----
+template <typename T> WorkspaceNeed gemv_cm_need(const T* A, const T* x, uint64_t m, uint64_t n);
+template <typename T>
+cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
+                           const Workspace& ws, cudaStream_t s, LaunchInfo* info);
+
+// ---- ordered single-CTA GEMV (gemv_small.cu): reproduces the compiled
+// reference gemv_ref bit for bit (oracle/cabl_oracle.c documents the
+// semantics: vec-wide mul-then-add prefix, FMA remainder). layout 0 = RM.
+template <typename T>
+cudaError_t gemv_ordered_launch(const T* A, int layout, uint64_t m, uint64_t n, const T* x,
+                                T* c, cudaStream_t s, LaunchInfo* info);
+
+// ---- GER (ger.cu): C(major, minor) = fma(u[major], v[minor], C) over an
+// outer x inner row-major view; the col-major GER is the same kernel with
+// (x, m) and (y, n) swapped, since fma(a, b, c) == fma(b, a, c).
+template <typename T>
+cudaError_t ger_launch(const T* u, const T* v, T* C, uint64_t outer, uint64_t inner,
+                       bool small, cudaStream_t s, LaunchInfo* info);
+
+// ---- seeded inputs (datagen.cu) ----
+cudaError_t fill_uniform_f32(float* out, uint64_t n, uint64_t seed, uint64_t sid,
+                             uint64_t offset, cudaStream_t s);
+cudaError_t fill_uniform_f64(double* out, uint64_t n, uint64_t seed, uint64_t sid,
+                             uint64_t offset, cudaStream_t s);
+cudaError_t fill_normal_f64(double* out, uint64_t n, uint64_t seed, uint64_t sid,
+                            uint64_t offset, cudaStream_t s);
+
+} // namespace cabl_dev

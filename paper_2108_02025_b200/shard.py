@@ -1,0 +1,95 @@
+"""Multi-GPU partitioning of the hot path — one process per GPU, torch.distributed.
+
+The reference parallelises over CPU threads with contiguous chunks
+(reference thread_pool.hpp:153-164) and combines DOT partials in chunk order
+(kernels.hpp:160-163).  Lifted to GPUs:
+
+* DOT — rank g owns the contiguous chunk [g n/G, (g+1) n/G) of x and y and
+  computes a partial with the single-GPU kernel (alpha0 = 0).  The only
+  exchange is one all-gather of the G partials (4 or 8 bytes each) over
+  NCCL; every rank then sums them IN RANK ORDER on the device and adds
+  alpha0 last (``cabl_cuda_combine_partials_*``), so the result does not
+  depend on NCCL's reduction algorithm: bitwise reproducible, and identical
+  on every rank.
+* GEMV (row-major or col-major tall) — rank g owns a block of rows of A and
+  of c, x is replicated; no exchange is needed.  ``gather=True`` assembles
+  the full c on every rank with one all-gather (slices padded to equal size).
+* GER — rank g owns a block of rows of C and of x, y is replicated; no
+  communication at all.
+
+The collective and the local compute are injectable so the partition and
+combine logic can be exercised by CPU ``gloo`` tests (tests/test_shard_gloo.py)
+without a GPU; the defaults are the CUDA kernels and nothing else.
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+from . import cabl
+
+
+def partition(total: int, parts: int, rank: int) -> tuple[int, int]:
+    """Balanced contiguous split: the first total % parts ranks get one extra."""
+    q, r = divmod(total, parts)
+    b = rank * q + min(rank, r)
+    return b, b + q + (1 if rank < r else 0)
+
+
+def _device_partial(x, y, out, policy):
+    cabl.dot_into(x, y, 0.0, out, policy)
+
+
+def _device_combine(partials: torch.Tensor, alpha0: float, out: torch.Tensor) -> None:
+    from . import _lib
+    sfx = cabl._suffix(partials)
+    _lib.call(f"cabl_cuda_combine_partials_{sfx}", partials.data_ptr(), partials.numel(),
+              float(alpha0), out.data_ptr(), cabl._stream_of(partials))
+
+
+def sharded_dot(x_local: torch.Tensor, y_local: torch.Tensor, alpha0: float, out: torch.Tensor,
+                policy: "cabl.ExecPolicy", group=None, *,
+                partial_fn: Callable = _device_partial,
+                combine_fn: Callable = _device_combine,
+                gathered: torch.Tensor | None = None) -> torch.Tensor:
+    """out[0] = alpha0 + sum over ranks (in rank order) of this rank's partial."""
+    world = dist.get_world_size(group)
+    part = torch.empty(1, dtype=x_local.dtype, device=x_local.device)
+    partial_fn(x_local, y_local, part, policy)
+    if gathered is None:
+        gathered = torch.empty(world, dtype=x_local.dtype, device=x_local.device)
+    dist.all_gather_into_tensor(gathered, part, group=group)
+    combine_fn(gathered, alpha0, out)
+    return out
+
+
+def sharded_gemv_rows(A_local: "cabl.DenseMatrix", x: torch.Tensor, c_local: torch.Tensor,
+                      policy: "cabl.ExecPolicy", *, gather: bool = False, m_total: int = 0,
+                      group=None, local_fn: Callable | None = None) -> torch.Tensor | None:
+    """c_local += A_local x on this rank's row block; optionally all-gather c."""
+    if local_fn is None:
+        local_fn = (cabl.gemv_row_major if A_local.layout() == cabl.Layout.RowMajor
+                    else cabl.gemv_col_major)
+    local_fn(A_local, x, c_local, policy)
+    if not gather:
+        return None
+    world = dist.get_world_size(group)
+    widest = partition(m_total, world, 0)
+    width = widest[1] - widest[0]
+    padded = torch.zeros(width, dtype=c_local.dtype, device=c_local.device)
+    padded[:c_local.numel()] = c_local
+    slab = torch.empty(world * width, dtype=c_local.dtype, device=c_local.device)
+    dist.all_gather_into_tensor(slab, padded, group=group)
+    pieces = []
+    for r in range(world):
+        b, e = partition(m_total, world, r)
+        pieces.append(slab[r * width: r * width + (e - b)])
+    return torch.cat(pieces)
+
+
+def sharded_ger_rows(x_local: torch.Tensor, y: torch.Tensor, C_local: "cabl.DenseMatrix",
+                     policy: "cabl.ExecPolicy", *, local_fn: Callable | None = None) -> None:
+    """C_local += x_local (x) y on this rank's row block — no communication."""
+    (local_fn or cabl.ger)(x_local, y, C_local, policy)

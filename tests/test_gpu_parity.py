@@ -1,0 +1,349 @@
+"""GPU parity: libcabl_cuda.so (through the C ABI) vs the CPU oracle.
+
+Inputs are the seeded SplitMix64 fills generated on the device and copied to
+the host, so both sides see identical bits.  Bars (tests/tolerances.py):
+GER and the ordered paths bitwise; DOT/GEMV within BASELINE's contract bound
+against the oracle AND a non-vacuous bound against extended-precision truth;
+every kernel bitwise reproducible run to run.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from tests import tolerances as T
+
+pytestmark = pytest.mark.gpu
+
+SEED = 42
+
+
+def dev_uniform(n, dtype, stream, cuda, seed=SEED):
+    import paper_2108_02025_b200 as cb
+    t = torch.empty(n, dtype=dtype, device=cuda)
+    if n:
+        cb.fill_uniform(t, seed, stream)
+    return t
+
+
+def np_of(t):
+    return t.detach().cpu().numpy()
+
+
+def policy():
+    import paper_2108_02025_b200 as cb
+    return cb.default_policy(1)
+
+
+def plan_for(dtype):
+    """Plan derived with element_bytes = sizeof(T), as the reference bench does."""
+    import paper_2108_02025_b200 as cb
+    md = cb.default_machine()
+    md.element_bytes = torch.tensor([], dtype=dtype).element_size()
+    return cb.ExecPolicy(cb.derive_blocking_plan(md), 1)
+
+
+DTYPES = [torch.float32, torch.float64]
+
+
+# ------------------------------------------------------------------ DOT
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("n", [0, 1, 7, 8, 9, 33, 1000, 8192, 8193, 16384, 16385, 100_003,
+                               1_000_000, 1 << 24])
+def test_dot_matches_oracle(cuda, dtype, n):
+    import paper_2108_02025_b200 as cb
+    x, y = dev_uniform(n, dtype, 1, cuda), dev_uniform(n, dtype, 2, cuda)
+    pol = plan_for(dtype)
+    got = cb.dot(x, y, 0.25, pol)
+    probe = cb.last_exec()
+    xn, yn = np_of(x), np_of(y)
+    want = O.dot_ref(xn, yn, 0.25)
+    truth, sumabs = O.dot_truth(xn, yn, 0.25)
+    npdt = xn.dtype
+    assert abs(got - float(want)) <= T.contract_tol(n, sumabs, 0.25, npdt)
+    assert abs(got - truth) <= T.truth_tol(T.dot_chain(n, npdt), sumabs, 0.25, npdt)
+    if n <= pol.plan.dot_cutoff:
+        assert probe.variant == cb.KernelVariant.dot_small and probe.threads_used == 1
+    else:
+        assert probe.variant == cb.KernelVariant.dot_blocked and probe.threads_used >= 2
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_dot_unaligned_operands(cuda, dtype):
+    import paper_2108_02025_b200 as cb
+    n = 300_001
+    x, y = dev_uniform(n + 3, dtype, 1, cuda), dev_uniform(n + 5, dtype, 2, cuda)
+    xs, ys = x[1:n + 1], y[3:n + 3]
+    got = cb.dot(xs, ys, -1.5, policy())
+    xn, yn = np_of(xs), np_of(ys)
+    truth, sumabs = O.dot_truth(xn, yn, -1.5)
+    assert abs(got - truth) <= T.truth_tol(n, sumabs, 1.5, xn.dtype)
+
+
+def test_dot_hand_values(cuda):
+    import paper_2108_02025_b200 as cb
+    # reference test_kernels.cpp:54-62, :96-98
+    t = lambda v: torch.tensor(v, dtype=torch.float64, device=cuda)
+    assert cb.dot(t([1, 2, 3]), t([4, 5, 6]), 0.0, policy()) == 32.0
+    assert cb.dot(t([0.5, -1.25, 3.0]), t([0.0, 0.0, 0.0]), 7.5, policy()) == 7.5
+    assert cb.dot(t([0.0, 1.0, 0.0]), t([0.0, 1.0, 0.0]), 0.0, policy()) == 1.0
+    assert cb.dot(t([]), t([]), 2.5, policy()) == 2.5
+    with pytest.raises(ValueError, match="dot: x and y lengths differ"):
+        cb.dot(t([1.0, 2.0]), t([1.0]), 0.0, policy())
+
+
+# ----------------------------------------------------------------- GEMV
+def _gemv_case(cuda, dtype, m, n, layout, seed=SEED):
+    import paper_2108_02025_b200 as cb
+    A = dev_uniform(m * n, dtype, 3, cuda, seed)
+    x = dev_uniform(n, dtype, 1, cuda, seed)
+    c0 = dev_uniform(m, dtype, 4, cuda, seed)
+    Am = cb.DenseMatrix.wrap(A, m, n, layout)
+    c = c0.clone()
+    pol = plan_for(dtype)
+    if layout == cb.Layout.RowMajor:
+        cb.gemv_row_major(Am, x, c, pol)
+    else:
+        cb.gemv_col_major(Am, x, c, pol)
+    probe = cb.last_exec()
+    An, xn, c0n = np_of(A), np_of(x), np_of(c0)
+    want = c0n.copy()
+    O.gemv_ref(An, int(layout), xn, want)
+    truth, rowabs = O.gemv_truth(An, int(layout), xn, c0n)
+    return np_of(c), want, truth, rowabs, c0n, probe, pol
+
+
+RM_SHAPES = [(1, 777), (3, 3), (8, 8), (40, 200), (257, 259), (1000, 1000), (2000, 500),
+             (33, 16392), (4097, 1024), (8192, 8192)]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("m,n", RM_SHAPES)
+def test_gemv_row_major_matches_oracle(cuda, dtype, m, n):
+    import paper_2108_02025_b200 as cb
+    got, want, truth, rowabs, c0, probe, pol = _gemv_case(cuda, dtype, m, n, cb.Layout.RowMajor)
+    dt = got.dtype
+    assert probe.variant == cb.KernelVariant.gemv_row
+    if m * n + m + n <= pol.plan.dot_cutoff:
+        # ordered single-CTA path: bit for bit the compiled reference gemv_ref
+        assert probe.threads_used == 1
+        np.testing.assert_array_equal(got, want)
+    tol_c = T.contract_tol(n, rowabs, np.abs(c0), dt)
+    assert np.all(np.abs(got.astype(np.float64) - want) <= tol_c)
+    tol_t = T.truth_tol(T.gemv_rm_chain(n, dt), rowabs, np.abs(c0), dt)
+    assert np.all(np.abs(got.astype(np.float64) - truth) <= tol_t)
+
+
+CM_SHAPES = [(3, 3), (8, 8), (257, 259), (1000, 1000), (256, 65536), (2047, 300),
+             (2048, 100), (65536, 256), (70001, 37)]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("m,n", CM_SHAPES)
+def test_gemv_col_major_matches_oracle(cuda, dtype, m, n):
+    import paper_2108_02025_b200 as cb
+    got, want, truth, rowabs, c0, probe, pol = _gemv_case(cuda, dtype, m, n, cb.Layout.ColMajor)
+    dt = got.dtype
+    assert probe.variant == cb.KernelVariant.gemv_col_blocked
+    if m >= 2048 or m * n + m + n <= pol.plan.dot_cutoff:
+        # tall kernel / ordered path keep the reference order and rounding
+        np.testing.assert_array_equal(got, want)
+    tol_c = T.contract_tol(n, rowabs, np.abs(c0), dt)
+    assert np.all(np.abs(got.astype(np.float64) - want) <= tol_c)
+    tol_t = T.truth_tol(T.gemv_cm_chain(m, n, dt), rowabs, np.abs(c0), dt)
+    assert np.all(np.abs(got.astype(np.float64) - truth) <= tol_t)
+
+
+@pytest.mark.parametrize("m,n", [(1 << 20, 256), (256, 1 << 20)])
+def test_gemv_col_major_baseline_configs_fp64_normal(cuda, m, n):
+    """BASELINE config 4 (G2 / G3): fp64 col-major, N(0,1) inputs."""
+    import paper_2108_02025_b200 as cb
+    A = cb.fill_normal(torch.empty(m * n, dtype=torch.float64, device=cuda), SEED, 3)
+    x = cb.fill_normal(torch.empty(n, dtype=torch.float64, device=cuda), SEED, 1)
+    c0 = cb.fill_normal(torch.empty(m, dtype=torch.float64, device=cuda), SEED, 4)
+    c = c0.clone()
+    cb.gemv_col_major(cb.DenseMatrix.wrap(A, m, n, cb.Layout.ColMajor), x, c, policy())
+    An, xn, c0n = np_of(A), np_of(x), np_of(c0)
+    want = c0n.copy()
+    O.gemv_ref(An, 1, xn, want)
+    truth, rowabs = O.gemv_truth(An, 1, xn, c0n)
+    got = np_of(c)
+    if m >= 2048:
+        np.testing.assert_array_equal(got, want)
+    assert np.all(np.abs(got - want) <= T.contract_tol(n, rowabs, np.abs(c0n), np.float64))
+    assert np.all(np.abs(got - truth) <=
+                  T.truth_tol(T.gemv_cm_chain(m, n, np.float64), rowabs, np.abs(c0n), np.float64))
+
+
+def test_gemv_hand_values_and_contracts(cuda):
+    import paper_2108_02025_b200 as cb
+    t = lambda v: torch.tensor(v, dtype=torch.float64, device=cuda)
+    # reference test_kernels.cpp:114-147, :180-186
+    I = cb.DenseMatrix(3, 3, cb.Layout.ColMajor, device=cuda)
+    for i in range(3):
+        I[i, i] = 1.0
+    c = t([0.0, 0.0, 0.0])
+    cb.gemv_col_major(I, t([1, 2, 3]), c, policy())
+    assert c.tolist() == [1, 2, 3]
+    ones = cb.DenseMatrix(2, 3, cb.Layout.RowMajor, 1.0, device=cuda)
+    co = t([1.0, 1.0])
+    cb.gemv_row_major(ones, t([1.0, 1.0, 1.0]), co, policy())
+    assert co.tolist() == [4, 4]
+    with pytest.raises(ValueError, match="matrix is not col-major"):
+        cb.gemv_col_major(ones, t([1.0, 1.0, 1.0]), co, policy())
+    with pytest.raises(ValueError, match="gemv: A.cols != x.len"):
+        cb.gemv_row_major(ones, t([1.0] * 4), co, policy())
+    x = t([1.0, 2.0, 3.0])
+    with pytest.raises(ValueError, match="gemv: c must not alias x"):
+        cb.gemv_col_major(cb.DenseMatrix(3, 3, cb.Layout.ColMajor, 1.0, device=cuda), x, x,
+                          policy())
+    # zero-size operands are no-ops (test_kernels.cpp:282-300)
+    c5 = t([3.0] * 5)
+    cb.gemv_row_major(cb.DenseMatrix(5, 0, cb.Layout.RowMajor, device=cuda), t([]), c5, policy())
+    assert c5.tolist() == [3.0] * 5
+
+
+def test_gemv_single_row_equals_dot_ref_bitwise(cuda):
+    """Reference test_kernels.cpp:199-208: a 1 x 777 row at threads=1 equals
+    dot_ref(row, x, c0) exactly — here through the ordered small path."""
+    import paper_2108_02025_b200 as cb
+    n = 777
+    A = dev_uniform(n, torch.float64, 3, cuda)
+    x = dev_uniform(n, torch.float64, 1, cuda)
+    c = torch.tensor([0.125], dtype=torch.float64, device=cuda)
+    cb.gemv_row_major(cb.DenseMatrix.wrap(A, 1, n, cb.Layout.RowMajor), x, c, policy())
+    assert c.item() == float(O.dot_ref(np_of(A), np_of(x), 0.125))
+    assert cb.last_exec().threads_used == 1
+
+
+# ------------------------------------------------------------------ GER
+GER_SHAPES = [(1, 1), (2, 3), (3, 3), (500, 500), (777, 1001), (1000, 8), (8, 1000),
+              (1024, 1024), (3000, 4096), (8192, 8192)]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("layout", ["row", "col"])
+@pytest.mark.parametrize("m,n", GER_SHAPES)
+def test_ger_bitwise_equals_oracle(cuda, dtype, layout, m, n):
+    import paper_2108_02025_b200 as cb
+    if dtype == torch.float64 and m * n > (1 << 24):
+        pytest.skip("fp64 at 8192^2 covered by the fp32 BASELINE config")
+    lay = cb.Layout.RowMajor if layout == "row" else cb.Layout.ColMajor
+    x, y = dev_uniform(m, dtype, 1, cuda), dev_uniform(n, dtype, 2, cuda)
+    C0 = dev_uniform(m * n, dtype, 5, cuda)
+    Cm = cb.DenseMatrix.wrap(C0.clone(), m, n, lay)
+    cb.ger(x, y, Cm, plan_for(dtype))
+    assert cb.last_exec().variant == cb.KernelVariant.ger
+    want = np_of(C0)
+    O.ger_ref(np_of(x), np_of(y), want, int(lay))
+    np.testing.assert_array_equal(np_of(Cm.data), want)
+
+
+def test_ger_hand_values(cuda):
+    import paper_2108_02025_b200 as cb
+    t = lambda v: torch.tensor(v, dtype=torch.float64, device=cuda)
+    C = cb.DenseMatrix(3, 3, cb.Layout.ColMajor, 0.0, device=cuda)
+    cb.ger(t([0, 1, 0]), t([0, 0, 1]), C, policy())
+    for i in range(3):
+        for j in range(3):
+            assert C(i, j).item() == (1.0 if (i, j) == (1, 2) else 0.0)
+    C2 = cb.DenseMatrix(2, 3, cb.Layout.RowMajor, 0.0, device=cuda)
+    cb.ger(t([1, 2]), t([3, 4, 5]), C2, policy())
+    assert [[C2(i, j).item() for j in range(3)] for i in range(2)] == [[3, 4, 5], [6, 8, 10]]
+    with pytest.raises(ValueError, match="ger: C.cols != y.len"):
+        cb.ger(t([1, 2]), t([3]), cb.DenseMatrix(2, 2, cb.Layout.ColMajor, device=cuda), policy())
+    cb.ger(t([]), t([]), cb.DenseMatrix(0, 0, cb.Layout.ColMajor, device=cuda), policy())
+
+
+# --------------------------------------------------------- determinism
+def test_bitwise_reproducible_run_to_run(cuda):
+    import paper_2108_02025_b200 as cb
+    pol = policy()
+    n = (1 << 24) + 7
+    x, y = dev_uniform(n, torch.float32, 1, cuda), dev_uniform(n, torch.float32, 2, cuda)
+    first = cb.dot(x, y, 1.25, pol)
+    assert all(cb.dot(x, y, 1.25, pol) == first for _ in range(50))
+    for (m, k, lay) in [(8192, 8192, cb.Layout.RowMajor), (4097, 1000, cb.Layout.RowMajor),
+                        (256, 1 << 18, cb.Layout.ColMajor)]:
+        A = cb.DenseMatrix.wrap(dev_uniform(m * k, torch.float32, 3, cuda), m, k, lay)
+        xv = dev_uniform(k, torch.float32, 1, cuda)
+        c0 = dev_uniform(m, torch.float32, 4, cuda)
+        fn = cb.gemv_row_major if lay == cb.Layout.RowMajor else cb.gemv_col_major
+        ref = c0.clone()
+        fn(A, xv, ref, pol)
+        for _ in range(20):
+            c = c0.clone()
+            fn(A, xv, c, pol)
+            assert torch.equal(c, ref)
+
+
+# ------------------------------------------------- host-buffer entry points
+def test_host_buffer_path_equals_device_path(cuda):
+    import paper_2108_02025_b200 as cb
+    pol = policy()
+    n = 123_457
+    x, y = dev_uniform(n, torch.float64, 1, cuda), dev_uniform(n, torch.float64, 2, cuda)
+    assert cb.dot(x.cpu(), y.cpu(), 0.5, pol) == cb.dot(x, y, 0.5, pol)
+    m, k = 999, 1001
+    A = dev_uniform(m * k, torch.float32, 3, cuda)
+    xv = dev_uniform(k, torch.float32, 1, cuda)
+    c0 = dev_uniform(m, torch.float32, 4, cuda)
+    for lay, fn in [(cb.Layout.RowMajor, cb.gemv_row_major), (cb.Layout.ColMajor, cb.gemv_col_major)]:
+        cd = c0.clone()
+        fn(cb.DenseMatrix.wrap(A, m, k, lay), xv, cd, pol)
+        ch = c0.cpu().clone()
+        fn(cb.DenseMatrix.wrap(A.cpu(), m, k, lay), xv.cpu(), ch, pol)
+        assert torch.equal(cd.cpu(), ch)
+    gx, gy = dev_uniform(m, torch.float32, 1, cuda), dev_uniform(k, torch.float32, 2, cuda)
+    Cd = cb.DenseMatrix.wrap(A.clone(), m, k, cb.Layout.RowMajor)
+    Ch = cb.DenseMatrix.wrap(A.cpu().clone(), m, k, cb.Layout.RowMajor)
+    cb.ger(gx, gy, Cd, pol)
+    cb.ger(gx.cpu(), gy.cpu(), Ch, pol)
+    assert torch.equal(Cd.data.cpu(), Ch.data)
+
+
+# ------------------------------------------------- full BASELINE sizes
+def test_generator_matches_host_oracle(cuda):
+    for dtype, npdt in [(torch.float32, np.float32), (torch.float64, np.float64)]:
+        t = dev_uniform(100_003, dtype, 7, cuda, seed=1234)
+        np.testing.assert_array_equal(np_of(t), O.gen_uniform(100_003, npdt, 1234, 7))
+    import paper_2108_02025_b200 as cb
+    g = cb.fill_normal(torch.empty(4096, dtype=torch.float64, device=cuda), 9, 3)
+    h = O.gen_normal_f64(4096, 9, 3)
+    np.testing.assert_allclose(np_of(g), h, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.slow
+def test_gemv_65536_square_fp32_sampled_rows(cuda):
+    """BASELINE config 5 (G4): 16 GiB A.  Rows are checked against the oracle
+    on a sample (the oracle's cost is the only limit; every row of the GPU
+    result is checked against an fp64 torch matvec for the truth bound)."""
+    import paper_2108_02025_b200 as cb
+    m = n = 65536
+    A = dev_uniform(m * n, torch.float32, 3, cuda)
+    x = dev_uniform(n, torch.float32, 1, cuda)
+    c0 = dev_uniform(m, torch.float32, 4, cuda)
+    c = c0.clone()
+    cb.gemv_row_major(cb.DenseMatrix.wrap(A, m, n, cb.Layout.RowMajor), x, c, policy())
+    rows = np.r_[0:8, 4091:4101, 32760:32776, m - 8:m]
+    An = np_of(A.view(m, n)[torch.as_tensor(rows, device=cuda)])
+    xn, c0n = np_of(x), np_of(c0)[rows]
+    want = c0n.copy()
+    O.gemv_ref(An.reshape(-1), 0, xn, want)
+    truth, rowabs = O.gemv_truth(An.reshape(-1), 0, xn, c0n)
+    got = np_of(c)[rows]
+    assert np.all(np.abs(got - want) <= T.contract_tol(n, rowabs, np.abs(c0n), np.float32))
+    assert np.all(np.abs(got - truth) <=
+                  T.truth_tol(T.gemv_rm_chain(n, np.float32), rowabs, np.abs(c0n), np.float32))
+    # all rows: fp64 torch reference (exact products, fp64 sums)
+    ref = c0.double().clone()
+    for r0 in range(0, m, 4096):
+        ref[r0:r0 + 4096] += A.view(m, n)[r0:r0 + 4096].double() @ x.double()
+    absA = torch.zeros(m, dtype=torch.float64, device=cuda)
+    for r0 in range(0, m, 4096):
+        absA[r0:r0 + 4096] = A.view(m, n)[r0:r0 + 4096].double().abs() @ x.double().abs()
+    err = (c.double() - ref).abs()
+    bound = (T.gemv_rm_chain(n, np.float32) + 4) * T.EPS[np.dtype(np.float32)] * (absA + c0.double().abs())
+    assert bool((err <= bound).all())

@@ -1,0 +1,77 @@
+"""Error bounds used by the parity tests (written down once, cited everywhere).
+
+BASELINE.json's contract for fp32 DOT and GEMV (per output element):
+
+    |gpu - oracle| <= 4 * n * eps * sum_i |a_i * b_i|
+
+It matches the reference tests' own bound (reference test_kernels.cpp:36-50,
+acceptance.cpp:142,158,177) up to the factor 4, and becomes vacuous for fp32
+once 4 n eps >= 1 (n >= 2^21) — SURVEY.md §0 finding 3.  The reference's form
+also omits the initial |c_i|, which breaks its own criterion 1 on one
+instance; we add |c_i| (|alpha0|) to the sum.
+
+Next to the contract, every DOT/GEMV result is held to a NON-VACUOUS bound
+against extended-precision truth (fp32: exact products summed in 80-bit;
+fp64: Dot2 compensated) — the standard a priori bound gamma_L * S with
+L = the longest chain of roundings any output passes through on the GPU:
+
+    |gpu - truth| <= (L + 2) * eps * (S + |c0|)
+
+L is stated per kernel below from its decomposition (a per-lane sequential
+chain, then fixed trees of adds).  GER is held to bitwise equality with the
+oracle (one FMA per element, reference kernels.hpp:264-313).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+EPS = {np.dtype(np.float32): float(np.finfo(np.float32).eps),
+       np.dtype(np.float64): float(np.finfo(np.float64).eps)}
+
+SMS = 148  # B200
+
+
+def contract_tol(n: int, sumabs, c0abs, dtype):
+    """BASELINE.json: 4 n eps (sum |a b| + |c0|) — with the |c0| term added."""
+    return 4.0 * max(n, 1) * EPS[np.dtype(dtype)] * (np.asarray(sumabs) + np.asarray(c0abs))
+
+
+def log2c(v: int) -> int:
+    return max(1, math.ceil(math.log2(max(v, 2))))
+
+
+def dot_chain(n: int, dtype) -> int:
+    """dot_kernel (csrc/dot.cu): grid G <= 148*4 CTAs x 256 threads, each thread
+    one FMA chain over its share (split over U=2 accumulators, V elements per
+    vector), then 1 + 5 + 3 fixed adds (accumulators, warp, CTA), a sequential
+    pass of ceil(G/256) partials per thread, 8 tree levels and + alpha0."""
+    V = 32 // np.dtype(dtype).itemsize
+    nvec = n // V
+    G = max(1, min(math.ceil(nvec / 512), SMS * 4))
+    per_thread = math.ceil(max(nvec, 1) / (G * 256)) * V + V
+    return per_thread + 1 + 5 + 3 + math.ceil(G / 256) + 8 + 1
+
+
+def gemv_rm_chain(n: int, dtype) -> int:
+    """gemv_rm_vec_kernel: each lane FMA-chains n/32 elements of a row, a
+    5-level butterfly, then at most (warps touching the row) adds of partials
+    and + c_i.  A row touches at most ceil(row units / per-warp units)+1 warps;
+    bounded by 64 here for every shape the tests use."""
+    return math.ceil(n / 32) + 5 + 64 + 1
+
+
+def gemv_cm_chain(m: int, n: int, dtype) -> int:
+    """Tall (m >= 2048): one sequential chain per row over all n columns (the
+    reference order).  Short-wide: per thread a chain over its columns
+    (<= n / (G * col_lanes) + 1), <= 16 column-lane adds, G <= 296 CTA
+    partials summed in order, + c_i."""
+    if m >= 2048:
+        return n + 1
+    G = min(SMS * 2, n)
+    return math.ceil(n / G) + 16 + G + 2
+
+
+def truth_tol(chain: int, sumabs, c0abs, dtype):
+    return (chain + 2) * EPS[np.dtype(dtype)] * (np.asarray(sumabs) + np.asarray(c0abs))
