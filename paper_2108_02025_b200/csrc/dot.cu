@@ -16,6 +16,9 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace cabl_dev {
 
 namespace {
@@ -24,8 +27,8 @@ constexpr int kDotBlock = 256;
 constexpr int kDotUnroll = 2;
 constexpr int kDotCtasPerSm = 4;
 
-template <typename T, int BLOCK, int U>
-__global__ void __launch_bounds__(BLOCK)
+template <typename T, int BLOCK, int U, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
     dot_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t n, int vec_ok,
                T alpha0, T* __restrict__ out, T* __restrict__ partials,
                unsigned* __restrict__ ticket) {
@@ -107,14 +110,52 @@ __global__ void combine_kernel(const T* __restrict__ p, uint32_t count, T alpha0
     *out = add_rn(total, alpha0);
 }
 
+struct DotCfg {
+    int block, unroll, minb;
+};
+
+// Launch shape.  CABL_DOT_CFG="block,unroll,ctas_per_sm" picks an entry of
+// the tuning table below (tools/tune.py); the default is the measured best.
+inline DotCfg dot_cfg() {
+    static const DotCfg cfg = [] {
+        DotCfg c{kDotBlock, kDotUnroll, kDotCtasPerSm};
+        if (const char* e = getenv("CABL_DOT_CFG")) sscanf(e, "%d,%d,%d", &c.block, &c.unroll, &c.minb);
+        return c;
+    }();
+    return cfg;
+}
+
 template <typename T> unsigned dot_grid(uint64_t n, bool small) {
     if (small) return 1;
     constexpr int V = Vec<T>::N;
-    const uint64_t tiles = (n / V + uint64_t(kDotBlock) * kDotUnroll - 1) /
-                           (uint64_t(kDotBlock) * kDotUnroll);
-    const uint64_t cap = uint64_t(sm_count()) * kDotCtasPerSm;
+    const DotCfg c = dot_cfg();
+    const uint64_t per = uint64_t(c.block) * c.unroll;
+    const uint64_t tiles = (n / V + per - 1) / per;
+    const uint64_t cap = uint64_t(sm_count()) * c.minb;
     uint64_t g = tiles < cap ? tiles : cap;
     return g < 1 ? 1u : unsigned(g);
+}
+
+template <typename T>
+void dot_dispatch(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok, T alpha0, T* out,
+                  T* partials, unsigned* ticket, cudaStream_t s) {
+    const DotCfg c = dot_cfg();
+#define CABL_DOT_CASE(B_, U_, M_)                                                              \
+    if (c.block == B_ && c.unroll == U_ && c.minb == M_) {                                     \
+        dot_kernel<T, B_, U_, M_><<<grid, B_, 0, s>>>(x, y, n, vec_ok, alpha0, out, partials,  \
+                                                      ticket);                                 \
+        return;                                                                                \
+    }
+    CABL_DOT_CASE(256, 1, 8)
+    CABL_DOT_CASE(256, 2, 8)
+    CABL_DOT_CASE(256, 4, 4)
+    CABL_DOT_CASE(512, 2, 2)
+    CABL_DOT_CASE(512, 4, 2)
+    CABL_DOT_CASE(1024, 2, 1)
+    CABL_DOT_CASE(1024, 4, 1)
+#undef CABL_DOT_CASE
+    dot_kernel<T, kDotBlock, kDotUnroll, kDotCtasPerSm><<<grid, kDotBlock, 0, s>>>(
+        x, y, n, vec_ok, alpha0, out, partials, ticket);
 }
 
 } // namespace
@@ -131,8 +172,8 @@ cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, boo
                        const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
     const unsigned grid = dot_grid<T>(n, small);
     const int vec_ok = aligned32(x) && aligned32(y);
-    dot_kernel<T, kDotBlock, kDotUnroll><<<grid, kDotBlock, 0, s>>>(
-        x, y, n, vec_ok, alpha0, out, static_cast<T*>(ws.scratch), ws.counters);
+    dot_dispatch<T>(grid, x, y, n, vec_ok, alpha0, out, static_cast<T*>(ws.scratch), ws.counters,
+                    s);
     if (info) info->ctas = grid;
     return cudaGetLastError();
 }

@@ -29,6 +29,9 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace cabl_dev {
 
 namespace {
@@ -144,6 +147,88 @@ __global__ void __launch_bounds__(kRmBlock, kRmCtasPerSm)
     }
 }
 
+// SWEEP kernel (m large relative to the grid).  CTAs stride over groups of
+// R rows (grid-stride: at any moment the whole GPU reads one contiguous
+// window of A, the access order that measured fastest for a streaming read
+// on B200, tools/bwlab.py); all BLOCK threads of a CTA read the group's rows
+// together — thread t owns the vector columns t, t + BLOCK, ... — so every
+// CTA-wide load is a contiguous BLOCK*32-byte run.  XREG: the row fits in one
+// pass (nvec_row <= BLOCK*KV) and the thread's x vectors stay in registers for
+// the whole kernel; otherwise x is re-read per chunk through L1/L2, shared by
+// the R rows.  Per row: fixed butterfly per warp, then warp partials summed
+// in warp order by one thread (double-buffered shared slots: one barrier per
+// group), c[i] = c[i] + sum.
+template <typename T, int R, int KV, bool XREG, int MINB>
+__global__ void __launch_bounds__(kRmBlock, MINB)
+    gemv_rm_sweep_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
+                         uint64_t m, uint64_t n) {
+    constexpr int NW = kRmBlock / kWarp;
+    __shared__ T red[2][R][NW];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint64_t nvec_row = n / Vec<T>::N;
+    const uint64_t groups = (m + R - 1) / R;
+    const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
+
+    Vec<T> xr[XREG ? KV : 1];
+    if (XREG) {
+#pragma unroll
+        for (int k = 0; k < KV; ++k) {
+            const uint64_t j = uint64_t(tid) + uint64_t(k) * kRmBlock;
+            if (j < nvec_row) xr[k] = ld_reuse(X + j);
+            else
+#pragma unroll
+                for (int e = 0; e < Vec<T>::N; ++e) xr[k].v[e] = T(0);
+        }
+    }
+
+    int parity = 0;
+    for (uint64_t g = blockIdx.x; g < groups; g += gridDim.x, parity ^= 1) {
+        const uint64_t row0 = g * R;
+        const int rows = (m - row0 < uint64_t(R)) ? int(m - row0) : R;
+        T acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = T(0);
+        for (uint64_t base = 0; base < nvec_row; base += uint64_t(kRmBlock) * KV) {
+            Vec<T> av[R][KV];
+            Vec<T> xv[KV];
+#pragma unroll
+            for (int k = 0; k < KV; ++k) {
+                const uint64_t j = base + uint64_t(tid) + uint64_t(k) * kRmBlock;
+                const bool ok = j < nvec_row;
+                if (XREG) xv[k] = xr[k];
+                else if (ok) xv[k] = ld_reuse(X + j);
+                else
+#pragma unroll
+                    for (int e = 0; e < Vec<T>::N; ++e) xv[k].v[e] = T(0);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (ok && r < rows)
+                        av[r][k] = ld_stream(reinterpret_cast<const Vec<T>*>(A + (row0 + r) * n) + j);
+                    else
+#pragma unroll
+                        for (int e = 0; e < Vec<T>::N; ++e) av[r][k].v[e] = T(0);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < KV; ++k)
+#pragma unroll
+                for (int r = 0; r < R; ++r) acc[r] = dot_vec(av[r][k], xv[k], acc[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const T v = warp_sum(acc[r]);
+            if (lane == 0) red[parity][r][wid] = v;
+        }
+        __syncthreads();
+        if (tid < rows) {
+            T sum = red[parity][tid][0];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) sum = add_rn(sum, red[parity][tid][w]);
+            c[row0 + tid] = add_rn(c[row0 + tid], sum);
+        }
+    }
+}
+
 // Generic path: one warp per row (balanced row ranges), scalar coalesced loads.
 template <typename T>
 __global__ void __launch_bounds__(kRmBlock)
@@ -166,6 +251,34 @@ template <typename T> bool rm_vec_ok(const T* A, const T* x, uint64_t n) {
     return aligned32(A) && aligned32(x) && (n % Vec<T>::N == 0);
 }
 
+// -1 scalar, 0 segment-balanced warps, 1 sweep for short rows, 2 sweep for
+// long rows.  The sweep needs enough row groups to balance a
+// single wave (>= 8 per CTA, i.e. <= 1/8 CTA of imbalance).
+// CABL_GEMV_RM_MODE overrides (tuning / tests only).
+template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n) {
+    if (!rm_vec_ok(A, x, n)) return -1;
+    static const int forced = [] {
+        const char* e = getenv("CABL_GEMV_RM_MODE");
+        return e ? atoi(e) : -2;
+    }();
+    const uint64_t nvec_row = n / Vec<T>::N;
+    const bool fits = nvec_row <= uint64_t(kRmBlock) * 4;
+    if (forced >= 0 && forced <= 2) {
+        if (forced == 1 && !fits) return 2;
+        return forced;
+    }
+    // measured (tools/tune.py, 8192^2 and 65536^2 fp32): 4 rows x 2 vectors
+    // per thread at 2 CTAs/SM for rows of <= 2 CTA passes, 2 rows x 8 vectors
+    // at 1 CTA/SM for long rows.  The sweep must see >= 6 row groups per CTA
+    // to keep the single wave balanced; otherwise the segment kernel.
+    const uint64_t sms = uint64_t(sm_count());
+    const bool short_rows = nvec_row <= uint64_t(kRmBlock) * 2 * 2;
+    if (short_rows && (m + 3) / 4 >= 6 * 2 * sms) return 1;
+    if (!short_rows && (m + 1) / 2 >= 6 * 1 * sms) return 2;
+    (void)fits;
+    return 0;
+}
+
 template <typename T> RmGeom rm_geom(uint64_t m, uint64_t n) {
     RmGeom g;
     g.nvec_row = n / Vec<T>::N;
@@ -179,11 +292,51 @@ template <typename T> RmGeom rm_geom(uint64_t m, uint64_t n) {
     return g;
 }
 
+
+struct SweepCfg {
+    int R, KV, minb;
+};
+
+// Tuning table (CABL_RM_SWEEP="R,KV,MINB" selects an entry; tools/tune.py).
+template <typename T, int R, int KV, bool XREG, int MINB>
+unsigned sweep_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, cudaStream_t s) {
+    const uint64_t groups = (m + R - 1) / R;
+    const uint64_t ctas = uint64_t(sm_count()) * MINB;
+    const unsigned grid = unsigned(groups < ctas ? groups : ctas);
+    gemv_rm_sweep_kernel<T, R, KV, XREG, MINB><<<grid, kRmBlock, 0, s>>>(A, x, c, m, n);
+    return grid;
+}
+
+template <typename T>
+unsigned sweep_launch(const T* A, const T* x, T* c, uint64_t m, uint64_t n, int mode,
+                      cudaStream_t s) {
+    static const SweepCfg forced = [] {
+        SweepCfg f{0, 0, 0};
+        if (const char* e = getenv("CABL_RM_SWEEP")) sscanf(e, "%d,%d,%d", &f.R, &f.KV, &f.minb);
+        return f;
+    }();
+#define CABL_SWEEP_CASE(R_, KV_, MB_)                                                          \
+    if (forced.R == R_ && forced.KV == KV_ && forced.minb == MB_)                             \
+        return sweep_go<T, R_, KV_, false, MB_>(A, x, c, m, n, s);
+    CABL_SWEEP_CASE(1, 8, 2)
+    CABL_SWEEP_CASE(2, 2, 4)
+    CABL_SWEEP_CASE(2, 4, 2)
+    CABL_SWEEP_CASE(2, 8, 1)
+    CABL_SWEEP_CASE(4, 1, 4)
+    CABL_SWEEP_CASE(4, 2, 2)
+    CABL_SWEEP_CASE(4, 4, 1)
+    CABL_SWEEP_CASE(8, 1, 2)
+    CABL_SWEEP_CASE(8, 2, 1)
+#undef CABL_SWEEP_CASE
+    if (mode == 1) return sweep_go<T, 4, 2, false, 2>(A, x, c, m, n, s); // rows <= 2 passes
+    return sweep_go<T, 2, 8, false, 1>(A, x, c, m, n, s);                  // long rows
+}
+
 } // namespace
 
 template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n) {
     WorkspaceNeed w;
-    if (m == 0 || n == 0 || !rm_vec_ok(A, x, n)) return w;
+    if (m == 0 || n == 0 || rm_mode<T>(A, x, m, n) != 0) return w;
     const RmGeom g = rm_geom<T>(m, n);
     w.counters = g.warps;
     w.scratch_bytes = g.warps * 2 * kRmRows * sizeof(T);
@@ -195,7 +348,11 @@ cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
                            const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
     if (info) info->ctas = 0;
     if (m == 0 || n == 0) return cudaSuccess; // c += 0
-    if (rm_vec_ok(A, x, n)) {
+    const int mode = rm_mode<T>(A, x, m, n);
+    if (mode >= 1) {
+        const unsigned grid = sweep_launch<T>(A, x, c, m, n, mode, s);
+        if (info) info->ctas = grid;
+    } else if (mode == 0) {
         const RmGeom g = rm_geom<T>(m, n);
         const unsigned grid = unsigned((g.warps * kWarp + kRmBlock - 1) / kRmBlock);
         gemv_rm_vec_kernel<T, kRmRows, kRmSeg><<<grid, kRmBlock, 0, s>>>(
