@@ -2,28 +2,30 @@
 // reference cabl::gemv_col_major (proj/include/cabl/kernels.hpp:187-224,
 // Algorithm 1 of the paper: row blocks x column blocks x m_r register panels).
 //
-// Two shapes, two kernels:
+// Two shapes, three kernels:
 //
-// (1) ROWS (tall: m >= kSplitMaxRows, e.g. 2^20 x 256).  The CPU panel keeps
-//     m_r rows of c in registers across a column block; here a LANE keeps one
-//     row of c in a register across ALL columns and a warp owns 32 adjacent
-//     rows, so every column read is a contiguous 32*s-byte run and the 148
-//     SMs stream A with 16 independent loads in flight per lane.  Warps own
-//     balanced contiguous ranges of 32-row units.  Each row's sum runs j
-//     ascending from c_i — the reference order — with the reference's
-//     compiled rounding (multiply-then-add over the 16-byte-vector prefix,
-//     FMA on the remainder; see oracle/cabl_oracle.c), so this path is bit
-//     for bit equal to the compiled reference gemv_ref.
+// (1) TALL (m >= kSplitMaxRows, e.g. 2^20 x 256).  The CPU panel keeps m_r
+//     rows of c in registers across a column block.  Here a THREAD keeps one
+//     32-byte vector of rows (4 doubles / 8 floats) of c in registers across
+//     ALL columns, and a CTA owns BLOCK consecutive row vectors, so every
+//     column read of a CTA is one contiguous BLOCK*32-byte run; CTAs (one per
+//     SM) own balanced ranges of such row units and keep U = 16 column loads
+//     in flight per thread.  Each row's sum runs j ascending from c_i — the
+//     reference order — with the reference's compiled rounding (multiply then
+//     add over the 16-byte-vector prefix, FMA on the remainder; see
+//     oracle/cabl_oracle.c): bit for bit the compiled reference gemv_ref.
+//     If m is not a multiple of the vector (columns misaligned), the same
+//     order runs with one row per lane (gemv_cm_rows_kernel).
 //
 // (2) SPLIT (short-wide: m < kSplitMaxRows, e.g. 256 x 2^20).  The reference
-//     runs this shape on ONE thread (one m_c row block).
-//     Here the columns are split over a single wave of CTAs (balanced ±1
-//     column); inside a CTA, threads are (row lane, column lane) pairs,
-//     accumulate with FMA over their columns, and column lanes combine in
+//     runs this shape on ONE thread (a single m_c row block).
+//     Here one CTA per SM sweeps column tiles in grid-stride order (the whole
+//     GPU reads one contiguous window at a time); threads are (row lane,
+//     column lane) pairs accumulating with FMA; column lanes combine in
 //     shared memory in a fixed order -> partials[cta][m].  The last CTA to
-//     arrive sums the partials in CTA order per row and adds them to c.
-//     Bitwise reproducible run to run; within the BASELINE tolerance of
-//     gemv_ref.
+//     arrive sums the partials per row in CTA order with batched L2 loads and
+//     adds them to c.  Bitwise reproducible run to run; within the BASELINE
+//     tolerance of gemv_ref.
 //
 // Algorithmic bytes per launch: m*n*s + n*s + 2*m*s.
 #include "common.cuh"
@@ -33,13 +35,66 @@ namespace cabl_dev {
 
 namespace {
 
+constexpr int kTallBlock = 256;
+constexpr int kTallUnroll = 16;
 constexpr int kCmBlock = 256;
 constexpr int kCmUnroll = 16;
 constexpr int kCmRowsCtasPerSm = 4;
 constexpr uint64_t kSplitMaxRows = 2048;
-constexpr int kSplitBlock = 512;
-constexpr int kSplitCtasPerSm = 2;
+constexpr int kSplitBlock = 1024;
+// column loads in flight per thread: 32 registers of A operands either way
+template <typename T> __host__ __device__ constexpr int split_u() { return sizeof(T) == 4 ? 16 : 8; }
 
+// acc + a*x with the compiled reference's rounding for term j:
+// separately rounded multiply then add for j < cut, FMA after.
+template <typename T> __device__ __forceinline__ T ref_step(T acc, T a, T xj, bool fused) {
+    return fused ? fma_rn(a, xj, acc) : add_rn(acc, mul_rn(a, xj));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTallBlock, 1)
+    gemv_cm_tall_vec_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
+                            uint64_t m, uint64_t n) {
+    constexpr int V = Vec<T>::N;
+    constexpr uint64_t kRefVec = 16 / sizeof(T);
+    const uint64_t mv = m / V; // row vectors == vectors per column
+    // CTAs own balanced ranges of BLOCK-row-vector units; every thread runs
+    // the same number of rounds (measured faster than balancing single row
+    // vectors, whose ragged last round idles most of each CTA).
+    const uint64_t units = (mv + kTallBlock - 1) / kTallBlock;
+    const Partition part(units, gridDim.x);
+    const uint64_t cut = (n / kRefVec) * kRefVec;
+    const Vec<T>* Av = reinterpret_cast<const Vec<T>*>(A);
+    Vec<T>* Cv = reinterpret_cast<Vec<T>*>(c);
+
+    for (uint64_t u = part.begin(blockIdx.x); u < part.begin(blockIdx.x + 1); ++u) {
+        const uint64_t rv = u * kTallBlock + threadIdx.x;
+        if (rv >= mv) continue; // no barrier below: early exit is safe
+        Vec<T> acc = Cv[rv];
+        const Vec<T>* col = Av + rv;
+        uint64_t j = 0;
+        for (; j + kTallUnroll <= cut; j += kTallUnroll) {
+            Vec<T> a[kTallUnroll];
+#pragma unroll
+            for (int k = 0; k < kTallUnroll; ++k) a[k] = ld_stream(col + (j + k) * mv);
+#pragma unroll
+            for (int k = 0; k < kTallUnroll; ++k) {
+                const T xj = __ldg(x + j + k);
+#pragma unroll
+                for (int e = 0; e < V; ++e) acc.v[e] = ref_step(acc.v[e], a[k].v[e], xj, false);
+            }
+        }
+        for (; j < n; ++j) {
+            const Vec<T> a = ld_stream(col + j * mv);
+            const T xj = __ldg(x + j);
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc.v[e] = ref_step(acc.v[e], a.v[e], xj, j >= cut);
+        }
+        Cv[rv] = acc;
+    }
+}
+
+// Tall, any m: one row per lane, warps own balanced ranges of 32-row units.
 template <typename T>
 __global__ void __launch_bounds__(kCmBlock, kCmRowsCtasPerSm)
     gemv_cm_rows_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
@@ -50,7 +105,7 @@ __global__ void __launch_bounds__(kCmBlock, kCmRowsCtasPerSm)
     if (gw >= warps) return;
     const uint64_t units = (m + kWarp - 1) / kWarp;
     const Partition part(units, warps);
-    const uint64_t cut = (n / kRefVec) * kRefVec; // mul-then-add prefix length
+    const uint64_t cut = (n / kRefVec) * kRefVec;
 
     for (uint64_t unit = part.begin(gw); unit < part.begin(gw + 1); ++unit) {
         const uint64_t i = unit * kWarp + lane;
@@ -61,28 +116,124 @@ __global__ void __launch_bounds__(kCmBlock, kCmRowsCtasPerSm)
         for (; j + kCmUnroll <= cut; j += kCmUnroll) {
             T av[kCmUnroll];
 #pragma unroll
-            for (int k = 0; k < kCmUnroll; ++k)
-                av[k] = live ? __ldcs(a + (j + k) * m) : T(0);
+            for (int k = 0; k < kCmUnroll; ++k) av[k] = live ? __ldcs(a + (j + k) * m) : T(0);
 #pragma unroll
-            for (int k = 0; k < kCmUnroll; ++k) acc = add_rn(acc, mul_rn(av[k], __ldg(x + j + k)));
-        }
-        for (; j < cut; ++j) {
-            const T av = live ? __ldcs(a + j * m) : T(0);
-            acc = add_rn(acc, mul_rn(av, __ldg(x + j)));
+            for (int k = 0; k < kCmUnroll; ++k) acc = ref_step(acc, av[k], __ldg(x + j + k), false);
         }
         for (; j < n; ++j) {
             const T av = live ? __ldcs(a + j * m) : T(0);
-            acc = fma_rn(av, __ldg(x + j), acc);
+            acc = ref_step(acc, av, __ldg(x + j), j >= cut);
         }
         if (live) c[i] = acc;
     }
 }
 
+// Last CTA of a split launch: c[r] += sum over CTAs b (in order) of
+// partials[b][r].  Thread (r, q) sums CTAs q, q+Q, ... with 16 loads in
+// flight, then the Q sums per row are added in q order; `sm` holds >= Q*m.
+template <typename T>
+__device__ void split_final(const T* __restrict__ partials, T* __restrict__ c, uint64_t m, T* sm) {
+    const unsigned G = gridDim.x;
+    const int block = blockDim.x;
+    int rl = 32;
+    while (uint64_t(rl) < m && rl < block) rl *= 2;
+    const int Q = block / rl;
+    const int r0 = threadIdx.x % rl, q = threadIdx.x / rl;
+    for (uint64_t rb = 0; rb < m; rb += uint64_t(rl)) {
+        const uint64_t r = rb + r0;
+        T total = T(0);
+        if (r < m) {
+            for (unsigned b0 = q; b0 < G; b0 += 16u * Q) {
+                T v[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const unsigned b = b0 + unsigned(e) * Q;
+                    v[e] = b < G ? ld_cg(partials + uint64_t(b) * m + r) : T(0);
+                }
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    if (b0 + unsigned(e) * Q < G) total = add_rn(total, v[e]);
+            }
+        }
+        __syncthreads(); // sm reuse
+        if (r < m) sm[uint64_t(q) * rl + r0] = total;
+        __syncthreads();
+        if (q == 0 && r < m) {
+            T v = sm[r0];
+            for (int k = 1; k < Q; ++k) v = add_rn(v, sm[uint64_t(k) * rl + r0]);
+            c[r] = add_rn(c[r], v);
+        }
+    }
+}
+
+// Vectorised split kernel (m % V == 0, aligned): a thread owns one 32-byte
+// row vector (V rows) for its column lane; row_lanes = pow2 >= m/V, U = 4
+// 256-bit column loads in flight per thread.
+template <typename T>
+__global__ void __launch_bounds__(kSplitBlock, 1)
+    gemv_cm_split_vec_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
+                             uint64_t m, uint64_t n, int row_lanes, T* __restrict__ partials,
+                             unsigned* __restrict__ ticket) {
+    constexpr int V = Vec<T>::N;
+    constexpr int U = 4;
+    __shared__ alignas(32) T sm[kSplitBlock * V]; // [col_lanes][m] <= 1024 * V entries
+    __shared__ bool am_last;
+    const int tid = threadIdx.x;
+    const int col_lanes = kSplitBlock / row_lanes;
+    const int rl = tid % row_lanes, cl = tid / row_lanes;
+    const uint64_t mv = m / V;
+    const bool live = uint64_t(rl) < mv;
+    const Vec<T>* Av = reinterpret_cast<const Vec<T>*>(A) + (live ? rl : 0);
+    const uint64_t tile = uint64_t(col_lanes) * U;
+    const uint64_t tiles = (n + tile - 1) / tile;
+
+    Vec<T> acc;
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc.v[e] = T(0);
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const uint64_t j0 = t * tile + cl;
+        Vec<T> av[U];
+        T xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t j = j0 + uint64_t(u) * col_lanes;
+            const bool ok = live && j < n;
+            xv[u] = j < n ? __ldg(x + j) : T(0);
+            if (ok) av[u] = ld_stream(Av + j * mv);
+            else
+#pragma unroll
+                for (int e = 0; e < V; ++e) av[u].v[e] = T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc.v[e] = fma_rn(av[u].v[e], xv[u], acc.v[e]);
+    }
+    if (live)
+#pragma unroll
+        for (int e = 0; e < V; ++e) sm[uint64_t(cl) * m + uint64_t(rl) * V + e] = acc.v[e];
+    __syncthreads();
+    for (uint64_t r = tid; r < m; r += kSplitBlock) {
+        T v = sm[r];
+        for (int q = 1; q < col_lanes; ++q) v = add_rn(v, sm[uint64_t(q) * m + r]);
+        partials[uint64_t(blockIdx.x) * m + r] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    split_final(partials, c, m, sm);
+    if (tid == 0) *ticket = 0u;
+}
+
 // Split-columns kernel.  Thread layout: row_lanes x col_lanes = kSplitBlock,
-// row_lanes = 32 * ceil(min(m, kSplitBlock) / 32); each thread accumulates
-// RPT rows (r = row_lane + k*row_lanes).
+// row_lanes a power of two >= min(m, kSplitBlock); each thread accumulates
+// RPT rows (r = row_lane + k*row_lanes).  Column tiles of col_lanes*kSplitU
+// columns are visited in grid-stride order.
 template <typename T, int RPT>
-__global__ void __launch_bounds__(kSplitBlock, kSplitCtasPerSm)
+__global__ void __launch_bounds__(kSplitBlock, 1)
     gemv_cm_split_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                          uint64_t m, uint64_t n, int row_lanes, T* __restrict__ partials,
                          unsigned* __restrict__ ticket) {
@@ -92,43 +243,34 @@ __global__ void __launch_bounds__(kSplitBlock, kSplitCtasPerSm)
     const int tid = threadIdx.x;
     const int col_lanes = kSplitBlock / row_lanes;
     const int rl = tid % row_lanes, cl = tid / row_lanes;
-    const Partition part(n, gridDim.x);
-    const uint64_t j0 = part.begin(blockIdx.x), j1 = part.begin(blockIdx.x + 1);
+    constexpr int kSplitU = split_u<T>();
+    const uint64_t tile = uint64_t(col_lanes) * kSplitU;
+    const uint64_t tiles = (n + tile - 1) / tile;
 
     T acc[RPT];
 #pragma unroll
     for (int k = 0; k < RPT; ++k) acc[k] = T(0);
 
-    // columns j0 + cl, j0 + cl + col_lanes, ...: U at a time
-    constexpr int U = (RPT == 1) ? 16 : (RPT == 2 ? 8 : 4);
-    uint64_t j = j0 + cl;
-    const uint64_t step = uint64_t(col_lanes);
-    for (; j + (U - 1) * step < j1; j += U * step) {
-        T av[U][RPT];
-        T xv[U];
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const uint64_t j0 = t * tile + cl;
+        T av[kSplitU][RPT];
+        T xv[kSplitU];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const T* col = A + (j + u * step) * m;
-            xv[u] = __ldg(x + j + u * step);
+        for (int u = 0; u < kSplitU; ++u) {
+            const uint64_t j = j0 + uint64_t(u) * col_lanes;
+            const bool ok = j < n;
+            xv[u] = ok ? __ldg(x + j) : T(0);
+            const T* col = A + (ok ? j : 0) * m;
 #pragma unroll
             for (int k = 0; k < RPT; ++k) {
                 const uint64_t r = uint64_t(rl) + uint64_t(k) * row_lanes;
-                av[u][k] = r < m ? __ldcs(col + r) : T(0);
+                av[u][k] = (ok && r < m) ? __ldcs(col + r) : T(0);
             }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int u = 0; u < kSplitU; ++u)
 #pragma unroll
             for (int k = 0; k < RPT; ++k) acc[k] = fma_rn(av[u][k], xv[u], acc[k]);
-    }
-    for (; j < j1; j += step) {
-        const T* col = A + j * m;
-        const T xj = __ldg(x + j);
-#pragma unroll
-        for (int k = 0; k < RPT; ++k) {
-            const uint64_t r = uint64_t(rl) + uint64_t(k) * row_lanes;
-            if (r < m) acc[k] = fma_rn(__ldcs(col + r), xj, acc[k]);
-        }
     }
 
     // column lanes -> CTA partial, fixed order
@@ -149,11 +291,8 @@ __global__ void __launch_bounds__(kSplitBlock, kSplitCtasPerSm)
     __syncthreads();
     if (!am_last) return;
     __threadfence();
-    for (uint64_t r = tid; r < m; r += kSplitBlock) {
-        T total = T(0);
-        for (unsigned b = 0; b < gridDim.x; ++b) total = add_rn(total, ld_cg(partials + uint64_t(b) * m + r));
-        c[r] = add_rn(c[r], total);
-    }
+
+    split_final(partials, c, m, sm);
     if (tid == 0) *ticket = 0u;
 }
 
@@ -170,19 +309,47 @@ template <typename T> SplitGeom split_geom(uint64_t m, uint64_t n) {
     g.row_lanes = int(rl);
     g.col_lanes = kSplitBlock / g.row_lanes;
     g.rpt = int((m + rl - 1) / rl);
-    const uint64_t cap = uint64_t(sm_count()) * kSplitCtasPerSm;
-    const uint64_t want = (n + g.col_lanes - 1) / g.col_lanes; // >= 1 column per column lane
-    g.grid = unsigned(want < cap ? (want < 1 ? 1 : want) : cap);
-    g.smem = size_t(g.col_lanes) * m * sizeof(T); // <= 512*s (m<=512) or m*s (m<2048): < 48 KB
+    const uint64_t cap = uint64_t(sm_count());
+    const uint64_t tile = uint64_t(g.col_lanes) * split_u<T>();
+    const uint64_t tiles = (n + tile - 1) / tile;
+    g.grid = unsigned(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
+    // [col_lanes][m] for the column-lane combine, >= one entry per thread for
+    // split_final: <= max(kSplitBlock, m) entries, 16 KB for fp64
+    const size_t entries = size_t(g.col_lanes) * m;
+    g.smem = (entries > size_t(kSplitBlock) ? entries : size_t(kSplitBlock)) * sizeof(T);
     return g;
+}
+
+template <typename T> bool split_vec_ok(const T* A, uint64_t m) {
+    return aligned32(A) && m % Vec<T>::N == 0;
+}
+
+template <typename T> SplitGeom split_vec_geom(uint64_t m, uint64_t n) {
+    SplitGeom g;
+    const uint64_t mv = m / Vec<T>::N;
+    uint64_t rl = 1;
+    while (rl < mv) rl *= 2;
+    g.row_lanes = int(rl);
+    g.col_lanes = kSplitBlock / g.row_lanes;
+    g.rpt = 1;
+    const uint64_t tile = uint64_t(g.col_lanes) * 4;
+    const uint64_t tiles = (n + tile - 1) / tile;
+    const uint64_t cap = uint64_t(sm_count());
+    g.grid = unsigned(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
+    g.smem = 0;
+    return g;
+}
+
+template <typename T> bool tall_vec_ok(const T* A, const T* c, uint64_t m) {
+    return aligned32(A) && aligned32(c) && m % Vec<T>::N == 0;
 }
 
 } // namespace
 
-template <typename T> WorkspaceNeed gemv_cm_need(const T*, const T*, uint64_t m, uint64_t n) {
+template <typename T> WorkspaceNeed gemv_cm_need(const T* A, const T*, uint64_t m, uint64_t n) {
     WorkspaceNeed w;
     if (m == 0 || n == 0 || m >= kSplitMaxRows) return w;
-    const SplitGeom g = split_geom<T>(m, n);
+    const SplitGeom g = split_vec_ok(A, m) ? split_vec_geom<T>(m, n) : split_geom<T>(m, n);
     w.counters = 1;
     w.scratch_bytes = size_t(g.grid) * m * sizeof(T);
     return w;
@@ -193,7 +360,13 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
                            const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
     if (info) info->ctas = 0;
     if (m == 0 || n == 0) return cudaSuccess;
-    if (m >= kSplitMaxRows) {
+    if (m >= kSplitMaxRows && tall_vec_ok(A, c, m)) {
+        const uint64_t mv = m / Vec<T>::N;
+        const uint64_t sms = uint64_t(sm_count());
+        const unsigned grid = unsigned(mv < sms ? mv : sms);
+        gemv_cm_tall_vec_kernel<T><<<grid, kTallBlock, 0, s>>>(A, x, c, m, n);
+        if (info) info->ctas = grid;
+    } else if (m >= kSplitMaxRows) {
         const uint64_t units = (m + kWarp - 1) / kWarp;
         const uint64_t max_warps = uint64_t(sm_count()) * kCmRowsCtasPerSm * (kCmBlock / kWarp);
         // smallest per-warp unit count that fits one wave, then as few warps
@@ -203,23 +376,20 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         const unsigned grid = unsigned((warps * kWarp + kCmBlock - 1) / kCmBlock);
         gemv_cm_rows_kernel<T><<<grid, kCmBlock, 0, s>>>(A, x, c, m, n, warps);
         if (info) info->ctas = grid;
+    } else if (split_vec_ok(A, m)) {
+        const SplitGeom g = split_vec_geom<T>(m, n);
+        gemv_cm_split_vec_kernel<T><<<g.grid, kSplitBlock, 0, s>>>(
+            A, x, c, m, n, g.row_lanes, static_cast<T*>(ws.scratch), ws.counters);
+        if (info) info->ctas = g.grid;
     } else {
         const SplitGeom g = split_geom<T>(m, n);
         T* partials = static_cast<T*>(ws.scratch);
-        switch (g.rpt) {
-        case 1:
+        if (g.rpt == 1)
             gemv_cm_split_kernel<T, 1><<<g.grid, kSplitBlock, g.smem, s>>>(
                 A, x, c, m, n, g.row_lanes, partials, ws.counters);
-            break;
-        case 2:
+        else
             gemv_cm_split_kernel<T, 2><<<g.grid, kSplitBlock, g.smem, s>>>(
                 A, x, c, m, n, g.row_lanes, partials, ws.counters);
-            break;
-        default:
-            gemv_cm_split_kernel<T, 4><<<g.grid, kSplitBlock, g.smem, s>>>(
-                A, x, c, m, n, g.row_lanes, partials, ws.counters);
-            break;
-        }
         if (info) info->ctas = g.grid;
     }
     return cudaGetLastError();

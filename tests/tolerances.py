@@ -64,13 +64,13 @@ def gemv_rm_chain(n: int, dtype) -> int:
 
 def gemv_cm_chain(m: int, n: int, dtype) -> int:
     """Tall (m >= 2048): one sequential chain per row over all n columns (the
-    reference order).  Short-wide: per thread a chain over its columns
-    (<= n / (G * col_lanes) + 1), <= 16 column-lane adds, G <= 296 CTA
-    partials summed in order, + c_i."""
+    reference order).  Short-wide (csrc/gemv_cm.cu split kernel): G <= 148
+    CTAs, each thread a chain over <= ceil(n / G) columns, <= 32 column-lane
+    adds, then the G CTA partials summed in order, + c_i."""
     if m >= 2048:
         return n + 1
-    G = min(SMS * 2, n)
-    return math.ceil(n / G) + 16 + G + 2
+    G = max(1, min(SMS, n))
+    return math.ceil(n / G) + 32 + G + 2
 
 
 def truth_tol(chain: int, sumabs, c0abs, dtype):
