@@ -1,0 +1,125 @@
+"""The C-ABI library without a GPU: it loads, exports exactly what
+include/cabl_cuda.h declares, and fails loudly (CABL_ECUDA + message) instead
+of computing anything on the CPU.  Plus the Python mirror's host-side
+validation, which must match the reference's messages (kernels.hpp)."""
+from __future__ import annotations
+
+import ctypes as C
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "cabl_cuda.h"
+
+
+def declared_symbols() -> set[str]:
+    text = HEADER.read_text()
+    return set(re.findall(r"CABL_API\s+[\w\s\*]+?\b(cabl_\w+)\s*\(", text))
+
+
+def test_library_builds_for_sm100a():
+    from paper_2108_02025_b200 import _lib
+    _lib.build()
+    assert _lib.LIB_PATH.exists()
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_every_declared_symbol_is_exported():
+    from paper_2108_02025_b200 import _lib
+    declared = declared_symbols()
+    assert len(declared) >= 24
+    nm = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True,
+                        text=True, check=True).stdout
+    exported = {ln.split()[-1] for ln in nm.splitlines() if " T " in ln}
+    assert declared <= exported, declared - exported
+    # and nothing else leaks (hidden visibility for internals)
+    assert {s for s in exported if s.startswith("cabl_")} == declared
+    assert declared == set(_lib.SIGNATURES)
+    L = _lib.lib()
+    for name in declared:
+        assert getattr(L, name) is not None
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_gpu_means_loud_failure_not_fallback():
+    import paper_2108_02025_b200 as cb
+    from paper_2108_02025_b200 import _lib
+    L = _lib.lib()
+    assert L.cabl_device_count() == 0
+    x = np.ones(4, np.float32)
+    out = np.zeros(1, np.float32)
+    rc = L.cabl_cuda_dot_f32(x.ctypes.data, x.ctypes.data, 4, C.c_float(0.0), out.ctypes.data,
+                             8192, None, None)
+    assert rc == _lib.CABL_ECUDA
+    assert "no CUDA device" in L.cabl_last_error().decode()
+    assert out[0] == 0.0  # nothing was computed
+    with pytest.raises(_lib.CablError, match="no CPU fallback"):
+        cb.dot(torch.ones(3, dtype=torch.float64), torch.ones(3, dtype=torch.float64), 0.0,
+               cb.default_policy(1))
+    A = cb.DenseMatrix(4, 4, cb.Layout.RowMajor, 1.0)
+    with pytest.raises(_lib.CablError):
+        cb.gemv_row_major(A, torch.ones(4, dtype=torch.float64),
+                          torch.zeros(4, dtype=torch.float64), cb.default_policy(1))
+
+
+def test_abi_version():
+    from paper_2108_02025_b200 import _lib
+    assert _lib.lib().cabl_abi_version() >= 100
+
+
+# ---------------------------------------------------- host-side validation
+def test_plan_derivation_matches_reference_defaults():
+    import paper_2108_02025_b200 as cb
+    plan = cb.derive_blocking_plan(cb.default_machine())
+    # reference README: m_c = n_c = 256, m_r = 8, dot_block = 2048, dot_cutoff = 8192
+    assert (plan.m_c, plan.n_c, plan.m_r, plan.dot_block, plan.dot_cutoff) == (256, 256, 8, 2048, 8192)
+    md = cb.default_machine()
+    md.element_bytes = 4
+    p32 = cb.derive_blocking_plan(md)
+    assert (p32.dot_block, p32.dot_cutoff) == (4096, 16384)
+    with pytest.raises(ValueError, match=r"ExecPolicy: threads must be in \[1, plan.max_threads\]"):
+        cb.ExecPolicy(plan, 0)
+    with pytest.raises(ValueError):
+        cb.ExecPolicy(plan, plan.max_threads + 1)
+    bad = cb.MachineDescriptor(levels=[cb.CacheLevel(64, 8, 64, True), cb.CacheLevel(64, 8, 1024)])
+    with pytest.raises(cb.DescriptorError, match="level 1 must be private"):
+        cb.validate_machine(bad)
+
+
+def test_reference_precondition_messages():
+    import paper_2108_02025_b200 as cb
+    pol = cb.default_policy(1)
+    f = lambda *v: torch.tensor(v, dtype=torch.float64)  # noqa: E731
+    with pytest.raises(ValueError, match="dot: x and y lengths differ"):
+        cb.dot(f(1, 2), f(1), 0.0, pol)
+    A = cb.DenseMatrix(2, 3, cb.Layout.RowMajor, 1.0)
+    with pytest.raises(ValueError, match="gemv_col_major: matrix is not col-major"):
+        cb.gemv_col_major(A, f(1, 1, 1), f(0, 0), pol)
+    with pytest.raises(ValueError, match="gemv: A.cols != x.len"):
+        cb.gemv_row_major(A, f(1, 1), f(0, 0), pol)
+    with pytest.raises(ValueError, match="gemv: A.rows != c.len"):
+        cb.gemv_row_major(A, f(1, 1, 1), f(0, 0, 0), pol)
+    sq = cb.DenseMatrix(3, 3, cb.Layout.ColMajor, 1.0)
+    x = f(1, 2, 3)
+    with pytest.raises(ValueError, match="gemv: c must not alias x"):
+        cb.gemv_col_major(sq, x, x, pol)
+    C2 = cb.DenseMatrix(2, 2, cb.Layout.ColMajor)
+    with pytest.raises(ValueError, match="ger: C.cols != y.len"):
+        cb.ger(f(1, 2), f(3), C2, pol)
+    with pytest.raises(ValueError, match="ger: C.rows != x.len"):
+        cb.ger(f(1, 2, 3), f(3, 4), C2, pol)
+
+
+def test_dense_matrix_indexing_matches_reference_layout():
+    import paper_2108_02025_b200 as cb
+    rm = cb.DenseMatrix(2, 3, cb.Layout.RowMajor)
+    cm = cb.DenseMatrix(2, 3, cb.Layout.ColMajor)
+    assert rm.index(1, 2) == 2 + 1 * 3   # j + i*cols
+    assert cm.index(1, 2) == 1 + 2 * 2   # i + j*rows

@@ -1,0 +1,150 @@
+"""Multi-GPU partition and exchange logic of paper_2108_02025_b200.shard,
+exercised as 2 (and 3) CPU processes over gloo — the same collectives the GPU
+ranks issue over NCCL, with the per-rank compute injected (the oracle as the
+local op, a rank-ordered numpy sum as the combine).  The GPU build only ever
+runs one GPU here, so this is where the N > 1 host path is tested.
+
+Checks: balanced contiguous partition; sharded DOT = rank-ordered sum of the
+shard partials + alpha0 (bitwise, identical on every rank, independent of
+which rank finishes first); row-sharded GEMV with gather reproduces the
+single-process oracle bitwise (rows are independent); row-sharded GER needs no
+communication and reproduces the oracle bitwise.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_2108_02025_b200 import shard
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _ordered_combine(gathered: torch.Tensor, alpha0: float, out: torch.Tensor) -> None:
+    dt = gathered.numpy().dtype.type
+    total = dt(0)
+    for p in gathered.numpy():
+        total = dt(total + p)
+    out[0] = torch.tensor(dt(total + dt(alpha0)))
+
+
+def _oracle_partial(x, y, out, policy):
+    out[0] = torch.tensor(O.dot_ref(x.numpy(), y.numpy(), 0.0))
+
+
+def _oracle_gemv_rows(A, x, c, policy):
+    cn = c.numpy()
+    O.gemv_ref(A.data.numpy(), int(A.layout()), x.numpy(), cn)
+
+
+def _oracle_ger(x, y, C, policy):
+    O.ger_ref(x.numpy(), y.numpy(), C.data.numpy(), int(C.layout()))
+
+
+def _worker(rank, world, port, results):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2108_02025_b200 as cb
+    pol = cb.default_policy(1)
+    try:
+        # ---- DOT: chunk-sharded, all-gather of partials, ordered combine
+        n = 100_003
+        for dt in (np.float32, np.float64):
+            x = O.gen_uniform(n, dt, 42, 1)
+            y = O.gen_uniform(n, dt, 42, 2)
+            b, e = shard.partition(n, world, rank)
+            out = torch.zeros(1, dtype=torch.from_numpy(x).dtype)
+            shard.sharded_dot(torch.from_numpy(x[b:e].copy()), torch.from_numpy(y[b:e].copy()),
+                              0.75, out, pol, partial_fn=_oracle_partial,
+                              combine_fn=_ordered_combine)
+            results[f"dot_{np.dtype(dt).name}_{rank}"] = float(out[0])
+        # ---- GEMV row blocks + gather
+        m, k = 1001, 257
+        A = O.gen_uniform(m * k, np.float64, 42, 3).reshape(m, k)
+        xv = O.gen_uniform(k, np.float64, 42, 1)
+        c0 = O.gen_uniform(m, np.float64, 42, 4)
+        b, e = shard.partition(m, world, rank)
+        Aloc = cb.DenseMatrix.wrap(torch.from_numpy(A[b:e].reshape(-1).copy()), e - b, k,
+                                   cb.Layout.RowMajor)
+        cloc = torch.from_numpy(c0[b:e].copy())
+        full = shard.sharded_gemv_rows(Aloc, torch.from_numpy(xv), cloc, pol, gather=True,
+                                       m_total=m, local_fn=_oracle_gemv_rows)
+        results[f"gemv_{rank}"] = full.numpy().copy()
+        # ---- GER row blocks, no communication
+        gx = O.gen_uniform(m, np.float32, 42, 1)
+        gy = O.gen_uniform(k, np.float32, 42, 2)
+        C0 = O.gen_uniform(m * k, np.float32, 42, 5).reshape(m, k)
+        Cloc = cb.DenseMatrix.wrap(torch.from_numpy(C0[b:e].reshape(-1).copy()), e - b, k,
+                                   cb.Layout.RowMajor)
+        shard.sharded_ger_rows(torch.from_numpy(gx[b:e].copy()), torch.from_numpy(gy), Cloc, pol,
+                               local_fn=_oracle_ger)
+        results[f"ger_{rank}"] = (b, e, Cloc.data.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_paths_over_gloo(world):
+    O.lib()
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+
+    # DOT: every rank holds the same value = ordered sum of shard partials + alpha0
+    n = 100_003
+    for dt in (np.float32, np.float64):
+        x, y = O.gen_uniform(n, dt, 42, 1), O.gen_uniform(n, dt, 42, 2)
+        total = dt(0)
+        for r in range(world):
+            b, e = shard.partition(n, world, r)
+            total = dt(total + O.dot_ref(x[b:e], y[b:e], 0.0))
+        want = float(dt(total + dt(0.75)))
+        got = {results[f"dot_{np.dtype(dt).name}_{r}"] for r in range(world)}
+        assert got == {want}
+        # and it agrees with the single-process oracle within the contract bound
+        truth, sumabs = O.dot_truth(x, y, 0.75)
+        assert abs(want - truth) <= 4 * n * np.finfo(dt).eps * (sumabs + 0.75)
+
+    # GEMV: gathered c equals the single-process oracle bitwise on every rank
+    m, k = 1001, 257
+    A = O.gen_uniform(m * k, np.float64, 42, 3)
+    xv = O.gen_uniform(k, np.float64, 42, 1)
+    c = O.gen_uniform(m, np.float64, 42, 4)
+    O.gemv_ref(A, 0, xv, c)
+    for r in range(world):
+        np.testing.assert_array_equal(results[f"gemv_{r}"], c)
+
+    # GER: the row blocks tile C and match the oracle bitwise
+    gx, gy = O.gen_uniform(m, np.float32, 42, 1), O.gen_uniform(k, np.float32, 42, 2)
+    C = O.gen_uniform(m * k, np.float32, 42, 5)
+    O.ger_ref(gx, gy, C, 0)
+    C = C.reshape(m, k)
+    covered = 0
+    for r in range(world):
+        b, e, blk = results[f"ger_{r}"]
+        np.testing.assert_array_equal(blk.reshape(e - b, k), C[b:e])
+        covered += e - b
+    assert covered == m
+
+
+def test_partition_is_balanced_and_contiguous():
+    for total in (0, 1, 7, 8192, 65536, 100_003, 1 << 32):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard.partition(total, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == total
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            sizes = [e - b for b, e in spans]
+            assert max(sizes) - min(sizes) <= 1
