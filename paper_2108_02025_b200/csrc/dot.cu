@@ -8,7 +8,9 @@
 //   * fixed butterfly warp sums, fixed-order CTA sum -> partials[cta];
 //   * the last CTA to arrive (atomic ticket) sums the partials in a fixed
 //     order, adds alpha0 LAST (as the reference does, kernels.hpp:142,163)
-//     and resets the ticket for the next launch on this stream.
+//     and resets the ticket for the next launch on this stream.  (A variant
+//     where CTA 0 acquire-polls per-CTA release flags measured 0-2 us slower
+//     on B200 and was dropped.)
 // The element -> thread mapping depends only on n and the grid, so the result
 // is bitwise reproducible run to run (reference kernels.hpp:9-13).
 //
@@ -23,9 +25,11 @@ namespace cabl_dev {
 
 namespace {
 
-constexpr int kDotBlock = 256;
+// measured best on n = 2^24 fp32 (tools/tune.py): 512 x 2 CTAs/SM, 2 vectors
+// of x and y in flight per thread per iteration
+constexpr int kDotBlock = 512;
 constexpr int kDotUnroll = 2;
-constexpr int kDotCtasPerSm = 4;
+constexpr int kDotCtasPerSm = 2;
 
 template <typename T, int BLOCK, int U, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB)
@@ -136,16 +140,20 @@ template <typename T> unsigned dot_grid(uint64_t n, bool small) {
     return g < 1 ? 1u : unsigned(g);
 }
 
+template <typename T, int B, int U, int M>
+cudaError_t dot_go(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok, T alpha0,
+                   T* out, T* partials, unsigned* ticket, cudaStream_t s) {
+    dot_kernel<T, B, U, M><<<grid, B, 0, s>>>(x, y, n, vec_ok, alpha0, out, partials, ticket);
+    return cudaGetLastError();
+}
+
 template <typename T>
-void dot_dispatch(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok, T alpha0, T* out,
-                  T* partials, unsigned* ticket, cudaStream_t s) {
+cudaError_t dot_dispatch(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok, T alpha0,
+                         T* out, T* partials, unsigned* ticket, cudaStream_t s) {
     const DotCfg c = dot_cfg();
 #define CABL_DOT_CASE(B_, U_, M_)                                                              \
-    if (c.block == B_ && c.unroll == U_ && c.minb == M_) {                                     \
-        dot_kernel<T, B_, U_, M_><<<grid, B_, 0, s>>>(x, y, n, vec_ok, alpha0, out, partials,  \
-                                                      ticket);                                 \
-        return;                                                                                \
-    }
+    if (c.block == B_ && c.unroll == U_ && c.minb == M_)                                       \
+        return dot_go<T, B_, U_, M_>(grid, x, y, n, vec_ok, alpha0, out, partials, ticket, s);
     CABL_DOT_CASE(256, 1, 8)
     CABL_DOT_CASE(256, 2, 8)
     CABL_DOT_CASE(256, 4, 4)
@@ -154,8 +162,8 @@ void dot_dispatch(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok,
     CABL_DOT_CASE(1024, 2, 1)
     CABL_DOT_CASE(1024, 4, 1)
 #undef CABL_DOT_CASE
-    dot_kernel<T, kDotBlock, kDotUnroll, kDotCtasPerSm><<<grid, kDotBlock, 0, s>>>(
-        x, y, n, vec_ok, alpha0, out, partials, ticket);
+    return dot_go<T, kDotBlock, kDotUnroll, kDotCtasPerSm>(grid, x, y, n, vec_ok, alpha0, out,
+                                                          partials, ticket, s);
 }
 
 } // namespace
@@ -172,10 +180,10 @@ cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, boo
                        const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
     const unsigned grid = dot_grid<T>(n, small);
     const int vec_ok = aligned32(x) && aligned32(y);
-    dot_dispatch<T>(grid, x, y, n, vec_ok, alpha0, out, static_cast<T*>(ws.scratch), ws.counters,
-                    s);
+    const cudaError_t e = dot_dispatch<T>(grid, x, y, n, vec_ok, alpha0, out,
+                                          static_cast<T*>(ws.scratch), ws.counters, s);
     if (info) info->ctas = grid;
-    return cudaGetLastError();
+    return e;
 }
 
 template <typename T>
