@@ -198,10 +198,12 @@ int ger_impl(const T* x, const T* y, T* C, int layout, uint64_t m, uint64_t n, u
     const bool small = touched <= cutoff;
     LaunchInfo info;
     cudaStream_t s = as_stream(stream);
+    Workspace ws;
+    if (int rc = get_workspace(dev, s, ger_need<T>(x, y, m, n), &ws)) return rc;
     if (layout == CABL_ROW_MAJOR)
-        CABL_TRY_CUDA(ger_launch<T>(x, y, C, m, n, small, s, &info), "ger kernel");
+        CABL_TRY_CUDA(ger_launch<T>(x, y, C, m, n, small, ws, s, &info), "ger kernel");
     else
-        CABL_TRY_CUDA(ger_launch<T>(y, x, C, n, m, small, s, &info), "ger kernel");
+        CABL_TRY_CUDA(ger_launch<T>(y, x, C, n, m, small, ws, s, &info), "ger kernel");
     set_probe(probe, CABL_VARIANT_GER, info.ctas);
     return CABL_OK;
 }

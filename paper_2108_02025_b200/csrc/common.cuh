@@ -151,6 +151,19 @@ struct Partition {
     }
 };
 
+// Dynamic work queue over items [0, total) for a grid of <= total CTAs: CTA b
+// starts on item b with no atomic on the critical path, then draws
+// gridDim.x + atomicAdd(counter, 1) until it gets an item >= total.  That is
+// exactly `total` draws overall (total - grid successful + one failing per
+// CTA), so whoever draws raw value total - 1 is the counter's last user in
+// this launch and resets it to zero for the next launch on the stream.
+__device__ __forceinline__ unsigned long long dyn_next(unsigned* counter,
+                                                       unsigned long long total) {
+    const unsigned long long raw = atomicAdd(counter, 1u);
+    if (raw == total - 1) *counter = 0u;
+    return raw + gridDim.x;
+}
+
 inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
 
 } // namespace cabl_dev

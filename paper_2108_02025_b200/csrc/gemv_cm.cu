@@ -31,6 +31,8 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 namespace cabl_dev {
 
 namespace {
@@ -51,46 +53,57 @@ template <typename T> __device__ __forceinline__ T ref_step(T acc, T a, T xj, bo
     return fused ? fma_rn(a, xj, acc) : add_rn(acc, mul_rn(a, xj));
 }
 
-template <typename T>
+template <typename T, bool DYN>
 __global__ void __launch_bounds__(kTallBlock, 1)
     gemv_cm_tall_vec_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
-                            uint64_t m, uint64_t n) {
+                            uint64_t m, uint64_t n, unsigned* __restrict__ counter) {
     constexpr int V = Vec<T>::N;
     constexpr uint64_t kRefVec = 16 / sizeof(T);
+    __shared__ unsigned long long next_sh[2];
     const uint64_t mv = m / V; // row vectors == vectors per column
-    // CTAs own balanced ranges of BLOCK-row-vector units; every thread runs
-    // the same number of rounds (measured faster than balancing single row
-    // vectors, whose ragged last round idles most of each CTA).
     const uint64_t units = (mv + kTallBlock - 1) / kTallBlock;
-    const Partition part(units, gridDim.x);
     const uint64_t cut = (n / kRefVec) * kRefVec;
     const Vec<T>* Av = reinterpret_cast<const Vec<T>*>(A);
     Vec<T>* Cv = reinterpret_cast<Vec<T>*>(c);
-
-    for (uint64_t u = part.begin(blockIdx.x); u < part.begin(blockIdx.x + 1); ++u) {
+    // DYN: first unit static, the rest from the queue (common.cuh dyn_next);
+    // otherwise CTAs own balanced contiguous unit ranges.
+    const Partition part(units, gridDim.x);
+    uint64_t u = DYN ? uint64_t(blockIdx.x) : part.begin(blockIdx.x);
+    const uint64_t u_end = DYN ? units : part.begin(blockIdx.x + 1);
+    int parity = 0;
+    while (u < u_end) {
+        if (DYN && threadIdx.x == 0) next_sh[parity ^ 1] = dyn_next(counter, units); // prefetch
         const uint64_t rv = u * kTallBlock + threadIdx.x;
-        if (rv >= mv) continue; // no barrier below: early exit is safe
-        Vec<T> acc = Cv[rv];
-        const Vec<T>* col = Av + rv;
-        uint64_t j = 0;
-        for (; j + kTallUnroll <= cut; j += kTallUnroll) {
-            Vec<T> a[kTallUnroll];
+        if (rv < mv) {
+            Vec<T> acc = Cv[rv];
+            const Vec<T>* col = Av + rv;
+            uint64_t j = 0;
+            for (; j + kTallUnroll <= cut; j += kTallUnroll) {
+                Vec<T> a[kTallUnroll];
 #pragma unroll
-            for (int k = 0; k < kTallUnroll; ++k) a[k] = ld_stream(col + (j + k) * mv);
+                for (int k = 0; k < kTallUnroll; ++k) a[k] = ld_stream(col + (j + k) * mv);
 #pragma unroll
-            for (int k = 0; k < kTallUnroll; ++k) {
-                const T xj = __ldg(x + j + k);
+                for (int k = 0; k < kTallUnroll; ++k) {
+                    const T xj = __ldg(x + j + k);
 #pragma unroll
-                for (int e = 0; e < V; ++e) acc.v[e] = ref_step(acc.v[e], a[k].v[e], xj, false);
+                    for (int e = 0; e < V; ++e) acc.v[e] = ref_step(acc.v[e], a[k].v[e], xj, false);
+                }
             }
-        }
-        for (; j < n; ++j) {
-            const Vec<T> a = ld_stream(col + j * mv);
-            const T xj = __ldg(x + j);
+            for (; j < n; ++j) {
+                const Vec<T> a = ld_stream(col + j * mv);
+                const T xj = __ldg(x + j);
 #pragma unroll
-            for (int e = 0; e < V; ++e) acc.v[e] = ref_step(acc.v[e], a.v[e], xj, j >= cut);
+                for (int e = 0; e < V; ++e) acc.v[e] = ref_step(acc.v[e], a.v[e], xj, j >= cut);
+            }
+            Cv[rv] = acc;
         }
-        Cv[rv] = acc;
+        if (DYN) {
+            __syncthreads(); // publishes next_sh[parity ^ 1]
+            parity ^= 1;
+            u = next_sh[parity];
+        } else {
+            ++u;
+        }
     }
 }
 
@@ -348,7 +361,11 @@ template <typename T> bool tall_vec_ok(const T* A, const T* c, uint64_t m) {
 
 template <typename T> WorkspaceNeed gemv_cm_need(const T* A, const T*, uint64_t m, uint64_t n) {
     WorkspaceNeed w;
-    if (m == 0 || n == 0 || m >= kSplitMaxRows) return w;
+    if (m == 0 || n == 0) return w;
+    if (m >= kSplitMaxRows) {
+        w.counters = 1; // unit counter of the tall kernel
+        return w;
+    }
     const SplitGeom g = split_vec_ok(A, m) ? split_vec_geom<T>(m, n) : split_geom<T>(m, n);
     w.counters = 1;
     w.scratch_bytes = size_t(g.grid) * m * sizeof(T);
@@ -361,10 +378,20 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
     if (info) info->ctas = 0;
     if (m == 0 || n == 0) return cudaSuccess;
     if (m >= kSplitMaxRows && tall_vec_ok(A, c, m)) {
-        const uint64_t mv = m / Vec<T>::N;
+        const uint64_t units = (m / Vec<T>::N + kTallBlock - 1) / kTallBlock;
         const uint64_t sms = uint64_t(sm_count());
-        const unsigned grid = unsigned(mv < sms ? mv : sms);
-        gemv_cm_tall_vec_kernel<T><<<grid, kTallBlock, 0, s>>>(A, x, c, m, n);
+        const unsigned grid = unsigned(units < sms ? units : sms); // grid <= units (dyn_next)
+        // dynamic unit queue for large matrices (2^20 x 256 fp64: 310 -> 301 us),
+        // static unit ranges otherwise; CABL_GEMV_DYN=0|1 overrides (tuning)
+        static const int forced = [] {
+            const char* e = getenv("CABL_GEMV_DYN");
+            return e ? atoi(e) : -1;
+        }();
+        const bool dyn = forced >= 0 ? forced != 0 : m * n * sizeof(T) >= (uint64_t(512) << 20);
+        if (dyn)
+            gemv_cm_tall_vec_kernel<T, true><<<grid, kTallBlock, 0, s>>>(A, x, c, m, n, ws.counters);
+        else
+            gemv_cm_tall_vec_kernel<T, false><<<grid, kTallBlock, 0, s>>>(A, x, c, m, n, ws.counters);
         if (info) info->ctas = grid;
     } else if (m >= kSplitMaxRows) {
         const uint64_t units = (m + kWarp - 1) / kWarp;

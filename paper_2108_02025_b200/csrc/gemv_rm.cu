@@ -147,42 +147,34 @@ __global__ void __launch_bounds__(kRmBlock, kRmCtasPerSm)
     }
 }
 
-// SWEEP kernel (m large relative to the grid).  CTAs stride over groups of
-// R rows (grid-stride: at any moment the whole GPU reads one contiguous
-// window of A, the access order that measured fastest for a streaming read
-// on B200, tools/bwlab.py); all BLOCK threads of a CTA read the group's rows
-// together — thread t owns the vector columns t, t + BLOCK, ... — so every
-// CTA-wide load is a contiguous BLOCK*32-byte run.  XREG: the row fits in one
-// pass (nvec_row <= BLOCK*KV) and the thread's x vectors stay in registers for
-// the whole kernel; otherwise x is re-read per chunk through L1/L2, shared by
-// the R rows.  Per row: fixed butterfly per warp, then warp partials summed
-// in warp order by one thread (double-buffered shared slots: one barrier per
-// group), c[i] = c[i] + sum.
-template <typename T, int R, int KV, bool XREG, int MINB>
+// SWEEP kernel (m large relative to the grid).  Work is cut into groups of R
+// rows; all BLOCK threads of a CTA read a group's rows together — thread t
+// owns the vector columns t, t + BLOCK, ... — so every CTA-wide load is one
+// contiguous BLOCK*32-byte run, and consecutive groups are consecutive
+// stretches of A, so the GPU sweeps A front to back (the access order that
+// measured fastest for a streaming read on B200, tools/bwlab.py).  Groups are
+// handed out in grid-stride order (DYN = false) or drawn from an atomic
+// counter (DYN = true): SMs that get faster memory service take more groups.
+// x is re-read per chunk through L1 and shared by the R rows.  Per row: fixed
+// butterfly per warp, then the warp partials summed in warp order by one
+// thread (double-buffered shared slots: one barrier per group),
+// c[i] = c[i] + sum.  A group's result does not depend on which CTA took it:
+// bitwise reproducible either way.
+template <typename T, int R, int KV, int MINB, bool DYN>
 __global__ void __launch_bounds__(kRmBlock, MINB)
     gemv_rm_sweep_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
-                         uint64_t m, uint64_t n) {
+                         uint64_t m, uint64_t n, unsigned* __restrict__ counter) {
     constexpr int NW = kRmBlock / kWarp;
     __shared__ T red[2][R][NW];
+    __shared__ unsigned long long next_sh[2];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint64_t nvec_row = n / Vec<T>::N;
     const uint64_t groups = (m + R - 1) / R;
     const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
-
-    Vec<T> xr[XREG ? KV : 1];
-    if (XREG) {
-#pragma unroll
-        for (int k = 0; k < KV; ++k) {
-            const uint64_t j = uint64_t(tid) + uint64_t(k) * kRmBlock;
-            if (j < nvec_row) xr[k] = ld_reuse(X + j);
-            else
-#pragma unroll
-                for (int e = 0; e < Vec<T>::N; ++e) xr[k].v[e] = T(0);
-        }
-    }
-
+    uint64_t g = blockIdx.x; // first group static, the rest from the queue (DYN)
     int parity = 0;
-    for (uint64_t g = blockIdx.x; g < groups; g += gridDim.x, parity ^= 1) {
+    while (g < groups) {
+        if (DYN && tid == 0) next_sh[parity ^ 1] = dyn_next(counter, groups); // prefetch
         const uint64_t row0 = g * R;
         const int rows = (m - row0 < uint64_t(R)) ? int(m - row0) : R;
         T acc[R];
@@ -195,8 +187,7 @@ __global__ void __launch_bounds__(kRmBlock, MINB)
             for (int k = 0; k < KV; ++k) {
                 const uint64_t j = base + uint64_t(tid) + uint64_t(k) * kRmBlock;
                 const bool ok = j < nvec_row;
-                if (XREG) xv[k] = xr[k];
-                else if (ok) xv[k] = ld_reuse(X + j);
+                if (ok) xv[k] = ld_reuse(X + j);
                 else
 #pragma unroll
                     for (int e = 0; e < Vec<T>::N; ++e) xv[k].v[e] = T(0);
@@ -219,13 +210,15 @@ __global__ void __launch_bounds__(kRmBlock, MINB)
             const T v = warp_sum(acc[r]);
             if (lane == 0) red[parity][r][wid] = v;
         }
-        __syncthreads();
+        __syncthreads(); // also publishes next_sh[parity ^ 1]
         if (tid < rows) {
             T sum = red[parity][tid][0];
 #pragma unroll
             for (int w = 1; w < NW; ++w) sum = add_rn(sum, red[parity][tid][w]);
             c[row0 + tid] = add_rn(c[row0 + tid], sum);
         }
+        parity ^= 1;
+        g = DYN ? next_sh[parity] : g + gridDim.x;
     }
 }
 
@@ -297,19 +290,36 @@ struct SweepCfg {
     int R, KV, minb;
 };
 
-// Tuning table (CABL_RM_SWEEP="R,KV,MINB" selects an entry; tools/tune.py).
-template <typename T, int R, int KV, bool XREG, int MINB>
-unsigned sweep_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, cudaStream_t s) {
+// Dynamic group queue or static grid-stride order.  Measured (tools/tune.py):
+// 65536^2 fp32 2331 -> 2270 us with the queue, 8192^2 fp32 43.5 -> 44.8 us
+// (the queue's atomics do not pay off on a 40 us kernel).  CABL_GEMV_DYN=0|1
+// overrides the size rule (tuning only).
+inline bool use_dyn_queue(uint64_t bytes) {
+    static const int forced = [] {
+        const char* e = getenv("CABL_GEMV_DYN");
+        return e ? atoi(e) : -1;
+    }();
+    if (forced >= 0) return forced != 0;
+    return bytes >= (uint64_t(512) << 20);
+}
+
+template <typename T, int R, int KV, int MINB>
+unsigned sweep_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, unsigned* counter,
+                  cudaStream_t s) {
     const uint64_t groups = (m + R - 1) / R;
     const uint64_t ctas = uint64_t(sm_count()) * MINB;
     const unsigned grid = unsigned(groups < ctas ? groups : ctas);
-    gemv_rm_sweep_kernel<T, R, KV, XREG, MINB><<<grid, kRmBlock, 0, s>>>(A, x, c, m, n);
+    if (use_dyn_queue(m * n * sizeof(T)))
+        gemv_rm_sweep_kernel<T, R, KV, MINB, true><<<grid, kRmBlock, 0, s>>>(A, x, c, m, n, counter);
+    else
+        gemv_rm_sweep_kernel<T, R, KV, MINB, false><<<grid, kRmBlock, 0, s>>>(A, x, c, m, n, counter);
     return grid;
 }
 
+// Tuning table (CABL_RM_SWEEP="R,KV,MINB" selects an entry; tools/tune.py).
 template <typename T>
 unsigned sweep_launch(const T* A, const T* x, T* c, uint64_t m, uint64_t n, int mode,
-                      cudaStream_t s) {
+                      unsigned* counter, cudaStream_t s) {
     static const SweepCfg forced = [] {
         SweepCfg f{0, 0, 0};
         if (const char* e = getenv("CABL_RM_SWEEP")) sscanf(e, "%d,%d,%d", &f.R, &f.KV, &f.minb);
@@ -317,9 +327,7 @@ unsigned sweep_launch(const T* A, const T* x, T* c, uint64_t m, uint64_t n, int 
     }();
 #define CABL_SWEEP_CASE(R_, KV_, MB_)                                                          \
     if (forced.R == R_ && forced.KV == KV_ && forced.minb == MB_)                             \
-        return sweep_go<T, R_, KV_, false, MB_>(A, x, c, m, n, s);
-    CABL_SWEEP_CASE(1, 8, 2)
-    CABL_SWEEP_CASE(2, 2, 4)
+        return sweep_go<T, R_, KV_, MB_>(A, x, c, m, n, counter, s);
     CABL_SWEEP_CASE(2, 4, 2)
     CABL_SWEEP_CASE(2, 8, 1)
     CABL_SWEEP_CASE(4, 1, 4)
@@ -328,15 +336,21 @@ unsigned sweep_launch(const T* A, const T* x, T* c, uint64_t m, uint64_t n, int 
     CABL_SWEEP_CASE(8, 1, 2)
     CABL_SWEEP_CASE(8, 2, 1)
 #undef CABL_SWEEP_CASE
-    if (mode == 1) return sweep_go<T, 4, 2, false, 2>(A, x, c, m, n, s); // rows <= 2 passes
-    return sweep_go<T, 2, 8, false, 1>(A, x, c, m, n, s);                  // long rows
+    if (mode == 1) return sweep_go<T, 4, 2, 2>(A, x, c, m, n, counter, s); // rows <= 2 passes
+    return sweep_go<T, 2, 8, 1>(A, x, c, m, n, counter, s);                  // long rows
 }
 
 } // namespace
 
 template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n) {
     WorkspaceNeed w;
-    if (m == 0 || n == 0 || rm_mode<T>(A, x, m, n) != 0) return w;
+    if (m == 0 || n == 0) return w;
+    const int mode = rm_mode<T>(A, x, m, n);
+    if (mode >= 1) {
+        w.counters = 1; // group counter of the dynamic sweep
+        return w;
+    }
+    if (mode != 0) return w;
     const RmGeom g = rm_geom<T>(m, n);
     w.counters = g.warps;
     w.scratch_bytes = g.warps * 2 * kRmRows * sizeof(T);
@@ -350,7 +364,7 @@ cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
     if (m == 0 || n == 0) return cudaSuccess; // c += 0
     const int mode = rm_mode<T>(A, x, m, n);
     if (mode >= 1) {
-        const unsigned grid = sweep_launch<T>(A, x, c, m, n, mode, s);
+        const unsigned grid = sweep_launch<T>(A, x, c, m, n, mode, ws.counters, s);
         if (info) info->ctas = grid;
     } else if (mode == 0) {
         const RmGeom g = rm_geom<T>(m, n);

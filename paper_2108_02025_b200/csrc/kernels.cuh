@@ -61,9 +61,10 @@ cudaError_t gemv_ordered_launch(const T* A, int layout, uint64_t m, uint64_t n, 
 // ---- GER (ger.cu): C(major, minor) = fma(u[major], v[minor], C) over an
 // outer x inner row-major view; the col-major GER is the same kernel with
 // (x, m) and (y, n) swapped, since fma(a, b, c) == fma(b, a, c).
+template <typename T> WorkspaceNeed ger_need(const T* u, const T* v, uint64_t outer, uint64_t inner);
 template <typename T>
 cudaError_t ger_launch(const T* u, const T* v, T* C, uint64_t outer, uint64_t inner,
-                       bool small, cudaStream_t s, LaunchInfo* info);
+                       bool small, const Workspace& ws, cudaStream_t s, LaunchInfo* info);
 
 // ---- seeded inputs (datagen.cu) ----
 cudaError_t fill_uniform_f32(float* out, uint64_t n, uint64_t seed, uint64_t sid,

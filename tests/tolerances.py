@@ -42,16 +42,19 @@ def log2c(v: int) -> int:
     return max(1, math.ceil(math.log2(max(v, 2))))
 
 
-def dot_chain(n: int, dtype) -> int:
-    """dot_kernel (csrc/dot.cu): grid G <= 148*4 CTAs x 256 threads, each thread
-    one FMA chain over its share (split over U=2 accumulators, V elements per
-    vector), then 1 + 5 + 3 fixed adds (accumulators, warp, CTA), a sequential
-    pass of ceil(G/256) partials per thread, 8 tree levels and + alpha0."""
+def dot_chain(n: int, dtype, block: int = 512, unroll: int = 2, ctas_per_sm: int = 2) -> int:
+    """dot_kernel (csrc/dot.cu): grid G <= 148*ctas_per_sm CTAs x block
+    threads, each thread one FMA chain per accumulator over its share (U
+    accumulators, V elements per vector), then U-1 adds, a 5-level warp
+    butterfly, log2(warps) levels across warps, a sequential pass of
+    ceil(G/block) partials per thread in the last CTA, the same two trees
+    again, and + alpha0."""
     V = 32 // np.dtype(dtype).itemsize
     nvec = n // V
-    G = max(1, min(math.ceil(nvec / 512), SMS * 4))
-    per_thread = math.ceil(max(nvec, 1) / (G * 256)) * V + V
-    return per_thread + 1 + 5 + 3 + math.ceil(G / 256) + 8 + 1
+    G = max(1, min(math.ceil(nvec / (block * unroll)), SMS * ctas_per_sm))
+    per_thread = math.ceil(max(nvec, 1) / (G * block)) * V + V
+    tree = 5 + log2c(block // 32)
+    return per_thread + unroll + tree + math.ceil(G / block) + tree + 1
 
 
 def gemv_rm_chain(n: int, dtype) -> int:
