@@ -1,0 +1,102 @@
+"""Every launch-shape / scheduling variant of the kernels gives the same bits.
+
+The library picks launch shapes and work distribution (static ranges, grid-
+stride order, atomic work queues) by problem size; the tuning environment
+variables CABL_GEMV_DYN / CABL_GER_MODE / CABL_GEMV_RM_MODE / CABL_RM_SWEEP
+force each variant.  For the paths whose per-element order does not depend on
+the schedule (GER: one FMA per element; GEMV row groups and tall col-major
+units: each output owned by one CTA), results must be bitwise identical
+across variants — and equal to the oracle where the path is bit-exact.  Each
+variant runs in its own process (the variables are read once per process).
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r"""
+import hashlib, json, sys, torch
+sys.path.insert(0, %(root)r)
+import paper_2108_02025_b200 as cb
+dev = torch.device('cuda:0'); pol = cb.default_policy(1)
+def fill(n, dt, st):
+    return cb.fill_uniform(torch.empty(n, dtype=dt, device=dev), 42, st)
+out = {}
+for dt in (torch.float32, torch.float64):
+    # GER, both layouts, shapes with ragged tile edges
+    for lay in (cb.Layout.RowMajor, cb.Layout.ColMajor):
+        m, n = 1037, 2056
+        C = cb.DenseMatrix.wrap(fill(m * n, dt, 5), m, n, lay)
+        cb.ger(fill(m, dt, 1), fill(n, dt, 2), C, pol)
+        out[f"ger/{dt}/{int(lay)}"] = hashlib.sha256(C.data.cpu().numpy().tobytes()).hexdigest()
+    # row-major GEMV, tall col-major GEMV
+    for lay, m, n in ((cb.Layout.RowMajor, 20000, 2048), (cb.Layout.ColMajor, 40960, 96)):
+        A = cb.DenseMatrix.wrap(fill(m * n, dt, 3), m, n, lay)
+        c = fill(m, dt, 4)
+        (cb.gemv_row_major if lay == cb.Layout.RowMajor else cb.gemv_col_major)(A, fill(n, dt, 1), c, pol)
+        out[f"gemv/{dt}/{int(lay)}"] = hashlib.sha256(c.cpu().numpy().tobytes()).hexdigest()
+print(json.dumps(out))
+"""
+
+VARIANTS = [
+    {},
+    {"CABL_GEMV_DYN": "1", "CABL_GER_MODE": "2"},
+    {"CABL_GEMV_DYN": "0", "CABL_GER_MODE": "0"},
+    {"CABL_GER_MODE": "1", "CABL_RM_SWEEP": "2,8,1"},
+    {"CABL_GEMV_DYN": "1", "CABL_RM_SWEEP": "8,1,2"},
+]
+
+
+def _run(env_extra):
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, "-c", SCRIPT % {"root": str(ROOT)}], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def test_scheduling_variants_are_bitwise_identical(cuda):
+    ref = _run(VARIANTS[0])
+    for v in VARIANTS[1:]:
+        got = _run(v)
+        assert got == ref, (v, {k for k in ref if ref[k] != got.get(k)})
+
+
+def test_row_major_gemv_modes_agree_with_oracle_tolerance(cuda):
+    """The segment kernel (mode 0) and the sweep (1, 2) sum a row in different
+    orders: not bitwise equal to each other, each within the contract bound."""
+    import numpy as np
+    from oracle import oracle as O
+    script = r"""
+import sys, json, torch
+sys.path.insert(0, %(root)r)
+import paper_2108_02025_b200 as cb
+dev = torch.device('cuda:0'); pol = cb.default_policy(1)
+f = lambda n, st: cb.fill_uniform(torch.empty(n, dtype=torch.float32, device=dev), 42, st)
+m, n = 20000, 2048
+A = cb.DenseMatrix.wrap(f(m * n, 3), m, n, cb.Layout.RowMajor); c = f(m, 4)
+cb.gemv_row_major(A, f(n, 1), c, pol)
+print(json.dumps(c.cpu().numpy().astype(float).tolist()))
+"""
+    m, n = 20000, 2048
+    A = O.gen_uniform(m * n, np.float32, 42, 3)
+    x = O.gen_uniform(n, np.float32, 42, 1)
+    c0 = O.gen_uniform(m, np.float32, 42, 4)
+    truth, rowabs = O.gemv_truth(A, 0, x, c0)
+    for mode in ("0", "1", "2"):
+        r = subprocess.run([sys.executable, "-c", script % {"root": str(ROOT)}],
+                           env=dict(os.environ, CABL_GEMV_RM_MODE=mode), capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr
+        got = np.array(json.loads(r.stdout.strip().splitlines()[-1]))
+        bound = (n / 32 + 80) * np.finfo(np.float32).eps * (rowabs + np.abs(c0))
+        assert np.all(np.abs(got - truth) <= bound), mode
