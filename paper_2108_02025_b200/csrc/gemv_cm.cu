@@ -28,9 +28,11 @@
 //     tolerance of gemv_ref.
 //
 // Algorithmic bytes per launch: m*n*s + n*s + 2*m*s.
+#include "bulk.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <cstdio>
 #include <cstdlib>
 
 namespace cabl_dev {
@@ -147,15 +149,17 @@ __global__ void __launch_bounds__(kCmBlock, kCmRowsCtasPerSm)
 template <typename T>
 __device__ void split_final(const T* __restrict__ partials, T* __restrict__ c, uint64_t m, T* sm) {
     const unsigned G = gridDim.x;
-    const int block = blockDim.x;
+    int block = 32; // largest power of two <= blockDim.x
+    while (block * 2 <= int(blockDim.x)) block *= 2;
     int rl = 32;
     while (uint64_t(rl) < m && rl < block) rl *= 2;
     const int Q = block / rl;
     const int r0 = threadIdx.x % rl, q = threadIdx.x / rl;
+    const bool part = int(threadIdx.x) < block;
     for (uint64_t rb = 0; rb < m; rb += uint64_t(rl)) {
         const uint64_t r = rb + r0;
         T total = T(0);
-        if (r < m) {
+        if (part && r < m) {
             for (unsigned b0 = q; b0 < G; b0 += 16u * Q) {
                 T v[16];
 #pragma unroll
@@ -169,9 +173,9 @@ __device__ void split_final(const T* __restrict__ partials, T* __restrict__ c, u
             }
         }
         __syncthreads(); // sm reuse
-        if (r < m) sm[uint64_t(q) * rl + r0] = total;
+        if (part && r < m) sm[uint64_t(q) * rl + r0] = total;
         __syncthreads();
-        if (q == 0 && r < m) {
+        if (part && q == 0 && r < m) {
             T v = sm[r0];
             for (int k = 1; k < Q; ++k) v = add_rn(v, sm[uint64_t(k) * rl + r0]);
             c[r] = add_rn(c[r], v);
@@ -238,6 +242,120 @@ __global__ void __launch_bounds__(kSplitBlock, 1)
     if (!am_last) return;
     __threadfence();
     split_final(partials, c, m, sm);
+    if (tid == 0) *ticket = 0u;
+}
+
+// Bulk-copy split kernel (m < kSplitMaxRows, m % V == 0, aligned).  The
+// column tiles are contiguous in a col-major matrix (tc consecutive columns =
+// tc*m*s bytes), so one elected producer thread streams each tile into a ring
+// of kBulkStages shared-memory stages with a single cp.async.bulk (TMA engine;
+// completion counted on an mbarrier), keeping up to 3 x 64 KB per SM in flight
+// without spending registers on it (the tile's x slice rides in the same
+// stage).  Measured equal to the register-load kernel below (311.9 vs 312.0 us
+// on 256 x 2^20 fp64); it is the default because it frees the consumer
+// threads' registers and scales its bytes in flight with shared memory.  16 consumer warps = (row-vector lane,
+// column lane) pairs read their 32-byte row vectors from the stage and FMA into
+// register accumulators, then free the stage (one arrive per warp).  Tiles go
+// to CTAs in grid-stride (sweep) order; the per-row combine is the same as
+// the register kernel's: column lanes in smem in order, then the CTA
+// partials in CTA order by the last CTA.
+constexpr int kBulkConsumerWarps = 16;
+constexpr int kBulkConsumers = kBulkConsumerWarps * 32;
+constexpr int kBulkThreads = kBulkConsumers + 32; // + 1 producer warp
+constexpr unsigned kBulkXBytes = 1024;            // the tile's slice of x rides along
+constexpr unsigned kBulkCombineBytes = 16384;     // >= 512*V*s and >= kBulkThreads*s
+constexpr unsigned bulk_smem(int stages, unsigned stage_bytes) {
+    return stages * (stage_bytes + kBulkXBytes) + kBulkCombineBytes;
+}
+
+template <typename T, int kBulkStages, unsigned kBulkStageBytes>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+    gemv_cm_split_bulk_kernel(const T* __restrict__ A, const T* __restrict__ x,
+                              T* __restrict__ c, uint64_t m, uint64_t n, int row_lanes, int tc,
+                              T* __restrict__ partials, unsigned* __restrict__ ticket) {
+    constexpr int V = Vec<T>::N;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* stages = reinterpret_cast<T*>(smem_raw);
+    constexpr unsigned kBulkStageStride = kBulkStageBytes + kBulkXBytes;
+    T* comb = reinterpret_cast<T*>(smem_raw + kBulkStages * kBulkStageStride);
+    __shared__ __align__(8) uint64_t full[kBulkStages];
+    __shared__ __align__(8) uint64_t empty[kBulkStages];
+    __shared__ bool am_last;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint64_t tiles = (n + tc - 1) / tc;
+    const uint64_t stage_elems = kBulkStageStride / sizeof(T);
+    const uint64_t x_off = kBulkStageBytes / sizeof(T); // x slice after the A tile
+    const int col_lanes = kBulkConsumers / row_lanes;
+
+    if (tid == 0) {
+        for (int s = 0; s < kBulkStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kBulkConsumerWarps);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == kBulkConsumerWarps) {
+        if (lane == 0) { // producer
+            const uint64_t pol = l2_evict_first_policy();
+            uint64_t it = 0;
+            for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+                const int st = int(it % kBulkStages);
+                const unsigned use = unsigned(it / kBulkStages);
+                if (use > 0) mbar_wait(&empty[st], (use - 1) & 1u);
+                const uint64_t col0 = t * tc;
+                const uint64_t cols = (n - col0 < uint64_t(tc)) ? n - col0 : uint64_t(tc);
+                const unsigned bytes = unsigned(cols * m * sizeof(T));
+                // x slice: a full tile's is a multiple of 16 B (tc is); a ragged
+                // last tile's x is read with plain loads by the consumers
+                const unsigned xbytes = cols == uint64_t(tc) ? unsigned(cols * sizeof(T)) : 0u;
+                mbar_arrive_expect_tx(&full[st], bytes + xbytes);
+                bulk_g2s(stages + st * stage_elems, A + col0 * m, bytes, &full[st], pol);
+                if (xbytes) bulk_g2s(stages + st * stage_elems + x_off, x + col0, xbytes, &full[st], pol);
+            }
+        }
+    } else {
+        const int rl = tid % row_lanes, cl = tid / row_lanes;
+        const bool live = uint64_t(rl) * V < m;
+        Vec<T> acc;
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc.v[e] = T(0);
+        uint64_t it = 0;
+        for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            const int st = int(it % kBulkStages);
+            mbar_wait(&full[st], unsigned(it / kBulkStages) & 1u);
+            const uint64_t col0 = t * tc;
+            const int cols = int((n - col0 < uint64_t(tc)) ? n - col0 : uint64_t(tc));
+            const T* sb = stages + st * stage_elems;
+            if (live) {
+                for (int j = cl; j < cols; j += col_lanes) {
+                    const Vec<T> a = *reinterpret_cast<const Vec<T>*>(sb + uint64_t(j) * m + uint64_t(rl) * V);
+                    const T xj = cols == tc ? sb[x_off + j] : __ldg(x + col0 + j);
+#pragma unroll
+                    for (int e = 0; e < V; ++e) acc.v[e] = fma_rn(a.v[e], xj, acc.v[e]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+        }
+        if (live)
+#pragma unroll
+            for (int e = 0; e < V; ++e) comb[uint64_t(cl) * m + uint64_t(rl) * V + e] = acc.v[e];
+    }
+    __syncthreads();
+    for (uint64_t r = tid; r < m; r += blockDim.x) {
+        T v = comb[r];
+        for (int q = 1; q < col_lanes; ++q) v = add_rn(v, comb[uint64_t(q) * m + r]);
+        partials[uint64_t(blockIdx.x) * m + r] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    split_final(partials, c, m, comb);
     if (tid == 0) *ticket = 0u;
 }
 
@@ -353,6 +471,66 @@ template <typename T> SplitGeom split_vec_geom(uint64_t m, uint64_t n) {
     return g;
 }
 
+struct BulkCfg {
+    int stages;
+    unsigned stage_bytes;
+};
+
+inline BulkCfg bulk_cfg() {
+    static const BulkCfg c = [] {
+        BulkCfg b{3, 65536}; // measured on 256 x 2^20 fp64: 3x64 KB 311.9 us, 4x48 313.3,
+                             // 6x32 322.4, 12x16 338.7 (fewer, larger stages win)
+        if (const char* e = getenv("CABL_BULK")) { // "stages,KiB" (tuning only)
+            int st = 6, kb = 32;
+            if (sscanf(e, "%d,%d", &st, &kb) == 2) b = BulkCfg{st, unsigned(kb) * 1024u};
+        }
+        return b;
+    }();
+    return c;
+}
+
+template <typename T> SplitGeom split_bulk_geom(uint64_t m, uint64_t n, int* tc) {
+    SplitGeom g;
+    const BulkCfg bc = bulk_cfg();
+    const uint64_t mv = m / Vec<T>::N;
+    uint64_t rl = 1;
+    while (rl < mv) rl *= 2;
+    g.row_lanes = int(rl);
+    g.col_lanes = kBulkConsumers / g.row_lanes;
+    g.rpt = 1;
+    // columns per stage, a multiple of 16/s so the x slice is a whole number of
+    // 16-byte bulk units (m*s <= 16 KB for m < 2048, so tc >= 2 fp64 / 4 fp32)
+    const int xq = int(16 / sizeof(T));
+    *tc = int(bc.stage_bytes / (m * sizeof(T))) / xq * xq;
+    if (*tc < xq) *tc = xq;
+    const uint64_t tiles = (n + *tc - 1) / *tc;
+    const uint64_t cap = uint64_t(sm_count());
+    g.grid = unsigned(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
+    g.smem = bulk_smem(bc.stages, bc.stage_bytes);
+    return g;
+}
+
+template <typename T, int NS, unsigned SB>
+void bulk_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const SplitGeom& g, int tc,
+             T* partials, unsigned* ticket, cudaStream_t s) {
+    static bool configured = [] {
+        cudaFuncSetAttribute(gemv_cm_split_bulk_kernel<T, NS, SB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(bulk_smem(NS, SB)));
+        return true;
+    }();
+    (void)configured;
+    gemv_cm_split_bulk_kernel<T, NS, SB><<<g.grid, kBulkThreads, bulk_smem(NS, SB), s>>>(
+        A, x, c, m, n, g.row_lanes, tc, partials, ticket);
+}
+
+inline int split_mode() {
+    static const int v = [] {
+        const char* e = getenv("CABL_CM_SPLIT");
+        return e ? atoi(e) : 1;
+    }();
+    return v; // 1 = bulk-copy pipeline, 0 = register loads
+}
+
 template <typename T> bool tall_vec_ok(const T* A, const T* c, uint64_t m) {
     return aligned32(A) && aligned32(c) && m % Vec<T>::N == 0;
 }
@@ -366,7 +544,10 @@ template <typename T> WorkspaceNeed gemv_cm_need(const T* A, const T*, uint64_t 
         w.counters = 1; // unit counter of the tall kernel
         return w;
     }
-    const SplitGeom g = split_vec_ok(A, m) ? split_vec_geom<T>(m, n) : split_geom<T>(m, n);
+    int tc = 1;
+    const SplitGeom g = !split_vec_ok(A, m) ? split_geom<T>(m, n)
+                        : split_mode() == 1 ? split_bulk_geom<T>(m, n, &tc)
+                                            : split_vec_geom<T>(m, n);
     w.counters = 1;
     w.scratch_bytes = size_t(g.grid) * m * sizeof(T);
     return w;
@@ -403,6 +584,18 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         const unsigned grid = unsigned((warps * kWarp + kCmBlock - 1) / kCmBlock);
         gemv_cm_rows_kernel<T><<<grid, kCmBlock, 0, s>>>(A, x, c, m, n, warps);
         if (info) info->ctas = grid;
+    } else if (split_vec_ok(A, m) && split_mode() == 1) {
+        int tc = 1;
+        const SplitGeom g = split_bulk_geom<T>(m, n, &tc);
+        const BulkCfg bc = bulk_cfg();
+        T* partials = static_cast<T*>(ws.scratch);
+        if (bc.stages == 6 && bc.stage_bytes == 32768)
+            bulk_go<T, 6, 32768>(A, x, c, m, n, g, tc, partials, ws.counters, s);
+        else if (bc.stages == 4 && bc.stage_bytes == 49152)
+            bulk_go<T, 4, 49152>(A, x, c, m, n, g, tc, partials, ws.counters, s);
+        else
+            bulk_go<T, 3, 65536>(A, x, c, m, n, g, tc, partials, ws.counters, s);
+        if (info) info->ctas = g.grid;
     } else if (split_vec_ok(A, m)) {
         const SplitGeom g = split_vec_geom<T>(m, n);
         gemv_cm_split_vec_kernel<T><<<g.grid, kSplitBlock, 0, s>>>(
