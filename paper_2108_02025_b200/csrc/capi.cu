@@ -66,7 +66,7 @@ struct WsKey {
 
 struct WsEntry {
     Workspace ws;
-    std::mutex mu; // serialises growth; launches on one stream are ordered anyway
+    std::mutex mu; // held from scratch sizing to kernel enqueue (WsLease)
 };
 
 std::mutex g_ws_mu;
@@ -75,9 +75,18 @@ std::map<WsKey, WsEntry*>& ws_map() {
     return *m;
 }
 
-int get_workspace(int device, cudaStream_t s, const WorkspaceNeed& need, Workspace* out) {
+// A lease holds the (device, stream) entry's lock from before the scratch is
+// (re)sized until after the kernel that uses it is enqueued, so a concurrent
+// caller on the same stream cannot free (stream-ordered) a buffer that an
+// earlier-acquired, not-yet-enqueued launch is about to use.
+struct WsLease {
+    std::unique_lock<std::mutex> lock;
+    Workspace ws;
+};
+
+int get_workspace(int device, cudaStream_t s, const WorkspaceNeed& need, WsLease* out) {
     if (need.counters == 0 && need.scratch_bytes == 0) {
-        *out = Workspace{};
+        out->ws = Workspace{};
         return CABL_OK;
     }
     WsKey key{device, s, s == cudaStreamPerThread ? std::this_thread::get_id() : std::thread::id()};
@@ -89,7 +98,7 @@ int get_workspace(int device, cudaStream_t s, const WorkspaceNeed& need, Workspa
         if (it == m.end()) it = m.emplace(key, new WsEntry()).first;
         ent = it->second;
     }
-    std::lock_guard<std::mutex> lk(ent->mu);
+    out->lock = std::unique_lock<std::mutex>(ent->mu);
     Workspace& ws = ent->ws;
     if (need.counters > ws.n_counters) {
         size_t cnt = need.counters < 1024 ? 1024 : need.counters * 2;
@@ -108,7 +117,7 @@ int get_workspace(int device, cudaStream_t s, const WorkspaceNeed& need, Workspa
         ws.scratch = p;
         ws.scratch_bytes = bytes;
     }
-    *out = ws;
+    out->ws = ws;
     return CABL_OK;
 }
 
@@ -135,10 +144,10 @@ int dot_impl(const T* x, const T* y, uint64_t n, T alpha0, T* out, uint64_t cuto
     if (int rc = current_device(&dev)) return rc;
     const bool small = n <= cutoff; // reference kernels.hpp:140
     cudaStream_t s = as_stream(stream);
-    Workspace ws;
-    if (int rc = get_workspace(dev, s, dot_need<T>(n, small), &ws)) return rc;
+    WsLease lease;
+    if (int rc = get_workspace(dev, s, dot_need<T>(n, small), &lease)) return rc;
     LaunchInfo info;
-    CABL_TRY_CUDA(dot_launch<T>(x, y, n, alpha0, out, small, ws, s, &info), "dot kernel");
+    CABL_TRY_CUDA(dot_launch<T>(x, y, n, alpha0, out, small, lease.ws, s, &info), "dot kernel");
     set_probe(probe, small ? CABL_VARIANT_DOT_SMALL : CABL_VARIANT_DOT_BLOCKED, info.ctas);
     return CABL_OK;
 }
@@ -171,13 +180,13 @@ int gemv_impl(const T* A, int layout, uint64_t m, uint64_t n, const T* x, T* c,
     if (touched <= cutoff) {
         CABL_TRY_CUDA(gemv_ordered_launch<T>(A, layout, m, n, x, c, s, &info), "gemv kernel");
     } else if (layout == CABL_ROW_MAJOR) {
-        Workspace ws;
-        if (int rc = get_workspace(dev, s, gemv_rm_need<T>(A, x, m, n), &ws)) return rc;
-        CABL_TRY_CUDA(gemv_rm_launch<T>(A, m, n, x, c, ws, s, &info), "gemv_rm kernel");
+        WsLease lease;
+        if (int rc = get_workspace(dev, s, gemv_rm_need<T>(A, x, m, n), &lease)) return rc;
+        CABL_TRY_CUDA(gemv_rm_launch<T>(A, m, n, x, c, lease.ws, s, &info), "gemv_rm kernel");
     } else {
-        Workspace ws;
-        if (int rc = get_workspace(dev, s, gemv_cm_need<T>(A, x, m, n), &ws)) return rc;
-        CABL_TRY_CUDA(gemv_cm_launch<T>(A, m, n, x, c, ws, s, &info), "gemv_cm kernel");
+        WsLease lease;
+        if (int rc = get_workspace(dev, s, gemv_cm_need<T>(A, x, m, n), &lease)) return rc;
+        CABL_TRY_CUDA(gemv_cm_launch<T>(A, m, n, x, c, lease.ws, s, &info), "gemv_cm kernel");
     }
     set_probe(probe, variant, info.ctas);
     return CABL_OK;
@@ -198,12 +207,12 @@ int ger_impl(const T* x, const T* y, T* C, int layout, uint64_t m, uint64_t n, u
     const bool small = touched <= cutoff;
     LaunchInfo info;
     cudaStream_t s = as_stream(stream);
-    Workspace ws;
-    if (int rc = get_workspace(dev, s, ger_need<T>(x, y, m, n), &ws)) return rc;
+    WsLease lease;
+    if (int rc = get_workspace(dev, s, ger_need<T>(x, y, m, n), &lease)) return rc;
     if (layout == CABL_ROW_MAJOR)
-        CABL_TRY_CUDA(ger_launch<T>(x, y, C, m, n, small, ws, s, &info), "ger kernel");
+        CABL_TRY_CUDA(ger_launch<T>(x, y, C, m, n, small, lease.ws, s, &info), "ger kernel");
     else
-        CABL_TRY_CUDA(ger_launch<T>(y, x, C, n, m, small, ws, s, &info), "ger kernel");
+        CABL_TRY_CUDA(ger_launch<T>(y, x, C, n, m, small, lease.ws, s, &info), "ger kernel");
     set_probe(probe, CABL_VARIANT_GER, info.ctas);
     return CABL_OK;
 }

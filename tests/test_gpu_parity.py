@@ -347,3 +347,49 @@ def test_gemv_65536_square_fp32_sampled_rows(cuda):
     err = (c.double() - ref).abs()
     bound = (T.gemv_rm_chain(n, np.float32) + 4) * T.EPS[np.dtype(np.float32)] * (absA + c0.double().abs())
     assert bool((err <= bound).all())
+
+
+def test_concurrent_host_threads_share_a_stream_safely(cuda):
+    """Several host threads issue calls on the same (legacy default) stream
+    while the per-stream scratch keeps growing (DOT partials, split-GEMV
+    partials): results must equal the single-threaded ones bitwise.  Guards
+    the scratch lease in csrc/capi.cu."""
+    import threading
+    import paper_2108_02025_b200 as cb
+    pol = policy()
+    jobs = []
+    for i, n in enumerate([10_000, 1 << 20, 3 << 20, 1 << 22]):
+        x, y = dev_uniform(n, torch.float32, 1 + i, cuda), dev_uniform(n, torch.float32, 7 + i, cuda)
+        jobs.append(("dot", x, y))
+    for i, (m, k) in enumerate([(256, 1 << 16), (128, 1 << 18), (1024, 1 << 15)]):
+        A = cb.DenseMatrix.wrap(dev_uniform(m * k, torch.float64, 3 + i, cuda), m, k, cb.Layout.ColMajor)
+        jobs.append(("gemv", A, dev_uniform(k, torch.float64, 1, cuda), dev_uniform(m, torch.float64, 4, cuda)))
+
+    def run(job):
+        if job[0] == "dot":
+            return cb.dot(job[1], job[2], 0.5, pol)
+        c = job[3].clone()
+        cb.gemv_col_major(job[1], job[2], c, pol)
+        torch.cuda.synchronize()
+        return c.cpu()
+
+    want = [run(j) for j in jobs]
+    errors = []
+
+    def worker(seed):
+        order = list(range(len(jobs)))
+        rng = np.random.default_rng(seed)
+        for _ in range(20):
+            rng.shuffle(order)
+            for k in order:
+                got = run(jobs[k])
+                same = got == want[k] if jobs[k][0] == "dot" else torch.equal(got, want[k])
+                if not same:
+                    errors.append((seed, k))
+
+    threads = [threading.Thread(target=worker, args=(s,)) for s in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors[:5]
