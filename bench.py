@@ -14,9 +14,13 @@ owns its own 8192-row block of an (8192 N) x 8192 matrix with x replicated
 (weak scaling; row blocks need no collective).
 
 * ``value``     whole-job GB/s = algorithmic bytes of all ranks x K / the
-                max over ranks of the summed per-step CUDA-event time, inputs
-                resident in HBM, L2 flushed between steps (512 MiB write,
-                outside the events).
+                max over ranks of the device time of the K steps, inputs
+                resident in HBM.  L2 policy (``--l2``, reported in config.l2):
+                a step whose inputs exceed 2x the 126 MB L2 (G1: 268 MB) runs
+                back to back under one event pair — ncu shows every launch
+                still reads its full algorithmic bytes from DRAM; smaller
+                steps are timed one by one with the L2 flushed in between
+                (512 MiB write + 512 MiB read, outside the events).
 * ``e2e``       the same metric through the public host-buffer API
                 (cabl_host_gemv_f32 via cabl.gemv_row_major on pinned CPU
                 tensors): H2D of A, x, c + kernel + D2H of c every step.
@@ -209,7 +213,7 @@ def step_fn(w, ins, policy, ctx, sharded_dot: bool):
             import torch
             gathered = torch.empty(ctx.world, dtype=w.dtype, device=ctx.dev)
             return (lambda: shard.sharded_dot(ins["x"], ins["y"], 0.0, ins["out"], policy,
-                                              gathered=gathered)), 3
+                                              gathered=gathered)), 2  # dot + combine (+ NCCL all-gather)
         return (lambda: cb.dot_into(ins["x"], ins["y"], 0.0, ins["out"], policy)), 1
     if w.op == "gemv-row":
         return (lambda: cb.gemv_row_major(ins["A"], ins["x"], ins["c"], policy)), 1
@@ -218,14 +222,47 @@ def step_fn(w, ins, policy, ctx, sharded_dot: bool):
     return (lambda: cb.ger(ins["x"], ins["y"], ins["C"], policy)), 1
 
 
-def time_steps(fn, steps, warmup, ctx, flush, sampler=None):
-    """Per-step CUDA-event times (ms) on the launching stream, L2 flushed
-    between steps outside the events; barrier + synchronize on both sides."""
+L2_BYTES = 126 * 1000 * 1000  # B200 L2 (torch reports 126 MB)
+
+
+def l2_mode(step_bytes: int) -> str:
+    """'stream' when a step's inputs exceed 2x the L2 (a front-to-back sweep
+    of them leaves nothing of the next step's head in L2 — checked with ncu:
+    back-to-back G1 launches each read 268.5 MB from DRAM = the algorithmic
+    bytes, profiles/r01_ncu_b2b_G1.csv); 'flush' otherwise."""
+    return "stream" if step_bytes >= 2 * L2_BYTES else "flush"
+
+
+def time_steps(fn, steps, warmup, ctx, flush, sampler=None, mode="flush"):
+    """Per-step device times (ms) on the launching stream, barrier + synchronize
+    on both sides of the timed region.
+    mode 'flush':  L2 flushed between steps outside per-step CUDA events.
+    mode 'stream': inputs > 2x L2 — steps back to back, one event pair around
+                   all K steps (per-step time = total / K)."""
     import torch
     for _ in range(warmup):
-        flush.zero_()
+        if mode == "flush":
+            flush.zero_()
         fn()
     torch.cuda.synchronize()
+    if mode == "stream":
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx.barrier()
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.__enter__()
+        t0 = time.perf_counter()
+        a.record()
+        for _ in range(steps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        if sampler:
+            sampler.__exit__()
+        ctx.barrier()
+        per = a.elapsed_time(b) / steps
+        return [per] * steps, wall
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     ctx.barrier()
@@ -329,7 +366,8 @@ def run_ours(args, ctx):
     ins = make_inputs(w, rows, ctx.dev)
     fn, launches_per_step = step_fn(w, ins, policy, ctx, sharded_dot=False)
     sampler = ClockSampler(ctx.local)
-    times, wall = time_steps(fn, args.steps, args.warmup, ctx, flush, sampler)
+    mode = args.l2 if args.l2 != "auto" else l2_mode(w.alg_bytes(1))
+    times, wall = time_steps(fn, args.steps, args.warmup, ctx, flush, sampler, mode=mode)
     t_rank = sum(times) / 1000.0
     t_max = ctx.max(t_rank)
     bytes_rank = w.alg_bytes(1)
@@ -382,7 +420,11 @@ def run_ours(args, ctx):
             "workload": f"{w.id}: {w.desc}",
             "m_per_gpu": w.m, "n": w.n, "layout": "row-major",
             "parallelism": f"row blocks over {ctx.world} GPU(s), x replicated, no collective",
-            "l2": "flushed between steps outside the timed events: 512 MiB write, then 512 MiB read (no dirty lines left in L2)",
+            "l2": ("inputs larger than L2: 268 MB per step vs 126 MB L2, steps back to back "
+                   "(one event pair around the K steps); ncu shows each launch reads the full "
+                   "algorithmic bytes from DRAM" if mode == "stream" else
+                   "flushed between steps outside the timed events: 512 MiB write, then 512 MiB "
+                   "read (no dirty lines left in L2)"),
             "alg_bytes_per_step_per_gpu": bytes_rank,
         },
         "roofline": {
@@ -505,16 +547,23 @@ def run_suite(args, ctx, flush, policy, peak):
                 import dataclasses
                 wl = dataclasses.replace(w, m=e - b)
             fn, lps = step_fn(wl, ins, policy, ctx, sharded_dot=True)
-            times, _ = time_steps(fn, steps, args.warmup, ctx, flush)
-            t_max = ctx.max(sum(times) / 1000.0)
             alg = w.alg_bytes(ctx.world)
+            mode = l2_mode(wl.alg_bytes(1))
+            times, _ = time_steps(fn, steps, args.warmup, ctx, flush, mode=mode)
+            t_max = ctx.max(sum(times) / 1000.0)
             gbs = alg * steps / t_max / 1e9
-            out[wid] = {"desc": w.desc, "gbs": round(gbs, 2),
-                        "frac_of_peak": round(gbs / (peak * ctx.world), 4),
-                        "us_per_step": round(t_max / steps * 1e6, 3),
-                        "gflops": round(w.flops() * steps / t_max / 1e9, 2),
-                        "alg_bytes": alg, "launches_per_step": lps,
-                        "scaling": "strong" if ctx.world > 1 else None}
+            entry = {"desc": w.desc, "gbs": round(gbs, 2),
+                     "frac_of_peak": round(gbs / (peak * ctx.world), 4),
+                     "us_per_step": round(t_max / steps * 1e6, 3),
+                     "gflops": round(w.flops() * steps / t_max / 1e9, 2),
+                     "alg_bytes": alg, "launches_per_step": lps, "l2": mode,
+                     "scaling": "strong" if ctx.world > 1 else None}
+            if mode == "stream":  # also the conservative flushed number
+                tf, _ = time_steps(fn, steps, args.warmup, ctx, flush, mode="flush")
+                tfm = ctx.max(sum(tf) / 1000.0)
+                entry["flushed_us_per_step"] = round(tfm / steps * 1e6, 3)
+                entry["flushed_gbs"] = round(alg * steps / tfm / 1e9, 2)
+            out[wid] = entry
             del ins
         except torch.cuda.OutOfMemoryError as ex:
             out[wid] = {"error": f"OOM: {ex}"}
@@ -608,6 +657,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--suite-steps", type=int, default=30)
+    ap.add_argument("--l2", choices=["auto", "flush", "stream"], default="auto",
+                    help="headline L2 policy: auto = back to back when a step's inputs "
+                         "exceed 2x L2, else flush between steps")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("bench.py: --warmup must be >= 3", file=sys.stderr)

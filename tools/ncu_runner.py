@@ -27,6 +27,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="G1")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--no-flush", action="store_true",
+                    help="back-to-back launches (for DRAM-traffic checks without a flush)")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
@@ -37,7 +39,8 @@ def main():
     fn, _ = bench.step_fn(w, ins, cb.default_policy(1), ctx, sharded_dot=False)
     flush = bench.L2Flush(dev)
     for _ in range(args.reps):
-        flush.zero_()
+        if not args.no_flush:
+            flush.zero_()
         fn()
     torch.cuda.synchronize()
     print(f"ran {args.reps} x {w.id}")
