@@ -104,6 +104,81 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     }
 }
 
+// CHUNKED DOT for large n (2ns >= 512 MiB, e.g. D2 = 2^32): the vector range
+// is cut into chunks of kChunkVecs 32-byte vectors; CTAs take chunks from an
+// atomic queue (common.cuh dyn_next), so SMs that get faster memory service
+// take more chunks.  A chunk's partial is a fixed function of its data (fixed
+// thread mapping inside the chunk, fixed trees) and goes to partials[chunk];
+// the last CTA to finish sums the partials in chunk order, adds the < V
+// trailing elements, then alpha0.  The result depends on n only — not on
+// the grid, the scheduling, or the GPU's SM count — and every rounding chain
+// is short (<= kChunkVecs/(BLOCK*U) vectors per accumulator).
+constexpr uint64_t kChunkVecs = 65536; // 2 MiB of x and 2 MiB of y (fp32)
+
+template <typename T, int BLOCK, int U, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
+    dot_chunk_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t n, T alpha0,
+                     T* __restrict__ out, T* __restrict__ partials,
+                     unsigned* __restrict__ counters) {
+    __shared__ T red[32];
+    __shared__ unsigned long long next_sh;
+    __shared__ bool am_last;
+    constexpr int V = Vec<T>::N;
+    const int tid = threadIdx.x;
+    const uint64_t nvec = n / V;
+    const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
+    const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
+    const Vec<T>* Y = reinterpret_cast<const Vec<T>*>(y);
+
+    uint64_t ch = blockIdx.x; // first chunk static, the rest from the queue
+    while (ch < nchunks) {
+        if (tid == 0) next_sh = dyn_next(counters, nchunks); // prefetch
+        T acc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] = T(0);
+        const uint64_t c0 = ch * kChunkVecs;
+        const uint64_t c1 = (c0 + kChunkVecs < nvec) ? c0 + kChunkVecs : nvec;
+        for (uint64_t base = c0; base < c1; base += uint64_t(BLOCK) * U) {
+            Vec<T> xv[U], yv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t i = base + uint64_t(u) * BLOCK + tid;
+                if (i < c1) {
+                    xv[u] = ld_stream(X + i);
+                    yv[u] = ld_stream(Y + i);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < V; ++k) xv[u].v[k] = yv[u].v[k] = T(0);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u] = dot_vec(xv[u], yv[u], acc[u]);
+        }
+        T v = acc[0];
+#pragma unroll
+        for (int u = 1; u < U; ++u) v = add_rn(v, acc[u]);
+        const T chunk_total = block_sum(v, red); // its barriers publish next_sh
+        if (tid == 0) partials[ch] = chunk_total;
+        ch = next_sh;
+        __syncthreads(); // next_sh is rewritten at the top of the next chunk
+    }
+    if (tid == 0) {
+        __threadfence();
+        am_last = atomicAdd(counters + 1, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    T v = T(0);
+    for (uint64_t i = tid; i < nchunks; i += BLOCK) v = add_rn(v, ld_cg(partials + i));
+    T total = block_sum(v, red);
+    if (tid == 0) {
+        for (uint64_t i = nvec * V; i < n; ++i) total = fma_rn(x[i], y[i], total);
+        *out = add_rn(total, alpha0);
+        counters[1] = 0u;
+    }
+}
+
 template <typename T>
 __global__ void combine_kernel(const T* __restrict__ p, uint32_t count, T alpha0,
                                T* __restrict__ out) {
@@ -168,20 +243,43 @@ cudaError_t dot_dispatch(unsigned grid, const T* x, const T* y, uint64_t n, int 
 
 } // namespace
 
+// large operands (2ns >= 512 MiB) take the chunked, queue-scheduled kernel
+inline bool dot_chunked(uint64_t n, size_t s, bool small, bool vec_ok) {
+    static const int forced = [] {
+        const char* e = getenv("CABL_DOT_CHUNKED");
+        return e ? atoi(e) : -1;
+    }();
+    if (small || !vec_ok) return false;
+    if (n / (32 / s) < uint64_t(sm_count()) * kDotCtasPerSm) return false; // grid <= chunks
+    if (forced >= 0) return forced != 0;
+    return 2 * n * s >= (uint64_t(512) << 20);
+}
+
 template <typename T> WorkspaceNeed dot_need(uint64_t n, bool small) {
     WorkspaceNeed w;
-    w.counters = 1;
-    w.scratch_bytes = size_t(dot_grid<T>(n, small)) * sizeof(T);
+    w.counters = 2;
+    const uint64_t chunks = (n / Vec<T>::N + kChunkVecs - 1) / kChunkVecs;
+    const uint64_t g = dot_grid<T>(n, small);
+    w.scratch_bytes = size_t(chunks > g ? chunks : g) * sizeof(T);
     return w;
 }
 
 template <typename T>
 cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, bool small,
                        const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
-    const unsigned grid = dot_grid<T>(n, small);
     const int vec_ok = aligned32(x) && aligned32(y);
+    if (dot_chunked(n, sizeof(T), small, vec_ok)) {
+        const uint64_t chunks = (n / Vec<T>::N + kChunkVecs - 1) / kChunkVecs;
+        const uint64_t cap = uint64_t(sm_count()) * kDotCtasPerSm;
+        const unsigned grid = unsigned(chunks < cap ? chunks : cap);
+        dot_chunk_kernel<T, kDotBlock, kDotUnroll, kDotCtasPerSm><<<grid, kDotBlock, 0, s>>>(
+            x, y, n, alpha0, out, static_cast<T*>(ws.scratch), ws.counters);
+        if (info) info->ctas = grid;
+        return cudaGetLastError();
+    }
+    const unsigned grid = dot_grid<T>(n, small);
     const cudaError_t e = dot_dispatch<T>(grid, x, y, n, vec_ok, alpha0, out,
-                                          static_cast<T*>(ws.scratch), ws.counters, s);
+                                          static_cast<T*>(ws.scratch), ws.counters + 1, s);
     if (info) info->ctas = grid;
     return e;
 }

@@ -393,3 +393,21 @@ def test_concurrent_host_threads_share_a_stream_safely(cuda):
     for t in threads:
         t.join()
     assert not errors, errors[:5]
+
+
+@pytest.mark.slow
+def test_dot_chunked_large_n(cuda):
+    """2ns >= 512 MiB takes the chunked, queue-scheduled DOT (csrc/dot.cu):
+    n = 2^28 + 3 fp32 (1 GiB per operand, 513 chunks, 3 trailing elements)."""
+    import paper_2108_02025_b200 as cb
+    n = (1 << 28) + 3
+    x, y = dev_uniform(n, torch.float32, 1, cuda), dev_uniform(n, torch.float32, 2, cuda)
+    pol = plan_for(torch.float32)
+    got = cb.dot(x, y, 0.25, pol)
+    assert cb.last_exec().variant == cb.KernelVariant.dot_blocked
+    again = [cb.dot(x, y, 0.25, pol) for _ in range(5)]
+    assert all(a == got for a in again)
+    xn, yn = np_of(x), np_of(y)
+    truth, sumabs = O.dot_truth(xn, yn, 0.25)
+    assert abs(got - float(O.dot_ref(xn, yn, 0.25))) <= T.contract_tol(n, sumabs, 0.25, np.float32)
+    assert abs(got - truth) <= T.truth_tol(T.dot_chain(n, np.float32), sumabs, 0.25, np.float32)
