@@ -6,9 +6,9 @@
 //     CTAs stride over tiles of BLOCK*U 32-byte vectors, every thread keeps
 //     2*U 256-bit loads in flight and accumulates with FMA in registers;
 //   * fixed butterfly warp sums, fixed-order CTA sum -> partials[cta];
-//   * the last CTA to arrive (atomic ticket) sums the partials in a fixed
-//     order, adds alpha0 LAST (as the reference does, kernels.hpp:142,163)
-//     and resets the ticket for the next launch on this stream.  (A variant
+//   * the last CTA to arrive (an acq_rel atomic ticket — no separate fence)
+//     sums the partials in a fixed order, adds alpha0 LAST (as the reference
+//     does, kernels.hpp:142,163) and resets the ticket for the next launch.  (A variant
 //     where CTA 0 acquire-polls per-CTA release flags measured 0-2 us slower
 //     on B200 and was dropped.)
 // The element -> thread mapping depends only on n and the grid, so the result
@@ -88,13 +88,17 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     }
     if (tid == 0) {
         partials[blockIdx.x] = cta_total;
-        __threadfence();
-        const unsigned t = atomicAdd(ticket, 1u);
+        // release: the partial is visible before the ticket moves; acquire:
+        // the last arriver sees every partial (one fence-free RMW)
+        unsigned t;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                     : "=r"(t)
+                     : "l"(ticket)
+                     : "memory");
         am_last = (t == gridDim.x - 1);
     }
     __syncthreads();
     if (!am_last) return;
-    __threadfence();
     T v = T(0);
     for (unsigned i = tid; i < gridDim.x; i += BLOCK) v = add_rn(v, ld_cg(partials + i));
     const T total = block_sum(v, red);
