@@ -90,6 +90,15 @@ def traffic_for(kernel_key: str):
     return e.get("dram_bytes_per_launch"), e.get("source")
 
 
+def traffic_kernel(cfg: str):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    e = json.loads(p.read_text()).get(cfg) or {}
+    k = e.get("kernel")
+    return k.split("::")[-1] if k else None
+
+
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
     """Samples SM clock and throttle reasons through NVML while running."""
@@ -431,7 +440,7 @@ def run_ours(args, ctx):
             "bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "peak_source": peak_src,
             "traffic": traffic, "traffic_source": traffic_src,
-            "kernel": "gemv_rm_vec_kernel" if w.op == "gemv-row" else w.op,
+            "kernel": traffic_kernel(w.id) or w.op,
             "mean_launch_us": round(mean_launch_s * 1e6, 3),
         },
         "e2e": e2e,

@@ -1,16 +1,15 @@
-# Round evidence: full GPU tests, bench (plain + torchrun world 1), ncu launch list, ncu full captures
+# Round evidence: full GPU tests, smoke, bench, reference arm, ncu launch list + full captures
 mkdir -p gpurun_out
-nvidia-smi > gpurun_out/nvsmi.txt 2>&1
-timeout 1200 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out/bench_torchrun1.json 2> gpurun_out/bench_torchrun1.err; echo "rc=$?" >> gpurun_out/bench_torchrun1.err
-timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 600 python bench.py --impl reference --steps 20 --warmup 2 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 CMD="python bench.py --steps 20 --warmup 3 --no-suite --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain_launches.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
-for cfg in "G1 gemv_rm_sweep" "D1 dot_kernel" "R1 ger_vec" "G2 gemv_cm_tall" "G3 gemv_cm_split"; do
+python tools/ncu_runner.py --config G1 --reps 6 --no-flush > gpurun_out/plain_b2b.log 2>&1 && timeout 600 ncu --cache-control none --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:gemv_rm -c 6 --csv --log-file gpurun_out/ncu_b2b_G1.csv python tools/ncu_runner.py --config G1 --reps 6 --no-flush > gpurun_out/ncu_b2b.log 2>&1
+for cfg in "G1 gemv_rm_sweep" "D1 dot_kernel" "R1 ger_tile" "G2 gemv_cm_tall" "G3 gemv_cm_split" "D2 dot_chunk" "G4 gemv_rm_sweep"; do
   set -- $cfg
   python tools/ncu_runner.py --config $1 --reps 2 > gpurun_out/plain_$1.log 2>&1 && \
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$2 -s 1 -c 1 -o gpurun_out/prof_$1 -f python tools/ncu_runner.py --config $1 --reps 2 > gpurun_out/ncu_$1.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$2 -s 1 -c 1 -o gpurun_out/prof_$1 -f python tools/ncu_runner.py --config $1 --reps 2 > gpurun_out/ncu_$1.log 2>&1
   echo "$1 ncu rc=$?"
 done

@@ -116,9 +116,11 @@ def main():
         out = [f"# launch list, round {a.round}", "",
                "`ncu --metrics gpu__time_duration.sum --clock-control none -c 400` of "
                "`python bench.py --steps 20 --warmup 3 --no-suite --no-e2e --no-cpu-baseline` "
-               "(cold-cache, serialised: compare shares, not absolutes).  The at:: kernels are "
-               "input filling and the L2 flush between steps (write + read of 512 MiB), outside "
-               "the timed events.", "",
+               "(cold-cache, serialised: compare shares, not absolutes).  fill_* seed the inputs; "
+               "the at:: kernels are the L2 flush (write + read of 512 MiB) that bench.py runs "
+               "before timing / between flushed steps.  G1 steps run back to back (inputs 2.1x "
+               "the L2, see r01_ncu_b2b_G1.csv), so the step is one launch of the GEMV kernel.",
+               "",
                "| kernel | launches | mean us | share of all GPU time |", "|---|---|---|---|"]
         for k, v in agg.items():
             out.append(f"| `{k}` | {len(v)} | {sum(v) / len(v) / 1e3:.2f} | {sum(v) / total:.3f} |")
