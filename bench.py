@@ -16,11 +16,12 @@ owns its own 8192-row block of an (8192 N) x 8192 matrix with x replicated
 * ``value``     whole-job GB/s = algorithmic bytes of all ranks x K / the
                 max over ranks of the device time of the K steps, inputs
                 resident in HBM.  L2 policy (``--l2``, reported in config.l2):
-                a step whose inputs exceed 2x the 126 MB L2 (G1: 268 MB) runs
-                back to back under one event pair — ncu shows every launch
-                still reads its full algorithmic bytes from DRAM; smaller
-                steps are timed one by one with the L2 flushed in between
-                (512 MiB write + 512 MiB read, outside the events).
+                a step whose inputs exceed the 126 MB L2 (every BASELINE
+                config: D1 134 MB ... D2 34 GB) runs back to back under one
+                event pair — ncu shows every back-to-back launch still reads
+                its full algorithmic bytes from DRAM; steps that fit in L2
+                are timed one by one with the L2 flushed in between (512 MiB
+                write + 512 MiB read, outside the events).
 * ``e2e``       the same metric through the public host-buffer API
                 (cabl_host_gemv_f32 via cabl.gemv_row_major on pinned CPU
                 tensors): H2D of A, x, c + kernel + D2H of c every step.
@@ -235,11 +236,13 @@ L2_BYTES = 126 * 1000 * 1000  # B200 L2 (torch reports 126 MB)
 
 
 def l2_mode(step_bytes: int) -> str:
-    """'stream' when a step's inputs exceed 2x the L2 (a front-to-back sweep
-    of them leaves nothing of the next step's head in L2 — checked with ncu:
-    back-to-back G1 launches each read 268.5 MB from DRAM = the algorithmic
-    bytes, profiles/r01_ncu_b2b_G1.csv); 'flush' otherwise."""
-    return "stream" if step_bytes >= 2 * L2_BYTES else "flush"
+    """'stream' when a step's inputs exceed the L2: the front-to-back sweep of
+    step k+1 misses on everything step k left behind.  Checked with ncu
+    (--cache-control none) on back-to-back launches of the two smallest
+    configs: every D1 launch (134.2 MB alg.) reads 133.95 MB from DRAM and
+    every G1 launch (268.5 MB) 268.5 MB (profiles/r01_ncu_b2b_{D1,G1}.csv).
+    'flush' otherwise (inputs that fit in L2)."""
+    return "stream" if step_bytes > L2_BYTES else "flush"
 
 
 def time_steps(fn, steps, warmup, ctx, flush, sampler=None, mode="flush"):
@@ -429,9 +432,10 @@ def run_ours(args, ctx):
             "workload": f"{w.id}: {w.desc}",
             "m_per_gpu": w.m, "n": w.n, "layout": "row-major",
             "parallelism": f"row blocks over {ctx.world} GPU(s), x replicated, no collective",
-            "l2": ("inputs larger than L2: 268 MB per step vs 126 MB L2, steps back to back "
-                   "(one event pair around the K steps); ncu shows each launch reads the full "
-                   "algorithmic bytes from DRAM" if mode == "stream" else
+            "l2": (f"inputs larger than L2: {bytes_rank / 1e6:.0f} MB per step vs 126 MB L2, "
+                   "steps back to back (one event pair around the K steps); ncu shows each "
+                   "back-to-back launch reads its full algorithmic bytes from DRAM "
+                   "(profiles/r01_ncu_b2b_*.csv)" if mode == "stream" else
                    "flushed between steps outside the timed events: 512 MiB write, then 512 MiB "
                    "read (no dirty lines left in L2)"),
             "alg_bytes_per_step_per_gpu": bytes_rank,

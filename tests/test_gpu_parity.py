@@ -411,3 +411,32 @@ def test_dot_chunked_large_n(cuda):
     truth, sumabs = O.dot_truth(xn, yn, 0.25)
     assert abs(got - float(O.dot_ref(xn, yn, 0.25))) <= T.contract_tol(n, sumabs, 0.25, np.float32)
     assert abs(got - truth) <= T.truth_tol(T.dot_chain(n, np.float32), sumabs, 0.25, np.float32)
+
+
+@pytest.mark.slow
+def test_dot_2pow32_baseline_config(cuda):
+    """BASELINE config 5 (D2): n = 2^32 fp32, 32 GiB of operands.  Size-
+    independent properties (exact power-of-two scaling, symmetry, run-to-run
+    bits) plus the non-vacuous truth bound against an fp64 torch reduction
+    computed chunk by chunk on the device (fp32 products are exact in fp64)."""
+    import paper_2108_02025_b200 as cb
+    n = 1 << 32
+    x = dev_uniform(n, torch.float32, 1, cuda)
+    y = dev_uniform(n, torch.float32, 2, cuda)
+    pol = plan_for(torch.float32)
+    got = cb.dot(x, y, 0.0, pol)
+    assert cb.dot(x, y, 0.0, pol) == got
+    assert cb.dot(y, x, 0.0, pol) == got          # fma(a,b,c) == fma(b,a,c)
+    x.mul_(2.0)                                    # exact: a power of two
+    assert cb.dot(x, y, 0.0, pol) == 2.0 * got
+    x.mul_(0.5)
+    truth = 0.0
+    sumabs = 0.0
+    step = 1 << 28
+    for b in range(0, n, step):
+        p = x[b:b + step].double() * y[b:b + step].double()
+        truth += float(p.sum())
+        sumabs += float(p.abs().sum())
+    eps = float(np.finfo(np.float32).eps)
+    # fp64 chunk sums carry ~1e-16 relative error: far below the fp32 bound
+    assert abs(got - truth) <= (T.dot_chain(n, np.float32) + 2) * eps * sumabs

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q --timeout 600 -p no:cacheprovider -k "dot and not chunked" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-for i in 1 2 3; do timeout 300 python tools/tune.py D1 >> gpurun_out/tune14.jsonl 2>&1; done
+python tools/ncu_runner.py --config D1 --reps 8 --no-flush > gpurun_out/plain_b2b_D1.log 2>&1 && timeout 600 ncu --cache-control none --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct -k regex:dot_kernel -c 8 --csv --log-file gpurun_out/ncu_b2b_D1.csv python tools/ncu_runner.py --config D1 --reps 8 --no-flush > gpurun_out/ncu_b2b_D1.log 2>&1
+timeout 300 python tools/b2b.py D1 R1 > gpurun_out/b2b2.jsonl 2>&1
