@@ -1,0 +1,97 @@
+"""GPU mode of the reference bench harness / CLI (paper_2108_02025_b200.benchcli),
+checked against the reference's own CLI contract (acceptance criterion 10,
+reference acceptance.cpp:533-580): exit status, one CSV record per
+(kernel, size, threads), CSV round trip, an SVG with one polyline per
+(kernel, threads)."""
+from __future__ import annotations
+
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+
+from paper_2108_02025_b200 import benchcli as B
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_parse_sizes_and_rects():
+    assert B.parse_sizes("256,1024,4096") == [256, 1024, 4096]
+    assert B.parse_sizes("256:1048576:4") == [256, 1024, 4096, 16384, 65536, 262144, 1048576]
+    with pytest.raises(ValueError):
+        B.parse_sizes("1:10")
+    with pytest.raises(ValueError):
+        B.parse_sizes("0:10:2")
+    assert B.parse_rects("256x1048576,8x9") == [(256, 1048576), (8, 9)]
+
+
+def test_csv_round_trip_and_svg():
+    recs = []
+    for k in B.KERNELS:
+        for size in (64, 256):
+            for t in (1, 2):
+                recs.append(B.BenchRecord(k, 0 if k == "dot" else size, size, t, 3,
+                                          1.0e-5 * size, 1.1e-5 * size, 3.14159265 * size,
+                                          -0.123456789e3, "f32", 1234.5678, 0.1885))
+    text = B.emit_csv(recs)
+    assert text.splitlines()[0] == B.CSV_HEADER + B.CSV_GPU_SUFFIX
+    back = B.parse_csv(text)
+    assert len(back) == 16
+    assert B.emit_csv(back) == text
+    # the reference's own 9-column CSV still parses
+    plain = B.CSV_HEADER + "\n" + "dot,0,64,1,3,1e-05,2e-05,3,4\n"
+    assert B.parse_csv(plain)[0].kernel == "dot"
+    svg = B.emit_svg(recs)
+    assert svg.startswith("<?xml") and svg.rstrip().endswith("</svg>")
+    assert svg.count("<polyline") == 8
+
+
+def test_descriptor_loading(tmp_path):
+    p = tmp_path / "m.json"
+    p.write_text('{"element_bytes": 8, "cores": 16, "levels": ['
+                 '{"line_bytes": 64, "associativity": 8, "num_sets": 64, "shared": false},'
+                 '{"line_bytes": 64, "associativity": 8, "num_sets": 1024, "shared": true}]}')
+    md = B.load_descriptor(str(p))
+    assert md.cores == 16 and md.levels[1].size_bytes() == 512 * 1024
+
+
+def test_cli_errors_exit_2():
+    r = subprocess.run([sys.executable, "-m", "paper_2108_02025_b200.benchcli", "--bounds"],
+                       capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert r.returncode == 2 and "out of scope" in r.stderr
+    if not torch.cuda.is_available():
+        r = subprocess.run([sys.executable, "-m", "paper_2108_02025_b200.benchcli", "--sizes", "64",
+                            "--reps", "3"], capture_output=True, text=True, cwd=ROOT, timeout=300)
+        assert r.returncode == 2 and "no CUDA device" in r.stderr
+
+
+@pytest.mark.gpu
+def test_cli_contract_criterion_10(cuda, tmp_path):
+    csv, svg = tmp_path / "sweep.csv", tmp_path / "sweep.svg"
+    r = subprocess.run([sys.executable, "-m", "paper_2108_02025_b200.benchcli", "--kernel", "all",
+                        "--sizes", "64,256", "--threads", "1,2", "--reps", "3", "--seed", "7",
+                        "--csv", str(csv), "--svg", str(svg)],
+                       capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert r.returncode == 0, r.stderr
+    text = csv.read_text()
+    recs = B.parse_csv(text)
+    assert len(recs) == 4 * 2 * 2
+    assert B.emit_csv(recs) == text
+    s = svg.read_text()
+    assert s.startswith("<?xml") and "</svg>" in s and s.count("<polyline") == 8
+    assert all(rec.gbs > 0 and rec.median_s > 0 for rec in recs)
+
+
+@pytest.mark.gpu
+def test_cli_fp32_rectangular_baseline_shapes(cuda, tmp_path):
+    csv = tmp_path / "rect.csv"
+    r = subprocess.run([sys.executable, "-m", "paper_2108_02025_b200.benchcli", "--kernel",
+                        "gemv-col", "--sizes", "4096", "--rect", "256x262144,262144x256",
+                        "--dtype", "f64", "--reps", "3", "--csv", str(csv)],
+                       capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert r.returncode == 0, r.stderr
+    recs = B.parse_csv(csv.read_text())
+    assert [(x.m, x.n) for x in recs] == [(4096, 4096), (256, 262144), (262144, 256)]
+    assert all(x.dtype == "f64" and x.roofline_frac > 0.2 for x in recs)
