@@ -143,29 +143,30 @@ __global__ void __launch_bounds__(kCmBlock, kCmRowsCtasPerSm)
     }
 }
 
-// Last CTA of a split launch: c[r] += sum over CTAs b (in order) of
-// partials[b][r].  Thread (r, q) sums CTAs q, q+Q, ... with 16 loads in
-// flight, then the Q sums per row are added in q order; `sm` holds >= Q*m.
+// Last CTA of a split launch over one row tile: c[r] += sum over the G column
+// parts b (in order) of partials[b*stride + r], r < rows.  Thread (r, q)
+// sums parts q, q+Q, ... with 16 loads in flight, then the Q sums per row
+// are added in q order; `sm` holds >= blockDim.x entries.
 template <typename T>
-__device__ void split_final(const T* __restrict__ partials, T* __restrict__ c, uint64_t m, T* sm) {
-    const unsigned G = gridDim.x;
+__device__ void split_final(const T* __restrict__ partials, T* __restrict__ c, uint64_t rows,
+                            uint64_t stride, unsigned G, T* sm) {
     int block = 32; // largest power of two <= blockDim.x
     while (block * 2 <= int(blockDim.x)) block *= 2;
     int rl = 32;
-    while (uint64_t(rl) < m && rl < block) rl *= 2;
+    while (uint64_t(rl) < rows && rl < block) rl *= 2;
     const int Q = block / rl;
     const int r0 = threadIdx.x % rl, q = threadIdx.x / rl;
     const bool part = int(threadIdx.x) < block;
-    for (uint64_t rb = 0; rb < m; rb += uint64_t(rl)) {
+    for (uint64_t rb = 0; rb < rows; rb += uint64_t(rl)) {
         const uint64_t r = rb + r0;
         T total = T(0);
-        if (part && r < m) {
+        if (part && r < rows) {
             for (unsigned b0 = q; b0 < G; b0 += 16u * Q) {
                 T v[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
                     const unsigned b = b0 + unsigned(e) * Q;
-                    v[e] = b < G ? ld_cg(partials + uint64_t(b) * m + r) : T(0);
+                    v[e] = b < G ? ld_cg(partials + uint64_t(b) * stride + r) : T(0);
                 }
 #pragma unroll
                 for (int e = 0; e < 16; ++e)
@@ -173,9 +174,9 @@ __device__ void split_final(const T* __restrict__ partials, T* __restrict__ c, u
             }
         }
         __syncthreads(); // sm reuse
-        if (part && r < m) sm[uint64_t(q) * rl + r0] = total;
+        if (part && r < rows) sm[uint64_t(q) * rl + r0] = total;
         __syncthreads();
-        if (part && q == 0 && r < m) {
+        if (part && q == 0 && r < rows) {
             T v = sm[r0];
             for (int k = 1; k < Q; ++k) v = add_rn(v, sm[uint64_t(k) * rl + r0]);
             c[r] = add_rn(c[r], v);
@@ -183,24 +184,30 @@ __device__ void split_final(const T* __restrict__ partials, T* __restrict__ c, u
     }
 }
 
-// Vectorised split kernel (m % V == 0, aligned): a thread owns one 32-byte
-// row vector (V rows) for its column lane; row_lanes = pow2 >= m/V, U = 4
-// 256-bit column loads in flight per thread.
+// Vectorised split kernel (m % V == 0, aligned), 2-D: blockIdx.y picks a row
+// tile of mt rows (column stride lda = m), blockIdx.x one of gridDim.x column
+// parts (column tiles in grid-stride order).  A thread owns one 32-byte row
+// vector (V rows) of the tile for its column lane; row_lanes = pow2 >= mt/V,
+// U = 4 256-bit column loads in flight per thread.  Partials per (row tile,
+// column part); the last part to finish a row tile (per-tile ticket) adds
+// them into c in part order.
 template <typename T>
 __global__ void __launch_bounds__(kSplitBlock, 1)
     gemv_cm_split_vec_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
-                             uint64_t m, uint64_t n, int row_lanes, T* __restrict__ partials,
-                             unsigned* __restrict__ ticket) {
+                             uint64_t m, uint64_t n, uint64_t mt, int row_lanes,
+                             T* __restrict__ partials, unsigned* __restrict__ tickets) {
     constexpr int V = Vec<T>::N;
     constexpr int U = 4;
-    __shared__ alignas(32) T sm[kSplitBlock * V]; // [col_lanes][m] <= 1024 * V entries
+    __shared__ alignas(32) T sm[kSplitBlock * V]; // [col_lanes][mt] <= 1024 * V entries
     __shared__ bool am_last;
     const int tid = threadIdx.x;
     const int col_lanes = kSplitBlock / row_lanes;
     const int rl = tid % row_lanes, cl = tid / row_lanes;
-    const uint64_t mv = m / V;
-    const bool live = uint64_t(rl) < mv;
-    const Vec<T>* Av = reinterpret_cast<const Vec<T>*>(A) + (live ? rl : 0);
+    const uint64_t r0 = uint64_t(blockIdx.y) * mt;
+    const uint64_t rows = (m - r0 < mt) ? m - r0 : mt;
+    const uint64_t mv = m / V, rows_v = rows / V;
+    const bool live = uint64_t(rl) < rows_v;
+    const Vec<T>* Av = reinterpret_cast<const Vec<T>*>(A) + r0 / V + (live ? rl : 0);
     const uint64_t tile = uint64_t(col_lanes) * U;
     const uint64_t tiles = (n + tile - 1) / tile;
 
@@ -228,21 +235,22 @@ __global__ void __launch_bounds__(kSplitBlock, 1)
     }
     if (live)
 #pragma unroll
-        for (int e = 0; e < V; ++e) sm[uint64_t(cl) * m + uint64_t(rl) * V + e] = acc.v[e];
+        for (int e = 0; e < V; ++e) sm[uint64_t(cl) * rows + uint64_t(rl) * V + e] = acc.v[e];
     __syncthreads();
-    for (uint64_t r = tid; r < m; r += kSplitBlock) {
+    T* tile_partials = partials + uint64_t(blockIdx.y) * gridDim.x * mt;
+    for (uint64_t r = tid; r < rows; r += kSplitBlock) {
         T v = sm[r];
-        for (int q = 1; q < col_lanes; ++q) v = add_rn(v, sm[uint64_t(q) * m + r]);
-        partials[uint64_t(blockIdx.x) * m + r] = v;
+        for (int q = 1; q < col_lanes; ++q) v = add_rn(v, sm[uint64_t(q) * rows + r]);
+        tile_partials[uint64_t(blockIdx.x) * mt + r] = v;
     }
     __threadfence();
     __syncthreads();
-    if (tid == 0) am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    if (tid == 0) am_last = atomicAdd(tickets + blockIdx.y, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!am_last) return;
     __threadfence();
-    split_final(partials, c, m, sm);
-    if (tid == 0) *ticket = 0u;
+    split_final(tile_partials, c + r0, rows, mt, gridDim.x, sm);
+    if (tid == 0) tickets[blockIdx.y] = 0u;
 }
 
 // Bulk-copy split kernel (m < kSplitMaxRows, m % V == 0, aligned).  The
@@ -355,28 +363,32 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     __syncthreads();
     if (!am_last) return;
     __threadfence();
-    split_final(partials, c, m, comb);
+    split_final(partials, c, m, m, gridDim.x, comb);
     if (tid == 0) *ticket = 0u;
 }
 
-// Split-columns kernel.  Thread layout: row_lanes x col_lanes = kSplitBlock,
-// row_lanes a power of two >= min(m, kSplitBlock); each thread accumulates
-// RPT rows (r = row_lane + k*row_lanes).  Column tiles of col_lanes*kSplitU
-// columns are visited in grid-stride order.
+// Scalar split kernel (any m, any alignment), 2-D like the vector one: row
+// tile blockIdx.y of mt rows, column part blockIdx.x.  Thread layout
+// row_lanes x col_lanes = kSplitBlock, row_lanes a power of two >=
+// min(mt, kSplitBlock); each thread accumulates RPT rows of the tile
+// (r = row_lane + k*row_lanes).
 template <typename T, int RPT>
 __global__ void __launch_bounds__(kSplitBlock, 1)
     gemv_cm_split_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
-                         uint64_t m, uint64_t n, int row_lanes, T* __restrict__ partials,
-                         unsigned* __restrict__ ticket) {
+                         uint64_t m, uint64_t n, uint64_t mt, int row_lanes,
+                         T* __restrict__ partials, unsigned* __restrict__ tickets) {
     extern __shared__ unsigned char smem_raw[];
-    T* sm = reinterpret_cast<T*>(smem_raw); // [col_lanes][m]
+    T* sm = reinterpret_cast<T*>(smem_raw); // [col_lanes][rows], >= kSplitBlock entries
     __shared__ bool am_last;
     const int tid = threadIdx.x;
     const int col_lanes = kSplitBlock / row_lanes;
     const int rl = tid % row_lanes, cl = tid / row_lanes;
     constexpr int kSplitU = split_u<T>();
+    const uint64_t r0 = uint64_t(blockIdx.y) * mt;
+    const uint64_t rows = (m - r0 < mt) ? m - r0 : mt;
     const uint64_t tile = uint64_t(col_lanes) * kSplitU;
     const uint64_t tiles = (n + tile - 1) / tile;
+    const T* At = A + r0;
 
     T acc[RPT];
 #pragma unroll
@@ -391,11 +403,11 @@ __global__ void __launch_bounds__(kSplitBlock, 1)
             const uint64_t j = j0 + uint64_t(u) * col_lanes;
             const bool ok = j < n;
             xv[u] = ok ? __ldg(x + j) : T(0);
-            const T* col = A + (ok ? j : 0) * m;
+            const T* col = At + (ok ? j : 0) * m;
 #pragma unroll
             for (int k = 0; k < RPT; ++k) {
                 const uint64_t r = uint64_t(rl) + uint64_t(k) * row_lanes;
-                av[u][k] = (ok && r < m) ? __ldcs(col + r) : T(0);
+                av[u][k] = (ok && r < rows) ? __ldcs(col + r) : T(0);
             }
         }
 #pragma unroll
@@ -404,49 +416,64 @@ __global__ void __launch_bounds__(kSplitBlock, 1)
             for (int k = 0; k < RPT; ++k) acc[k] = fma_rn(av[u][k], xv[u], acc[k]);
     }
 
-    // column lanes -> CTA partial, fixed order
+    // column lanes -> partial of this (row tile, column part), fixed order
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
         const uint64_t r = uint64_t(rl) + uint64_t(k) * row_lanes;
-        if (r < m) sm[uint64_t(cl) * m + r] = acc[k];
+        if (r < rows) sm[uint64_t(cl) * rows + r] = acc[k];
     }
     __syncthreads();
-    for (uint64_t r = tid; r < m; r += kSplitBlock) {
+    T* tile_partials = partials + uint64_t(blockIdx.y) * gridDim.x * mt;
+    for (uint64_t r = tid; r < rows; r += kSplitBlock) {
         T v = sm[r];
-        for (int q = 1; q < col_lanes; ++q) v = add_rn(v, sm[uint64_t(q) * m + r]);
-        partials[uint64_t(blockIdx.x) * m + r] = v;
+        for (int q = 1; q < col_lanes; ++q) v = add_rn(v, sm[uint64_t(q) * rows + r]);
+        tile_partials[uint64_t(blockIdx.x) * mt + r] = v;
     }
     __threadfence();
     __syncthreads();
-    if (tid == 0) am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    if (tid == 0) am_last = atomicAdd(tickets + blockIdx.y, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!am_last) return;
     __threadfence();
-
-    split_final(partials, c, m, sm);
-    if (tid == 0) *ticket = 0u;
+    split_final(tile_partials, c + r0, rows, mt, gridDim.x, sm);
+    if (tid == 0) tickets[blockIdx.y] = 0u;
 }
 
 struct SplitGeom {
     int row_lanes, col_lanes, rpt;
-    unsigned grid;
+    unsigned grid;       // column parts (gridDim.x)
+    unsigned row_tiles;  // gridDim.y
+    uint64_t mt;         // rows per row tile
     size_t smem;
 };
 
+// Row tiles: one tile when m < kSplitMaxRows, else tiles of kSplitTileRows.
+// Column parts: enough that row_tiles * parts covers every SM once
+// (1 CTA/SM at 1024 threads).
+constexpr uint64_t kSplitTileRows = 1024;
+
+inline void split_tiles(uint64_t m, uint64_t n, uint64_t cols_per_tile, SplitGeom* g) {
+    g->mt = m < kSplitMaxRows ? m : kSplitTileRows;
+    g->row_tiles = unsigned((m + g->mt - 1) / g->mt);
+    const uint64_t sms = uint64_t(sm_count());
+    uint64_t parts = (sms + g->row_tiles - 1) / g->row_tiles;
+    const uint64_t tiles = (n + cols_per_tile - 1) / cols_per_tile;
+    if (parts > tiles) parts = tiles;
+    g->grid = unsigned(parts < 1 ? 1 : parts);
+}
+
 template <typename T> SplitGeom split_geom(uint64_t m, uint64_t n) {
     SplitGeom g;
+    const uint64_t mt = m < kSplitMaxRows ? m : kSplitTileRows;
     uint64_t rl = 32; // a power of two, so row_lanes divides the block
-    while (rl < m && rl < uint64_t(kSplitBlock)) rl *= 2;
+    while (rl < mt && rl < uint64_t(kSplitBlock)) rl *= 2;
     g.row_lanes = int(rl);
     g.col_lanes = kSplitBlock / g.row_lanes;
-    g.rpt = int((m + rl - 1) / rl);
-    const uint64_t cap = uint64_t(sm_count());
-    const uint64_t tile = uint64_t(g.col_lanes) * split_u<T>();
-    const uint64_t tiles = (n + tile - 1) / tile;
-    g.grid = unsigned(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
-    // [col_lanes][m] for the column-lane combine, >= one entry per thread for
-    // split_final: <= max(kSplitBlock, m) entries, 16 KB for fp64
-    const size_t entries = size_t(g.col_lanes) * m;
+    g.rpt = int((mt + rl - 1) / rl);
+    split_tiles(m, n, uint64_t(g.col_lanes) * split_u<T>(), &g);
+    // [col_lanes][rows] for the column-lane combine, >= one entry per thread for
+    // split_final: <= max(kSplitBlock, mt) entries, 16 KB for fp64
+    const size_t entries = size_t(g.col_lanes) * g.mt;
     g.smem = (entries > size_t(kSplitBlock) ? entries : size_t(kSplitBlock)) * sizeof(T);
     return g;
 }
@@ -457,16 +484,14 @@ template <typename T> bool split_vec_ok(const T* A, uint64_t m) {
 
 template <typename T> SplitGeom split_vec_geom(uint64_t m, uint64_t n) {
     SplitGeom g;
-    const uint64_t mv = m / Vec<T>::N;
+    const uint64_t mt = m < kSplitMaxRows ? m : kSplitTileRows;
+    const uint64_t mv = mt / Vec<T>::N;
     uint64_t rl = 1;
     while (rl < mv) rl *= 2;
     g.row_lanes = int(rl);
     g.col_lanes = kSplitBlock / g.row_lanes;
     g.rpt = 1;
-    const uint64_t tile = uint64_t(g.col_lanes) * 4;
-    const uint64_t tiles = (n + tile - 1) / tile;
-    const uint64_t cap = uint64_t(sm_count());
-    g.grid = unsigned(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
+    split_tiles(m, n, uint64_t(g.col_lanes) * 4, &g);
     g.smem = 0;
     return g;
 }
@@ -506,6 +531,8 @@ template <typename T> SplitGeom split_bulk_geom(uint64_t m, uint64_t n, int* tc)
     const uint64_t tiles = (n + *tc - 1) / *tc;
     const uint64_t cap = uint64_t(sm_count());
     g.grid = unsigned(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
+    g.row_tiles = 1;
+    g.mt = m;
     g.smem = bulk_smem(bc.stages, bc.stage_bytes);
     return g;
 }
@@ -535,21 +562,45 @@ template <typename T> bool tall_vec_ok(const T* A, const T* c, uint64_t m) {
     return aligned32(A) && aligned32(c) && m % Vec<T>::N == 0;
 }
 
+enum CmPath { kPathTallVec, kPathTallScalar, kPathBulk, kPathSplitVec, kPathSplitScalar };
+
+// The bit-exact tall kernels keep each row's sum on one thread, so their
+// parallelism is m/V threads: they are used only when that fills the GPU
+// (>= one 256-row-vector unit per SM, or >= 1024 rows per SM for the scalar
+// variant).  Everything else splits the columns (2-D row tiles x column
+// parts; a single bulk-streamed row tile when m < kSplitMaxRows).
+template <typename T> CmPath cm_path(const T* A, const T* c, uint64_t m) {
+    const uint64_t sms = uint64_t(sm_count());
+    if (tall_vec_ok(A, c, m)) {
+        if (m / Vec<T>::N >= sms * kTallBlock) return kPathTallVec;
+    } else if (m >= sms * 1024) {
+        return kPathTallScalar;
+    }
+    if (split_vec_ok(A, m)) return (m < kSplitMaxRows && split_mode() == 1) ? kPathBulk : kPathSplitVec;
+    return kPathSplitScalar;
+}
+
+template <typename T> SplitGeom cm_split_geom(CmPath p, uint64_t m, uint64_t n, int* tc) {
+    if (p == kPathBulk) return split_bulk_geom<T>(m, n, tc);
+    if (p == kPathSplitVec) return split_vec_geom<T>(m, n);
+    return split_geom<T>(m, n);
+}
+
 } // namespace
 
 template <typename T> WorkspaceNeed gemv_cm_need(const T* A, const T*, uint64_t m, uint64_t n) {
     WorkspaceNeed w;
     if (m == 0 || n == 0) return w;
-    if (m >= kSplitMaxRows) {
+    const CmPath p = cm_path<T>(A, A, m); // c's alignment only matters to the tall kernels
+
+    if (p == kPathTallVec || p == kPathTallScalar) {
         w.counters = 1; // unit counter of the tall kernel
         return w;
     }
     int tc = 1;
-    const SplitGeom g = !split_vec_ok(A, m) ? split_geom<T>(m, n)
-                        : split_mode() == 1 ? split_bulk_geom<T>(m, n, &tc)
-                                            : split_vec_geom<T>(m, n);
-    w.counters = 1;
-    w.scratch_bytes = size_t(g.grid) * m * sizeof(T);
+    const SplitGeom g = cm_split_geom<T>(p, m, n, &tc);
+    w.counters = g.row_tiles;
+    w.scratch_bytes = size_t(g.row_tiles) * g.grid * g.mt * sizeof(T);
     return w;
 }
 
@@ -558,7 +609,10 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
                            const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
     if (info) info->ctas = 0;
     if (m == 0 || n == 0) return cudaSuccess;
-    if (m >= kSplitMaxRows && tall_vec_ok(A, c, m)) {
+    const CmPath path = cm_path<T>(A, A, m);
+    // (a c whose alignment differs from A's falls back to the scalar-lane
+    // tall kernel: same order and rounding)
+    if (path == kPathTallVec && aligned32(c)) {
         const uint64_t units = (m / Vec<T>::N + kTallBlock - 1) / kTallBlock;
         const uint64_t sms = uint64_t(sm_count());
         const unsigned grid = unsigned(units < sms ? units : sms); // grid <= units (dyn_next)
@@ -574,7 +628,7 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         else
             gemv_cm_tall_vec_kernel<T, false><<<grid, kTallBlock, 0, s>>>(A, x, c, m, n, ws.counters);
         if (info) info->ctas = grid;
-    } else if (m >= kSplitMaxRows) {
+    } else if (path == kPathTallScalar || path == kPathTallVec) {
         const uint64_t units = (m + kWarp - 1) / kWarp;
         const uint64_t max_warps = uint64_t(sm_count()) * kCmRowsCtasPerSm * (kCmBlock / kWarp);
         // smallest per-warp unit count that fits one wave, then as few warps
@@ -584,33 +638,30 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         const unsigned grid = unsigned((warps * kWarp + kCmBlock - 1) / kCmBlock);
         gemv_cm_rows_kernel<T><<<grid, kCmBlock, 0, s>>>(A, x, c, m, n, warps);
         if (info) info->ctas = grid;
-    } else if (split_vec_ok(A, m) && split_mode() == 1) {
-        int tc = 1;
-        const SplitGeom g = split_bulk_geom<T>(m, n, &tc);
-        const BulkCfg bc = bulk_cfg();
-        T* partials = static_cast<T*>(ws.scratch);
-        if (bc.stages == 6 && bc.stage_bytes == 32768)
-            bulk_go<T, 6, 32768>(A, x, c, m, n, g, tc, partials, ws.counters, s);
-        else if (bc.stages == 4 && bc.stage_bytes == 49152)
-            bulk_go<T, 4, 49152>(A, x, c, m, n, g, tc, partials, ws.counters, s);
-        else
-            bulk_go<T, 3, 65536>(A, x, c, m, n, g, tc, partials, ws.counters, s);
-        if (info) info->ctas = g.grid;
-    } else if (split_vec_ok(A, m)) {
-        const SplitGeom g = split_vec_geom<T>(m, n);
-        gemv_cm_split_vec_kernel<T><<<g.grid, kSplitBlock, 0, s>>>(
-            A, x, c, m, n, g.row_lanes, static_cast<T*>(ws.scratch), ws.counters);
-        if (info) info->ctas = g.grid;
     } else {
-        const SplitGeom g = split_geom<T>(m, n);
+        int tc = 1;
+        const SplitGeom g = cm_split_geom<T>(path, m, n, &tc);
         T* partials = static_cast<T*>(ws.scratch);
-        if (g.rpt == 1)
-            gemv_cm_split_kernel<T, 1><<<g.grid, kSplitBlock, g.smem, s>>>(
-                A, x, c, m, n, g.row_lanes, partials, ws.counters);
-        else
-            gemv_cm_split_kernel<T, 2><<<g.grid, kSplitBlock, g.smem, s>>>(
-                A, x, c, m, n, g.row_lanes, partials, ws.counters);
-        if (info) info->ctas = g.grid;
+        const dim3 grid(g.grid, g.row_tiles);
+        if (path == kPathBulk) {
+            const BulkCfg bc = bulk_cfg();
+            if (bc.stages == 6 && bc.stage_bytes == 32768)
+                bulk_go<T, 6, 32768>(A, x, c, m, n, g, tc, partials, ws.counters, s);
+            else if (bc.stages == 4 && bc.stage_bytes == 49152)
+                bulk_go<T, 4, 49152>(A, x, c, m, n, g, tc, partials, ws.counters, s);
+            else
+                bulk_go<T, 3, 65536>(A, x, c, m, n, g, tc, partials, ws.counters, s);
+        } else if (path == kPathSplitVec) {
+            gemv_cm_split_vec_kernel<T><<<grid, kSplitBlock, 0, s>>>(
+                A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);
+        } else if (g.rpt == 1) {
+            gemv_cm_split_kernel<T, 1><<<grid, kSplitBlock, g.smem, s>>>(
+                A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);
+        } else {
+            gemv_cm_split_kernel<T, 2><<<grid, kSplitBlock, g.smem, s>>>(
+                A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);
+        }
+        if (info) info->ctas = g.grid * g.row_tiles;
     }
     return cudaGetLastError();
 }

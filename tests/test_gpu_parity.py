@@ -137,7 +137,8 @@ def test_gemv_row_major_matches_oracle(cuda, dtype, m, n):
 
 
 CM_SHAPES = [(3, 3), (8, 8), (257, 259), (1000, 1000), (256, 65536), (2047, 300),
-             (2048, 100), (65536, 256), (70001, 37)]
+             (2048, 100), (4096, 4096), (5000, 3001), (65536, 256), (70001, 37),
+             (151552, 40), (303104, 24), (160001, 9)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -147,7 +148,7 @@ def test_gemv_col_major_matches_oracle(cuda, dtype, m, n):
     got, want, truth, rowabs, c0, probe, pol = _gemv_case(cuda, dtype, m, n, cb.Layout.ColMajor)
     dt = got.dtype
     assert probe.variant == cb.KernelVariant.gemv_col_blocked
-    if m >= 2048 or m * n + m + n <= pol.plan.dot_cutoff:
+    if T.cm_is_tall(m, dt) or m * n + m + n <= pol.plan.dot_cutoff:
         # tall kernel / ordered path keep the reference order and rounding
         np.testing.assert_array_equal(got, want)
     tol_c = T.contract_tol(n, rowabs, np.abs(c0), dt)
@@ -170,7 +171,7 @@ def test_gemv_col_major_baseline_configs_fp64_normal(cuda, m, n):
     O.gemv_ref(An, 1, xn, want)
     truth, rowabs = O.gemv_truth(An, 1, xn, c0n)
     got = np_of(c)
-    if m >= 2048:
+    if T.cm_is_tall(m, np.float64):
         np.testing.assert_array_equal(got, want)
     assert np.all(np.abs(got - want) <= T.contract_tol(n, rowabs, np.abs(c0n), np.float64))
     assert np.all(np.abs(got - truth) <=

@@ -71,12 +71,22 @@ def gemv_rm_chain(n: int, dtype) -> int:
     return math.ceil(n / 32) + 5 + 64 + 1
 
 
+def cm_is_tall(m: int, dtype, aligned: bool = True) -> bool:
+    """csrc/gemv_cm.cu cm_path: the bit-exact tall kernels run when m/V >= 148
+    units of 256 row vectors (V = 32/s, aligned, m % V == 0) or, otherwise,
+    m >= 148 * 1024."""
+    V = 32 // np.dtype(dtype).itemsize
+    if aligned and m % V == 0:
+        return m // V >= SMS * 256
+    return m >= SMS * 1024
+
+
 def gemv_cm_chain(m: int, n: int, dtype) -> int:
-    """Tall (m >= 2048): one sequential chain per row over all n columns (the
-    reference order).  Short-wide (csrc/gemv_cm.cu split kernel): G <= 148
-    CTAs, each thread a chain over <= ceil(n / G) columns, <= 32 column-lane
-    adds, then the G CTA partials summed in order, + c_i."""
-    if m >= 2048:
+    """Tall kernels: one sequential chain per row over all n columns (the
+    reference order).  Split kernels (csrc/gemv_cm.cu): <= 148 column parts,
+    each thread a chain over <= ceil(n / G) columns, <= 32 column-lane adds,
+    then the G part partials summed in order, + c_i."""
+    if cm_is_tall(m, dtype):
         return n + 1
     G = max(1, min(SMS, n))
     return math.ceil(n / G) + 32 + G + 2

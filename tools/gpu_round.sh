@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-python tools/ncu_runner.py --config D1 --reps 8 --no-flush > gpurun_out/plain_b2b_D1.log 2>&1 && timeout 600 ncu --cache-control none --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct -k regex:dot_kernel -c 8 --csv --log-file gpurun_out/ncu_b2b_D1.csv python tools/ncu_runner.py --config D1 --reps 8 --no-flush > gpurun_out/ncu_b2b_D1.log 2>&1
-timeout 300 python tools/b2b.py D1 R1 > gpurun_out/b2b2.jsonl 2>&1
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_modes.py tests/test_benchcli.py -m gpu -q --timeout 600 -p no:cacheprovider -k "col_major or modes or cli" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python tools/tune.py G2 G3 > gpurun_out/tune15.jsonl 2>&1
+timeout 600 python -m paper_2108_02025_b200.benchcli --kernel gemv-col --sizes 1024:16384:2 --rect 65536x1024,1024x65536 --dtype f64 --reps 5 --csv gpurun_out/sweep_cm.csv > gpurun_out/sweep.log 2>&1; echo "rc=$?" >> gpurun_out/sweep.log
