@@ -130,9 +130,6 @@ void set_probe(cabl_probe* p, int variant, unsigned ctas) {
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
-template <typename T> const char* tname();
-template <> const char* tname<float>() { return "f32"; }
-template <> const char* tname<double>() { return "f64"; }
 
 // ------------------------------------------------------------------- DOT
 template <typename T>

@@ -448,15 +448,17 @@ struct SplitGeom {
 };
 
 // Row tiles: one tile when m < kSplitMaxRows, else tiles of kSplitTileRows.
-// Column parts: enough that row_tiles * parts covers every SM once
-// (1 CTA/SM at 1024 threads).
+// Column parts: as many as keep row_tiles * parts within one CTA per SM
+// (1024 threads each), i.e. a single wave.
 constexpr uint64_t kSplitTileRows = 1024;
 
 inline void split_tiles(uint64_t m, uint64_t n, uint64_t cols_per_tile, SplitGeom* g) {
     g->mt = m < kSplitMaxRows ? m : kSplitTileRows;
     g->row_tiles = unsigned((m + g->mt - 1) / g->mt);
     const uint64_t sms = uint64_t(sm_count());
-    uint64_t parts = (sms + g->row_tiles - 1) / g->row_tiles;
+    // floor: row_tiles * parts must not exceed one CTA per SM, or the extra
+    // CTAs run as a second wave (8192^2 fp32: 152 CTAs took 65.6 us, 144 ...)
+    uint64_t parts = sms / g->row_tiles;
     const uint64_t tiles = (n + cols_per_tile - 1) / cols_per_tile;
     if (parts > tiles) parts = tiles;
     g->grid = unsigned(parts < 1 ? 1 : parts);

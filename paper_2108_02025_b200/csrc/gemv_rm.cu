@@ -245,30 +245,22 @@ template <typename T> bool rm_vec_ok(const T* A, const T* x, uint64_t n) {
 }
 
 // -1 scalar, 0 segment-balanced warps, 1 sweep for short rows, 2 sweep for
-// long rows.  The sweep needs enough row groups to balance a
-// single wave (>= 8 per CTA, i.e. <= 1/8 CTA of imbalance).
-// CABL_GEMV_RM_MODE overrides (tuning / tests only).
+// long rows.  CABL_GEMV_RM_MODE overrides (tuning / tests only).
 template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n) {
     if (!rm_vec_ok(A, x, n)) return -1;
     static const int forced = [] {
         const char* e = getenv("CABL_GEMV_RM_MODE");
         return e ? atoi(e) : -2;
     }();
-    const uint64_t nvec_row = n / Vec<T>::N;
-    const bool fits = nvec_row <= uint64_t(kRmBlock) * 4;
-    if (forced >= 0 && forced <= 2) {
-        if (forced == 1 && !fits) return 2;
-        return forced;
-    }
+    if (forced >= 0 && forced <= 2) return forced;
     // measured (tools/tune.py, 8192^2 and 65536^2 fp32): 4 rows x 2 vectors
     // per thread at 2 CTAs/SM for rows of <= 2 CTA passes, 2 rows x 8 vectors
     // at 1 CTA/SM for long rows.  The sweep must see >= 6 row groups per CTA
     // to keep the single wave balanced; otherwise the segment kernel.
     const uint64_t sms = uint64_t(sm_count());
-    const bool short_rows = nvec_row <= uint64_t(kRmBlock) * 2 * 2;
+    const bool short_rows = n / Vec<T>::N <= uint64_t(kRmBlock) * 2 * 2;
     if (short_rows && (m + 3) / 4 >= 6 * 2 * sms) return 1;
     if (!short_rows && (m + 1) / 2 >= 6 * 1 * sms) return 2;
-    (void)fits;
     return 0;
 }
 
