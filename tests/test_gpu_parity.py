@@ -441,3 +441,49 @@ def test_dot_2pow32_baseline_config(cuda):
     eps = float(np.finfo(np.float32).eps)
     # fp64 chunk sums carry ~1e-16 relative error: far below the fp32 bound
     assert abs(got - truth) <= (T.dot_chain(n, np.float32) + 2) * eps * sumabs
+
+
+def test_resident_gemv_operator_graph_equals_direct_call(cuda):
+    """operators.ResidentGemv (A resident, x/c streamed, CUDA-graph step)
+    gives the same bits as the plain call, call after call."""
+    import paper_2108_02025_b200 as cb
+    from paper_2108_02025_b200.operators import ResidentGemv
+    for lay, m, n in [(cb.Layout.RowMajor, 8192, 8192), (cb.Layout.ColMajor, 256, 1 << 16)]:
+        A = cb.DenseMatrix.wrap(dev_uniform(m * n, torch.float32, 3, cuda), m, n, lay)
+        pol = policy()
+        ops = [ResidentGemv(A, pol, use_graph=True), ResidentGemv(A, pol, use_graph=False)]
+        for step in range(3):
+            x = dev_uniform(n, torch.float32, 10 + step, cuda)
+            c = dev_uniform(m, torch.float32, 20 + step, cuda)
+            want = c.clone()
+            (cb.gemv_row_major if lay == cb.Layout.RowMajor else cb.gemv_col_major)(A, x, want, pol)
+            for op in ops:
+                got = op(x.cpu(), c.cpu())
+                assert torch.equal(got, want.cpu())
+
+
+def test_gemv_pipeline_results_in_order(cuda):
+    """operators.GemvPipeline: with 2 steps in flight every step's result is
+    the GEMV of that step's inputs (no buffer reuse before read-back)."""
+    import paper_2108_02025_b200 as cb
+    from paper_2108_02025_b200.operators import GemvPipeline
+    m, n = 4096, 4096
+    A = cb.DenseMatrix.wrap(dev_uniform(m * n, torch.float32, 3, cuda), m, n, cb.Layout.RowMajor)
+    pol = policy()
+    pipe = GemvPipeline(A, pol, depth=2)
+    xs = [dev_uniform(n, torch.float32, 30 + k, cuda) for k in range(6)]
+    cs = [dev_uniform(m, torch.float32, 40 + k, cuda) for k in range(6)]
+    wants = []
+    for x, c in zip(xs, cs):
+        w = c.clone()
+        cb.gemv_row_major(A, x, w, pol)
+        wants.append(w.cpu())
+    got = []
+    for x, c in zip(xs, cs):
+        r = pipe.step(x.cpu(), c.cpu())
+        if r is not None:
+            got.append(r.clone())
+    got += [r.clone() for r in pipe.drain()]
+    assert len(got) == 6
+    for g, w in zip(got, wants):
+        assert torch.equal(g, w)
