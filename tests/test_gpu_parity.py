@@ -487,3 +487,54 @@ def test_gemv_pipeline_results_in_order(cuda):
     assert len(got) == 6
     for g, w in zip(got, wants):
         assert torch.equal(g, w)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_special_values_propagate_like_the_oracle(cuda, dtype):
+    """NaN / Inf / signed zero / subnormals flow through every kernel as they
+    do through the reference's CPU code (no flush-to-zero, no fast math)."""
+    import paper_2108_02025_b200 as cb
+    npdt = np.float32 if dtype == torch.float32 else np.float64
+    tiny = np.finfo(npdt).smallest_subnormal
+    pol = policy()
+    # DOT: NaN poisons, +Inf survives, subnormal products are kept
+    for n in (100, 100_003):
+        x = np.full(n, 0.5, npdt)
+        y = np.full(n, 2.0, npdt)
+        y[7] = np.nan
+        assert np.isnan(cb.dot(torch.from_numpy(x).to(cuda), torch.from_numpy(y).to(cuda), 0.0, pol))
+        y[7] = np.inf
+        assert cb.dot(torch.from_numpy(x).to(cuda), torch.from_numpy(y).to(cuda), 0.0, pol) == np.inf
+        xs = np.full(n, tiny, npdt)
+        ys = np.ones(n, npdt)
+        got = cb.dot(torch.from_numpy(xs).to(cuda), torch.from_numpy(ys).to(cuda), 0.0, pol)
+        assert got == float(O.dot_ref(xs, ys, 0.0)) and got > 0
+    # signed zero: alpha0 added last to +0 (reference kernels.hpp:142)
+    e = torch.empty(0, dtype=dtype, device=cuda)
+    assert str(cb.dot(e, e, -0.0, pol)) == "0.0"
+    # GEMV / GER with a NaN and an Inf planted: same non-finite pattern as the oracle
+    m, n = 300, 1024
+    for lay in (cb.Layout.RowMajor, cb.Layout.ColMajor):
+        A = O.gen_uniform(m * n, npdt, 42, 3)
+        A[5] = np.nan
+        A[777] = np.inf
+        x = O.gen_uniform(n, npdt, 42, 1)
+        c0 = O.gen_uniform(m, npdt, 42, 4)
+        c = torch.from_numpy(c0.copy()).to(cuda)
+        f = cb.gemv_row_major if lay == cb.Layout.RowMajor else cb.gemv_col_major
+        f(cb.DenseMatrix.wrap(torch.from_numpy(A).to(cuda), m, n, lay), torch.from_numpy(x).to(cuda), c, pol)
+        want = c0.copy()
+        O.gemv_ref(A, int(lay), x, want)
+        got = c.cpu().numpy()
+        np.testing.assert_array_equal(np.isnan(got), np.isnan(want))
+        np.testing.assert_array_equal(np.isinf(got), np.isinf(want))
+        C0 = O.gen_uniform(m * n, npdt, 42, 5)
+        C0[3] = np.nan
+        gx = O.gen_uniform(m, npdt, 42, 1)
+        gx[2] = np.inf
+        gy = O.gen_uniform(n, npdt, 42, 2)
+        Cm = cb.DenseMatrix.wrap(torch.from_numpy(C0.copy()).to(cuda), m, n, lay)
+        cb.ger(torch.from_numpy(gx).to(cuda), torch.from_numpy(gy).to(cuda), Cm, pol)
+        want = C0.copy()
+        O.ger_ref(gx, gy, want, int(lay))
+        np.testing.assert_array_equal(Cm.data.cpu().numpy(), want)  # NaN == NaN positions too
