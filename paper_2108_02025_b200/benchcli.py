@@ -39,6 +39,11 @@ from pathlib import Path
 
 CSV_HEADER = "kernel,m,n,threads,reps,min_s,median_s,gflops,checksum"
 CSV_GPU_SUFFIX = ",dtype,gbs,roofline_frac"
+# --bounds: the HBM traffic model in place of the reference's CPU-cache bound
+# columns (reference bench.hpp:214-226, io_bounds.hpp report()): the bytes the
+# operation must move and the time they take at the measured
+# HBM peak — the B200 lower bound the measured median is compared against.
+CSV_BOUNDS_SUFFIX = ",alg_bytes,hbm_bound_s"
 KERNELS = ("dot", "ger", "gemv-row", "gemv-col")
 
 
@@ -56,6 +61,8 @@ class BenchRecord:
     dtype: str = "f64"
     gbs: float = 0.0
     roofline_frac: float = 0.0
+    alg_bytes: int | None = None      # --bounds
+    hbm_bound_s: float | None = None  # --bounds
 
 
 @dataclass
@@ -68,6 +75,7 @@ class SweepConfig:
     seed: int = 42
     dtype: str = "f64"
     max_threads: int = 8
+    bounds: bool = False
 
 
 # ------------------------------------------------------------------ parsing
@@ -117,11 +125,15 @@ def _g9(v: float) -> str:
 def emit_csv(records: list[BenchRecord]) -> str:
     if not records:
         raise ValueError("emit_csv: no records")
-    lines = [CSV_HEADER + CSV_GPU_SUFFIX]
+    bounds = records[0].alg_bytes is not None
+    lines = [CSV_HEADER + CSV_GPU_SUFFIX + (CSV_BOUNDS_SUFFIX if bounds else "")]
     for r in records:
-        lines.append(",".join([r.kernel, str(r.m), str(r.n), str(r.threads), str(r.reps),
-                               _g9(r.min_s), _g9(r.median_s), _g9(r.gflops), _g9(r.checksum),
-                               r.dtype, _g9(r.gbs), _g9(r.roofline_frac)]))
+        f = [r.kernel, str(r.m), str(r.n), str(r.threads), str(r.reps), _g9(r.min_s),
+             _g9(r.median_s), _g9(r.gflops), _g9(r.checksum), r.dtype, _g9(r.gbs),
+             _g9(r.roofline_frac)]
+        if bounds:
+            f += [str(r.alg_bytes), _g9(r.hbm_bound_s)]
+        lines.append(",".join(f))
     return "\n".join(lines) + "\n"
 
 
@@ -129,20 +141,25 @@ def parse_csv(text: str) -> list[BenchRecord]:
     rows = text.splitlines()
     if not rows:
         raise ValueError("parse_csv: empty document")
-    gpu = rows[0] == CSV_HEADER + CSV_GPU_SUFFIX
-    if not gpu and rows[0] != CSV_HEADER:
+    head = rows[0]
+    bounds = head == CSV_HEADER + CSV_GPU_SUFFIX + CSV_BOUNDS_SUFFIX
+    gpu = bounds or head == CSV_HEADER + CSV_GPU_SUFFIX
+    if not gpu and head != CSV_HEADER:
         raise ValueError("parse_csv: unexpected header")
+    want = 14 if bounds else (12 if gpu else 9)
     out = []
     for line in rows[1:]:
         if not line:
             continue
         f = line.split(",")
-        if len(f) != (12 if gpu else 9):
+        if len(f) != want:
             raise ValueError("parse_csv: bad field count")
         r = BenchRecord(f[0], int(f[1]), int(f[2]), int(f[3]), int(f[4]), float(f[5]),
                         float(f[6]), float(f[7]), float(f[8]))
         if gpu:
             r.dtype, r.gbs, r.roofline_frac = f[9], float(f[10]), float(f[11])
+        if bounds:
+            r.alg_bytes, r.hbm_bound_s = int(f[12]), float(f[13])
         out.append(r)
     return out
 
@@ -277,6 +294,9 @@ def run_config(kernel: str, m: int, n: int, threads: int, cfg: SweepConfig, flus
     rec.gflops = flops / rec.median_s / 1e9
     rec.gbs = _alg_bytes(kernel, m, n, s) / rec.median_s / 1e9
     rec.roofline_frac = rec.gbs / peak
+    if cfg.bounds:
+        rec.alg_bytes = _alg_bytes(kernel, m, n, s)
+        rec.hbm_bound_s = rec.alg_bytes / (peak * 1e9)
     return rec
 
 
@@ -335,12 +355,10 @@ def main(argv=None) -> int:
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--dtype", default="f64", choices=["f32", "f64"])
     ap.add_argument("--bounds", action="store_true",
-                    help="transfer-bound columns (reference io_bounds.hpp): not provided")
+                    help="append the HBM traffic-model columns alg_bytes, hbm_bound_s")
     a = ap.parse_args(argv)
     try:
-        if a.bounds:
-            raise ValueError("--bounds needs the reference's CPU cache model (out of scope)")
-        cfg = SweepConfig(kernels=list(KERNELS) if a.kernel == "all" else [a.kernel],
+        cfg = SweepConfig(bounds=a.bounds, kernels=list(KERNELS) if a.kernel == "all" else [a.kernel],
                           sizes=parse_sizes(a.sizes), rects=parse_rects(a.rect),
                           threads=[int(t) for t in a.threads.split(",") if t.strip()],
                           reps=a.reps, seed=a.seed, dtype=a.dtype)

@@ -57,10 +57,19 @@ def test_descriptor_loading(tmp_path):
     assert md.cores == 16 and md.levels[1].size_bytes() == 512 * 1024
 
 
+def test_bounds_columns_round_trip():
+    r = B.BenchRecord("gemv-row", 8192, 8192, 1, 3, 4.1e-5, 4.2e-5, 3.2e3, 1.0, "f32", 6.4e3,
+                      0.98, alg_bytes=268533760, hbm_bound_s=268533760 / 6547.8e9)
+    text = B.emit_csv([r])
+    assert text.splitlines()[0].endswith(B.CSV_BOUNDS_SUFFIX)
+    back = B.parse_csv(text)
+    assert back[0].alg_bytes == 268533760 and B.emit_csv(back) == text
+
+
 def test_cli_errors_exit_2():
-    r = subprocess.run([sys.executable, "-m", "paper_2108_02025_b200.benchcli", "--bounds"],
+    r = subprocess.run([sys.executable, "-m", "paper_2108_02025_b200.benchcli", "--sizes", "0"],
                        capture_output=True, text=True, cwd=ROOT, timeout=300)
-    assert r.returncode == 2 and "out of scope" in r.stderr
+    assert r.returncode == 2
     if not torch.cuda.is_available():
         r = subprocess.run([sys.executable, "-m", "paper_2108_02025_b200.benchcli", "--sizes", "64",
                             "--reps", "3"], capture_output=True, text=True, cwd=ROOT, timeout=300)
