@@ -117,20 +117,28 @@ __global__ void __launch_bounds__(BLOCK, MINB)
 // trailing elements, then alpha0.  The result depends on n only — not on
 // the grid, the scheduling, or the GPU's SM count — and every rounding chain
 // is short (<= kChunkVecs/(BLOCK*U) vectors per accumulator).
-constexpr uint64_t kChunkVecs = 65536; // 2 MiB of x and 2 MiB of y (fp32)
+constexpr uint64_t kChunkVecs = 65536; // default: 2 MiB of x and 2 MiB of y (fp32)
+
+inline uint64_t chunk_vecs() { // CABL_DOT_CHUNK (vectors per chunk): tuning only
+    static const uint64_t v = [] {
+        const char* e = getenv("CABL_DOT_CHUNK");
+        return e ? uint64_t(atoll(e)) : kChunkVecs;
+    }();
+    return v;
+}
 
 template <typename T, int BLOCK, int U, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB)
     dot_chunk_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t n, T alpha0,
                      T* __restrict__ out, T* __restrict__ partials,
-                     unsigned* __restrict__ counters) {
+                     unsigned* __restrict__ counters, uint64_t chunk) {
     __shared__ T red[32];
     __shared__ unsigned long long next_sh;
     __shared__ bool am_last;
     constexpr int V = Vec<T>::N;
     const int tid = threadIdx.x;
     const uint64_t nvec = n / V;
-    const uint64_t nchunks = (nvec + kChunkVecs - 1) / kChunkVecs;
+    const uint64_t nchunks = (nvec + chunk - 1) / chunk;
     const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
     const Vec<T>* Y = reinterpret_cast<const Vec<T>*>(y);
 
@@ -140,8 +148,8 @@ __global__ void __launch_bounds__(BLOCK, MINB)
         T acc[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) acc[u] = T(0);
-        const uint64_t c0 = ch * kChunkVecs;
-        const uint64_t c1 = (c0 + kChunkVecs < nvec) ? c0 + kChunkVecs : nvec;
+        const uint64_t c0 = ch * chunk;
+        const uint64_t c1 = (c0 + chunk < nvec) ? c0 + chunk : nvec;
         for (uint64_t base = c0; base < c1; base += uint64_t(BLOCK) * U) {
             Vec<T> xv[U], yv[U];
 #pragma unroll
@@ -254,7 +262,7 @@ inline bool dot_chunked(uint64_t n, size_t s, bool small, bool vec_ok) {
         return e ? atoi(e) : -1;
     }();
     if (small || !vec_ok) return false;
-    if (n / (32 / s) < uint64_t(sm_count()) * kDotCtasPerSm) return false; // grid <= chunks
+    if (n / (32 / s) < uint64_t(sm_count()) * kDotCtasPerSm) return false; // grid <= vectors
     if (forced >= 0) return forced != 0;
     return 2 * n * s >= (uint64_t(512) << 20);
 }
@@ -262,7 +270,7 @@ inline bool dot_chunked(uint64_t n, size_t s, bool small, bool vec_ok) {
 template <typename T> WorkspaceNeed dot_need(uint64_t n, bool small) {
     WorkspaceNeed w;
     w.counters = 2;
-    const uint64_t chunks = (n / Vec<T>::N + kChunkVecs - 1) / kChunkVecs;
+    const uint64_t chunks = (n / Vec<T>::N + chunk_vecs() - 1) / chunk_vecs();
     const uint64_t g = dot_grid<T>(n, small);
     w.scratch_bytes = size_t(chunks > g ? chunks : g) * sizeof(T);
     return w;
@@ -273,11 +281,11 @@ cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, boo
                        const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
     const int vec_ok = aligned32(x) && aligned32(y);
     if (dot_chunked(n, sizeof(T), small, vec_ok)) {
-        const uint64_t chunks = (n / Vec<T>::N + kChunkVecs - 1) / kChunkVecs;
+        const uint64_t chunks = (n / Vec<T>::N + chunk_vecs() - 1) / chunk_vecs();
         const uint64_t cap = uint64_t(sm_count()) * kDotCtasPerSm;
         const unsigned grid = unsigned(chunks < cap ? chunks : cap);
         dot_chunk_kernel<T, kDotBlock, kDotUnroll, kDotCtasPerSm><<<grid, kDotBlock, 0, s>>>(
-            x, y, n, alpha0, out, static_cast<T*>(ws.scratch), ws.counters);
+            x, y, n, alpha0, out, static_cast<T*>(ws.scratch), ws.counters, chunk_vecs());
         if (info) info->ctas = grid;
         return cudaGetLastError();
     }
