@@ -1,0 +1,157 @@
+// cabl/nccl.hpp — multi-GPU DOT / GEMV / GER for C++ callers, one process
+// driving G devices over NCCL (NVLink 5 / NVSwitch), the process model of
+// SURVEY.md §8(e).  (Python callers use paper_2108_02025_b200/shard.py: one
+// process per GPU under torchrun.)
+//
+// Partitioning (reference parallel_chunks, thread_pool.hpp:153-164, lifted to
+// devices): balanced contiguous ranges.
+//   DOT   chunks of x and y; each device computes its partial with alpha0 = 0;
+//         one ncclAllGather of the G partials; each device sums them in device
+//         order and adds alpha0 last (cabl_cuda_combine_partials_*), as the
+//         reference combines thread partials (kernels.hpp:160-163) — the
+//         result is independent of NCCL's algorithm and identical everywhere.
+//   GEMV  row blocks of A and c, x replicated, no exchange needed.
+//   GER   row blocks of C and x, y replicated, no exchange at all.
+//
+// Needs nccl.h and -lnccl in addition to cabl/device.hpp's requirements.
+#pragma once
+
+#include <nccl.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "device.hpp"
+
+namespace cabl::nccl {
+
+inline void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw std::runtime_error(std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+struct Range {
+    std::uint64_t begin, end;
+};
+
+// balanced contiguous split: the first total % parts ranges get one extra
+inline Range partition(std::uint64_t total, int parts, int rank) {
+    const std::uint64_t q = total / parts, r = total % parts;
+    const std::uint64_t b = rank * q + (std::uint64_t(rank) < r ? rank : r);
+    return Range{b, b + q + (std::uint64_t(rank) < r ? 1 : 0)};
+}
+
+// One communicator clique over `devices` (ncclCommInitAll), one stream each.
+class Group {
+public:
+    explicit Group(std::vector<int> devices) : devs_(std::move(devices)) {
+        comms_.resize(devs_.size());
+        nccl_check(ncclCommInitAll(comms_.data(), int(devs_.size()), devs_.data()), "ncclCommInitAll");
+        for (int d : devs_) {
+            detail::cuda_check(cudaSetDevice(d), "cudaSetDevice");
+            cudaStream_t s;
+            detail::cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+            streams_.push_back(s);
+        }
+    }
+    Group(const Group&) = delete;
+    Group& operator=(const Group&) = delete;
+    ~Group() {
+        for (std::size_t i = 0; i < devs_.size(); ++i) {
+            cudaSetDevice(devs_[i]);
+            cudaStreamDestroy(streams_[i]);
+            ncclCommDestroy(comms_[i]);
+        }
+    }
+    int size() const { return int(devs_.size()); }
+    int device(int r) const { return devs_[r]; }
+    ncclComm_t comm(int r) const { return comms_[r]; }
+    cudaStream_t stream(int r) const { return streams_[r]; }
+    void synchronize() const {
+        for (int r = 0; r < size(); ++r) {
+            detail::cuda_check(cudaSetDevice(devs_[r]), "cudaSetDevice");
+            detail::cuda_check(cudaStreamSynchronize(streams_[r]), "sync");
+        }
+    }
+
+private:
+    std::vector<int> devs_;
+    std::vector<ncclComm_t> comms_;
+    std::vector<cudaStream_t> streams_;
+};
+
+namespace detail {
+template <typename T> ncclDataType_t nccl_type();
+template <> inline ncclDataType_t nccl_type<float>() { return ncclFloat32; }
+template <> inline ncclDataType_t nccl_type<double>() { return ncclFloat64; }
+inline int combine(const float* p, std::uint32_t k, float a, float* o, cudaStream_t s) {
+    return cabl_cuda_combine_partials_f32(p, k, a, o, s);
+}
+inline int combine(const double* p, std::uint32_t k, double a, double* o, cudaStream_t s) {
+    return cabl_cuda_combine_partials_f64(p, k, a, o, s);
+}
+} // namespace detail
+
+// alpha0 + x.y with x, y given as per-device chunks (x[r], y[r] on
+// g.device(r), equal lengths per rank).  Returns the host value (every device
+// holds the same bits in its `out`).
+template <typename T>
+T sharded_dot(Group& g, const std::vector<const DeviceVector<T>*>& x,
+              const std::vector<const DeviceVector<T>*>& y, T alpha0, const ExecPolicy& policy) {
+    const int G = g.size();
+    cabl::detail::require(int(x.size()) == G && int(y.size()) == G, "sharded_dot: one chunk per device");
+    std::vector<DeviceVector<T>> partial, gathered, out;
+    for (int r = 0; r < G; ++r) {
+        cabl::detail::cuda_check(cudaSetDevice(g.device(r)), "cudaSetDevice");
+        partial.emplace_back(1);
+        gathered.emplace_back(std::size_t(G));
+        out.emplace_back(1);
+        dot_async(*x[r], *y[r], T(0), partial[r].data(), policy, g.stream(r));
+    }
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    for (int r = 0; r < G; ++r)
+        nccl_check(ncclAllGather(partial[r].data(), gathered[r].data(), 1, detail::nccl_type<T>(),
+                                 g.comm(r), g.stream(r)),
+                   "ncclAllGather");
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    for (int r = 0; r < G; ++r) {
+        cabl::detail::cuda_check(cudaSetDevice(g.device(r)), "cudaSetDevice");
+        cabl::detail::check(detail::combine(gathered[r].data(), std::uint32_t(G), alpha0,
+                                            out[r].data(), g.stream(r)));
+    }
+    T result{};
+    cabl::detail::cuda_check(cudaSetDevice(g.device(0)), "cudaSetDevice");
+    cabl::detail::cuda_check(cudaMemcpyAsync(&result, out[0].data(), sizeof(T),
+                                             cudaMemcpyDeviceToHost, g.stream(0)), "D2H");
+    g.synchronize();
+    return result;
+}
+
+// c[r] += A[r] x[r] on every device's row block (no exchange).
+template <typename T>
+void sharded_gemv_rows(Group& g, const std::vector<const DeviceMatrix<T>*>& A,
+                       const std::vector<const DeviceVector<T>*>& x,
+                       const std::vector<DeviceVector<T>*>& c, const ExecPolicy& policy) {
+    for (int r = 0; r < g.size(); ++r) {
+        cabl::detail::cuda_check(cudaSetDevice(g.device(r)), "cudaSetDevice");
+        if (A[r]->layout() == Layout::RowMajor)
+            gemv_row_major(*A[r], *x[r], *c[r], policy, g.stream(r));
+        else
+            gemv_col_major(*A[r], *x[r], *c[r], policy, g.stream(r));
+    }
+    g.synchronize();
+}
+
+// C[r] += x[r] (x) y[r] on every device's row block (no communication).
+template <typename T>
+void sharded_ger_rows(Group& g, const std::vector<const DeviceVector<T>*>& x,
+                      const std::vector<const DeviceVector<T>*>& y,
+                      const std::vector<DeviceMatrix<T>*>& C, const ExecPolicy& policy) {
+    for (int r = 0; r < g.size(); ++r) {
+        cabl::detail::cuda_check(cudaSetDevice(g.device(r)), "cudaSetDevice");
+        ger(*x[r], *y[r], *C[r], policy, g.stream(r));
+    }
+    g.synchronize();
+}
+
+} // namespace cabl::nccl

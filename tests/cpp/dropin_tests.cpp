@@ -43,7 +43,8 @@ struct Group {
 };
 
 void run_group(const char* name, const std::function<void(Group&)>& body) {
-    Group g{name};
+    Group g;
+    g.name = name;
     try {
         body(g);
     } catch (const std::exception& e) {

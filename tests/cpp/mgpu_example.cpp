@@ -1,0 +1,125 @@
+// Multi-GPU drop-in use (cabl/nccl.hpp): one process drives every visible
+// device through an NCCL clique.  Checks the sharded results bit for bit
+// against the same per-shard computations run one by one on device 0:
+//   DOT  = rank-ordered sum of the per-shard partials + alpha0,
+//   GEMV = each row block, GER = each row block.
+// With one GPU (this run's boxes) the clique has one member and the path
+// still goes through ncclCommInitAll / ncclAllGather / the ordered combine.
+#include <cabl/nccl.hpp>
+
+#include <cstdio>
+#include <random>
+
+using namespace cabl;
+
+int main() {
+    int ndev = 0;
+    cudaGetDeviceCount(&ndev);
+    if (ndev < 1) {
+        std::printf("no CUDA device\n");
+        return 2;
+    }
+    std::vector<int> devs;
+    for (int d = 0; d < ndev; ++d) devs.push_back(d);
+    nccl::Group g(devs);
+    const int G = g.size();
+    const ExecPolicy pol(derive_blocking_plan(default_machine()), 1);
+    std::mt19937_64 rng(2026);
+    std::uniform_real_distribution<float> U(-1.f, 1.f);
+    bool ok = true;
+
+    // ---- DOT
+    const std::size_t n = (std::size_t(1) << 24) + 5;
+    Vector<float> x(n), y(n);
+    for (auto& v : x) v = U(rng);
+    for (auto& v : y) v = U(rng);
+    std::vector<DeviceVector<float>> xs, ys;
+    float expect = 0.f;
+    for (int r = 0; r < G; ++r) {
+        const nccl::Range rg = nccl::partition(n, G, r);
+        Vector<float> xc(rg.end - rg.begin), yc(rg.end - rg.begin);
+        std::copy(x.begin() + rg.begin, x.begin() + rg.end, xc.begin());
+        std::copy(y.begin() + rg.begin, y.begin() + rg.end, yc.begin());
+        cudaSetDevice(0);
+        const float p = dot(DeviceVector<float>(xc), DeviceVector<float>(yc), 0.0f, pol);
+        expect = expect + p; // rank order, alpha0 last (kernels.hpp:160-163)
+        cudaSetDevice(g.device(r));
+        xs.emplace_back(xc);
+        ys.emplace_back(yc);
+    }
+    expect = expect + 0.75f;
+    std::vector<const DeviceVector<float>*> xp, yp;
+    for (int r = 0; r < G; ++r) {
+        xp.push_back(&xs[r]);
+        yp.push_back(&ys[r]);
+    }
+    const float got = nccl::sharded_dot(g, xp, yp, 0.75f, pol);
+    ok &= got == expect;
+    std::printf("sharded dot over %d GPU(s): %.9g (expected %.9g) %s\n", G, double(got),
+                double(expect), got == expect ? "ok" : "MISMATCH");
+
+    // ---- GEMV (row blocks) and GER (row blocks)
+    const std::size_t m = 8192, k = 4096;
+    DenseMatrix<float> A(m, k, Layout::RowMajor), C(m, k, Layout::RowMajor);
+    Vector<float> xv(k), cv(m), gx(m), gy(k);
+    for (std::size_t i = 0; i < A.size(); ++i) A.data()[i] = U(rng);
+    for (std::size_t i = 0; i < C.size(); ++i) C.data()[i] = U(rng);
+    for (auto& v : xv) v = U(rng);
+    for (auto& v : cv) v = U(rng);
+    for (auto& v : gx) v = U(rng);
+    for (auto& v : gy) v = U(rng);
+    std::vector<DeviceMatrix<float>> Ab, Cb;
+    std::vector<DeviceVector<float>> xb, cb, gxb, gyb;
+    std::vector<Vector<float>> c_expect;
+    std::vector<DenseMatrix<float>> C_expect;
+    for (int r = 0; r < G; ++r) {
+        const nccl::Range rg = nccl::partition(m, G, r);
+        const std::size_t mr = rg.end - rg.begin;
+        DenseMatrix<float> Ar(mr, k, Layout::RowMajor), Cr(mr, k, Layout::RowMajor);
+        std::copy(A.data() + rg.begin * k, A.data() + rg.end * k, Ar.data());
+        std::copy(C.data() + rg.begin * k, C.data() + rg.end * k, Cr.data());
+        Vector<float> cr(mr), gxr(mr);
+        std::copy(cv.begin() + rg.begin, cv.begin() + rg.end, cr.begin());
+        std::copy(gx.begin() + rg.begin, gx.begin() + rg.end, gxr.begin());
+        // expected: the same shard computed alone on device 0
+        cudaSetDevice(0);
+        {
+            DeviceMatrix<float> dA(Ar), dC(Cr);
+            DeviceVector<float> dx(xv), dc(cr), dgx(gxr), dgy(gy);
+            gemv_row_major(dA, dx, dc, pol);
+            ger(dgx, dgy, dC, pol);
+            c_expect.push_back(dc.download());
+            C_expect.push_back(dC.download());
+        }
+        cudaSetDevice(g.device(r));
+        Ab.emplace_back(Ar);
+        Cb.emplace_back(Cr);
+        xb.emplace_back(xv);
+        cb.emplace_back(cr);
+        gxb.emplace_back(gxr);
+        gyb.emplace_back(gy);
+    }
+    std::vector<const DeviceMatrix<float>*> Ap;
+    std::vector<const DeviceVector<float>*> xq, gxq, gyq;
+    std::vector<DeviceVector<float>*> cq;
+    std::vector<DeviceMatrix<float>*> Cq;
+    for (int r = 0; r < G; ++r) {
+        Ap.push_back(&Ab[r]);
+        xq.push_back(&xb[r]);
+        cq.push_back(&cb[r]);
+        gxq.push_back(&gxb[r]);
+        gyq.push_back(&gyb[r]);
+        Cq.push_back(&Cb[r]);
+    }
+    nccl::sharded_gemv_rows(g, Ap, xq, cq, pol);
+    nccl::sharded_ger_rows(g, gxq, gyq, Cq, pol);
+    for (int r = 0; r < G; ++r) {
+        cudaSetDevice(g.device(r));
+        const bool gemv_ok = cb[r].download() == c_expect[r];
+        const bool ger_ok = Cb[r].download() == C_expect[r];
+        ok &= gemv_ok && ger_ok;
+        std::printf("rank %d: gemv rows %s, ger rows %s\n", r, gemv_ok ? "ok" : "MISMATCH",
+                    ger_ok ? "ok" : "MISMATCH");
+    }
+    return ok ? 0 : 1;
+}

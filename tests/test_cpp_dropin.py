@@ -26,6 +26,7 @@ def _build():
 def test_dropin_header_compiles_and_links():
     _build()
     assert (CPP / "dropin_tests").exists() and (CPP / "device_example").exists()
+    assert (CPP / "mgpu_example").exists()
 
 
 def test_dropin_fails_loudly_without_gpu():
@@ -52,3 +53,13 @@ def test_device_container_example(cuda):
     _build()
     r = subprocess.run([str(CPP / "device_example")], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_multi_gpu_nccl_example(cuda):
+    """include/cabl/nccl.hpp: one process, an NCCL clique over every visible
+    device; sharded DOT / GEMV / GER bitwise equal to the shard-by-shard runs."""
+    _build()
+    r = subprocess.run([str(CPP / "mgpu_example")], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "MISMATCH" not in r.stdout

@@ -1,6 +1,3 @@
 mkdir -p gpurun_out
-rm -f gpurun_out/tune16.jsonl
-python tools/b2b.py D1 >> gpurun_out/tune16.jsonl 2>&1
-for ch in 1024 2048 4096 8192; do
-CABL_DOT_CHUNKED=1 CABL_DOT_CHUNK=$ch python tools/b2b.py D1 | sed "s/^/chunk=$ch /" >> gpurun_out/tune16.jsonl 2>&1
-done
+timeout 900 python -m pytest tests/test_cpp_dropin.py -m gpu -q --timeout 800 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+(cd tests/cpp && ./mgpu_example > ../../gpurun_out/mgpu.log 2>&1; echo "rc=$?" >> ../../gpurun_out/mgpu.log)
