@@ -9,7 +9,9 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
+#include <utility>
 
 namespace cabl_dev {
 
@@ -162,6 +164,45 @@ __device__ __forceinline__ unsigned long long dyn_next(unsigned* counter,
     const unsigned long long raw = atomicAdd(counter, 1u);
     if (raw == total - 1) *counter = 0u;
     return raw + gridDim.x;
+}
+
+// ---- programmatic dependent launch (PDL) ---------------------------------
+// Every kernel of the library starts with pdl_enter(): it lets the NEXT
+// kernel on the stream begin launching (its CTAs take SMs as this grid's
+// CTAs retire) and then waits until the PREVIOUS grid has fully completed and
+// its memory is visible.  No global memory is touched before the wait, so the
+// stream semantics are exactly the usual ones; what overlaps is only launch
+// latency and CTA rasterisation with the previous kernel's tail — back-to-back
+// calls (an iterative solver, a serving loop, K bench steps) lose the gap
+// between kernels.  Without the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("CABL_PDL");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
+}
+
+// kernel<<<grid, block, smem, s>>>(args...) with the PDL attribute
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                   Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }

@@ -28,6 +28,7 @@ __host__ __device__ inline uint64_t sm_key_host(uint64_t seed, uint64_t sid) {
 
 __global__ void fill_u32_kernel(float* __restrict__ out, uint64_t n, uint64_t key,
                                 uint64_t offset) {
+    pdl_enter();
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         const uint64_t u = sm_mix(key + kGolden * (offset + i + 1ULL));
@@ -37,6 +38,7 @@ __global__ void fill_u32_kernel(float* __restrict__ out, uint64_t n, uint64_t ke
 
 __global__ void fill_u64_kernel(double* __restrict__ out, uint64_t n, uint64_t key,
                                 uint64_t offset) {
+    pdl_enter();
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         const uint64_t u = sm_mix(key + kGolden * (offset + i + 1ULL));
@@ -46,6 +48,7 @@ __global__ void fill_u64_kernel(double* __restrict__ out, uint64_t n, uint64_t k
 
 __global__ void fill_n64_kernel(double* __restrict__ out, uint64_t n, uint64_t key,
                                 uint64_t offset) {
+    pdl_enter();
     const double two_pi = 6.283185307179586476925286766559;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -69,21 +72,21 @@ unsigned fill_grid(uint64_t n) {
 cudaError_t fill_uniform_f32(float* out, uint64_t n, uint64_t seed, uint64_t sid,
                              uint64_t offset, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    fill_u32_kernel<<<fill_grid(n), 256, 0, s>>>(out, n, sm_key_host(seed, sid), offset);
+    launch(fill_u32_kernel, fill_grid(n), 256, 0, s, out, n, sm_key_host(seed, sid), offset);
     return cudaGetLastError();
 }
 
 cudaError_t fill_uniform_f64(double* out, uint64_t n, uint64_t seed, uint64_t sid,
                              uint64_t offset, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    fill_u64_kernel<<<fill_grid(n), 256, 0, s>>>(out, n, sm_key_host(seed, sid), offset);
+    launch(fill_u64_kernel, fill_grid(n), 256, 0, s, out, n, sm_key_host(seed, sid), offset);
     return cudaGetLastError();
 }
 
 cudaError_t fill_normal_f64(double* out, uint64_t n, uint64_t seed, uint64_t sid,
                             uint64_t offset, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    fill_n64_kernel<<<fill_grid(n), 256, 0, s>>>(out, n, sm_key_host(seed, sid), offset);
+    launch(fill_n64_kernel, fill_grid(n), 256, 0, s, out, n, sm_key_host(seed, sid), offset);
     return cudaGetLastError();
 }
 

@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     dot_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t n, int vec_ok,
                T alpha0, T* __restrict__ out, T* __restrict__ partials,
                unsigned* __restrict__ ticket) {
+    pdl_enter();
     __shared__ T red[32];
     __shared__ bool am_last;
     constexpr int V = Vec<T>::N;
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     dot_chunk_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t n, T alpha0,
                      T* __restrict__ out, T* __restrict__ partials,
                      unsigned* __restrict__ counters, uint64_t chunk) {
+    pdl_enter();
     __shared__ T red[32];
     __shared__ unsigned long long next_sh;
     __shared__ bool am_last;
@@ -194,6 +196,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
 template <typename T>
 __global__ void combine_kernel(const T* __restrict__ p, uint32_t count, T alpha0,
                                T* __restrict__ out) {
+    pdl_enter();
     // Reference kernels.hpp:160-163: total{} += partials[c] in index order,
     // then + alpha0.
     T total = T(0);
@@ -230,7 +233,7 @@ template <typename T> unsigned dot_grid(uint64_t n, bool small) {
 template <typename T, int B, int U, int M>
 cudaError_t dot_go(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok, T alpha0,
                    T* out, T* partials, unsigned* ticket, cudaStream_t s) {
-    dot_kernel<T, B, U, M><<<grid, B, 0, s>>>(x, y, n, vec_ok, alpha0, out, partials, ticket);
+    launch(dot_kernel<T, B, U, M>, grid, B, 0, s, x, y, n, vec_ok, alpha0, out, partials, ticket);
     return cudaGetLastError();
 }
 
@@ -284,7 +287,7 @@ cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, boo
         const uint64_t chunks = (n / Vec<T>::N + chunk_vecs() - 1) / chunk_vecs();
         const uint64_t cap = uint64_t(sm_count()) * kDotCtasPerSm;
         const unsigned grid = unsigned(chunks < cap ? chunks : cap);
-        dot_chunk_kernel<T, kDotBlock, kDotUnroll, kDotCtasPerSm><<<grid, kDotBlock, 0, s>>>(
+        launch(dot_chunk_kernel<T, kDotBlock, kDotUnroll, kDotCtasPerSm>, grid, kDotBlock, 0, s, 
             x, y, n, alpha0, out, static_cast<T*>(ws.scratch), ws.counters, chunk_vecs());
         if (info) info->ctas = grid;
         return cudaGetLastError();
@@ -299,7 +302,7 @@ cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, boo
 template <typename T>
 cudaError_t combine_partials_launch(const T* p, uint32_t count, T alpha0, T* out,
                                     cudaStream_t s) {
-    combine_kernel<T><<<1, 1, 0, s>>>(p, count, alpha0, out);
+    launch(combine_kernel<T>, 1, 1, 0, s, p, count, alpha0, out);
     return cudaGetLastError();
 }
 

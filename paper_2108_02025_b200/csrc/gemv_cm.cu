@@ -59,6 +59,7 @@ template <typename T, bool DYN>
 __global__ void __launch_bounds__(kTallBlock, 1)
     gemv_cm_tall_vec_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                             uint64_t m, uint64_t n, unsigned* __restrict__ counter) {
+    pdl_enter();
     constexpr int V = Vec<T>::N;
     constexpr uint64_t kRefVec = 16 / sizeof(T);
     __shared__ unsigned long long next_sh[2];
@@ -114,6 +115,7 @@ template <typename T>
 __global__ void __launch_bounds__(kCmBlock, kCmRowsCtasPerSm)
     gemv_cm_rows_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                         uint64_t m, uint64_t n, uint64_t warps) {
+    pdl_enter();
     constexpr uint64_t kRefVec = 16 / sizeof(T);
     const int lane = threadIdx.x & 31;
     const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -196,6 +198,7 @@ __global__ void __launch_bounds__(kSplitBlock, 1)
     gemv_cm_split_vec_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                              uint64_t m, uint64_t n, uint64_t mt, int row_lanes,
                              T* __restrict__ partials, unsigned* __restrict__ tickets) {
+    pdl_enter();
     constexpr int V = Vec<T>::N;
     constexpr int U = 4;
     __shared__ alignas(32) T sm[kSplitBlock * V]; // [col_lanes][mt] <= 1024 * V entries
@@ -281,6 +284,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     gemv_cm_split_bulk_kernel(const T* __restrict__ A, const T* __restrict__ x,
                               T* __restrict__ c, uint64_t m, uint64_t n, int row_lanes, int tc,
                               T* __restrict__ partials, unsigned* __restrict__ ticket) {
+    pdl_enter();
     constexpr int V = Vec<T>::N;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* stages = reinterpret_cast<T*>(smem_raw);
@@ -377,6 +381,7 @@ __global__ void __launch_bounds__(kSplitBlock, 1)
     gemv_cm_split_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                          uint64_t m, uint64_t n, uint64_t mt, int row_lanes,
                          T* __restrict__ partials, unsigned* __restrict__ tickets) {
+    pdl_enter();
     extern __shared__ unsigned char smem_raw[];
     T* sm = reinterpret_cast<T*>(smem_raw); // [col_lanes][rows], >= kSplitBlock entries
     __shared__ bool am_last;
@@ -548,7 +553,7 @@ void bulk_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const SplitGe
         return true;
     }();
     (void)configured;
-    gemv_cm_split_bulk_kernel<T, NS, SB><<<g.grid, kBulkThreads, bulk_smem(NS, SB), s>>>(
+    launch(gemv_cm_split_bulk_kernel<T, NS, SB>, g.grid, kBulkThreads, bulk_smem(NS, SB), s, 
         A, x, c, m, n, g.row_lanes, tc, partials, ticket);
 }
 
@@ -626,9 +631,9 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         }();
         const bool dyn = forced >= 0 ? forced != 0 : m * n * sizeof(T) >= (uint64_t(512) << 20);
         if (dyn)
-            gemv_cm_tall_vec_kernel<T, true><<<grid, kTallBlock, 0, s>>>(A, x, c, m, n, ws.counters);
+            launch(gemv_cm_tall_vec_kernel<T, true>, grid, kTallBlock, 0, s, A, x, c, m, n, ws.counters);
         else
-            gemv_cm_tall_vec_kernel<T, false><<<grid, kTallBlock, 0, s>>>(A, x, c, m, n, ws.counters);
+            launch(gemv_cm_tall_vec_kernel<T, false>, grid, kTallBlock, 0, s, A, x, c, m, n, ws.counters);
         if (info) info->ctas = grid;
     } else if (path == kPathTallScalar || path == kPathTallVec) {
         const uint64_t units = (m + kWarp - 1) / kWarp;
@@ -638,7 +643,7 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         const uint64_t per = (units + max_warps - 1) / max_warps;
         const uint64_t warps = (units + per - 1) / per;
         const unsigned grid = unsigned((warps * kWarp + kCmBlock - 1) / kCmBlock);
-        gemv_cm_rows_kernel<T><<<grid, kCmBlock, 0, s>>>(A, x, c, m, n, warps);
+        launch(gemv_cm_rows_kernel<T>, grid, kCmBlock, 0, s, A, x, c, m, n, warps);
         if (info) info->ctas = grid;
     } else {
         int tc = 1;
@@ -654,13 +659,13 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
             else
                 bulk_go<T, 3, 65536>(A, x, c, m, n, g, tc, partials, ws.counters, s);
         } else if (path == kPathSplitVec) {
-            gemv_cm_split_vec_kernel<T><<<grid, kSplitBlock, 0, s>>>(
+            launch(gemv_cm_split_vec_kernel<T>, grid, kSplitBlock, 0, s, 
                 A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);
         } else if (g.rpt == 1) {
-            gemv_cm_split_kernel<T, 1><<<grid, kSplitBlock, g.smem, s>>>(
+            launch(gemv_cm_split_kernel<T, 1>, grid, kSplitBlock, g.smem, s, 
                 A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);
         } else {
-            gemv_cm_split_kernel<T, 2><<<grid, kSplitBlock, g.smem, s>>>(
+            launch(gemv_cm_split_kernel<T, 2>, grid, kSplitBlock, g.smem, s, 
                 A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);
         }
         if (info) info->ctas = g.grid * g.row_tiles;

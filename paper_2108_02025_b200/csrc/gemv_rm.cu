@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kRmBlock, kRmCtasPerSm)
     gemv_rm_vec_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                        uint64_t m, uint64_t n, RmGeom geo, T* __restrict__ slots,
                        unsigned* __restrict__ tickets) {
+    pdl_enter();
     const int lane = threadIdx.x & 31;
     const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (gw >= geo.warps) return;
@@ -164,6 +165,7 @@ template <typename T, int R, int KV, int MINB, bool DYN>
 __global__ void __launch_bounds__(kRmBlock, MINB)
     gemv_rm_sweep_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                          uint64_t m, uint64_t n, unsigned* __restrict__ counter) {
+    pdl_enter();
     constexpr int NW = kRmBlock / kWarp;
     __shared__ T red[2][R][NW];
     __shared__ unsigned long long next_sh[2];
@@ -227,6 +229,7 @@ template <typename T>
 __global__ void __launch_bounds__(kRmBlock)
     gemv_rm_scalar_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                           uint64_t m, uint64_t n, uint64_t warps) {
+    pdl_enter();
     const int lane = threadIdx.x & 31;
     const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (gw >= warps) return;
@@ -302,9 +305,9 @@ unsigned sweep_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, unsigned
     const uint64_t ctas = uint64_t(sm_count()) * MINB;
     const unsigned grid = unsigned(groups < ctas ? groups : ctas);
     if (use_dyn_queue(m * n * sizeof(T)))
-        gemv_rm_sweep_kernel<T, R, KV, MINB, true><<<grid, kRmBlock, 0, s>>>(A, x, c, m, n, counter);
+        launch(gemv_rm_sweep_kernel<T, R, KV, MINB, true>, grid, kRmBlock, 0, s, A, x, c, m, n, counter);
     else
-        gemv_rm_sweep_kernel<T, R, KV, MINB, false><<<grid, kRmBlock, 0, s>>>(A, x, c, m, n, counter);
+        launch(gemv_rm_sweep_kernel<T, R, KV, MINB, false>, grid, kRmBlock, 0, s, A, x, c, m, n, counter);
     return grid;
 }
 
@@ -361,14 +364,14 @@ cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
     } else if (mode == 0) {
         const RmGeom g = rm_geom<T>(m, n);
         const unsigned grid = unsigned((g.warps * kWarp + kRmBlock - 1) / kRmBlock);
-        gemv_rm_vec_kernel<T, kRmRows, kRmSeg><<<grid, kRmBlock, 0, s>>>(
+        launch(gemv_rm_vec_kernel<T, kRmRows, kRmSeg>, grid, kRmBlock, 0, s, 
             A, x, c, m, n, g, static_cast<T*>(ws.scratch), ws.counters);
         if (info) info->ctas = grid;
     } else {
         const uint64_t max_warps = uint64_t(sm_count()) * 8 * (kRmBlock / kWarp);
         const uint64_t warps = m < max_warps ? m : max_warps;
         const unsigned grid = unsigned((warps * kWarp + kRmBlock - 1) / kRmBlock);
-        gemv_rm_scalar_kernel<T><<<grid, kRmBlock, 0, s>>>(A, x, c, m, n, warps);
+        launch(gemv_rm_scalar_kernel<T>, grid, kRmBlock, 0, s, A, x, c, m, n, warps);
         if (info) info->ctas = grid;
     }
     return cudaGetLastError();

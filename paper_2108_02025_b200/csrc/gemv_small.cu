@@ -21,6 +21,7 @@ template <typename T>
 __global__ void __launch_bounds__(kSmallBlock)
     gemv_ordered_kernel(const T* __restrict__ A, int layout, uint64_t m, uint64_t n,
                         const T* __restrict__ x, T* __restrict__ c) {
+    pdl_enter();
     constexpr uint64_t kRefVec = 16 / sizeof(T);
     const uint64_t cut = (n / kRefVec) * kRefVec;
     const uint64_t rs = layout == 0 ? n : 1; // row stride
@@ -42,7 +43,7 @@ cudaError_t gemv_ordered_launch(const T* A, int layout, uint64_t m, uint64_t n, 
                                 T* c, cudaStream_t s, LaunchInfo* info) {
     if (info) info->ctas = 1;
     if (m == 0 || n == 0) return cudaSuccess;
-    gemv_ordered_kernel<T><<<1, kSmallBlock, 0, s>>>(A, layout, m, n, x, c);
+    launch(gemv_ordered_kernel<T>, 1, kSmallBlock, 0, s, A, layout, m, n, x, c);
     return cudaGetLastError();
 }
 

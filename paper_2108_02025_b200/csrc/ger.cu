@@ -49,6 +49,7 @@ template <typename T, int U>
 __global__ void __launch_bounds__(kGerBlock, kGerCtasPerSm)
     ger_vec_kernel(const T* __restrict__ u, const T* __restrict__ v, T* __restrict__ C,
                    uint64_t outer, uint64_t nvec, unsigned col_blocks) {
+    pdl_enter();
     const unsigned cb = blockIdx.x % col_blocks;
     const unsigned rb = blockIdx.x / col_blocks;
     const unsigned row_blocks = gridDim.x / col_blocks;
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(kGerBlock, kGerCtasPerSm)
     ger_tile_kernel(const T* __restrict__ u, const T* __restrict__ v, T* __restrict__ C,
                     uint64_t outer, uint64_t nvec, unsigned col_blocks, uint64_t tiles,
                     unsigned* __restrict__ counter) {
+    pdl_enter();
     __shared__ unsigned long long next_sh[2];
     const Vec<T>* V_ = reinterpret_cast<const Vec<T>*>(v);
     Vec<T>* Cv = reinterpret_cast<Vec<T>*>(C);
@@ -146,6 +148,7 @@ template <typename T>
 __global__ void __launch_bounds__(kGerBlock)
     ger_generic_kernel(const T* __restrict__ u, const T* __restrict__ v, T* __restrict__ C,
                        uint64_t outer, uint64_t inner) {
+    pdl_enter();
     const uint64_t total = outer * inner;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
@@ -189,10 +192,10 @@ cudaError_t ger_launch(const T* u, const T* v, T* C, uint64_t outer, uint64_t in
         const uint64_t cap = uint64_t(sm_count()) * kGerCtasPerSm;
         const unsigned grid = unsigned(tiles < cap ? tiles : cap);
         if (mode == 2)
-            ger_tile_kernel<T, kGerTileRows, true><<<grid, kGerBlock, 0, s>>>(
+            launch(ger_tile_kernel<T, kGerTileRows, true>, grid, kGerBlock, 0, s, 
                 u, v, C, outer, nvec, col_blocks, tiles, ws.counters);
         else
-            ger_tile_kernel<T, kGerTileRows, false><<<grid, kGerBlock, 0, s>>>(
+            launch(ger_tile_kernel<T, kGerTileRows, false>, grid, kGerBlock, 0, s, 
                 u, v, C, outer, nvec, col_blocks, tiles, ws.counters);
         if (info) info->ctas = grid;
     } else if (!small && vec_ok) {
@@ -203,14 +206,14 @@ cudaError_t ger_launch(const T* u, const T* v, T* C, uint64_t outer, uint64_t in
         if (row_blocks < 1) row_blocks = 1;
         if (row_blocks > outer) row_blocks = outer;
         const unsigned grid = unsigned(row_blocks * col_blocks);
-        ger_vec_kernel<T, kGerUnroll><<<grid, kGerBlock, 0, s>>>(u, v, C, outer, nvec, col_blocks);
+        launch(ger_vec_kernel<T, kGerUnroll>, grid, kGerBlock, 0, s, u, v, C, outer, nvec, col_blocks);
         if (info) info->ctas = grid;
     } else {
         const uint64_t total = outer * inner;
         uint64_t grid = small ? 1 : (total + kGerBlock - 1) / kGerBlock;
         const uint64_t cap = uint64_t(sm_count()) * 8;
         if (grid > cap) grid = cap;
-        ger_generic_kernel<T><<<unsigned(grid), kGerBlock, 0, s>>>(u, v, C, outer, inner);
+        launch(ger_generic_kernel<T>, unsigned(grid), kGerBlock, 0, s, u, v, C, outer, inner);
         if (info) info->ctas = unsigned(grid);
     }
     return cudaGetLastError();
