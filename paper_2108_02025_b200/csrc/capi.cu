@@ -160,6 +160,18 @@ int combine_impl(const T* p, uint32_t count, T alpha0, T* out, void* stream) {
 }
 
 // ------------------------------------------------------------------ GEMV
+// Row-major GEMV runs the deterministic sweep kernels (BASELINE tolerance,
+// bitwise run to run) by default; CABL_GEMV_RM_ORDER=reference selects the
+// reference-order kernel (bit for bit gemv_ref, gemv_rm_ordered.cu) wherever
+// the shape allows.  The sweep is ~14% faster on G1/G4.
+bool rm_reference_order() {
+    static const bool ref = [] {
+        const char* e = getenv("CABL_GEMV_RM_ORDER");
+        return e && std::string(e) == "reference";
+    }();
+    return ref;
+}
+
 template <typename T>
 int gemv_impl(const T* A, int layout, uint64_t m, uint64_t n, const T* x, T* c,
               uint64_t cutoff, cabl_probe* probe, void* stream) {
@@ -176,6 +188,9 @@ int gemv_impl(const T* A, int layout, uint64_t m, uint64_t n, const T* x, T* c,
     LaunchInfo info;
     if (touched <= cutoff) {
         CABL_TRY_CUDA(gemv_ordered_launch<T>(A, layout, m, n, x, c, s, &info), "gemv kernel");
+    } else if (layout == CABL_ROW_MAJOR && rm_reference_order() &&
+               gemv_rm_ordered_ok<T>(A, x, m, n)) {
+        CABL_TRY_CUDA(gemv_rm_ordered_launch<T>(A, m, n, x, c, s, &info), "gemv_rm kernel");
     } else if (layout == CABL_ROW_MAJOR) {
         WsLease lease;
         if (int rc = get_workspace(dev, s, gemv_rm_need<T>(A, x, m, n), &lease)) return rc;

@@ -1,0 +1,205 @@
+// Row-major GEMV in the REFERENCE'S ORDER: c_i += A(i,:) x, one lane per row,
+// j ascending from c_i, with the compiled reference's rounding (separately
+// rounded multiply then add; oracle/cabl_oracle.c) — bit for bit the
+// reference gemv_row_major / gemv_ref (proj/include/cabl/kernels.hpp:171-181,
+// :230-257) at full HBM bandwidth.
+//
+// A lane owns a whole row, so the row's 8192 (G1) or 65536 (G4) dependent
+// adds are one sequential chain; that chain (4 cycles per add) is shorter
+// than the time to stream the row's bytes, so the order costs no bandwidth as
+// long as the bytes arrive in time.  They arrive through shared memory:
+//   * CTA b owns a balanced contiguous range of rows (±1 row per SM) and
+//     walks it in row blocks of up to kOrdRows rows;
+//   * a producer warp streams each row block column tile by column tile into
+//     a ring of kOrdStages shared-memory stages with cp.async (one 512-byte
+//     row segment per warp instruction, plus the tile's x slice), completion
+//     counted on the stage's mbarrier;
+//   * consumer lanes read 16-byte groups of their row (row pitch padded by
+//     16 B, so a quarter-warp covers all 32 banks once) and the broadcast x
+//     group, and run the ordered multiply-add chain.
+// (The copies are LDGSTS issued by a producer warp, one 512-byte row segment
+// per warp instruction, completion tracked on the stage mbarrier.)
+// Fast-path conditions: n * s a multiple of 16 B and A, x 16-byte aligned
+// (then the reference's FMA remainder n mod (16/s) is empty), and enough
+// rows that each CTA gets a full warp of them.
+#include "bulk.cuh"
+#include "common.cuh"
+#include "kernels.cuh"
+
+#include <cstdlib>
+#include <cstring>
+
+namespace cabl_dev {
+
+namespace {
+
+constexpr int kOrdConsumerWarps = 2;
+constexpr int kOrdRows = kOrdConsumerWarps * 32; // rows per block
+constexpr int kOrdThreads = kOrdRows + 32;       // + producer warp
+
+template <typename T, int SEG, int NS> struct OrdGeom {
+    static_assert(SEG % 512 == 0, "a warp instruction moves 512 B");
+    static constexpr int kStages = NS;
+    static constexpr int kCols = SEG / int(sizeof(T));   // SEG bytes of each row per stage
+    static constexpr int kPad = 16 / int(sizeof(T));     // pitch pad: 16 B
+    static constexpr int kPitch = kCols + kPad;
+    static constexpr int kStageElems = kOrdRows * kPitch + kCols;
+    static constexpr unsigned kSmem = unsigned(NS * kStageElems * sizeof(T));
+};
+
+template <typename T> struct Vec16;
+template <> struct alignas(16) Vec16<float> {
+    float v[4];
+};
+template <> struct alignas(16) Vec16<double> {
+    double v[2];
+};
+
+template <typename T, int SEG, int NS>
+__global__ void __launch_bounds__(kOrdThreads, 1)
+    gemv_rm_ordered_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
+                           uint64_t m, uint64_t n) {
+    pdl_enter();
+    using G = OrdGeom<T, SEG, NS>;
+    constexpr int kOrdStages = NS;
+    constexpr int E = 16 / int(sizeof(T)); // elements per 16-byte group
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* stages = reinterpret_cast<T*>(smem_raw);
+    __shared__ __align__(8) uint64_t full[NS];
+    __shared__ __align__(8) uint64_t empty[NS];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const Partition part(m, gridDim.x);
+    const uint64_t r_begin = part.begin(blockIdx.x), r_end = part.begin(blockIdx.x + 1);
+    const uint64_t tiles = (n + G::kCols - 1) / G::kCols;
+
+    if (tid == 0) {
+        for (int s = 0; s < kOrdStages; ++s) {
+            mbar_init(&full[s], 32); // one cp.async arrive per producer lane
+            mbar_init(&empty[s], kOrdConsumerWarps);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == kOrdConsumerWarps) { // producer warp
+        // One LDGSTS (cp.async, 16 B per lane) moves a 512-byte row segment:
+        // a stage is `rows` + 1 (x) warp instructions.  Each lane then makes
+        // the stage's mbarrier track its own copies (.noinc arrive), so the
+        // stage completes when all 32 lanes' copies have landed.  (Bulk TMA
+        // copies of 512 B per row ran 4.8x slower: per-copy overhead.)
+        uint64_t it = 0;
+        for (uint64_t rb = r_begin; rb < r_end; rb += kOrdRows) {
+            const int rows = int((r_end - rb < uint64_t(kOrdRows)) ? r_end - rb : kOrdRows);
+            for (uint64_t t = 0; t < tiles; ++t, ++it) {
+                const int st = int(it % kOrdStages);
+                const unsigned use = unsigned(it / kOrdStages);
+                if (use > 0) mbar_wait(&empty[st], (use - 1) & 1u);
+                const uint64_t j0 = t * G::kCols;
+                const unsigned cw = unsigned((n - j0 < uint64_t(G::kCols)) ? n - j0 : G::kCols);
+                T* sb = stages + uint64_t(st) * G::kStageElems;
+#pragma unroll
+                for (int q = 0; q < SEG / 512; ++q) {
+                    const unsigned e0 = unsigned(q * 32 + lane) * E; // this lane's 16 B
+                    if (e0 < cw) {
+                        const T* src = A + rb * n + j0 + e0;
+                        for (int r = 0; r < rows; ++r, src += n)
+                            cp_async16(sb + r * G::kPitch + e0, src);
+                        cp_async16(sb + kOrdRows * G::kPitch + e0, x + j0 + e0);
+                    }
+                }
+                cp_async_mbar_arrive(&full[st]);
+            }
+        }
+        return;
+    }
+
+    // consumers: lane = one row of the current block
+    uint64_t it = 0;
+    for (uint64_t rb = r_begin; rb < r_end; rb += kOrdRows) {
+        const int rr = warp * 32 + lane;
+        const bool live = rb + rr < r_end;
+        T acc = live ? c[rb + rr] : T(0);
+        for (uint64_t t = 0; t < tiles; ++t, ++it) {
+            const int st = int(it % kOrdStages);
+            mbar_wait(&full[st], unsigned(it / kOrdStages) & 1u);
+            const uint64_t j0 = t * G::kCols;
+            const int cw = int((n - j0 < uint64_t(G::kCols)) ? n - j0 : G::kCols);
+            const T* sb = stages + uint64_t(st) * G::kStageElems;
+            const T* row = sb + rr * G::kPitch;
+            const T* xs = sb + kOrdRows * G::kPitch;
+            if (live) {
+                for (int j = 0; j < cw; j += E) {
+                    const Vec16<T> a = *reinterpret_cast<const Vec16<T>*>(row + j);
+                    const Vec16<T> xv = *reinterpret_cast<const Vec16<T>*>(xs + j);
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc = add_rn(acc, mul_rn(a.v[e], xv.v[e]));
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+        }
+        if (live) c[rb + rr] = acc;
+    }
+}
+
+} // namespace
+
+template <typename T> bool gemv_rm_ordered_ok(const T* A, const T* x, uint64_t m, uint64_t n) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(A), xp = reinterpret_cast<uintptr_t>(x);
+    return (a & 15u) == 0 && (xp & 15u) == 0 && (n * sizeof(T)) % 16 == 0 &&
+           m >= uint64_t(sm_count()) * 32;
+}
+
+namespace {
+
+template <typename T, int SEG, int NS>
+void ordered_launch_cfg(const T* A, uint64_t m, uint64_t n, const T* x, T* c, cudaStream_t s,
+                        unsigned grid) {
+
+    using G = OrdGeom<T, SEG, NS>;
+    static bool configured = [] {
+        cudaFuncSetAttribute(gemv_rm_ordered_kernel<T, SEG, NS>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
+        return true;
+    }();
+    (void)configured;
+    launch(gemv_rm_ordered_kernel<T, SEG, NS>, grid, kOrdThreads, G::kSmem, s, A, x, c, m, n);
+}
+
+// CABL_ORD_CFG=seg,stages (tuning knob): 512,5 | 1024,3 | 1536,2
+int ordered_cfg() {
+    static const int cfg = [] {
+        const char* e = std::getenv("CABL_ORD_CFG");
+        if (!e) return 1;
+        if (!std::strcmp(e, "512,5")) return 0;
+        if (!std::strcmp(e, "1536,2")) return 2;
+        return 1;
+    }();
+    return cfg;
+}
+
+} // namespace
+
+template <typename T>
+cudaError_t gemv_rm_ordered_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
+                                   cudaStream_t s, LaunchInfo* info) {
+    const uint64_t sms = uint64_t(sm_count());
+    const unsigned grid = unsigned(m < sms ? m : sms);
+    switch (ordered_cfg()) {
+    case 0: ordered_launch_cfg<T, 512, 5>(A, m, n, x, c, s, grid); break;
+    case 2: ordered_launch_cfg<T, 1536, 2>(A, m, n, x, c, s, grid); break;
+    default: ordered_launch_cfg<T, 1024, 3>(A, m, n, x, c, s, grid); break;
+    }
+    if (info) info->ctas = grid;
+    return cudaGetLastError();
+}
+
+template bool gemv_rm_ordered_ok<float>(const float*, const float*, uint64_t, uint64_t);
+template bool gemv_rm_ordered_ok<double>(const double*, const double*, uint64_t, uint64_t);
+template cudaError_t gemv_rm_ordered_launch<float>(const float*, uint64_t, uint64_t, const float*,
+                                                   float*, cudaStream_t, LaunchInfo*);
+template cudaError_t gemv_rm_ordered_launch<double>(const double*, uint64_t, uint64_t,
+                                                    const double*, double*, cudaStream_t,
+                                                    LaunchInfo*);
+
+} // namespace cabl_dev

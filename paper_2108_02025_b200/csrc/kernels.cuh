@@ -45,6 +45,13 @@ template <typename T>
 cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
                            const Workspace& ws, cudaStream_t s, LaunchInfo* info);
 
+// ---- GEMV row-major in the reference's order (gemv_rm_ordered.cu): bit for
+// bit the compiled reference gemv_row_major / gemv_ref ----
+template <typename T> bool gemv_rm_ordered_ok(const T* A, const T* x, uint64_t m, uint64_t n);
+template <typename T>
+cudaError_t gemv_rm_ordered_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
+                                   cudaStream_t s, LaunchInfo* info);
+
 // ---- GEMV col-major (gemv_cm.cu) ----
 template <typename T> WorkspaceNeed gemv_cm_need(const T* A, const T* x, uint64_t m, uint64_t n);
 template <typename T>

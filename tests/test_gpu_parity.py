@@ -116,7 +116,7 @@ def _gemv_case(cuda, dtype, m, n, layout, seed=SEED):
 
 
 RM_SHAPES = [(1, 777), (3, 3), (8, 8), (40, 200), (257, 259), (1000, 1000), (2000, 500),
-             (33, 16392), (4097, 1024), (8192, 8192)]
+             (33, 16392), (4097, 1024), (8192, 8192), (4736, 100), (5000, 1028), (9001, 3000)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -130,10 +130,32 @@ def test_gemv_row_major_matches_oracle(cuda, dtype, m, n):
         # ordered single-CTA path: bit for bit the compiled reference gemv_ref
         assert probe.threads_used == 1
         np.testing.assert_array_equal(got, want)
+    if T.rm_is_ordered(m, n, dt):
+        # reference-order kernel: bit for bit the compiled reference gemv_ref
+        np.testing.assert_array_equal(got, want)
     tol_c = T.contract_tol(n, rowabs, np.abs(c0), dt)
     assert np.all(np.abs(got.astype(np.float64) - want) <= tol_c)
     tol_t = T.truth_tol(T.gemv_rm_chain(n, dt), rowabs, np.abs(c0), dt)
     assert np.all(np.abs(got.astype(np.float64) - truth) <= tol_t)
+
+
+def test_gemv_row_major_reference_order_mode_subprocess(cuda):
+    """CABL_GEMV_RM_ORDER=reference (read once per process): rerun the
+    row-major parity cases in a child process, where tolerances.rm_is_ordered
+    turns the reference-order shapes into bitwise assertions."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("CABL_GEMV_RM_ORDER") == "reference":
+        pytest.skip("already the reference-order process")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CABL_GEMV_RM_ORDER="reference")
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-m", "gpu",
+                        "-q", "-x", "-p", "no:cacheprovider",
+                        "-k", "(row_major_matches or 65536_square) and not subprocess"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
 
 
 CM_SHAPES = [(3, 3), (8, 8), (257, 259), (1000, 1000), (256, 65536), (2047, 300),
@@ -335,6 +357,8 @@ def test_gemv_65536_square_fp32_sampled_rows(cuda):
     O.gemv_ref(An.reshape(-1), 0, xn, want)
     truth, rowabs = O.gemv_truth(An.reshape(-1), 0, xn, c0n)
     got = np_of(c)[rows]
+    if T.rm_is_ordered(m, n, np.float32):
+        np.testing.assert_array_equal(got, want)
     assert np.all(np.abs(got - want) <= T.contract_tol(n, rowabs, np.abs(c0n), np.float32))
     assert np.all(np.abs(got - truth) <=
                   T.truth_tol(T.gemv_rm_chain(n, np.float32), rowabs, np.abs(c0n), np.float32))

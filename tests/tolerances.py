@@ -25,6 +25,8 @@ from __future__ import annotations
 
 import math
 
+import os
+
 import numpy as np
 
 EPS = {np.dtype(np.float32): float(np.finfo(np.float32).eps),
@@ -69,6 +71,14 @@ def gemv_rm_chain(n: int, dtype) -> int:
     and + c_i.  A row touches at most ceil(row units / per-warp units)+1 warps;
     bounded by 64 here for every shape the tests use."""
     return math.ceil(n / 32) + 5 + 64 + 1
+
+
+def rm_is_ordered(m: int, n: int, dtype, aligned: bool = True) -> bool:
+    """csrc/gemv_rm_ordered.cu gemv_rm_ordered_ok: with CABL_GEMV_RM_ORDER=
+    reference the reference-order row-major kernel (bitwise gemv_ref) runs when
+    rows are 16-byte multiples, operands 16-byte aligned and m >= 148 * 32 (a
+    full warp of rows per CTA)."""
+    return os.environ.get("CABL_GEMV_RM_ORDER") == "reference" and aligned and (n * np.dtype(dtype).itemsize) % 16 == 0 and m >= SMS * 32
 
 
 def cm_is_tall(m: int, dtype, aligned: bool = True) -> bool:
