@@ -51,20 +51,20 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 FALLBACK_HBM_GBS = 6650.0
-FLUSH_BYTES = 512 << 20
+FLUSH_BYTES = 512 << 20  # default; run_ours takes it from the GPU plan (4 x L2, pow2)
 
 
 class L2Flush:
-    """Between timed steps: WRITE a 512 MiB buffer (> the 126 MB L2), then READ
+    """Between timed steps: WRITE a 512 MiB buffer (> 4x the 126 MB L2), then READ
     a second one.  The write evicts every line of the step's operands; the
     read then evicts the flush's own dirty lines (their write-back happens
     here, outside the timed events), so each step starts from an L2 that
     holds nothing of its inputs and nothing dirty."""
 
-    def __init__(self, dev):
+    def __init__(self, dev, nbytes: int = FLUSH_BYTES):
         import torch
-        self.w = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-        self.r = torch.zeros(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+        self.w = torch.empty(nbytes // 4, dtype=torch.float32, device=dev)
+        self.r = torch.zeros(nbytes // 4, dtype=torch.float32, device=dev)
 
     def zero_(self):
         self.w.zero_()
@@ -232,7 +232,9 @@ def step_fn(w, ins, policy, ctx, sharded_dot: bool):
     return (lambda: cb.ger(ins["x"], ins["y"], ins["C"], policy)), 1
 
 
-L2_BYTES = 126 * 1000 * 1000  # B200 L2 (torch reports 126 MB)
+# L2 capacity: replaced in run_ours by the live device's (machines: the GPU
+# descriptor, paper_2108_02025_b200/machine.py); this is B200's value.
+L2_BYTES = 126 << 20
 
 
 def l2_mode(step_bytes: int) -> str:
@@ -370,7 +372,13 @@ def run_ours(args, ctx):
     peak, peak_src = peaks()
     policy = cb.default_policy(1)
     w = WL.WORKLOADS[args.workload]
-    flush = L2Flush(ctx.dev)
+    # launch parameters from the live GPU descriptor
+    from paper_2108_02025_b200 import machine as MC
+    global L2_BYTES
+    ginfo = MC.describe_device(ctx.local)
+    gplan = MC.derive_gpu_plan(MC.load_descriptor(json.dumps(MC.descriptor_of(ginfo))))
+    L2_BYTES = gplan.l2_bytes
+    flush = L2Flush(ctx.dev, gplan.l2_flush_bytes)
 
     # ---- headline: weak scaling, every rank its own full-size block
     span = w.n if w.op == "dot" else w.m
@@ -432,12 +440,16 @@ def run_ours(args, ctx):
             "workload": f"{w.id}: {w.desc}",
             "m_per_gpu": w.m, "n": w.n, "layout": "row-major",
             "parallelism": f"row blocks over {ctx.world} GPU(s), x replicated, no collective",
-            "l2": (f"inputs larger than L2: {bytes_rank / 1e6:.0f} MB per step vs 126 MB L2, "
+            "machine": {"gpu": ginfo.name, "sms": gplan.sm_count, "l2_bytes": gplan.l2_bytes,
+                        "source": "cabl_describe_device"},
+            "l2": (f"inputs larger than L2: {bytes_rank / 1e6:.0f} MB per step vs "
+                   f"{gplan.l2_bytes / 1e6:.0f} MB L2, "
                    "steps back to back (one event pair around the K steps); ncu shows each "
                    "back-to-back launch reads its full algorithmic bytes from DRAM "
                    "(profiles/r01_ncu_b2b_*.csv)" if mode == "stream" else
-                   "flushed between steps outside the timed events: 512 MiB write, then 512 MiB "
-                   "read (no dirty lines left in L2)"),
+                   f"flushed between steps outside the timed events: {gplan.l2_flush_bytes >> 20} "
+                   f"MiB write, then {gplan.l2_flush_bytes >> 20} MiB read (no dirty lines left "
+                   "in L2)"),
             "alg_bytes_per_step_per_gpu": bytes_rank,
         },
         "roofline": {

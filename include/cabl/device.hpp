@@ -207,4 +207,50 @@ void ger(const DeviceVector<T>& x, const DeviceVector<T>& y, DeviceMatrix<T>& C,
     detail::record(probe);
 }
 
+// ------------------------------------------------- GPU machine descriptor
+// the live device described in the reference's descriptor
+// model (machine.hpp:43-53): cores = SMs, L1 = per-SM shared memory
+// (private), L2 = device L2 (shared), 128-byte lines.  It passes
+// validate_machine, so derive_blocking_plan accepts it; derive_gpu_plan gives
+// the launch parameters the library derives from the same facts.
+inline cabl_gpu_machine describe_device(int device = 0) {
+    cabl_gpu_machine g{};
+    detail::check(cabl_describe_device(device, &g));
+    return g;
+}
+
+inline MachineDescriptor gpu_machine(int device = 0, std::uint64_t element_bytes = 4) {
+    const cabl_gpu_machine g = describe_device(device);
+    constexpr std::uint64_t line = 128, l1_ways = 4, l2_ways = 16;
+    MachineDescriptor md;
+    md.levels.push_back(CacheLevel{line, l1_ways, g.smem_per_sm / (line * l1_ways), false});
+    md.levels.push_back(CacheLevel{line, l2_ways, g.l2_bytes / (line * l2_ways), true});
+    md.cores = g.sm_count;
+    md.element_bytes = element_bytes;
+    validate_machine(md);
+    return md;
+}
+
+struct GpuPlan {
+    unsigned sm_count = 0;
+    std::uint64_t l2_bytes = 0;
+    std::uint64_t queue_threshold_bytes = 0; // operands >= this use the work queues
+    std::uint64_t l2_flush_bytes = 0;        // benchmark flush buffer
+    unsigned dot_ctas = 0;
+};
+
+// same rules as paper_2108_02025_b200/machine.py derive_gpu_plan
+inline GpuPlan derive_gpu_plan(const MachineDescriptor& md) {
+    validate_machine(md);
+    GpuPlan p;
+    p.sm_count = md.cores;
+    p.l2_bytes = md.levels.back().size_bytes();
+    std::uint64_t q = 1;
+    while (q < 4 * p.l2_bytes) q <<= 1;
+    p.queue_threshold_bytes = q;
+    p.l2_flush_bytes = q;
+    p.dot_ctas = 2 * md.cores;
+    return p;
+}
+
 } // namespace cabl

@@ -82,6 +82,35 @@ CABL_API int cabl_abi_version(void);
 /* Number of usable CUDA devices (0 when none; never a CPU fallback). */
 CABL_API int cabl_device_count(void);
 
+/* ------------------------------------------------- machine descriptor ---
+ * The GPU counterpart of the reference's MachineDescriptor (machine.hpp:43-53)
+ * and its flat JSON document (descriptor_json.hpp:3-15): the device's memory
+ * hierarchy, read from the driver.  The host mirrors map it onto the
+ * reference descriptor (cores = SMs; L1 = the per-SM shared-memory capacity,
+ * L2 = the device L2, 128-byte lines) and derive the launch parameters from it
+ * (derive_gpu_plan) instead of hard-coding B200 numbers.  The library itself
+ * sizes its grids from sm_count and its work-queue threshold from l2_bytes
+ * (queue_threshold_bytes below).  Returns CABL_ECUDA when `device` is not a
+ * usable CUDA device. */
+typedef struct cabl_gpu_machine {
+    int32_t device;
+    int32_t cc_major, cc_minor;
+    uint32_t sm_count;             /* "cores" of the descriptor */
+    uint32_t max_threads_per_sm;
+    uint32_t line_bytes;           /* L1 / L2 line (128) */
+    uint64_t smem_per_sm;          /* shared memory per SM (the descriptor's L1) */
+    uint64_t smem_per_block_optin; /* largest dynamic smem one CTA may opt into */
+    uint64_t l2_bytes;
+    uint64_t hbm_bytes;
+    uint32_t mem_bus_bits;
+    uint32_t reserved;
+    uint64_t queue_threshold_bytes; /* operands >= this take the atomic work queues:
+                                       4 x L2 rounded up to a power of two */
+    char name[96];
+} cabl_gpu_machine;
+
+CABL_API int cabl_describe_device(int device, cabl_gpu_machine* out);
+
 /* ---------------------------------------------------------------- DOT ---
  * *out = alpha0 + sum_p x[p]*y[p]   (device scalar; alpha0 is added last,
  * as reference kernels.hpp:142,163 do).

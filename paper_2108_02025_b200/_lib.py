@@ -33,11 +33,22 @@ class Probe(C.Structure):
 
 _P = C.POINTER(Probe)
 
+
+class GpuMachineC(C.Structure):
+    """cabl_gpu_machine (include/cabl_cuda.h)."""
+    _fields_ = [("device", C.c_int32), ("cc_major", C.c_int32), ("cc_minor", C.c_int32),
+                ("sm_count", C.c_uint32), ("max_threads_per_sm", C.c_uint32),
+                ("line_bytes", C.c_uint32), ("smem_per_sm", C.c_uint64),
+                ("smem_per_block_optin", C.c_uint64), ("l2_bytes", C.c_uint64),
+                ("hbm_bytes", C.c_uint64), ("mem_bus_bits", C.c_uint32), ("reserved", C.c_uint32),
+                ("queue_threshold_bytes", C.c_uint64), ("name", C.c_char * 96)]
+
 # symbol -> argtypes (restype is int unless listed in _RESTYPE)
 SIGNATURES: dict[str, list] = {
     "cabl_last_error": [],
     "cabl_abi_version": [],
     "cabl_device_count": [],
+    "cabl_describe_device": [i32, C.POINTER(GpuMachineC)],
     "cabl_cuda_dot_f32": [vp, vp, u64, f32, vp, u64, _P, vp],
     "cabl_cuda_dot_f64": [vp, vp, u64, f64, vp, u64, _P, vp],
     "cabl_cuda_combine_partials_f32": [vp, u32, f32, vp, vp],

@@ -105,16 +105,12 @@ def parse_rects(spec: str) -> list[tuple[int, int]]:
 
 
 def load_descriptor(path: str):
-    """Flat JSON machine descriptor (reference descriptor_json.hpp:3-15)."""
-    from . import cabl
-    d = json.loads(Path(path).read_text())
-    levels = [cabl.CacheLevel(int(lv["line_bytes"]), int(lv["associativity"]),
-                              int(lv["num_sets"]), bool(lv.get("shared", False)))
-              for lv in d["levels"]]
-    md = cabl.MachineDescriptor(levels=levels, cores=int(d.get("cores", 1)),
-                                element_bytes=int(d.get("element_bytes", 8)))
-    cabl.validate_machine(md)
-    return md
+    """Flat JSON machine descriptor (reference descriptor_json.hpp:3-15);
+    'gpu' = the live device's descriptor (machine.py)."""
+    from . import machine
+    if path == "gpu":
+        return machine.gpu_machine(0)
+    return machine.load_descriptor_file(path)
 
 
 # ---------------------------------------------------------------------- CSV
@@ -344,7 +340,10 @@ def _peak() -> float:
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="cabl-bench (B200)",
                                  description="cache-aware level-1/2 kernel benchmark, GPU mode")
-    ap.add_argument("--machine", default=None, help="machine descriptor JSON (default: built-in)")
+    ap.add_argument("--machine", default=None,
+                    help="machine descriptor JSON, or 'gpu' for the live device (default: built-in)")
+    ap.add_argument("--describe", action="store_true",
+                    help="print the live GPU's machine descriptor JSON and exit")
     ap.add_argument("--kernel", default="all", choices=list(KERNELS) + ["all"])
     ap.add_argument("--sizes", default="256,1024,4096,16384")
     ap.add_argument("--rect", default="", help="extra MxN shapes for matrix kernels, e.g. 256x1048576")
@@ -358,6 +357,11 @@ def main(argv=None) -> int:
                     help="append the HBM traffic-model columns alg_bytes, hbm_bound_s")
     a = ap.parse_args(argv)
     try:
+        if a.describe:
+            from . import machine
+            print(json.dumps(machine.descriptor_of(machine.describe_device(0),
+                                                   4 if a.dtype == "f32" else 8), indent=2))
+            return 0
         cfg = SweepConfig(bounds=a.bounds, kernels=list(KERNELS) if a.kernel == "all" else [a.kernel],
                           sizes=parse_sizes(a.sizes), rects=parse_rects(a.rect),
                           threads=[int(t) for t in a.threads.split(",") if t.strip()],

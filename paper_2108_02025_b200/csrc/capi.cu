@@ -352,19 +352,78 @@ int host_ger(const T* x, const T* y, T* C, int layout, uint64_t m, uint64_t n, u
 } // namespace
 
 namespace cabl_dev {
-int sm_count() {
-    static std::atomic<int> cache[64];
+
+namespace {
+// per-device facts, read once from the driver (cabl_describe_device)
+struct DevFacts {
+    std::atomic<int> sms{0};
+    std::atomic<uint64_t> l2{0};
+};
+DevFacts g_facts[64];
+
+DevFacts* facts_of_current() {
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
-    int v = cache[dev].load(std::memory_order_relaxed);
-    if (v == 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    DevFacts& f = g_facts[dev];
+    if (f.sms.load(std::memory_order_acquire) == 0) {
+        int v = 0, l2 = 0;
+        if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess || l2 <= 0)
+            l2 = 0;
+        f.l2.store(uint64_t(l2), std::memory_order_relaxed);
         if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
             v = 148;
-        cache[dev].store(v, std::memory_order_relaxed);
+        f.sms.store(v, std::memory_order_release);
     }
-    return v;
+    return &f;
 }
+
+uint64_t threshold_from_l2(uint64_t l2) {
+    uint64_t t = 1;
+    while (t < 4 * l2) t <<= 1;
+    return t;
+}
+} // namespace
+
+int sm_count() {
+    DevFacts* f = facts_of_current();
+    return f ? f->sms.load(std::memory_order_acquire) : 148;
+}
+
+// Operands of at least this many bytes take the atomic work queues (DOT
+// chunks, GEMV groups/units): 4 x L2 rounded up to a power of two, 512 MiB on
+// B200 — a kernel that long (>= ~80 us) amortises the queue's atomics, one
+// that fits a few L2s does not.
+uint64_t queue_threshold_bytes() {
+    DevFacts* f = facts_of_current();
+    const uint64_t l2 = f ? f->l2.load(std::memory_order_relaxed) : 0;
+    return threshold_from_l2(l2 ? l2 : uint64_t(126) << 20);
+}
+
 } // namespace cabl_dev
+
+extern "C" int cabl_describe_device(int device, cabl_gpu_machine* out) {
+    if (!out) return fail(CABL_EINVAL, "describe_device: out must not be null");
+    cudaDeviceProp p;
+    CABL_TRY_CUDA(cudaGetDeviceProperties(&p, device), "cudaGetDeviceProperties");
+    std::memset(out, 0, sizeof(*out));
+    out->device = device;
+    out->cc_major = p.major;
+    out->cc_minor = p.minor;
+    out->sm_count = unsigned(p.multiProcessorCount);
+    out->max_threads_per_sm = unsigned(p.maxThreadsPerMultiProcessor);
+    out->line_bytes = 128;
+    out->smem_per_sm = p.sharedMemPerMultiprocessor;
+    out->smem_per_block_optin = p.sharedMemPerBlockOptin;
+    out->l2_bytes = uint64_t(p.l2CacheSize);
+    out->hbm_bytes = p.totalGlobalMem;
+    out->mem_bus_bits = unsigned(p.memoryBusWidth);
+    out->queue_threshold_bytes = cabl_dev::threshold_from_l2(out->l2_bytes);
+    std::snprintf(out->name, sizeof(out->name), "%s", p.name);
+    return CABL_OK;
+}
 
 extern "C" {
 

@@ -267,7 +267,7 @@ inline bool dot_chunked(uint64_t n, size_t s, bool small, bool vec_ok) {
     if (small || !vec_ok) return false;
     if (n / (32 / s) < uint64_t(sm_count()) * kDotCtasPerSm) return false; // grid <= vectors
     if (forced >= 0) return forced != 0;
-    return 2 * n * s >= (uint64_t(512) << 20);
+    return 2 * n * s >= queue_threshold_bytes();
 }
 
 template <typename T> WorkspaceNeed dot_need(uint64_t n, bool small) {

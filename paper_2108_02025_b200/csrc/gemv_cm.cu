@@ -629,7 +629,7 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
             const char* e = getenv("CABL_GEMV_DYN");
             return e ? atoi(e) : -1;
         }();
-        const bool dyn = forced >= 0 ? forced != 0 : m * n * sizeof(T) >= (uint64_t(512) << 20);
+        const bool dyn = forced >= 0 ? forced != 0 : m * n * sizeof(T) >= queue_threshold_bytes();
         if (dyn)
             launch(gemv_cm_tall_vec_kernel<T, true>, grid, kTallBlock, 0, s, A, x, c, m, n, ws.counters);
         else

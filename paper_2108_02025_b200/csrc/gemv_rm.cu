@@ -295,7 +295,7 @@ inline bool use_dyn_queue(uint64_t bytes) {
         return e ? atoi(e) : -1;
     }();
     if (forced >= 0) return forced != 0;
-    return bytes >= (uint64_t(512) << 20);
+    return bytes >= queue_threshold_bytes();
 }
 
 template <typename T, int R, int KV, int MINB>

@@ -29,6 +29,7 @@ struct LaunchInfo {
 };
 
 int sm_count(); // of the current device (cached per device)
+uint64_t queue_threshold_bytes(); // work-queue size rule, from the device L2 (capi.cu)
 
 // ---- DOT (dot.cu) ----
 template <typename T> WorkspaceNeed dot_need(uint64_t n, bool small);

@@ -38,7 +38,18 @@ int main() {
     ger(y, x, C, pol);
     const bool ger_ok = dC.download() == C;
 
+    // the live GPU in the reference's descriptor model
+    const MachineDescriptor gm = gpu_machine(0, sizeof(float));
+    const BlockingPlan gbp = derive_blocking_plan(gm); // the reference rules accept it
+    const GpuPlan gp = derive_gpu_plan(gm);
+    const bool mach_ok = gm.cores == describe_device(0).sm_count && gp.dot_ctas == 2 * gm.cores &&
+                         gp.queue_threshold_bytes >= 4 * gp.l2_bytes && gbp.max_threads == gm.cores;
+    std::printf("machine: %u SMs, L1 %llu B, L2 %llu B, queue threshold %llu B (%s)\n", gm.cores,
+                (unsigned long long)gm.level(0).size_bytes(),
+                (unsigned long long)gm.level(1).size_bytes(),
+                (unsigned long long)gp.queue_threshold_bytes, mach_ok ? "ok" : "MISMATCH");
+
     std::printf("gemv %s, dot %s (%.6f), ger %s\n", gemv_ok ? "ok" : "MISMATCH",
                 dd == hd ? "ok" : "MISMATCH", double(dd), ger_ok ? "ok" : "MISMATCH");
-    return (gemv_ok && dd == hd && ger_ok) ? 0 : 1;
+    return (gemv_ok && dd == hd && ger_ok && mach_ok) ? 0 : 1;
 }
