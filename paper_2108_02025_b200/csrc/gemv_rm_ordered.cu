@@ -35,7 +35,6 @@ namespace {
 
 constexpr int kOrdConsumerWarps = 2;
 constexpr int kOrdRows = kOrdConsumerWarps * 32; // rows per block
-constexpr int kOrdThreads = kOrdRows + 32;       // + producer warp
 
 template <typename T, int SEG, int NS> struct OrdGeom {
     static_assert(SEG % 512 == 0, "a warp instruction moves 512 B");
@@ -55,8 +54,8 @@ template <> struct alignas(16) Vec16<double> {
     double v[2];
 };
 
-template <typename T, int SEG, int NS>
-__global__ void __launch_bounds__(kOrdThreads, 1)
+template <typename T, int SEG, int NS, int PW>
+__global__ void __launch_bounds__(kOrdRows + 32 * PW, 1)
     gemv_rm_ordered_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                            uint64_t m, uint64_t n) {
     pdl_enter();
@@ -74,14 +73,15 @@ __global__ void __launch_bounds__(kOrdThreads, 1)
 
     if (tid == 0) {
         for (int s = 0; s < kOrdStages; ++s) {
-            mbar_init(&full[s], 32); // one cp.async arrive per producer lane
+            mbar_init(&full[s], 32 * PW); // one cp.async arrive per producer lane
             mbar_init(&empty[s], kOrdConsumerWarps);
         }
         mbar_fence_init();
     }
     __syncthreads();
 
-    if (warp == kOrdConsumerWarps) { // producer warp
+    if (warp >= kOrdConsumerWarps) { // producer warps: rows pw, pw + PW, ...
+        const int pw = warp - kOrdConsumerWarps;
         // One LDGSTS (cp.async, 16 B per lane) moves a 512-byte row segment:
         // a stage is `rows` + 1 (x) warp instructions.  Each lane then makes
         // the stage's mbarrier track its own copies (.noinc arrive), so the
@@ -101,10 +101,10 @@ __global__ void __launch_bounds__(kOrdThreads, 1)
                 for (int q = 0; q < SEG / 512; ++q) {
                     const unsigned e0 = unsigned(q * 32 + lane) * E; // this lane's 16 B
                     if (e0 < cw) {
-                        const T* src = A + rb * n + j0 + e0;
-                        for (int r = 0; r < rows; ++r, src += n)
+                        const T* src = A + (rb + pw) * n + j0 + e0;
+                        for (int r = pw; r < rows; r += PW, src += PW * n)
                             cp_async16(sb + r * G::kPitch + e0, src);
-                        cp_async16(sb + kOrdRows * G::kPitch + e0, x + j0 + e0);
+                        if (pw == 0) cp_async16(sb + kOrdRows * G::kPitch + e0, x + j0 + e0);
                     }
                 }
                 cp_async_mbar_arrive(&full[st]);
@@ -152,27 +152,31 @@ template <typename T> bool gemv_rm_ordered_ok(const T* A, const T* x, uint64_t m
 
 namespace {
 
-template <typename T, int SEG, int NS>
+template <typename T, int SEG, int NS, int PW>
 void ordered_launch_cfg(const T* A, uint64_t m, uint64_t n, const T* x, T* c, cudaStream_t s,
                         unsigned grid) {
 
     using G = OrdGeom<T, SEG, NS>;
     static bool configured = [] {
-        cudaFuncSetAttribute(gemv_rm_ordered_kernel<T, SEG, NS>,
+        cudaFuncSetAttribute(gemv_rm_ordered_kernel<T, SEG, NS, PW>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
         return true;
     }();
     (void)configured;
-    launch(gemv_rm_ordered_kernel<T, SEG, NS>, grid, kOrdThreads, G::kSmem, s, A, x, c, m, n);
+    launch(gemv_rm_ordered_kernel<T, SEG, NS, PW>, grid, kOrdRows + 32 * PW, G::kSmem, s, A, x, c,
+           m, n);
 }
 
-// CABL_ORD_CFG=seg,stages (tuning knob): 512,5 | 1024,3 | 1536,2
+// CABL_ORD_CFG=seg,stages,producer_warps (tuning knob).  G1 / G4 b2b:
+// 1024,3,1 45.8 / 2647 us (default); 1024,3,2 46.6 / 2616; 1024,3,4 50.8 /
+// 2785; 512,5,1 51.8 / 2788; 512,5,2 52.1 / 2934; 1536,2,1 51.1 / 2805.
 int ordered_cfg() {
     static const int cfg = [] {
         const char* e = std::getenv("CABL_ORD_CFG");
         if (!e) return 1;
-        if (!std::strcmp(e, "512,5")) return 0;
-        if (!std::strcmp(e, "1536,2")) return 2;
+        if (!std::strcmp(e, "512,5,1")) return 0;
+        if (!std::strcmp(e, "1024,3,1")) return 1;
+        if (!std::strcmp(e, "1024,3,2")) return 2;
         return 1;
     }();
     return cfg;
@@ -186,9 +190,9 @@ cudaError_t gemv_rm_ordered_launch(const T* A, uint64_t m, uint64_t n, const T* 
     const uint64_t sms = uint64_t(sm_count());
     const unsigned grid = unsigned(m < sms ? m : sms);
     switch (ordered_cfg()) {
-    case 0: ordered_launch_cfg<T, 512, 5>(A, m, n, x, c, s, grid); break;
-    case 2: ordered_launch_cfg<T, 1536, 2>(A, m, n, x, c, s, grid); break;
-    default: ordered_launch_cfg<T, 1024, 3>(A, m, n, x, c, s, grid); break;
+    case 0: ordered_launch_cfg<T, 512, 5, 1>(A, m, n, x, c, s, grid); break;
+    case 2: ordered_launch_cfg<T, 1024, 3, 2>(A, m, n, x, c, s, grid); break;
+    default: ordered_launch_cfg<T, 1024, 3, 1>(A, m, n, x, c, s, grid); break;
     }
     if (info) info->ctas = grid;
     return cudaGetLastError();
