@@ -139,10 +139,12 @@ def test_gemv_row_major_matches_oracle(cuda, dtype, m, n):
     assert np.all(np.abs(got.astype(np.float64) - truth) <= tol_t)
 
 
-def test_gemv_row_major_reference_order_mode_subprocess(cuda):
+@pytest.mark.parametrize("cfg", ["", "tma"])
+def test_gemv_row_major_reference_order_mode_subprocess(cuda, cfg):
     """CABL_GEMV_RM_ORDER=reference (read once per process): rerun the
     row-major parity cases in a child process, where tolerances.rm_is_ordered
-    turns the reference-order shapes into bitwise assertions."""
+    turns the reference-order shapes into bitwise assertions.  cfg "tma" runs
+    the tensor-map producer variant (CABL_ORD_CFG=tma)."""
     import os
     import subprocess
     import sys
@@ -150,6 +152,8 @@ def test_gemv_row_major_reference_order_mode_subprocess(cuda):
         pytest.skip("already the reference-order process")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, CABL_GEMV_RM_ORDER="reference")
+    if cfg:
+        env["CABL_ORD_CFG"] = cfg
     r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-m", "gpu",
                         "-q", "-x", "-p", "no:cacheprovider",
                         "-k", "(row_major_matches or 65536_square) and not subprocess"],
