@@ -51,13 +51,16 @@ __global__ void __launch_bounds__(BLOCK, MINB)
         const uint64_t nvec = n / V;
         const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
         const Vec<T>* Y = reinterpret_cast<const Vec<T>*>(y);
-        const uint64_t per_iter = uint64_t(BLOCK) * U;
-        const uint64_t stride = uint64_t(gridDim.x) * per_iter;
-        for (uint64_t base = uint64_t(blockIdx.x) * per_iter; base < nvec; base += stride) {
+        // thread-level grid stride: with T threads in the grid, thread t takes
+        // vectors t, t + T, t + 2T, ... (U of them in flight per iteration), so
+        // every thread's share is within one vector of every other's and the
+        // grid sweeps the operands front to back in T-vector slabs
+        const uint64_t T_all = uint64_t(gridDim.x) * BLOCK;
+        for (uint64_t k0 = uint64_t(blockIdx.x) * BLOCK + tid; k0 < nvec; k0 += U * T_all) {
             Vec<T> xv[U], yv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const uint64_t i = base + uint64_t(u) * BLOCK + tid;
+                const uint64_t i = k0 + uint64_t(u) * T_all;
                 if (i < nvec) {
                     xv[u] = ld_stream(X + i);
                     yv[u] = ld_stream(Y + i);
@@ -251,6 +254,7 @@ cudaError_t dot_dispatch(unsigned grid, const T* x, const T* y, uint64_t n, int 
     CABL_DOT_CASE(512, 4, 2)
     CABL_DOT_CASE(1024, 2, 1)
     CABL_DOT_CASE(1024, 4, 1)
+    CABL_DOT_CASE(256, 8, 1)
 #undef CABL_DOT_CASE
     return dot_go<T, kDotBlock, kDotUnroll, kDotCtasPerSm>(grid, x, y, n, vec_ok, alpha0, out,
                                                           partials, ticket, s);
