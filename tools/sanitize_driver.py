@@ -5,6 +5,7 @@ shapes, for compute-sanitizer (memcheck / racecheck / synccheck):
     compute-sanitizer --tool memcheck python tools/sanitize_driver.py
 
 Paths: DOT small / main / chunked (forced) / unaligned; GEMV row-major
+(with CABL_GEMV_RM_ORDER=reference also the reference-order kernel)
 ordered / segment / sweep (static and queue) / scalar; col-major ordered /
 tall vec (static and queue) / tall scalar / 2-D split vec / 2-D split scalar /
 bulk-copy split; GER tile queue / static / generic; the fills and the
@@ -36,7 +37,7 @@ def main():
             ok &= bool(torch.isfinite(torch.tensor(cb.dot(x[:n], y[:n], 0.5, pol))))
             ok &= bool(torch.isfinite(torch.tensor(cb.dot(x[1:n + 1], y[2:n + 2], 0.5, pol))))
         # GEMV row-major: ordered, segment, sweep, scalar
-        for m, n in ((3, 5), (40, 1024), (2, 65536), (7200, 256), (3000, 999)):
+        for m, n in ((3, 5), (40, 1024), (2, 65536), (7200, 256), (3000, 999), (5000, 1028)):
             A = cb.DenseMatrix.wrap(f(m * n, dt, 3), m, n, cb.Layout.RowMajor)
             c = f(m, dt, 4)
             cb.gemv_row_major(A, f(n, dt, 1), c, pol)
