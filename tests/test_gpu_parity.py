@@ -154,9 +154,9 @@ def test_gemv_row_major_reference_order_mode_subprocess(cuda, cfg):
     env = dict(os.environ, CABL_GEMV_RM_ORDER="reference")
     if cfg:
         env["CABL_ORD_CFG"] = cfg
-    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-m", "gpu",
-                        "-q", "-x", "-p", "no:cacheprovider",
-                        "-k", "(row_major_matches or 65536_square) and not subprocess"],
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py",
+                        "tests/test_gpu_bounds.py", "-m", "gpu", "-q", "-x", "-p", "no:cacheprovider",
+                        "-k", "(row_major_matches or 65536_square or gemv_guard) and not subprocess"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
