@@ -480,6 +480,9 @@ def _time_host_loop(fn, steps, warmup, ctx):
     return ctx.max(time.perf_counter() - t0)
 
 
+E2E_DEPTH = 4
+
+
 def run_e2e(w, ins, policy, ctx, args):
     """End-to-end through the public API, host<->device copies inside the
     timed loop, wall clock (max over ranks).  Two usage patterns:
@@ -522,10 +525,14 @@ def run_e2e(w, ins, policy, ctx, args):
         return full, None
 
     # resident operator: A stays in HBM, x and c stream in, c streams out —
-    # the public GemvPipeline (2 steps in flight), one CUDA-graph replay per
-    # step; every step's result is read back before its buffers are reused
+    # the public GemvPipeline (E2E_DEPTH independent requests in flight, one
+    # stream each), one CUDA-graph replay per step; every step's result is
+    # read back before its buffers are reused.  G1 on B200 (tools/e2e_depth.py):
+    # depth 1 73.2 us/step, 2 42.5, 3 35.9, 4 35.9 — from depth 3 the next
+    # request's kernel fills the SMs the previous one's tail leaves idle
+    # (the same with a distinct copy of A per request, so not L2 sharing)
     from paper_2108_02025_b200.operators import GemvPipeline
-    pipe = GemvPipeline(ins["A"], policy, depth=2)
+    pipe = GemvPipeline(ins["A"], policy, depth=E2E_DEPTH)
     for op in pipe.ops:
         op.x_host.copy_(ins["x"].cpu())
         op.c_host.copy_(ins["c"].cpu())
@@ -549,10 +556,11 @@ def run_e2e(w, ins, policy, ctx, args):
                 "h2d_bytes_per_step": (op0.x_host.numel() + op0.c_host.numel()) * w.s,
                 "d2h_bytes_per_step": op0.out_host.numel() * w.s, "steps": steps_r,
                 "ms_per_step": round(t_res / steps_r * 1e3, 4),
-                "pattern": "resident operator, 2 steps in flight: A uploaded once before "
-                           "timing; every step H2D x, c from pinned host, GEMV kernel, D2H c "
-                           "(one CUDA graph replay); each result is waited for before its "
-                           "buffers are reused; wall clock over all K steps",
+                "pattern": f"resident operator, {E2E_DEPTH} independent requests in flight "
+                           "(one stream each): A uploaded once before timing; every step H2D "
+                           "x, c from pinned host, GEMV kernel, D2H c (one CUDA graph replay); "
+                           "each result is waited for before its buffers are reused; wall "
+                           "clock over all K steps",
                 "api": "paper_2108_02025_b200.operators.GemvPipeline -> cabl_cuda_gemv_rm_f32"}
     return resident, full
 

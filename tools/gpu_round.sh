@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_bounds.py tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider -k "guard or subprocess" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python tools/e2e_depth.py > gpurun_out/e2e_depth.jsonl 2>&1
+timeout 600 python tools/e2e_depth.py --distinct >> gpurun_out/e2e_depth.jsonl 2>&1
