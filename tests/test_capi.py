@@ -123,3 +123,22 @@ def test_dense_matrix_indexing_matches_reference_layout():
     cm = cb.DenseMatrix(2, 3, cb.Layout.ColMajor)
     assert rm.index(1, 2) == 2 + 1 * 3   # j + i*cols
     assert cm.index(1, 2) == 1 + 2 * 2   # i + j*rows
+
+
+def test_product_never_touches_the_oracle():
+    """The oracle is test infrastructure: the package sources never import it
+    and the shipped library links none of its objects."""
+    import re
+    import subprocess
+    pkg = ROOT / "paper_2108_02025_b200"
+    for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")):
+        text = f.read_text()
+        assert not re.search(r"^\s*(from|import)\s+oracle\b", text, re.M), f
+        assert not re.search(r"#\s*include\s*[<\"][^>\"]*oracle", text), f
+        assert "libcabl_oracle" not in text and "libcabl_ref" not in text, f
+    needed = subprocess.run(["readelf", "-d", str(pkg / "libcabl_cuda.so")],
+                            capture_output=True, text=True).stdout
+    assert "oracle" not in needed and "cabl_ref" not in needed
+    syms = subprocess.run(["nm", "-D", "--defined-only", str(pkg / "libcabl_cuda.so")],
+                          capture_output=True, text=True).stdout
+    assert "dot_ref" not in syms and "gemv_ref" not in syms and "ger_ref" not in syms
