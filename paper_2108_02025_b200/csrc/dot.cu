@@ -35,8 +35,19 @@ template <typename T, int BLOCK, int U, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB)
     dot_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t n, int vec_ok,
                T alpha0, T* __restrict__ out, T* __restrict__ partials,
-               unsigned* __restrict__ ticket) {
-    pdl_enter();
+               unsigned* __restrict__ ticket, int pf) {
+    pdl_trigger();
+    if (pf > 0 && vec_ok && threadIdx.x < 2 * U) { // warm L2: this CTA's first U slabs of x and y
+        const uint64_t nvec = n / Vec<T>::N;
+        const uint64_t T_all = uint64_t(gridDim.x) * BLOCK;
+        const uint64_t v0 = uint64_t(blockIdx.x) * BLOCK + uint64_t(threadIdx.x >> 1) * T_all;
+        if (v0 < nvec) {
+            const uint64_t cnt = nvec - v0 < uint64_t(BLOCK) ? nvec - v0 : uint64_t(BLOCK);
+            const T* base = (threadIdx.x & 1) ? y : x;
+            prefetch_l2_bulk(base + v0 * Vec<T>::N, unsigned(cnt * sizeof(Vec<T>)));
+        }
+    }
+    pdl_wait();
     __shared__ T red[32];
     __shared__ bool am_last;
     constexpr int V = Vec<T>::N;
@@ -236,7 +247,8 @@ template <typename T> unsigned dot_grid(uint64_t n, bool small) {
 template <typename T, int B, int U, int M>
 cudaError_t dot_go(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok, T alpha0,
                    T* out, T* partials, unsigned* ticket, cudaStream_t s) {
-    launch(dot_kernel<T, B, U, M>, grid, B, 0, s, x, y, n, vec_ok, alpha0, out, partials, ticket);
+    launch(dot_kernel<T, B, U, M>, grid, B, 0, s, x, y, n, vec_ok, alpha0, out, partials, ticket,
+           pdl_prefetch_enabled());
     return cudaGetLastError();
 }
 
