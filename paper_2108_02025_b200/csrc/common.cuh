@@ -197,7 +197,8 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* src, unsigned bytes
 }
 
 // CABL_PDL_PREFETCH=0 disables the pre-wait L2 prefetch (A/B measurement).
-// D1 back to back: 22.5 -> 21.9 us with it; the GEMV sweep is neutral.
+// D1 back to back: 22.5 -> 21.9 us with it; the GEMV sweep is neutral; on
+// GER (R1) it cost 0.7 us, so GER does not prefetch.
 inline int pdl_prefetch_enabled() {
     static const int on = [] {
         const char* e = getenv("CABL_PDL_PREFETCH");
