@@ -55,6 +55,13 @@ int current_device(int* dev) {
 }
 
 // ---------------------------------------------------------------- scratch
+// Keyed by (device, stream handle).  A destroyed stream may still be running
+// a kernel that uses its scratch when the driver hands the same handle to a
+// new stream; the entry therefore remembers the stream's process-unique ID
+// (cudaStreamGetId) and a call that finds a different ID gets a fresh entry
+// (the old buffers are abandoned, never freed under a running kernel).  The
+// ID cannot be queried while a stream is capturing a graph; captured calls
+// use the entry their warm-up call created.
 struct WsKey {
     int device;
     cudaStream_t stream;
@@ -66,7 +73,8 @@ struct WsKey {
 
 struct WsEntry {
     Workspace ws;
-    std::mutex mu; // held from scratch sizing to kernel enqueue (WsLease)
+    unsigned long long stream_id = 0; // 0 = not yet known
+    std::mutex mu;                    // held from scratch sizing to kernel enqueue (WsLease)
 };
 
 std::mutex g_ws_mu;
@@ -89,14 +97,29 @@ int get_workspace(int device, cudaStream_t s, const WorkspaceNeed& need, WsLease
         out->ws = Workspace{};
         return CABL_OK;
     }
+    unsigned long long sid = 0;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
+        cudaGetLastError();
+        cap = cudaStreamCaptureStatusActive; // cannot tell: do not query the ID
+    }
+    if (cap == cudaStreamCaptureStatusNone && cudaStreamGetId(s, &sid) != cudaSuccess) {
+        cudaGetLastError();
+        sid = 0;
+    }
     WsKey key{device, s, s == cudaStreamPerThread ? std::this_thread::get_id() : std::thread::id()};
     WsEntry* ent;
     {
         std::lock_guard<std::mutex> lk(g_ws_mu);
         auto& m = ws_map();
         auto it = m.find(key);
-        if (it == m.end()) it = m.emplace(key, new WsEntry()).first;
+        if (it == m.end()) {
+            it = m.emplace(key, new WsEntry()).first;
+        } else if (sid != 0 && it->second->stream_id != 0 && it->second->stream_id != sid) {
+            it->second = new WsEntry(); // handle reused by a new stream: abandon the old entry
+        }
         ent = it->second;
+        if (sid != 0) ent->stream_id = sid;
     }
     out->lock = std::unique_lock<std::mutex>(ent->mu);
     Workspace& ws = ent->ws;
