@@ -25,6 +25,7 @@ with the reference's message text (the reference throws
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import enum
 import math
@@ -265,6 +266,13 @@ def _ptr(t: torch.Tensor):
     return t.data_ptr() if t.numel() else None
 
 
+def _on_device(dev: torch.device):
+    """The C ABI launches on the current CUDA device: make it the operands'."""
+    if dev.index is None or dev.index == torch.cuda.current_device():
+        return contextlib.nullcontext()
+    return torch.cuda.device(dev)
+
+
 def _stream_of(t: torch.Tensor):
     return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
 
@@ -273,6 +281,8 @@ def _check_same(ts, what: str) -> tuple[str, bool]:
     dev = {t.device.type for t in ts}
     if len(dev) != 1:
         raise ValueError(f"{what}: operands must all be on the host or all on the GPU")
+    if len({t.device for t in ts}) != 1:
+        raise ValueError(f"{what}: CUDA operands must be on one device")
     dts = {t.dtype for t in ts}
     if len(dts) != 1:
         raise ValueError(f"{what}: operands must share one dtype")
@@ -294,8 +304,9 @@ def dot_into(x: torch.Tensor, y: torch.Tensor, alpha0: float, out: torch.Tensor,
     sfx, cuda = _check_same([x, y, out], "dot")
     _require(cuda, "dot_into: operands must be CUDA tensors")
     p = Probe()
-    _lib.call(f"cabl_cuda_dot_{sfx}", _ptr(x), _ptr(y), x.numel(), float(alpha0),
-              out.data_ptr(), policy.plan.dot_cutoff, C.byref(p), _stream_of(x))
+    with _on_device(x.device):
+        _lib.call(f"cabl_cuda_dot_{sfx}", _ptr(x), _ptr(y), x.numel(), float(alpha0),
+                  out.data_ptr(), policy.plan.dot_cutoff, C.byref(p), _stream_of(x))
     _record(p)
 
 
@@ -332,8 +343,9 @@ def _gemv(A: DenseMatrix, x, c, policy: ExecPolicy, layout: Layout, who: str) ->
     m, n = A.rows(), A.cols()
     if cuda:
         tag = "rm" if layout == Layout.RowMajor else "cm"
-        _lib.call(f"cabl_cuda_gemv_{tag}_{sfx}", _ptr(A.data), m, n, _ptr(x), _ptr(c),
-                  policy.plan.dot_cutoff, C.byref(p), _stream_of(c))
+        with _on_device(c.device):
+            _lib.call(f"cabl_cuda_gemv_{tag}_{sfx}", _ptr(A.data), m, n, _ptr(x), _ptr(c),
+                      policy.plan.dot_cutoff, C.byref(p), _stream_of(c))
     else:
         _lib.call(f"cabl_host_gemv_{sfx}", _ptr(A.data), int(layout), m, n, _ptr(x), _ptr(c),
                   policy.plan.dot_cutoff, C.byref(p), None)
@@ -366,8 +378,9 @@ def ger(x, y, C_: DenseMatrix, policy: ExecPolicy) -> None:
     m, n = C_.rows(), C_.cols()
     if cuda:
         tag = "rm" if C_.layout() == Layout.RowMajor else "cm"
-        _lib.call(f"cabl_cuda_ger_{tag}_{sfx}", _ptr(x), _ptr(y), _ptr(C_.data), m, n,
-                  policy.plan.dot_cutoff, C.byref(p), _stream_of(C_.data))
+        with _on_device(C_.data.device):
+            _lib.call(f"cabl_cuda_ger_{tag}_{sfx}", _ptr(x), _ptr(y), _ptr(C_.data), m, n,
+                      policy.plan.dot_cutoff, C.byref(p), _stream_of(C_.data))
     else:
         _lib.call(f"cabl_host_ger_{sfx}", _ptr(x), _ptr(y), _ptr(C_.data), int(C_.layout()),
                   m, n, policy.plan.dot_cutoff, C.byref(p), None)
@@ -382,16 +395,18 @@ def ger(x, y, C_: DenseMatrix, policy: ExecPolicy) -> None:
 def fill_uniform(t: torch.Tensor, seed: int, stream_id: int, offset: int = 0) -> torch.Tensor:
     sfx = _suffix(t)
     _require(t.is_cuda and t.is_contiguous(), "fill_uniform: needs a contiguous CUDA tensor")
-    _lib.call(f"cabl_cuda_fill_uniform_{sfx}", _ptr(t), t.numel(), seed, stream_id, offset,
-              _stream_of(t))
+    with _on_device(t.device):
+        _lib.call(f"cabl_cuda_fill_uniform_{sfx}", _ptr(t), t.numel(), seed, stream_id, offset,
+                  _stream_of(t))
     return t
 
 
 def fill_normal(t: torch.Tensor, seed: int, stream_id: int, offset: int = 0) -> torch.Tensor:
     _require(t.dtype == torch.float64, "fill_normal: float64 only")
     _require(t.is_cuda and t.is_contiguous(), "fill_normal: needs a contiguous CUDA tensor")
-    _lib.call("cabl_cuda_fill_normal_f64", _ptr(t), t.numel(), seed, stream_id, offset,
-              _stream_of(t))
+    with _on_device(t.device):
+        _lib.call("cabl_cuda_fill_normal_f64", _ptr(t), t.numel(), seed, stream_id, offset,
+                  _stream_of(t))
     return t
 
 
