@@ -45,8 +45,9 @@ def _device_partial(x, y, out, policy):
 def _device_combine(partials: torch.Tensor, alpha0: float, out: torch.Tensor) -> None:
     from . import _lib
     sfx = cabl._suffix(partials)
-    _lib.call(f"cabl_cuda_combine_partials_{sfx}", partials.data_ptr(), partials.numel(),
-              float(alpha0), out.data_ptr(), cabl._stream_of(partials))
+    with cabl._on_device(partials.device):
+        _lib.call(f"cabl_cuda_combine_partials_{sfx}", partials.data_ptr(), partials.numel(),
+                  float(alpha0), out.data_ptr(), cabl._stream_of(partials))
 
 
 def sharded_dot(x_local: torch.Tensor, y_local: torch.Tensor, alpha0: float, out: torch.Tensor,
