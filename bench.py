@@ -298,8 +298,13 @@ def time_steps(fn, steps, warmup, ctx, flush, sampler=None, mode="flush"):
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_reference_sample(w, max_bytes=1 << 30, reps=5, threads=None):
-    """Time the compiled reference (oracle/_ref) on a bounded sample of w."""
+_CPU_INPUTS: dict = {}
+
+
+def cpu_reference_sample(w, max_bytes=1 << 30, reps=5, threads=None, naive=False):
+    """Time the compiled reference (oracle/_ref) on a bounded sample of w:
+    its threaded path (cabl::dot / gemv_* / ger), or with naive=True its
+    naive oracle (dot_ref / gemv_ref / ger_ref, one thread)."""
     import numpy as np
 
     from oracle import oracle as O
@@ -308,8 +313,16 @@ def cpu_reference_sample(w, max_bytes=1 << 30, reps=5, threads=None):
     kind = "reference" if O.ref_available() else "port"
     npdt = np.float32 if w.dtype_name == "f32" else np.float64
     s = np.dtype(npdt).itemsize
-    gen = (lambda n, st, off=0: O.gen_normal_f64(n, WL.SEED, st, off)) if w.dist == "normal" \
+    gen0 = (lambda n, st, off=0: O.gen_normal_f64(n, WL.SEED, st, off)) if w.dist == "normal" \
         else (lambda n, st, off=0: O.gen_uniform(n, npdt, WL.SEED, st, off))
+
+    def gen(n, st, off=0):  # the last config's inputs are kept for the next path
+        key = (w.dist, w.dtype_name, n, st, off)
+        if key not in _CPU_INPUTS:
+            if len(_CPU_INPUTS) >= 3:
+                _CPU_INPUTS.clear()
+            _CPU_INPUTS[key] = gen0(n, st, off)
+        return _CPU_INPUTS[key]
     if w.op == "dot":
         n = min(w.n, max_bytes // (2 * s))
         m = 0
@@ -341,9 +354,9 @@ def cpu_reference_sample(w, max_bytes=1 << 30, reps=5, threads=None):
         else:
             sess = O.RefSession(w.op, npdt, 0 if w.op == "gemv-row" else 1, m, n, A, x, c,
                                 cores=cores)
-        times = O.time_ref(sess, use_ref=False, threads=cores, reps=reps)
+        used = 1 if naive else cores
+        times = O.time_ref(sess, use_ref=naive, threads=used, reps=reps)
         sess.close()
-        used = cores
     else:  # restated oracle, single thread
         used = 1
         for _ in range(reps):
@@ -358,7 +371,8 @@ def cpu_reference_sample(w, max_bytes=1 << 30, reps=5, threads=None):
     t = statistics.median(times)
     return {"value": round(alg / t / 1e9, 3), "unit": "GB/s", "cores": used, "kind": kind,
             "sample": f"{sample}, median of {reps} after 1 warm-up"
-                      + (", reference threaded path (ExecPolicy threads=%d)" % used
+                      + ((", reference naive oracle (1 thread)" if naive else
+                          ", reference threaded path (ExecPolicy threads=%d)" % used)
                          if kind == "reference" else ", restated oracle (1 thread)"),
             "median_s": t}
 
@@ -686,12 +700,37 @@ def run_reference(args, ctx):
     print(json.dumps(line), flush=True)
 
 
+def run_cpu_table(args):
+    """--cpu-table: the compiled reference on the host cores for every
+    BASELINE config at full size: threaded path at
+    1 thread and at all cores, and the naive oracle; one JSON line per
+    measurement.  Configs whose inputs would not fit 1/3 of free host memory
+    are sampled (rows or length cut) and say so."""
+    import psutil
+
+    from paper_2108_02025_b200 import workloads as WL
+    avail = psutil.virtual_memory().available
+    cores = os.cpu_count() or 1
+    for wid, w in WL.WORKLOADS.items():
+        full = w.alg_bytes(1)
+        cap = min(full, avail // 3)
+        reps = 5 if full < (1 << 31) else 3
+        for label, threads, naive in (("threads=1", 1, False), (f"threads={cores}", cores, False),
+                                      ("naive oracle", 1, True)):
+            r = cpu_reference_sample(w, max_bytes=cap, reps=reps, threads=threads, naive=naive)
+            r.update({"config": wid, "desc": w.desc, "path": label,
+                      "full_size": cap >= full})
+            print(json.dumps(r), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-table", action="store_true",
+                    help="time the compiled reference on the host for every config and exit")
     ap.add_argument("--workload", default="G1")
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -707,6 +746,10 @@ def main():
         args.warmup = 3
 
     world, rank, local = dist_env()
+    if args.cpu_table:
+        if rank == 0:
+            run_cpu_table(args)
+        return
     if args.impl == "reference":
         ctx = Ctx(world, rank, local, None)
         run_reference(args, ctx)
