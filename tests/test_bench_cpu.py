@@ -38,3 +38,18 @@ def test_gpu_arm_refuses_without_gpu():
                        capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 2
     assert "no CUDA device" in r.stdout
+
+
+@pytest.mark.parametrize("wid", ["D1", "G1", "R1", "G3"])
+def test_cpu_reference_sample_paths(wid):
+    """The --cpu-table leg on a small sample of each op: the threaded path and
+    the naive oracle both run and report algorithmic GB/s."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_2108_02025_b200 import workloads as WL
+    w = WL.WORKLOADS[wid]
+    for naive in (False, True):
+        r = bench.cpu_reference_sample(w, max_bytes=4 << 20, reps=1, threads=2, naive=naive)
+        assert r["value"] > 0 and r["unit"] == "GB/s"
+        assert r["cores"] == (1 if naive or r["kind"] == "port" else 2)
+        assert ("naive oracle" in r["sample"]) == (naive and r["kind"] == "reference")
