@@ -260,12 +260,12 @@ __global__ void __launch_bounds__(kSplitBlock, 1)
 // column tiles are contiguous in a col-major matrix (tc consecutive columns =
 // tc*m*s bytes), so one elected producer thread streams each tile into a ring
 // of kBulkStages shared-memory stages with a single cp.async.bulk (TMA engine;
-// completion counted on an mbarrier), keeping up to 3 x 64 KB per SM in flight
+// completion counted on an mbarrier), keeping up to 3 x 48 KB per SM in flight
 // without spending registers on it (the tile's x slice rides in the same
-// stage).  Measured equal to the register-load kernel below (311.9 vs 312.0 us
-// on 256 x 2^20 fp64); it is the default because it frees the consumer
-// threads' registers and scales its bytes in flight with shared memory.  16 consumer warps = (row-vector lane,
-// column lane) pairs read their 32-byte row vectors from the stage and FMA into
+// stage).  On 256 x 2^20 fp64 back to back: 299.1 us at 3 x 48 KB against
+// 311.0 us for the register-load kernel below — the bytes in flight per SM
+// are set exactly by the ring, not by register pressure.  16 consumer warps =
+// (row-vector lane, column lane) pairs read their 32-byte row vectors from the stage and FMA into
 // register accumulators, then free the stage (one arrive per warp).  Tiles go
 // to CTAs in grid-stride (sweep) order; the per-row combine is the same as
 // the register kernel's: column lanes in smem in order, then the CTA
@@ -510,8 +510,11 @@ struct BulkCfg {
 
 inline BulkCfg bulk_cfg() {
     static const BulkCfg c = [] {
-        BulkCfg b{3, 65536}; // measured on 256 x 2^20 fp64: 3x64 KB 311.9 us, 4x48 313.3,
-                             // 6x32 322.4, 12x16 338.7 (fewer, larger stages win)
+        // measured on 256 x 2^20 fp64, back to back (tools/b2b.py): the sweet
+        // spot is ~128-160 KB in flight per SM in stages of >= 48 KB —
+        // 3x48 KB 299.1 us, 2x80 299.7, 4x36 299.7, 3x40 300.2, 2x64 300.9,
+        // 3x64 307.0, 4x48 308.1, 2x48 311.8, 6x32 315.1
+        BulkCfg b{3, 49152};
         if (const char* e = getenv("CABL_BULK")) { // "stages,KiB" (tuning only)
             int st = 6, kb = 32;
             if (sscanf(e, "%d,%d", &st, &kb) == 2) b = BulkCfg{st, unsigned(kb) * 1024u};
@@ -652,12 +655,16 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         const dim3 grid(g.grid, g.row_tiles);
         if (path == kPathBulk) {
             const BulkCfg bc = bulk_cfg();
-            if (bc.stages == 6 && bc.stage_bytes == 32768)
+            if (bc.stages == 3 && bc.stage_bytes == 65536)
+                bulk_go<T, 3, 65536>(A, x, c, m, n, g, tc, partials, ws.counters, s);
+            else if (bc.stages == 2 && bc.stage_bytes == 81920)
+                bulk_go<T, 2, 81920>(A, x, c, m, n, g, tc, partials, ws.counters, s);
+            else if (bc.stages == 6 && bc.stage_bytes == 32768)
                 bulk_go<T, 6, 32768>(A, x, c, m, n, g, tc, partials, ws.counters, s);
             else if (bc.stages == 4 && bc.stage_bytes == 49152)
                 bulk_go<T, 4, 49152>(A, x, c, m, n, g, tc, partials, ws.counters, s);
             else
-                bulk_go<T, 3, 65536>(A, x, c, m, n, g, tc, partials, ws.counters, s);
+                bulk_go<T, 3, 49152>(A, x, c, m, n, g, tc, partials, ws.counters, s);
         } else if (path == kPathSplitVec) {
             launch(gemv_cm_split_vec_kernel<T>, grid, kSplitBlock, 0, s, 
                 A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);

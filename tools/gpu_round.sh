@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-(lscpu | head -20; free -g; nproc) > gpurun_out/host.txt 2>&1
-timeout 1800 python bench.py --cpu-table > gpurun_out/cpu_table.jsonl 2> gpurun_out/cpu_table.err; echo "rc=$?" >> gpurun_out/cpu_table.err
+timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python tools/b2b.py G3 G2 > gpurun_out/tune22.jsonl 2>&1
