@@ -490,17 +490,19 @@ def test_resident_gemv_operator_graph_equals_direct_call(cuda):
                 assert torch.equal(got, want.cpu())
 
 
-def test_gemv_pipeline_results_in_order(cuda):
-    """operators.GemvPipeline: with 2 steps in flight every step's result is
-    the GEMV of that step's inputs (no buffer reuse before read-back)."""
+@pytest.mark.parametrize("depth", [2, 4])
+def test_gemv_pipeline_results_in_order(cuda, depth):
+    """operators.GemvPipeline: with `depth` steps in flight (bench.py's e2e
+    runs 4) every step's result is the GEMV of that step's inputs (no buffer
+    reuse before read-back), returned in submission order."""
     import paper_2108_02025_b200 as cb
     from paper_2108_02025_b200.operators import GemvPipeline
     m, n = 4096, 4096
     A = cb.DenseMatrix.wrap(dev_uniform(m * n, torch.float32, 3, cuda), m, n, cb.Layout.RowMajor)
     pol = policy()
-    pipe = GemvPipeline(A, pol, depth=2)
-    xs = [dev_uniform(n, torch.float32, 30 + k, cuda) for k in range(6)]
-    cs = [dev_uniform(m, torch.float32, 40 + k, cuda) for k in range(6)]
+    pipe = GemvPipeline(A, pol, depth=depth)
+    xs = [dev_uniform(n, torch.float32, 30 + k, cuda) for k in range(9)]
+    cs = [dev_uniform(m, torch.float32, 40 + k, cuda) for k in range(9)]
     wants = []
     for x, c in zip(xs, cs):
         w = c.clone()
@@ -512,7 +514,7 @@ def test_gemv_pipeline_results_in_order(cuda):
         if r is not None:
             got.append(r.clone())
     got += [r.clone() for r in pipe.drain()]
-    assert len(got) == 6
+    assert len(got) == 9
     for g, w in zip(got, wants):
         assert torch.equal(g, w)
 
