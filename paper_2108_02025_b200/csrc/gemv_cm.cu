@@ -371,6 +371,132 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     if (tid == 0) *ticket = 0u;
 }
 
+// Bulk-copy split kernel for short-wide matrices whose rows do not form
+// 32-byte vectors (m % V != 0, or A only 16-byte aligned): the column tiles
+// are still contiguous, so the same single-producer bulk ring streams them
+// (tc a multiple of 16/s keeps every full tile and its x slice whole 16-byte
+// units; a ragged last tile's odd tail is read from global memory).
+// Consumers read scalars: thread (rl, cl) owns rows rl + k*row_lanes (k <
+// RPT = ceil(m / 512), row_lanes = min(m, 512)) and columns j = cl, cl + col_lanes, ...
+// of each tile, in order (rpt chosen per m, bulk_scalar_rpt).  The combine
+// is the vector kernel's.  Short-wide odd m, ~2 GiB, flushed: fp32 m = 255 /
+// 257 / 1001 in 94 / 90 / 100 us (5.4-6.0 TB/s); the 2-D scalar split kernel
+// below took 141 / 254 / 150 us.
+template <typename T, int kBulkStages, unsigned kBulkStageBytes, int RPT>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+    gemv_cm_split_bulk_scalar_kernel(const T* __restrict__ A, const T* __restrict__ x,
+                                     T* __restrict__ c, uint64_t m, uint64_t n, int row_lanes,
+                                     int tc, int x_bulk, T* __restrict__ partials,
+                                     unsigned* __restrict__ ticket) {
+    pdl_enter();
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* stages = reinterpret_cast<T*>(smem_raw);
+    constexpr unsigned kBulkStageStride = kBulkStageBytes + kBulkXBytes;
+    T* comb = reinterpret_cast<T*>(smem_raw + kBulkStages * kBulkStageStride);
+    __shared__ __align__(8) uint64_t full[kBulkStages];
+    __shared__ __align__(8) uint64_t empty[kBulkStages];
+    __shared__ bool am_last;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint64_t tiles = (n + tc - 1) / tc;
+    const uint64_t stage_elems = kBulkStageStride / sizeof(T);
+    const uint64_t x_off = kBulkStageBytes / sizeof(T);
+    const int col_lanes = kBulkConsumers / row_lanes;
+
+    if (tid == 0) {
+        for (int s = 0; s < kBulkStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kBulkConsumerWarps);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == kBulkConsumerWarps) {
+        if (lane == 0) { // producer
+            const uint64_t pol = l2_evict_first_policy();
+            uint64_t it = 0;
+            for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+                const int st = int(it % kBulkStages);
+                const unsigned use = unsigned(it / kBulkStages);
+                if (use > 0) mbar_wait(&empty[st], (use - 1) & 1u);
+                const uint64_t col0 = t * tc;
+                const uint64_t cols = (n - col0 < uint64_t(tc)) ? n - col0 : uint64_t(tc);
+                const unsigned bytes = unsigned(cols * m * sizeof(T)) & ~15u;
+                const unsigned xbytes =
+                    (x_bulk && cols == uint64_t(tc)) ? unsigned(cols * sizeof(T)) : 0u;
+                mbar_arrive_expect_tx(&full[st], bytes + xbytes);
+                if (bytes) bulk_g2s(stages + st * stage_elems, A + col0 * m, bytes, &full[st], pol);
+                if (xbytes) bulk_g2s(stages + st * stage_elems + x_off, x + col0, xbytes, &full[st], pol);
+            }
+        }
+    } else {
+        const int rl = tid % row_lanes, cl = tid / row_lanes;
+        const bool live = cl < col_lanes;
+        const unsigned mm = unsigned(m); // < kSplitMaxRows: 32-bit smem indexing
+        bool rok[RPT];
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) rok[k] = unsigned(rl) + unsigned(k * row_lanes) < mm;
+        T acc[RPT];
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) acc[k] = T(0);
+        uint64_t it = 0;
+        for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            const int st = int(it % kBulkStages);
+            mbar_wait(&full[st], unsigned(it / kBulkStages) & 1u);
+            const uint64_t col0 = t * tc;
+            const int cols = int((n - col0 < uint64_t(tc)) ? n - col0 : uint64_t(tc));
+            const T* sb = stages + st * stage_elems;
+            if (live) {
+                if (cols == tc) { // full tile: everything is in the stage
+                    const T* xs = x_bulk ? sb + x_off : nullptr;
+                    unsigned e = unsigned(cl) * mm + unsigned(rl);
+                    const unsigned step = unsigned(col_lanes) * mm;
+#pragma unroll 4
+                    for (int j = cl; j < cols; j += col_lanes, e += step) {
+                        const T xj = xs ? xs[j] : __ldg(x + col0 + j);
+#pragma unroll
+                        for (int k = 0; k < RPT; ++k)
+                            if (rok[k]) acc[k] = fma_rn(sb[e + unsigned(k * row_lanes)], xj, acc[k]);
+                    }
+                } else { // ragged last tile: its odd tail was not bulk-copied
+                    const uint64_t in_smem =
+                        (uint64_t(cols) * m * sizeof(T) & ~uint64_t(15)) / sizeof(T);
+                    for (int j = cl; j < cols; j += col_lanes) {
+                        const T xj = __ldg(x + col0 + j);
+#pragma unroll
+                        for (int k = 0; k < RPT; ++k)
+                            if (rok[k]) {
+                                const uint64_t e = uint64_t(j) * m + rl + uint64_t(k) * row_lanes;
+                                const T a = e < in_smem ? sb[e] : __ldg(A + col0 * m + e);
+                                acc[k] = fma_rn(a, xj, acc[k]);
+                            }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+        }
+        if (live)
+#pragma unroll
+            for (int k = 0; k < RPT; ++k)
+                if (rok[k]) comb[uint64_t(cl) * m + rl + uint64_t(k) * row_lanes] = acc[k];
+    }
+    __syncthreads();
+    for (uint64_t r = tid; r < m; r += blockDim.x) {
+        T v = comb[r];
+        for (int q = 1; q < col_lanes; ++q) v = add_rn(v, comb[uint64_t(q) * m + r]);
+        partials[uint64_t(blockIdx.x) * m + r] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    split_final(partials, c, m, m, gridDim.x, comb);
+    if (tid == 0) *ticket = 0u;
+}
+
 // Scalar split kernel (any m, any alignment), 2-D like the vector one: row
 // tile blockIdx.y of mt rows, column part blockIdx.x.  Thread layout
 // row_lanes x col_lanes = kSplitBlock, row_lanes a power of two >=
@@ -524,9 +650,9 @@ inline BulkCfg bulk_cfg() {
     return c;
 }
 
-template <typename T> SplitGeom split_bulk_geom(uint64_t m, uint64_t n, int* tc) {
+template <typename T>
+SplitGeom split_bulk_geom(uint64_t m, uint64_t n, int* tc, BulkCfg bc = bulk_cfg()) {
     SplitGeom g;
-    const BulkCfg bc = bulk_cfg();
     const uint64_t mv = m / Vec<T>::N;
     uint64_t rl = 1;
     while (rl < mv) rl *= 2;
@@ -560,6 +686,38 @@ void bulk_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const SplitGe
         A, x, c, m, n, g.row_lanes, tc, partials, ticket);
 }
 
+// Rows per consumer thread for the scalar bulk kernel: with row_lanes =
+// ceil(m / rpt) and col_lanes = 512 / row_lanes, a thread's share of a tile
+// is rpt / col_lanes of its columns; take the smallest (ties: fewer rows).
+// 257 rows: 1 -> 1 x 1 lane set, 4 -> 65 x 7 (4/7 of a tile per thread).
+inline int bulk_scalar_rpt(uint64_t m) {
+    int best = 0;
+    double best_work = 1e30;
+    for (int r : {1, 2, 4}) {
+        const uint64_t rl = (m + r - 1) / r;
+        if (rl > uint64_t(kBulkConsumers)) continue;
+        const double work = double(r) / double(uint64_t(kBulkConsumers) / rl);
+        if (work < best_work - 1e-12) {
+            best_work = work;
+            best = r;
+        }
+    }
+    return best ? best : 4;
+}
+
+template <typename T, int RPT>
+void bulk_scalar_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const SplitGeom& g,
+                    int tc, int x_bulk, T* partials, unsigned* ticket, cudaStream_t s) {
+    static bool configured = [] {
+        cudaFuncSetAttribute(gemv_cm_split_bulk_scalar_kernel<T, 3, 49152, RPT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(bulk_smem(3, 49152)));
+        return true;
+    }();
+    (void)configured;
+    launch(gemv_cm_split_bulk_scalar_kernel<T, 3, 49152, RPT>, g.grid, kBulkThreads,
+           bulk_smem(3, 49152), s, A, x, c, m, n, g.row_lanes, tc, x_bulk, partials, ticket);
+}
+
 inline int split_mode() {
     static const int v = [] {
         const char* e = getenv("CABL_CM_SPLIT");
@@ -572,7 +730,8 @@ template <typename T> bool tall_vec_ok(const T* A, const T* c, uint64_t m) {
     return aligned32(A) && aligned32(c) && m % Vec<T>::N == 0;
 }
 
-enum CmPath { kPathTallVec, kPathTallScalar, kPathBulk, kPathSplitVec, kPathSplitScalar };
+enum CmPath { kPathTallVec, kPathTallScalar, kPathBulk, kPathBulkScalar, kPathSplitVec,
+              kPathSplitScalar };
 
 // The bit-exact tall kernels keep each row's sum on one thread, so their
 // parallelism is m/V threads: they are used only when that fills the GPU
@@ -587,11 +746,20 @@ template <typename T> CmPath cm_path(const T* A, const T* c, uint64_t m) {
         return kPathTallScalar;
     }
     if (split_vec_ok(A, m)) return (m < kSplitMaxRows && split_mode() == 1) ? kPathBulk : kPathSplitVec;
+    if (m < kSplitMaxRows && split_mode() == 1 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0)
+        return kPathBulkScalar;
     return kPathSplitScalar;
 }
 
 template <typename T> SplitGeom cm_split_geom(CmPath p, uint64_t m, uint64_t n, int* tc) {
     if (p == kPathBulk) return split_bulk_geom<T>(m, n, tc);
+    if (p == kPathBulkScalar) {
+        SplitGeom g = split_bulk_geom<T>(m, n, tc, BulkCfg{3, 49152}); // tc, grid, smem
+        g.rpt = bulk_scalar_rpt(m);
+        g.row_lanes = int((m + g.rpt - 1) / g.rpt);
+        g.col_lanes = kBulkConsumers / g.row_lanes;
+        return g;
+    }
     if (p == kPathSplitVec) return split_vec_geom<T>(m, n);
     return split_geom<T>(m, n);
 }
@@ -665,6 +833,16 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
                 bulk_go<T, 4, 49152>(A, x, c, m, n, g, tc, partials, ws.counters, s);
             else
                 bulk_go<T, 3, 49152>(A, x, c, m, n, g, tc, partials, ws.counters, s);
+        } else if (path == kPathBulkScalar) {
+            // default ring shape only (3 x 48 KB); x rides in the ring when it
+            // is 16-byte aligned
+            const int x_bulk = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+            if (g.rpt == 1)
+                bulk_scalar_go<T, 1>(A, x, c, m, n, g, tc, x_bulk, partials, ws.counters, s);
+            else if (g.rpt == 2)
+                bulk_scalar_go<T, 2>(A, x, c, m, n, g, tc, x_bulk, partials, ws.counters, s);
+            else
+                bulk_scalar_go<T, 4>(A, x, c, m, n, g, tc, x_bulk, partials, ws.counters, s);
         } else if (path == kPathSplitVec) {
             launch(gemv_cm_split_vec_kernel<T>, grid, kSplitBlock, 0, s, 
                 A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);

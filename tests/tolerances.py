@@ -94,12 +94,13 @@ def cm_is_tall(m: int, dtype, aligned: bool = True) -> bool:
 def gemv_cm_chain(m: int, n: int, dtype) -> int:
     """Tall kernels: one sequential chain per row over all n columns (the
     reference order).  Split kernels (csrc/gemv_cm.cu): <= 148 column parts,
-    each thread a chain over <= ceil(n / G) columns, <= 32 column-lane adds,
-    then the G part partials summed in order, + c_i."""
+    each thread a chain over <= ceil(n / G) columns, then its column lanes
+    summed in order (< 512 adds in the bulk kernels, where a row can have up
+    to 512 column lanes), the G part partials summed in order, + c_i."""
     if cm_is_tall(m, dtype):
         return n + 1
     G = max(1, min(SMS, n))
-    return math.ceil(n / G) + 32 + G + 2
+    return math.ceil(n / G) + 512 + G + 2
 
 
 def truth_tol(chain: int, sumabs, c0abs, dtype):
