@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "col_major or guard or cm or modes" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python tools/cm_odd.py > gpurun_out/cm_odd.jsonl 2>&1
+timeout 600 python tools/odd_shapes.py > gpurun_out/odd.jsonl 2>&1
