@@ -271,6 +271,82 @@ __global__ void __launch_bounds__(kRmBlock)
     }
 }
 
+// Short rows (n*s <= rm_lane_max_bytes() = 4 KiB, e.g. 2^20 x 64): one THREAD per
+// row, in the reference's order and rounding — acc = c_i, then for j
+// ascending a separately rounded multiply and add (an FMA for the trailing
+// n mod 16/s terms), exactly gemv_ref (reference kernels.hpp:171-181): bit
+// for bit the compiled reference at bandwidth, because a short row's chain is
+// short.  Adjacent rows are adjacent in memory, so a warp's loads cover one
+// contiguous 32-row block; the 256 B L2 promotion turns each lane's 32-byte
+// requests into full bursts.  U loads in flight per thread; x comes through L1
+// (every lane of a warp reads the same x vector).  The sweep kernels spend a
+// 256-thread CTA per group of 4 rows.  256 MiB of A, flushed, sweep -> this
+// kernel: fp32 n = 1 / 16 / 64 / 256 / 1024: 0.11 / 0.07 / 0.27 / 1.0 / 3.3
+// -> 4.1 / 6.2 / 4.8 / 4.3 / 4.4 TB/s; at 8 KiB rows the sweep is ahead.
+template <typename T, bool VEC, int U>
+__global__ void __launch_bounds__(kRmBlock)
+    gemv_rm_lane_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
+                        uint64_t m, uint64_t n) {
+    pdl_enter();
+    constexpr uint64_t kRefVec = 16 / sizeof(T);
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
+        T acc = c[i];
+        if constexpr (VEC) { // n % V == 0, 32-byte aligned rows: every term is mul + add
+            constexpr int V = Vec<T>::N;
+            const Vec<T>* a = reinterpret_cast<const Vec<T>*>(A + i * n);
+            const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
+            const uint64_t nv = n / V;
+            uint64_t k = 0;
+            for (; k + U <= nv; k += U) {
+                Vec<T> av[U], xv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    av[u] = ld_stream(a + k + u);
+                    xv[u] = ld_reuse(X + k + u);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int e = 0; e < V; ++e) acc = add_rn(acc, mul_rn(av[u].v[e], xv[u].v[e]));
+            }
+            for (; k < nv; ++k) {
+                const Vec<T> av = ld_stream(a + k), xv = ld_reuse(X + k);
+#pragma unroll
+                for (int e = 0; e < V; ++e) acc = add_rn(acc, mul_rn(av.v[e], xv.v[e]));
+            }
+        } else {
+            const T* a = A + i * n;
+            const uint64_t cut = (n / kRefVec) * kRefVec;
+            uint64_t j = 0;
+            for (; j + U <= cut; j += U) {
+                T av[U], xv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    av[u] = __ldcs(a + j + u);
+                    xv[u] = __ldg(x + j + u);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(av[u], xv[u]));
+            }
+            for (; j < cut; ++j) acc = add_rn(acc, mul_rn(__ldcs(a + j), __ldg(x + j)));
+            for (; j < n; ++j) acc = fma_rn(__ldcs(a + j), __ldg(x + j), acc);
+        }
+        c[i] = acc;
+    }
+}
+
+// Row bytes up to which one thread per row beats the CTA-wide sweeps
+// (CABL_RM_LANE_MAX overrides, tuning only).  gemv_rm_is_lane (kernels.cuh)
+// adds the row-count condition.
+inline uint64_t rm_lane_max_bytes() {
+    static const uint64_t v = [] {
+        const char* e = getenv("CABL_RM_LANE_MAX");
+        return e ? uint64_t(atoll(e)) : uint64_t(4096);
+    }();
+    return v;
+}
+
 template <typename T> bool rm_vec_ok(const T* A, const T* x, uint64_t n) {
     return aligned32(A) && aligned32(x) && (n % Vec<T>::N == 0);
 }
@@ -278,11 +354,16 @@ template <typename T> bool rm_vec_ok(const T* A, const T* x, uint64_t n) {
 // -1 scalar, 0 segment-balanced warps, 1 sweep for short rows, 2 sweep for
 // long rows.  CABL_GEMV_RM_MODE overrides (tuning / tests only).
 template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n) {
-    if (!rm_vec_ok(A, x, n)) return -1;
+    const bool vec = rm_vec_ok(A, x, n);
     static const int forced = [] {
         const char* e = getenv("CABL_GEMV_RM_MODE");
         return e ? atoi(e) : -2;
     }();
+    // one thread per row (3 vector loads, 4 scalar loads): short rows, and
+    // enough of them to give every SM a few warps
+    const bool lane = gemv_rm_is_lane(m, n, sizeof(T));
+    if (forced == 3 || (forced < 0 && lane)) return vec ? 3 : 4;
+    if (!vec) return -1;
     if (forced >= 0 && forced <= 2) return forced;
     // measured (tools/tune.py, 8192^2 and 65536^2 fp32): 4 rows x 2 vectors
     // per thread at 2 CTAs/SM for rows of <= 2 CTA passes, 2 rows x 8 vectors
@@ -367,10 +448,15 @@ unsigned sweep_launch(const T* A, const T* x, T* c, uint64_t m, uint64_t n, int 
 
 } // namespace
 
+bool gemv_rm_is_lane(uint64_t m, uint64_t n, size_t elem) {
+    return n * elem <= rm_lane_max_bytes() && m >= uint64_t(sm_count()) * 64;
+}
+
 template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n) {
     WorkspaceNeed w;
     if (m == 0 || n == 0) return w;
     const int mode = rm_mode<T>(A, x, m, n);
+    if (mode >= 3) return w; // lane-per-row kernels: no scratch
     if (mode >= 1) {
         w.counters = 1; // group counter of the dynamic sweep
         return w;
@@ -388,7 +474,16 @@ cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
     if (info) info->ctas = 0;
     if (m == 0 || n == 0) return cudaSuccess; // c += 0
     const int mode = rm_mode<T>(A, x, m, n);
-    if (mode >= 1) {
+    if (mode >= 3) {
+        const uint64_t cap = uint64_t(sm_count()) * 8;
+        const uint64_t need = (m + kRmBlock - 1) / kRmBlock;
+        const unsigned grid = unsigned(need < cap ? need : cap);
+        if (mode == 3)
+            launch(gemv_rm_lane_kernel<T, true, 2>, grid, kRmBlock, 0, s, A, x, c, m, n);
+        else
+            launch(gemv_rm_lane_kernel<T, false, 8>, grid, kRmBlock, 0, s, A, x, c, m, n);
+        if (info) info->ctas = grid;
+    } else if (mode >= 1) {
         const unsigned grid = sweep_launch<T>(A, x, c, m, n, mode, ws.counters, s);
         if (info) info->ctas = grid;
     } else if (mode == 0) {

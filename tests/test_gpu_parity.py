@@ -116,7 +116,10 @@ def _gemv_case(cuda, dtype, m, n, layout, seed=SEED):
 
 
 RM_SHAPES = [(1, 777), (3, 3), (8, 8), (40, 200), (257, 259), (1000, 1000), (2000, 500),
-             (33, 16392), (4097, 1024), (8192, 8192), (4736, 100), (5000, 1028), (9001, 3000)]
+             (33, 16392), (4097, 1024), (8192, 8192), (4736, 100), (5000, 1028), (9001, 3000),
+             # short rows: one thread per row (bitwise), vector and scalar loads
+             (9472, 64), (100_000, 16), (20_001, 5), (9472, 256), (30_000, 255), (1 << 18, 1),
+             (9472, 1024), (12_000, 999)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -130,8 +133,8 @@ def test_gemv_row_major_matches_oracle(cuda, dtype, m, n):
         # ordered single-CTA path: bit for bit the compiled reference gemv_ref
         assert probe.threads_used == 1
         np.testing.assert_array_equal(got, want)
-    if T.rm_is_ordered(m, n, dt):
-        # reference-order kernel: bit for bit the compiled reference gemv_ref
+    if T.rm_is_ordered(m, n, dt) or T.rm_is_lane(m, n, dt):
+        # reference-order kernels: bit for bit the compiled reference gemv_ref
         np.testing.assert_array_equal(got, want)
     tol_c = T.contract_tol(n, rowabs, np.abs(c0), dt)
     assert np.all(np.abs(got.astype(np.float64) - want) <= tol_c)

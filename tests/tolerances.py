@@ -81,6 +81,13 @@ def rm_is_ordered(m: int, n: int, dtype, aligned: bool = True) -> bool:
     return os.environ.get("CABL_GEMV_RM_ORDER") == "reference" and aligned and (n * np.dtype(dtype).itemsize) % 16 == 0 and m >= SMS * 32
 
 
+def rm_is_lane(m: int, n: int, dtype) -> bool:
+    """csrc/gemv_rm.cu gemv_rm_is_lane: rows of <= 4 KiB and >= 148 * 64 of
+    them take the one-thread-per-row kernel — the reference's order and
+    rounding, so bitwise gemv_ref at any alignment."""
+    return n * np.dtype(dtype).itemsize <= 4096 and m >= SMS * 64
+
+
 def cm_is_tall(m: int, dtype, aligned: bool = True) -> bool:
     """csrc/gemv_cm.cu cm_path: the bit-exact tall kernels run when m/V >= 148
     units of 256 row vectors (V = 32/s, aligned, m % V == 0) or, otherwise,
