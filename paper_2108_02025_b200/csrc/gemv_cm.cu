@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     const uint64_t tiles = (n + tc - 1) / tc;
     const uint64_t stage_elems = kBulkStageStride / sizeof(T);
     const uint64_t x_off = kBulkStageBytes / sizeof(T); // x slice after the A tile
+    const bool x_stage = uint64_t(tc) * sizeof(T) <= kBulkXBytes;
     const int col_lanes = kBulkConsumers / row_lanes;
 
     if (tid == 0) {
@@ -319,9 +320,11 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
                 const uint64_t col0 = t * tc;
                 const uint64_t cols = (n - col0 < uint64_t(tc)) ? n - col0 : uint64_t(tc);
                 const unsigned bytes = unsigned(cols * m * sizeof(T));
-                // x slice: a full tile's is a multiple of 16 B (tc is); a ragged
-                // last tile's x is read with plain loads by the consumers
-                const unsigned xbytes = cols == uint64_t(tc) ? unsigned(cols * sizeof(T)) : 0u;
+                // x slice: a full tile's is a multiple of 16 B (tc is) and rides
+                // in the stage when it fits the slot (tc * s <= kBulkXBytes); a
+                // ragged last tile's, or a wider one's, is read with plain loads
+                const unsigned xbytes = (cols == uint64_t(tc) && x_stage)
+                                            ? unsigned(cols * sizeof(T)) : 0u;
                 mbar_arrive_expect_tx(&full[st], bytes + xbytes);
                 bulk_g2s(stages + st * stage_elems, A + col0 * m, bytes, &full[st], pol);
                 if (xbytes) bulk_g2s(stages + st * stage_elems + x_off, x + col0, xbytes, &full[st], pol);
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
             if (live) {
                 for (int j = cl; j < cols; j += col_lanes) {
                     const Vec<T> a = *reinterpret_cast<const Vec<T>*>(sb + uint64_t(j) * m + uint64_t(rl) * V);
-                    const T xj = cols == tc ? sb[x_off + j] : __ldg(x + col0 + j);
+                    const T xj = (cols == tc && x_stage) ? sb[x_off + j] : __ldg(x + col0 + j);
 #pragma unroll
                     for (int e = 0; e < V; ++e) acc.v[e] = fma_rn(a.v[e], xj, acc.v[e]);
                 }
@@ -422,8 +425,9 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
                 const uint64_t col0 = t * tc;
                 const uint64_t cols = (n - col0 < uint64_t(tc)) ? n - col0 : uint64_t(tc);
                 const unsigned bytes = unsigned(cols * m * sizeof(T)) & ~15u;
-                const unsigned xbytes =
-                    (x_bulk && cols == uint64_t(tc)) ? unsigned(cols * sizeof(T)) : 0u;
+                const unsigned xbytes = (x_bulk && cols == uint64_t(tc) &&
+                                         uint64_t(tc) * sizeof(T) <= kBulkXBytes)
+                                            ? unsigned(cols * sizeof(T)) : 0u;
                 mbar_arrive_expect_tx(&full[st], bytes + xbytes);
                 if (bytes) bulk_g2s(stages + st * stage_elems, A + col0 * m, bytes, &full[st], pol);
                 if (xbytes) bulk_g2s(stages + st * stage_elems + x_off, x + col0, xbytes, &full[st], pol);
@@ -448,7 +452,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
             const T* sb = stages + st * stage_elems;
             if (live) {
                 if (cols == tc) { // full tile: everything is in the stage
-                    const T* xs = x_bulk ? sb + x_off : nullptr;
+                    const T* xs =
+                        (x_bulk && uint64_t(tc) * sizeof(T) <= kBulkXBytes) ? sb + x_off : nullptr;
                     unsigned e = unsigned(cl) * mm + unsigned(rl);
                     const unsigned step = unsigned(col_lanes) * mm;
 #pragma unroll 4
