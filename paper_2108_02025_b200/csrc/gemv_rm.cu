@@ -133,13 +133,21 @@ __global__ void __launch_bounds__(kRmBlock, kRmCtasPerSm)
             arrived = __shfl_sync(0xffffffffu, arrived, 0);
             if (arrived == unsigned(wl - wf)) {
                 __threadfence();
-                if (lane < rows) {
+                // the row's warp partials, lane-strided (lane l sums warps wf + l,
+                // wf + l + 32, ... in order), then the fixed butterfly: a row
+                // split over thousands of warps (m = 1..64) no longer pays one
+                // dependent L2 round trip per warp (2^0 x 2^26 fp32: 870 us)
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (r >= rows) break;
                     T total = T(0);
-                    for (uint64_t w = wf; w <= wl; ++w) {
+#pragma unroll 4
+                    for (uint64_t w = wf + lane; w <= wl; w += kWarp) {
                         const int wh = (g == part.begin(w) / geo.S) ? 0 : 1;
-                        total = add_rn(total, ld_cg(slots + (w * 2 + wh) * R + lane));
+                        total = add_rn(total, ld_cg(slots + (w * 2 + wh) * R + r));
                     }
-                    c[row0 + lane] = add_rn(c[row0 + lane], total);
+                    total = warp_sum(total);
+                    if (lane == 0) c[row0 + r] = add_rn(c[row0 + r], total);
                 }
                 if (lane == 0) tickets[wf] = 0u;
             }
