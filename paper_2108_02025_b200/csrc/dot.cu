@@ -147,14 +147,22 @@ __global__ void __launch_bounds__(BLOCK, MINB)
 // trailing elements, then alpha0.  The result depends on n only — not on
 // the grid, the scheduling, or the GPU's SM count — and every rounding chain
 // is short (<= kChunkVecs/(BLOCK*U) vectors per accumulator).
-constexpr uint64_t kChunkVecs = 65536; // default: 2 MiB of x and 2 MiB of y (fp32)
+constexpr uint64_t kChunkVecs = 65536; // at most 2 MiB of x and 2 MiB of y (fp32)
 
-inline uint64_t chunk_vecs() { // CABL_DOT_CHUNK (vectors per chunk): tuning only
-    static const uint64_t v = [] {
+// Vectors per chunk: the largest power of two <= nvec / 2048, clamped to
+// [4096, kChunkVecs] — at least 2048 chunks, so the queue balances even at
+// the 512 MiB threshold (2^26 fp32 had 128 chunks for 148 SMs: 6.4 TB/s), and
+// a function of n alone, so the result still is.  CABL_DOT_CHUNK overrides
+// (tuning only).
+inline uint64_t chunk_vecs(uint64_t nvec) {
+    static const uint64_t forced = [] {
         const char* e = getenv("CABL_DOT_CHUNK");
-        return e ? uint64_t(atoll(e)) : kChunkVecs;
+        return e ? uint64_t(atoll(e)) : uint64_t(0);
     }();
-    return v;
+    if (forced) return forced;
+    uint64_t c = 4096;
+    while (c * 2 <= kChunkVecs && c * 2 * 2048 <= nvec) c *= 2;
+    return c;
 }
 
 template <typename T, int BLOCK, int U, int MINB>
@@ -304,7 +312,8 @@ inline bool dot_chunked(uint64_t n, size_t s, bool small, bool vec_ok) {
 template <typename T> WorkspaceNeed dot_need(uint64_t n, bool small) {
     WorkspaceNeed w;
     w.counters = 2;
-    const uint64_t chunks = (n / Vec<T>::N + chunk_vecs() - 1) / chunk_vecs();
+    const uint64_t cv = chunk_vecs(n / Vec<T>::N);
+    const uint64_t chunks = (n / Vec<T>::N + cv - 1) / cv;
     const uint64_t g = dot_grid<T>(n, small);
     w.scratch_bytes = size_t(chunks > g ? chunks : g) * sizeof(T);
     return w;
@@ -315,11 +324,12 @@ cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, boo
                        const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
     const int vec_ok = aligned32(x) && aligned32(y);
     if (dot_chunked(n, sizeof(T), small, vec_ok)) {
-        const uint64_t chunks = (n / Vec<T>::N + chunk_vecs() - 1) / chunk_vecs();
+        const uint64_t cv = chunk_vecs(n / Vec<T>::N);
+    const uint64_t chunks = (n / Vec<T>::N + cv - 1) / cv;
         const uint64_t cap = uint64_t(sm_count()) * kDotCtasPerSm;
         const unsigned grid = unsigned(chunks < cap ? chunks : cap);
         launch(dot_chunk_kernel<T, kDotBlock, kDotUnroll, kDotCtasPerSm>, grid, kDotBlock, 0, s, 
-            x, y, n, alpha0, out, static_cast<T*>(ws.scratch), ws.counters, chunk_vecs());
+            x, y, n, alpha0, out, static_cast<T*>(ws.scratch), ws.counters, cv);
         if (info) info->ctas = grid;
         return cudaGetLastError();
     }

@@ -144,53 +144,48 @@ __global__ void __launch_bounds__(kGerBlock, kGerCtasPerSm)
     }
 }
 
+// Any alignment, any width (the vector tile kernels need 32-byte-aligned
+// rows of >= kGerMinVecs vectors): C flattened, slabs of kGerBlock *
+// kGerFlatU consecutive elements in grid-stride (sweep) order; thread t takes
+// elements t, t + kGerBlock, ... of a slab — coalesced whatever the row width
+// — with all kGerFlatU loads of C (and y, x from L1) issued before any store.
+// A thread divides once per slab for its (row, column) and then steps by the
+// precomputed kGerBlock / inner, kGerBlock % inner.  One FMA per element:
+// bitwise ger_ref like every other path.  (Row tiles of 4096 columns, the
+// previous fallback, left short rows mostly idle: 256 x 262144 col-major fp32
+// ran at 1.2 TB/s.)
+constexpr int kGerFlatU = 16;
+
 template <typename T>
 __global__ void __launch_bounds__(kGerBlock)
-    ger_generic_kernel(const T* __restrict__ u, const T* __restrict__ v, T* __restrict__ C,
-                       uint64_t outer, uint64_t inner) {
+    ger_flat_kernel(const T* __restrict__ u, const T* __restrict__ v, T* __restrict__ C,
+                    uint64_t outer, uint64_t inner, uint64_t step_o, uint64_t step_i) {
     pdl_enter();
+    constexpr uint64_t kSlab = uint64_t(kGerBlock) * kGerFlatU;
     const uint64_t total = outer * inner;
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
-        const uint64_t o = e / inner, i = e - o * inner;
-        C[e] = fma_rn(u[o], v[i], C[e]);
-    }
-}
-
-// Any alignment / odd widths with rows of >= kGerBlock elements: tiles of
-// one row x (kGerBlock * kGerScalarU) columns in grid-stride (sweep) order;
-// each thread issues kGerScalarU coalesced scalar loads of C (and of y, from
-// L1) before it writes any of them back.  One FMA per element, so the bits
-// equal every other path's (ger_ref).  The flattened kernel above did one
-// element per step with a 64-bit division and ran odd widths at ~3 TB/s;
-// 8192 x 8193 fp32 now takes 131 us (4.1 TB/s), misaligned 8192^2 121 us.
-constexpr int kGerScalarU = 16;
-
-template <typename T>
-__global__ void __launch_bounds__(kGerBlock)
-    ger_rows_kernel(const T* __restrict__ u, const T* __restrict__ v, T* __restrict__ C,
-                    uint64_t outer, uint64_t inner, uint64_t chunks) {
-    pdl_enter();
-    constexpr uint64_t kChunk = uint64_t(kGerBlock) * kGerScalarU;
-    const uint64_t tiles = outer * chunks;
-    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const uint64_t o = t / chunks;
-        const uint64_t j0 = (t - o * chunks) * kChunk + threadIdx.x;
-        const T uo = __ldg(u + o);
-        T* row = C + o * inner;
-        T cv[kGerScalarU], vv[kGerScalarU];
+    for (uint64_t s0 = uint64_t(blockIdx.x) * kSlab; s0 < total; s0 += uint64_t(gridDim.x) * kSlab) {
+        const uint64_t e0 = s0 + threadIdx.x;
+        uint64_t o = e0 / inner, i = e0 - o * inner;
+        T cv[kGerFlatU], vv[kGerFlatU], uo[kGerFlatU];
 #pragma unroll
-        for (int k = 0; k < kGerScalarU; ++k) {
-            const uint64_t j = j0 + uint64_t(k) * kGerBlock;
-            if (j < inner) {
-                cv[k] = __ldcs(row + j);
-                vv[k] = __ldg(v + j);
+        for (int k = 0; k < kGerFlatU; ++k) {
+            const uint64_t e = e0 + uint64_t(k) * kGerBlock;
+            if (e < total) {
+                cv[k] = __ldcs(C + e);
+                vv[k] = __ldg(v + i);
+                uo[k] = __ldg(u + o);
+            }
+            o += step_o; // advance (o, i) by kGerBlock elements
+            i += step_i;
+            if (i >= inner) {
+                i -= inner;
+                ++o;
             }
         }
 #pragma unroll
-        for (int k = 0; k < kGerScalarU; ++k) {
-            const uint64_t j = j0 + uint64_t(k) * kGerBlock;
-            if (j < inner) __stcs(row + j, fma_rn(uo, vv[k], cv[k]));
+        for (int k = 0; k < kGerFlatU; ++k) {
+            const uint64_t e = e0 + uint64_t(k) * kGerBlock;
+            if (e < total) __stcs(C + e, fma_rn(uo[k], vv[k], cv[k]));
         }
     }
 }
@@ -246,21 +241,14 @@ cudaError_t ger_launch(const T* u, const T* v, T* C, uint64_t outer, uint64_t in
         const unsigned grid = unsigned(row_blocks * col_blocks);
         launch(ger_vec_kernel<T, kGerUnroll>, grid, kGerBlock, 0, s, u, v, C, outer, nvec, col_blocks);
         if (info) info->ctas = grid;
-    } else if (!small && inner >= uint64_t(kGerBlock)) {
-        constexpr uint64_t kChunk = uint64_t(kGerBlock) * kGerScalarU;
-        const uint64_t chunks = (inner + kChunk - 1) / kChunk;
-        const uint64_t tiles = outer * chunks;
-        const uint64_t cap = uint64_t(sm_count()) * 8;
-        const unsigned grid = unsigned(tiles < cap ? tiles : cap);
-        launch(ger_rows_kernel<T>, grid, kGerBlock, 0, s, u, v, C, outer, inner, chunks);
-        if (info) info->ctas = grid;
     } else {
-        const uint64_t total = outer * inner;
-        uint64_t grid = small ? 1 : (total + kGerBlock - 1) / kGerBlock;
+        constexpr uint64_t kSlab = uint64_t(kGerBlock) * kGerFlatU;
+        const uint64_t slabs = (outer * inner + kSlab - 1) / kSlab;
         const uint64_t cap = uint64_t(sm_count()) * 8;
-        if (grid > cap) grid = cap;
-        launch(ger_generic_kernel<T>, unsigned(grid), kGerBlock, 0, s, u, v, C, outer, inner);
-        if (info) info->ctas = unsigned(grid);
+        const unsigned grid = small ? 1u : unsigned(slabs < cap ? slabs : cap);
+        launch(ger_flat_kernel<T>, grid, kGerBlock, 0, s, u, v, C, outer, inner,
+               uint64_t(kGerBlock) / inner, uint64_t(kGerBlock) % inner);
+        if (info) info->ctas = grid;
     }
     return cudaGetLastError();
 }

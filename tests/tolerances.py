@@ -54,9 +54,13 @@ def dot_chain(n: int, dtype, block: int = 512, unroll: int = 2, ctas_per_sm: int
     V = 32 // np.dtype(dtype).itemsize
     nvec = n // V
     if 2 * n * np.dtype(dtype).itemsize >= (512 << 20) and nvec >= SMS * ctas_per_sm:
-        # chunked kernel: 65536-vector chunks, chunk partials summed in order
-        chunks = math.ceil(nvec / 65536)
-        per_acc = math.ceil(65536 / (block * unroll)) * V
+        # chunked kernel (csrc/dot.cu chunk_vecs): power-of-two chunks of
+        # <= nvec / 2048 vectors in [4096, 65536], partials summed in order
+        cv = 4096
+        while cv * 2 <= 65536 and cv * 2 * 2048 <= nvec:
+            cv *= 2
+        chunks = math.ceil(nvec / cv)
+        per_acc = math.ceil(cv / (block * unroll)) * V
         tree = 5 + log2c(block // 32)
         return per_acc + unroll + tree + math.ceil(chunks / block) + tree + V + 1
     G = max(1, min(math.ceil(nvec / (block * unroll)), SMS * ctas_per_sm))
