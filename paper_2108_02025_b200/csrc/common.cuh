@@ -139,6 +139,23 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
 // L1-bypassing loads for data another CTA produced in this kernel.
 __device__ __forceinline__ float ld_cg(const float* p) { return __ldcg(p); }
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ Vec<float> ld_cg(const Vec<float>* p) {
+    Vec<float> r;
+    asm volatile("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                   "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ Vec<double> ld_cg(const Vec<double>* p) {
+    Vec<double> r;
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
 
 // Balanced static partition of `total` units over `parts`: part w owns
 // [begin(w), begin(w+1)).  owner(u) inverts it.

@@ -149,6 +149,8 @@ __global__ void __launch_bounds__(kCmBlock, kCmRowsCtasPerSm)
 // parts b (in order) of partials[b*stride + r], r < rows.  Thread (r, q)
 // sums parts q, q+Q, ... with 16 loads in flight, then the Q sums per row
 // are added in q order; `sm` holds >= blockDim.x entries.
+constexpr int kFinalBatch = 32; // partial loads in flight per thread in split_final
+
 template <typename T>
 __device__ void split_final(const T* __restrict__ partials, T* __restrict__ c, uint64_t rows,
                             uint64_t stride, unsigned G, T* sm) {
@@ -163,15 +165,15 @@ __device__ void split_final(const T* __restrict__ partials, T* __restrict__ c, u
         const uint64_t r = rb + r0;
         T total = T(0);
         if (part && r < rows) {
-            for (unsigned b0 = q; b0 < G; b0 += 16u * Q) {
-                T v[16];
+            for (unsigned b0 = q; b0 < G; b0 += unsigned(kFinalBatch) * Q) {
+                T v[kFinalBatch];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
+                for (int e = 0; e < kFinalBatch; ++e) {
                     const unsigned b = b0 + unsigned(e) * Q;
                     v[e] = b < G ? ld_cg(partials + uint64_t(b) * stride + r) : T(0);
                 }
 #pragma unroll
-                for (int e = 0; e < 16; ++e)
+                for (int e = 0; e < kFinalBatch; ++e)
                     if (b0 + unsigned(e) * Q < G) total = add_rn(total, v[e]);
             }
         }
@@ -583,13 +585,41 @@ struct SplitGeom {
     size_t smem;
 };
 
-// Row tiles: one tile when m < kSplitMaxRows, else tiles of kSplitTileRows.
+// Row tiles: one tile when m < cm_single_max(), else tiles of cm_tile_rows().
 // Column parts: as many as keep row_tiles * parts within one CTA per SM
 // (1024 threads each), i.e. a single wave.
-constexpr uint64_t kSplitTileRows = 1024;
+constexpr uint64_t kSplitTileRows = 256;
+
+// Row tiling of the split kernels.  A single row tile (one last-arriving CTA
+// sums G partials per row) only below kSingleTileRows; above, row tiles of
+// kSplitTileRows rows, each finished by its own last arriver, so the final
+// combines run on different SMs at once.  256 MiB fp32 col-major, flushed,
+// single tile up to 2048 rows -> up to 512 rows with 256-row tiles: m = 1024
+// 61.5 -> 50.1 us, 2040 77.9 -> 52.0, 4096 52.3 -> 51.2.  Odd m keeps the
+// bulk ring with scalar consumers up to kBulkScalarMaxRows (m = 1001: 104 us
+// there, 143 in the 2-D scalar split).  CABL_CM_TILE="single,tile" overrides
+// the first two (tuning only).
+constexpr uint64_t kSingleTileRows = 512;
+constexpr uint64_t kBulkScalarMaxRows = 1024;
+inline uint64_t cm_single_max() {
+    static const uint64_t v = [] {
+        unsigned long a = kSingleTileRows, b = kSplitTileRows;
+        if (const char* e = getenv("CABL_CM_TILE")) sscanf(e, "%lu,%lu", &a, &b);
+        return uint64_t(a < kSplitMaxRows ? a : kSplitMaxRows);
+    }();
+    return v;
+}
+inline uint64_t cm_tile_rows() {
+    static const uint64_t v = [] {
+        unsigned long a = kSingleTileRows, b = kSplitTileRows;
+        if (const char* e = getenv("CABL_CM_TILE")) sscanf(e, "%lu,%lu", &a, &b);
+        return uint64_t(b);
+    }();
+    return v;
+}
 
 inline void split_tiles(uint64_t m, uint64_t n, uint64_t cols_per_tile, SplitGeom* g) {
-    g->mt = m < kSplitMaxRows ? m : kSplitTileRows;
+    g->mt = m < cm_single_max() ? m : cm_tile_rows();
     g->row_tiles = unsigned((m + g->mt - 1) / g->mt);
     const uint64_t sms = uint64_t(sm_count());
     // floor: row_tiles * parts must not exceed one CTA per SM, or the extra
@@ -602,7 +632,7 @@ inline void split_tiles(uint64_t m, uint64_t n, uint64_t cols_per_tile, SplitGeo
 
 template <typename T> SplitGeom split_geom(uint64_t m, uint64_t n) {
     SplitGeom g;
-    const uint64_t mt = m < kSplitMaxRows ? m : kSplitTileRows;
+    const uint64_t mt = m < cm_single_max() ? m : cm_tile_rows();
     uint64_t rl = 32; // a power of two, so row_lanes divides the block
     while (rl < mt && rl < uint64_t(kSplitBlock)) rl *= 2;
     g.row_lanes = int(rl);
@@ -622,7 +652,7 @@ template <typename T> bool split_vec_ok(const T* A, uint64_t m) {
 
 template <typename T> SplitGeom split_vec_geom(uint64_t m, uint64_t n) {
     SplitGeom g;
-    const uint64_t mt = m < kSplitMaxRows ? m : kSplitTileRows;
+    const uint64_t mt = m < cm_single_max() ? m : cm_tile_rows();
     const uint64_t mv = mt / Vec<T>::N;
     uint64_t rl = 1;
     while (rl < mv) rl *= 2;
@@ -750,8 +780,8 @@ template <typename T> CmPath cm_path(const T* A, const T* c, uint64_t m) {
     } else if (m >= sms * 1024) {
         return kPathTallScalar;
     }
-    if (split_vec_ok(A, m)) return (m < kSplitMaxRows && split_mode() == 1) ? kPathBulk : kPathSplitVec;
-    if (m < kSplitMaxRows && split_mode() == 1 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0)
+    if (split_vec_ok(A, m)) return (m < cm_single_max() && split_mode() == 1) ? kPathBulk : kPathSplitVec;
+    if (m < kBulkScalarMaxRows && split_mode() == 1 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0)
         return kPathBulkScalar;
     return kPathSplitScalar;
 }
