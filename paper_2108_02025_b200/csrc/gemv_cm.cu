@@ -285,7 +285,8 @@ template <typename T, int kBulkStages, unsigned kBulkStageBytes>
 __global__ void __launch_bounds__(kBulkThreads, 1)
     gemv_cm_split_bulk_kernel(const T* __restrict__ A, const T* __restrict__ x,
                               T* __restrict__ c, uint64_t m, uint64_t n, int row_lanes, int tc,
-                              T* __restrict__ partials, unsigned* __restrict__ ticket) {
+                              uint64_t x_off, T* __restrict__ partials,
+                              unsigned* __restrict__ ticket) {
     pdl_enter();
     constexpr int V = Vec<T>::N;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -298,8 +299,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint64_t tiles = (n + tc - 1) / tc;
     const uint64_t stage_elems = kBulkStageStride / sizeof(T);
-    const uint64_t x_off = kBulkStageBytes / sizeof(T); // x slice after the A tile
-    const bool x_stage = uint64_t(tc) * sizeof(T) <= kBulkXBytes;
+    // x slice right after the tile's tc*m elements (x_off = tc*m): the host
+    // picks tc so tile + slice fit the stage, (m + 1) * tc * s <= stride
     const int col_lanes = kBulkConsumers / row_lanes;
 
     if (tid == 0) {
@@ -325,8 +326,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
                 // x slice: a full tile's is a multiple of 16 B (tc is) and rides
                 // in the stage when it fits the slot (tc * s <= kBulkXBytes); a
                 // ragged last tile's, or a wider one's, is read with plain loads
-                const unsigned xbytes = (cols == uint64_t(tc) && x_stage)
-                                            ? unsigned(cols * sizeof(T)) : 0u;
+                const unsigned xbytes = cols == uint64_t(tc) ? unsigned(cols * sizeof(T)) : 0u;
                 mbar_arrive_expect_tx(&full[st], bytes + xbytes);
                 bulk_g2s(stages + st * stage_elems, A + col0 * m, bytes, &full[st], pol);
                 if (xbytes) bulk_g2s(stages + st * stage_elems + x_off, x + col0, xbytes, &full[st], pol);
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
             if (live) {
                 for (int j = cl; j < cols; j += col_lanes) {
                     const Vec<T> a = *reinterpret_cast<const Vec<T>*>(sb + uint64_t(j) * m + uint64_t(rl) * V);
-                    const T xj = (cols == tc && x_stage) ? sb[x_off + j] : __ldg(x + col0 + j);
+                    const T xj = cols == tc ? sb[x_off + j] : __ldg(x + col0 + j);
 #pragma unroll
                     for (int e = 0; e < V; ++e) acc.v[e] = fma_rn(a.v[e], xj, acc.v[e]);
                 }
@@ -391,7 +391,7 @@ template <typename T, int kBulkStages, unsigned kBulkStageBytes, int RPT>
 __global__ void __launch_bounds__(kBulkThreads, 1)
     gemv_cm_split_bulk_scalar_kernel(const T* __restrict__ A, const T* __restrict__ x,
                                      T* __restrict__ c, uint64_t m, uint64_t n, int row_lanes,
-                                     int tc, int x_bulk, T* __restrict__ partials,
+                                     int tc, uint64_t x_off, int x_bulk, T* __restrict__ partials,
                                      unsigned* __restrict__ ticket) {
     pdl_enter();
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -404,7 +404,6 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint64_t tiles = (n + tc - 1) / tc;
     const uint64_t stage_elems = kBulkStageStride / sizeof(T);
-    const uint64_t x_off = kBulkStageBytes / sizeof(T);
     const int col_lanes = kBulkConsumers / row_lanes;
 
     if (tid == 0) {
@@ -427,9 +426,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
                 const uint64_t col0 = t * tc;
                 const uint64_t cols = (n - col0 < uint64_t(tc)) ? n - col0 : uint64_t(tc);
                 const unsigned bytes = unsigned(cols * m * sizeof(T)) & ~15u;
-                const unsigned xbytes = (x_bulk && cols == uint64_t(tc) &&
-                                         uint64_t(tc) * sizeof(T) <= kBulkXBytes)
-                                            ? unsigned(cols * sizeof(T)) : 0u;
+                const unsigned xbytes =
+                    (x_bulk && cols == uint64_t(tc)) ? unsigned(cols * sizeof(T)) : 0u;
                 mbar_arrive_expect_tx(&full[st], bytes + xbytes);
                 if (bytes) bulk_g2s(stages + st * stage_elems, A + col0 * m, bytes, &full[st], pol);
                 if (xbytes) bulk_g2s(stages + st * stage_elems + x_off, x + col0, xbytes, &full[st], pol);
@@ -454,8 +452,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
             const T* sb = stages + st * stage_elems;
             if (live) {
                 if (cols == tc) { // full tile: everything is in the stage
-                    const T* xs =
-                        (x_bulk && uint64_t(tc) * sizeof(T) <= kBulkXBytes) ? sb + x_off : nullptr;
+                    const T* xs = x_bulk ? sb + x_off : nullptr;
                     unsigned e = unsigned(cl) * mm + unsigned(rl);
                     const unsigned step = unsigned(col_lanes) * mm;
 #pragma unroll 4
@@ -696,8 +693,11 @@ SplitGeom split_bulk_geom(uint64_t m, uint64_t n, int* tc, BulkCfg bc = bulk_cfg
     g.rpt = 1;
     // columns per stage, a multiple of 16/s so the x slice is a whole number of
     // 16-byte bulk units (m*s <= 16 KB for m < 2048, so tc >= 2 fp64 / 4 fp32)
+    // tile and its x slice share the stage: (m + 1) * tc * s <= SB + XB (for
+    // few rows the slice is as large as the tile: m = 1 fp32 streams 24 KB of
+    // A and 24 KB of x per stage instead of reading x element by element)
     const int xq = int(16 / sizeof(T));
-    *tc = int(bc.stage_bytes / (m * sizeof(T))) / xq * xq;
+    *tc = int((bc.stage_bytes + kBulkXBytes) / ((m + 1) * sizeof(T))) / xq * xq;
     if (*tc < xq) *tc = xq;
     const uint64_t tiles = (n + *tc - 1) / *tc;
     const uint64_t cap = uint64_t(sm_count());
@@ -718,7 +718,7 @@ void bulk_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const SplitGe
     }();
     (void)configured;
     launch(gemv_cm_split_bulk_kernel<T, NS, SB>, g.grid, kBulkThreads, bulk_smem(NS, SB), s, 
-        A, x, c, m, n, g.row_lanes, tc, partials, ticket);
+        A, x, c, m, n, g.row_lanes, tc, uint64_t(tc) * m, partials, ticket);
 }
 
 // Rows per consumer thread for the scalar bulk kernel: with row_lanes =
@@ -750,7 +750,8 @@ void bulk_scalar_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const 
     }();
     (void)configured;
     launch(gemv_cm_split_bulk_scalar_kernel<T, 3, 49152, RPT>, g.grid, kBulkThreads,
-           bulk_smem(3, 49152), s, A, x, c, m, n, g.row_lanes, tc, x_bulk, partials, ticket);
+           bulk_smem(3, 49152), s, A, x, c, m, n, g.row_lanes, tc, uint64_t(tc) * m, x_bulk,
+           partials, ticket);
 }
 
 inline int split_mode() {
