@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "col_major or guard or modes" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python tools/cm_odd.py > gpurun_out/cm_odd.jsonl 2>&1
-timeout 300 python tools/b2b.py G3 > gpurun_out/tune22.jsonl 2>&1
-timeout 1200 python tools/shape_sweep.py > gpurun_out/shape_sweep.md 2> gpurun_out/shape_sweep.err
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "ger or guard" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 900 python tools/ger_dot_sweep.py > gpurun_out/gd_sweep.jsonl 2>&1
