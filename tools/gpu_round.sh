@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 1200 python tools/shape_sweep.py > gpurun_out/shape_sweep.md 2> gpurun_out/shape_sweep.err
-timeout 600 python tools/odd_shapes.py > gpurun_out/odd.jsonl 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -k "ger" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
