@@ -15,6 +15,7 @@
 #include <string>
 #include <thread>
 #include <tuple>
+#include <vector>
 
 #include "cabl_cuda.h"
 #include "common.cuh"
@@ -282,12 +283,122 @@ void keep_pool_warm(int dev) {
     });
 }
 
+// ---- pageable host memory: multi-threaded staging through pinned slots ----
+// cudaMemcpyAsync from pageable memory is staged by the driver through one
+// thread (~12 GB/s on the GPU box: 22 ms for G1's 256 MB A, where pinned
+// memory takes 5.6 ms).  Large transfers from/to unregistered host memory
+// therefore go through kStageThreads worker threads, each owning a pinned
+// kStageChunk slot: a worker copies chunk k into its slot with memcpy and
+// enqueues the DMA from it (H2D), or waits for the DMA into it and copies
+// out (D2H); chunks k = t, t + T, ... belong to worker t, so T chunks are in
+// flight at once.  Each worker has its own stream: the caller's stream is
+// synchronized first (the destination is stream-ordered staging memory, and
+// a D2H source is produced by work on it — and the per-thread default stream
+// of the caller is not reachable from another thread), and every worker
+// waits for its last DMA, so the data is in place when the call returns.  One
+// staged transfer per device at a time (the slots are per device).
+constexpr size_t kStageChunk = size_t(8) << 20;
+constexpr size_t kStageMin = size_t(4) << 20; // smaller transfers: plain copy
+constexpr unsigned kStageThreads = 8;
+
+struct Stager {
+    std::mutex mu;
+    void* slot[kStageThreads] = {};
+    cudaEvent_t ev[kStageThreads] = {};
+    cudaStream_t stream[kStageThreads] = {};
+    bool ready = false;
+};
+
+Stager& stager(int dev) {
+    static Stager st[64];
+    return st[dev & 63];
+}
+
+bool is_pageable(const void* h) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+int stage_init(Stager& st) {
+    if (st.ready) return CABL_OK;
+    for (unsigned t = 0; t < kStageThreads; ++t) {
+        CABL_TRY_CUDA(cudaMallocHost(&st.slot[t], kStageChunk), "pinned staging slot");
+        CABL_TRY_CUDA(cudaEventCreateWithFlags(&st.ev[t], cudaEventDisableTiming), "staging event");
+        CABL_TRY_CUDA(cudaStreamCreateWithFlags(&st.stream[t], cudaStreamNonBlocking),
+                      "staging stream");
+    }
+    st.ready = true;
+    return CABL_OK;
+}
+
+// H2D (to_device) or D2H through the slots; returns the first CUDA error
+int staged_copy(int dev, void* dst, const void* src, size_t bytes, cudaStream_t s,
+                bool to_device) {
+    Stager& st = stager(dev);
+    std::lock_guard<std::mutex> lk(st.mu);
+    if (int rc = stage_init(st)) return rc;
+    CABL_TRY_CUDA(cudaStreamSynchronize(s), "staging sync");
+    const size_t chunks = (bytes + kStageChunk - 1) / kStageChunk;
+    const unsigned T = unsigned(chunks < kStageThreads ? chunks : kStageThreads);
+    std::atomic<int> err{0};
+    auto worker = [&](unsigned t) {
+        if (cudaSetDevice(dev) != cudaSuccess) {
+            err = 1;
+            return;
+        }
+        bool first = true;
+        for (size_t k = t; k < chunks && !err; k += T) {
+            const size_t off = k * kStageChunk;
+            const size_t len = bytes - off < kStageChunk ? bytes - off : kStageChunk;
+            if (to_device) {
+                // the slot's previous DMA must be done before it is overwritten
+                if (!first && cudaEventSynchronize(st.ev[t]) != cudaSuccess) { err = 1; return; }
+                std::memcpy(st.slot[t], static_cast<const char*>(src) + off, len);
+                if (cudaMemcpyAsync(static_cast<char*>(dst) + off, st.slot[t], len,
+                                    cudaMemcpyHostToDevice, st.stream[t]) != cudaSuccess ||
+                    cudaEventRecord(st.ev[t], st.stream[t]) != cudaSuccess) { err = 1; return; }
+            } else {
+                if (cudaMemcpyAsync(st.slot[t], static_cast<const char*>(src) + off, len,
+                                    cudaMemcpyDeviceToHost, st.stream[t]) != cudaSuccess ||
+                    cudaEventRecord(st.ev[t], st.stream[t]) != cudaSuccess ||
+                    cudaEventSynchronize(st.ev[t]) != cudaSuccess) { err = 1; return; }
+                std::memcpy(static_cast<char*>(dst) + off, st.slot[t], len);
+            }
+            first = false;
+        }
+        // H2D: the data must be in place before the caller's kernel runs, and
+        // the slot must not be reused before the last DMA from it has read it
+        if (to_device && !first && cudaEventSynchronize(st.ev[t]) != cudaSuccess) err = 1;
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < T; ++t) th.emplace_back(worker, t);
+    worker(0);
+    for (auto& x : th) x.join();
+    if (err) {
+        const cudaError_t e = cudaGetLastError();
+        return cuda_fail(e == cudaSuccess ? cudaErrorUnknown : e, "staged host copy");
+    }
+    return CABL_OK;
+}
+
 int h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
-    if (bytes) CABL_TRY_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s), "H2D copy");
+    if (!bytes) return CABL_OK;
+    int dev = 0;
+    if (bytes >= kStageMin && cudaGetDevice(&dev) == cudaSuccess && is_pageable(h))
+        return staged_copy(dev, d, h, bytes, s, true);
+    CABL_TRY_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s), "H2D copy");
     return CABL_OK;
 }
 int d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
-    if (bytes) CABL_TRY_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s), "D2H copy");
+    if (!bytes) return CABL_OK;
+    int dev = 0;
+    if (bytes >= kStageMin && cudaGetDevice(&dev) == cudaSuccess && is_pageable(h))
+        return staged_copy(dev, h, d, bytes, s, false);
+    CABL_TRY_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s), "D2H copy");
     return CABL_OK;
 }
 

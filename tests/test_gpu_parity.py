@@ -338,6 +338,34 @@ def test_host_buffer_path_equals_device_path(cuda):
     assert torch.equal(Cd.data.cpu(), Ch.data)
 
 
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_staged_copies_equal_device_path(cuda, pinned):
+    """Host containers above the 4 MiB staging threshold: pageable buffers go
+    through the multi-threaded pinned-slot staging (capi.cu staged_copy, H2D
+    and D2H, several 8 MiB chunks and a ragged last one), pinned ones straight
+    to the DMA engine.  Results equal the device-resident call bit for bit."""
+    import paper_2108_02025_b200 as cb
+    pol = policy()
+    host = (lambda t: t.cpu().pin_memory()) if pinned else (lambda t: t.cpu())
+    n = 5_000_003
+    x, y = dev_uniform(n, torch.float64, 1, cuda), dev_uniform(n, torch.float64, 2, cuda)
+    assert cb.dot(host(x), host(y), 0.25, pol) == cb.dot(x, y, 0.25, pol)
+    m, k = 3000, 5001
+    A = dev_uniform(m * k, torch.float32, 3, cuda)
+    xv, c0 = dev_uniform(k, torch.float32, 1, cuda), dev_uniform(m, torch.float32, 4, cuda)
+    cd = c0.clone()
+    cb.gemv_row_major(cb.DenseMatrix.wrap(A, m, k, cb.Layout.RowMajor), xv, cd, pol)
+    ch = host(c0)
+    cb.gemv_row_major(cb.DenseMatrix.wrap(host(A), m, k, cb.Layout.RowMajor), host(xv), ch, pol)
+    assert torch.equal(cd.cpu(), ch)
+    gx, gy = dev_uniform(m, torch.float32, 5, cuda), dev_uniform(k, torch.float32, 6, cuda)
+    Cd = cb.DenseMatrix.wrap(A.clone(), m, k, cb.Layout.ColMajor)
+    Ch = cb.DenseMatrix.wrap(host(A), m, k, cb.Layout.ColMajor)
+    cb.ger(gx, gy, Cd, pol)
+    cb.ger(host(gx), host(gy), Ch, pol)
+    assert torch.equal(Cd.data.cpu(), Ch.data)
+
+
 # ------------------------------------------------- full BASELINE sizes
 def test_generator_matches_host_oracle(cuda):
     for dtype, npdt in [(torch.float32, np.float32), (torch.float64, np.float64)]:
