@@ -344,44 +344,56 @@ int staged_copy(int dev, void* dst, const void* src, size_t bytes, cudaStream_t 
     CABL_TRY_CUDA(cudaStreamSynchronize(s), "staging sync");
     const size_t chunks = (bytes + kStageChunk - 1) / kStageChunk;
     const unsigned T = unsigned(chunks < kStageThreads ? chunks : kStageThreads);
-    std::atomic<int> err{0};
+    std::atomic<int> err{0}; // first failing cudaError_t
+    auto fail_with = [&](cudaError_t e) {
+        int expected = 0;
+        err.compare_exchange_strong(expected, int(e));
+    };
     auto worker = [&](unsigned t) {
-        if (cudaSetDevice(dev) != cudaSuccess) {
-            err = 1;
+        if (cudaError_t e = cudaSetDevice(dev)) {
+            fail_with(e);
             return;
         }
         bool first = true;
-        for (size_t k = t; k < chunks && !err; k += T) {
+        for (size_t k = t; k < chunks && !err.load(); k += T) {
             const size_t off = k * kStageChunk;
             const size_t len = bytes - off < kStageChunk ? bytes - off : kStageChunk;
+            cudaError_t e = cudaSuccess;
             if (to_device) {
-                // the slot's previous DMA must be done before it is overwritten
-                if (!first && cudaEventSynchronize(st.ev[t]) != cudaSuccess) { err = 1; return; }
-                std::memcpy(st.slot[t], static_cast<const char*>(src) + off, len);
-                if (cudaMemcpyAsync(static_cast<char*>(dst) + off, st.slot[t], len,
-                                    cudaMemcpyHostToDevice, st.stream[t]) != cudaSuccess ||
-                    cudaEventRecord(st.ev[t], st.stream[t]) != cudaSuccess) { err = 1; return; }
+                // the slot's previous DMA (this transfer's or an earlier, failed
+                // one's) must be done before it is overwritten; a never-recorded
+                // event is complete
+                e = cudaEventSynchronize(st.ev[t]);
+                if (e == cudaSuccess) {
+                    std::memcpy(st.slot[t], static_cast<const char*>(src) + off, len);
+                    e = cudaMemcpyAsync(static_cast<char*>(dst) + off, st.slot[t], len,
+                                        cudaMemcpyHostToDevice, st.stream[t]);
+                }
+                if (e == cudaSuccess) e = cudaEventRecord(st.ev[t], st.stream[t]);
             } else {
-                if (cudaMemcpyAsync(st.slot[t], static_cast<const char*>(src) + off, len,
-                                    cudaMemcpyDeviceToHost, st.stream[t]) != cudaSuccess ||
-                    cudaEventRecord(st.ev[t], st.stream[t]) != cudaSuccess ||
-                    cudaEventSynchronize(st.ev[t]) != cudaSuccess) { err = 1; return; }
-                std::memcpy(static_cast<char*>(dst) + off, st.slot[t], len);
+                e = cudaMemcpyAsync(st.slot[t], static_cast<const char*>(src) + off, len,
+                                    cudaMemcpyDeviceToHost, st.stream[t]);
+                if (e == cudaSuccess) e = cudaEventRecord(st.ev[t], st.stream[t]);
+                if (e == cudaSuccess) e = cudaEventSynchronize(st.ev[t]);
+                if (e == cudaSuccess)
+                    std::memcpy(static_cast<char*>(dst) + off, st.slot[t], len);
+            }
+            if (e != cudaSuccess) {
+                fail_with(e);
+                return;
             }
             first = false;
         }
         // H2D: the data must be in place before the caller's kernel runs, and
         // the slot must not be reused before the last DMA from it has read it
-        if (to_device && !first && cudaEventSynchronize(st.ev[t]) != cudaSuccess) err = 1;
+        if (to_device && !first)
+            if (cudaError_t e = cudaEventSynchronize(st.ev[t])) fail_with(e);
     };
     std::vector<std::thread> th;
     for (unsigned t = 1; t < T; ++t) th.emplace_back(worker, t);
     worker(0);
     for (auto& x : th) x.join();
-    if (err) {
-        const cudaError_t e = cudaGetLastError();
-        return cuda_fail(e == cudaSuccess ? cudaErrorUnknown : e, "staged host copy");
-    }
+    if (int e = err.load()) return cuda_fail(cudaError_t(e), "staged host copy");
     return CABL_OK;
 }
 
