@@ -13,7 +13,10 @@ import threading
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libcabl_cuda.so"
+import os as _os
+
+# CABL_LIB points at another build of the library (A/B measurements only)
+LIB_PATH = Path(_os.environ["CABL_LIB"]) if _os.environ.get("CABL_LIB") else PKG / "libcabl_cuda.so"
 CSRC = PKG / "csrc"
 
 CABL_OK, CABL_EINVAL, CABL_ECUDA, CABL_ENOMEM = 0, 1, 2, 3

@@ -31,19 +31,23 @@ constexpr int kDotBlock = 512;
 constexpr int kDotUnroll = 2;
 constexpr int kDotCtasPerSm = 2;
 
-template <typename T, int BLOCK, int U, int MINB>
+template <typename T, int BLOCK, int U, int MINB, bool PEEL = false>
 __global__ void __launch_bounds__(BLOCK, MINB)
     dot_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t n, int vec_ok,
-               T alpha0, T* __restrict__ out, T* __restrict__ partials,
+               uint64_t head_, T alpha0, T* __restrict__ out, T* __restrict__ partials,
                unsigned* __restrict__ ticket, int pf) {
+    const uint64_t head = PEEL ? head_ : 0; // the aligned instantiation keeps its old code
+    // vec_ok: x + head and y + head are 32-byte aligned (head < V elements are
+    // peeled when both operands share their misalignment); the head and the
+    // < V tail run in the scalar loop
     pdl_trigger();
     if (pf > 0 && vec_ok && threadIdx.x < 2 * U) { // warm L2: this CTA's first U slabs of x and y
-        const uint64_t nvec = n / Vec<T>::N;
+        const uint64_t nvec = (n - head) / Vec<T>::N;
         const uint64_t T_all = uint64_t(gridDim.x) * BLOCK;
         const uint64_t v0 = uint64_t(blockIdx.x) * BLOCK + uint64_t(threadIdx.x >> 1) * T_all;
         if (v0 < nvec) {
             const uint64_t cnt = nvec - v0 < uint64_t(BLOCK) ? nvec - v0 : uint64_t(BLOCK);
-            const T* base = (threadIdx.x & 1) ? y : x;
+            const T* base = ((threadIdx.x & 1) ? y : x) + head;
             prefetch_l2_bulk(base + v0 * Vec<T>::N, unsigned(cnt * sizeof(Vec<T>)));
         }
     }
@@ -57,11 +61,11 @@ __global__ void __launch_bounds__(BLOCK, MINB)
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = T(0);
 
-    uint64_t done = 0; // elements covered by the vector loop
+    uint64_t done = 0; // elements covered by the head and the vector loop
     if (vec_ok) {
-        const uint64_t nvec = n / V;
-        const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
-        const Vec<T>* Y = reinterpret_cast<const Vec<T>*>(y);
+        const uint64_t nvec = (n - head) / V;
+        const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x + head);
+        const Vec<T>* Y = reinterpret_cast<const Vec<T>*>(y + head);
         // thread-level grid stride: with T threads in the grid, thread t takes
         // vectors t, t + T, t + 2T, ... (U of them in flight per iteration), so
         // every thread's share is within one vector of every other's and the
@@ -83,7 +87,12 @@ __global__ void __launch_bounds__(BLOCK, MINB)
 #pragma unroll
             for (int u = 0; u < U; ++u) acc[u] = dot_vec(xv[u], yv[u], acc[u]);
         }
-        done = nvec * V;
+        // the peeled head: one element for each of the first `head` threads
+        if (PEEL) {
+            const uint64_t gt = uint64_t(blockIdx.x) * BLOCK + tid;
+            if (gt < head) acc[0] = fma_rn(x[gt], y[gt], acc[0]);
+        }
+        done = head + nvec * V;
     }
     // Scalar remainder (unaligned operands, or the < V trailing elements):
     // one chain per thread over i = done + gt, + gs, ... in order, with the
@@ -268,20 +277,26 @@ template <typename T> unsigned dot_grid(uint64_t n, bool small) {
 }
 
 template <typename T, int B, int U, int M>
-cudaError_t dot_go(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok, T alpha0,
-                   T* out, T* partials, unsigned* ticket, cudaStream_t s) {
-    launch(dot_kernel<T, B, U, M>, grid, B, 0, s, x, y, n, vec_ok, alpha0, out, partials, ticket,
-           pdl_prefetch_enabled());
+cudaError_t dot_go(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok,
+                   uint64_t head, T alpha0, T* out, T* partials, unsigned* ticket,
+                   cudaStream_t s) {
+    if (head)
+        launch(dot_kernel<T, B, U, M, true>, grid, B, 0, s, x, y, n, vec_ok, head, alpha0, out,
+               partials, ticket, pdl_prefetch_enabled());
+    else
+        launch(dot_kernel<T, B, U, M, false>, grid, B, 0, s, x, y, n, vec_ok, head, alpha0, out,
+               partials, ticket, pdl_prefetch_enabled());
     return cudaGetLastError();
 }
 
 template <typename T>
-cudaError_t dot_dispatch(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok, T alpha0,
-                         T* out, T* partials, unsigned* ticket, cudaStream_t s) {
+cudaError_t dot_dispatch(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok,
+                         uint64_t head, T alpha0, T* out, T* partials, unsigned* ticket,
+                         cudaStream_t s) {
     const DotCfg c = dot_cfg();
 #define CABL_DOT_CASE(B_, U_, M_)                                                              \
     if (c.block == B_ && c.unroll == U_ && c.minb == M_)                                       \
-        return dot_go<T, B_, U_, M_>(grid, x, y, n, vec_ok, alpha0, out, partials, ticket, s);
+        return dot_go<T, B_, U_, M_>(grid, x, y, n, vec_ok, head, alpha0, out, partials, ticket, s);
     CABL_DOT_CASE(256, 1, 8)
     CABL_DOT_CASE(256, 2, 8)
     CABL_DOT_CASE(256, 4, 4)
@@ -291,8 +306,8 @@ cudaError_t dot_dispatch(unsigned grid, const T* x, const T* y, uint64_t n, int 
     CABL_DOT_CASE(1024, 4, 1)
     CABL_DOT_CASE(256, 8, 1)
 #undef CABL_DOT_CASE
-    return dot_go<T, kDotBlock, kDotUnroll, kDotCtasPerSm>(grid, x, y, n, vec_ok, alpha0, out,
-                                                          partials, ticket, s);
+    return dot_go<T, kDotBlock, kDotUnroll, kDotCtasPerSm>(grid, x, y, n, vec_ok, head, alpha0,
+                                                          out, partials, ticket, s);
 }
 
 } // namespace
@@ -333,8 +348,20 @@ cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, boo
         if (info) info->ctas = grid;
         return cudaGetLastError();
     }
+    // operands that share their misalignment: peel head < V elements so the
+    // rest is 32-byte aligned (x[k:], y[k:] slices of aligned buffers)
+    uint64_t head = 0;
+    int peeled_ok = vec_ok;
+    if (!vec_ok) {
+        const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
+        if (xa % 32 == ya % 32 && xa % sizeof(T) == 0) {
+            head = ((32 - xa % 32) % 32) / sizeof(T);
+            peeled_ok = head < n ? 1 : 0;
+            if (!peeled_ok) head = 0;
+        }
+    }
     const unsigned grid = dot_grid<T>(n, small);
-    const cudaError_t e = dot_dispatch<T>(grid, x, y, n, vec_ok, alpha0, out,
+    const cudaError_t e = dot_dispatch<T>(grid, x, y, n, peeled_ok, head, alpha0, out,
                                           static_cast<T*>(ws.scratch), ws.counters + 1, s);
     if (info) info->ctas = grid;
     return e;

@@ -72,14 +72,18 @@ def test_dot_matches_oracle(cuda, dtype, n):
 
 @pytest.mark.parametrize("dtype", DTYPES)
 def test_dot_unaligned_operands(cuda, dtype):
+    """Different misalignments (scalar path) and a shared one (head peeled,
+    then the vector path): truth bound, and run-to-run bitwise."""
     import paper_2108_02025_b200 as cb
     n = 300_001
-    x, y = dev_uniform(n + 3, dtype, 1, cuda), dev_uniform(n + 5, dtype, 2, cuda)
-    xs, ys = x[1:n + 1], y[3:n + 3]
-    got = cb.dot(xs, ys, -1.5, policy())
-    xn, yn = np_of(xs), np_of(ys)
-    truth, sumabs = O.dot_truth(xn, yn, -1.5)
-    assert abs(got - truth) <= T.truth_tol(n, sumabs, 1.5, xn.dtype)
+    x, y = dev_uniform(n + 8, dtype, 1, cuda), dev_uniform(n + 8, dtype, 2, cuda)
+    for ox, oy in [(1, 3), (1, 1), (3, 3), (7, 7), (2, 2)]:
+        xs, ys = x[ox:ox + n], y[oy:oy + n]
+        got = cb.dot(xs, ys, -1.5, policy())
+        assert cb.dot(xs, ys, -1.5, policy()) == got
+        xn, yn = np_of(xs), np_of(ys)
+        truth, sumabs = O.dot_truth(xn, yn, -1.5)
+        assert abs(got - truth) <= T.truth_tol(n, sumabs, 1.5, xn.dtype), (ox, oy)
 
 
 def test_dot_hand_values(cuda):

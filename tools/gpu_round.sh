@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "host or cpp or concurrent or staged" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python tools/host_paths.py > gpurun_out/host_paths.jsonl 2>&1
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "dot or guard or reproducible or smoke" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
