@@ -110,6 +110,57 @@ __global__ void __launch_bounds__(kTallBlock, 1)
     }
 }
 
+// Tall and narrow (n < kTallUnroll): the tall kernel keeps only n column
+// loads in flight per thread there (2^24 x 4 fp32 ran at 3.6 TB/s).  Here a
+// thread owns P = 16 / NC row vectors (NC >= n, a power of two), so P * n
+// loads are issued before any is consumed; each row vector still runs its
+// own chain over j ascending with the reference's rounding: bitwise gemv_ref
+// like the tall kernel.  CTAs own balanced contiguous ranges of P*256-vector
+// units.
+template <typename T, int NC>
+__global__ void __launch_bounds__(kTallBlock, 1)
+    gemv_cm_narrow_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
+                          uint64_t m, uint64_t n) {
+    pdl_enter();
+    constexpr int V = Vec<T>::N;
+    constexpr int P = kTallUnroll / NC;
+    constexpr uint64_t kRefVec = 16 / sizeof(T);
+    const uint64_t mv = m / V;
+    const uint64_t per_unit = uint64_t(kTallBlock) * P;
+    const uint64_t units = (mv + per_unit - 1) / per_unit;
+    const uint64_t cut = (n / kRefVec) * kRefVec;
+    const Vec<T>* Av = reinterpret_cast<const Vec<T>*>(A);
+    Vec<T>* Cv = reinterpret_cast<Vec<T>*>(c);
+    T xs[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) xs[k] = uint64_t(k) < n ? __ldg(x + k) : T(0);
+    const Partition part(units, gridDim.x);
+    for (uint64_t u = part.begin(blockIdx.x); u < part.begin(blockIdx.x + 1); ++u) {
+        Vec<T> a[P][NC];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const uint64_t rv = u * per_unit + uint64_t(p) * kTallBlock + threadIdx.x;
+#pragma unroll
+            for (int k = 0; k < NC; ++k)
+                if (rv < mv && uint64_t(k) < n) a[p][k] = ld_stream(Av + rv + uint64_t(k) * mv);
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const uint64_t rv = u * per_unit + uint64_t(p) * kTallBlock + threadIdx.x;
+            if (rv < mv) {
+                Vec<T> acc = Cv[rv];
+#pragma unroll
+                for (int k = 0; k < NC; ++k)
+                    if (uint64_t(k) < n)
+#pragma unroll
+                        for (int e = 0; e < V; ++e)
+                            acc.v[e] = ref_step(acc.v[e], a[p][k].v[e], xs[k], uint64_t(k) >= cut);
+                Cv[rv] = acc;
+            }
+        }
+    }
+}
+
 // Tall, any m: one row per lane, warps own balanced ranges of 32-row units.
 template <typename T>
 __global__ void __launch_bounds__(kCmBlock, kCmRowsCtasPerSm)
@@ -826,7 +877,20 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
     const CmPath path = cm_path<T>(A, A, m);
     // (a c whose alignment differs from A's falls back to the scalar-lane
     // tall kernel: same order and rounding)
-    if (path == kPathTallVec && aligned32(c)) {
+    if (path == kPathTallVec && aligned32(c) && n < uint64_t(kTallUnroll)) {
+        const int nc = n <= 4 ? 4 : (n <= 8 ? 8 : 16);
+        const uint64_t per_unit = uint64_t(kTallBlock) * (kTallUnroll / nc);
+        const uint64_t units = (m / Vec<T>::N + per_unit - 1) / per_unit;
+        const uint64_t sms = uint64_t(sm_count());
+        const unsigned grid = unsigned(units < sms ? units : sms);
+        if (nc == 4)
+            launch(gemv_cm_narrow_kernel<T, 4>, grid, kTallBlock, 0, s, A, x, c, m, n);
+        else if (nc == 8)
+            launch(gemv_cm_narrow_kernel<T, 8>, grid, kTallBlock, 0, s, A, x, c, m, n);
+        else
+            launch(gemv_cm_narrow_kernel<T, 16>, grid, kTallBlock, 0, s, A, x, c, m, n);
+        if (info) info->ctas = grid;
+    } else if (path == kPathTallVec && aligned32(c)) {
         const uint64_t units = (m / Vec<T>::N + kTallBlock - 1) / kTallBlock;
         const uint64_t sms = uint64_t(sm_count());
         const unsigned grid = unsigned(units < sms ? units : sms); // grid <= units (dyn_next)
