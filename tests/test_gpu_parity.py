@@ -123,7 +123,9 @@ RM_SHAPES = [(1, 777), (3, 3), (8, 8), (40, 200), (257, 259), (1000, 1000), (200
              (33, 16392), (4097, 1024), (8192, 8192), (4736, 100), (5000, 1028), (9001, 3000),
              # short rows: one thread per row (bitwise), vector and scalar loads
              (9472, 64), (100_000, 16), (20_001, 5), (9472, 256), (30_000, 255), (1 << 18, 1),
-             (9472, 1024), (12_000, 999)]
+             (9472, 1024), (12_000, 999),
+             # rows of whole 16-byte (not 32-byte) vectors: the scalar-load kernel
+             (20_000, 2052), (3000, 20_002), (1800, 65_540)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)

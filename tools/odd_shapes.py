@@ -41,7 +41,7 @@ for n, off in ((1 << 24, 0), ((1 << 24) + 3, 0), (1 << 24, 1)):
     x, y = buf(n, off), buf(n, off)
     out = torch.empty(1, device=dev)
     report(f"dot n={n} off={off}", timeit(lambda: cb.dot_into(x, y, 0.0, out, pol)), 2 * n * s)
-for m, n, off in ((8192, 8192, 0), (8192, 8193, 0), (8192, 8192, 1)):
+for m, n, off in ((8192, 8192, 0), (8192, 8193, 0), (8192, 8192, 1), (8192, 8196, 0)):
     A, x, c = buf(m * n, off), buf(n, off), buf(m, off)
     M = cb.DenseMatrix.wrap(A, m, n, cb.Layout.RowMajor)
     report(f"gemv_rm {m}x{n} off={off}", timeit(lambda: cb.gemv_row_major(M, x, c, pol)), m * n * s)
