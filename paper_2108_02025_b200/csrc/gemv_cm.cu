@@ -666,8 +666,55 @@ inline uint64_t cm_tile_rows() {
     return v;
 }
 
-inline void split_tiles(uint64_t m, uint64_t n, uint64_t cols_per_tile, SplitGeom* g) {
-    g->mt = m < cm_single_max() ? m : cm_tile_rows();
+// Rows per tile for m >= cm_single_max(): every multiple of 32 rows from
+// kSplitTileRows to max_mt is scored by the share of SM slots doing useful
+// work — (row tiles x column parts) / (waves x SMs) times the share of row
+// lanes that hold rows (the vector kernel's row lanes are a power of two >=
+// the tile's row vectors), scaled down when a tile's final sum (parts x rows
+// partials, one CTA) exceeds kFinalBudget — and the best kept.  Fixed 256-row tiles gave m =
+// 3e5 x 223 fp32 1172 single-part CTAs in eight waves (80.9 us, 3.3 TB/s);
+// ~148 tiles of 2048 rows take 53 us.  CABL_CM_TILE overrides (fixed rows).
+constexpr uint64_t kFinalBudget = 16384; // partials one finishing CTA sums
+
+inline uint64_t choose_tile_rows(uint64_t m, uint64_t max_mt, int vec_elems) {
+    if (m < cm_single_max()) return m;
+    if (getenv("CABL_CM_TILE")) return cm_tile_rows();
+    const uint64_t sms = uint64_t(sm_count());
+    uint64_t best = kSplitTileRows;
+    double best_score = -1.0;
+    for (uint64_t mt = kSplitTileRows; mt <= max_mt; mt += 32) {
+        const uint64_t tiles = (m + mt - 1) / mt;
+        uint64_t parts = sms / tiles;
+        if (parts < 1) parts = 1;
+        const uint64_t ctas = tiles * parts;
+        const uint64_t waves = (ctas + sms - 1) / sms;
+        // row lanes: pow2 >= rows (in vectors for the vector kernel, capped at
+        // the block for the scalar one, whose extra rows go to RPT)
+        const uint64_t units = vec_elems > 1 ? mt / uint64_t(vec_elems) : mt;
+        uint64_t lanes = 1;
+        while (lanes < units && lanes < uint64_t(kSplitBlock)) lanes *= 2;
+        const uint64_t rpt = (units + lanes - 1) / lanes;
+        const double lane_eff = double(units) / double(lanes * rpt);
+        // useful share of the SM slots, of the row lanes and of the tiles'
+        // rows (a ragged last tile idles its CTAs); extra waves cost their
+        // ramp and per-CTA combine
+        double score = lane_eff * double(ctas) / double(waves * sms) * double(m) /
+                       double(tiles * mt) / (1.0 + 0.15 * double(waves - 1));
+        // each tile's last CTA sums parts x mt partials alone: keep that
+        // bounded (a single 2040-row tile x 148 parts took 78 us vs 52)
+        if (parts * mt > kFinalBudget) score *= double(kFinalBudget) / double(parts * mt);
+        if (score > best_score + 1e-9) {
+            best_score = score;
+            best = mt;
+        }
+        if (tiles == 1) break;
+    }
+    return best;
+}
+
+inline void split_tiles(uint64_t m, uint64_t n, uint64_t cols_per_tile, uint64_t mt,
+                        SplitGeom* g) {
+    g->mt = mt;
     g->row_tiles = unsigned((m + g->mt - 1) / g->mt);
     const uint64_t sms = uint64_t(sm_count());
     // floor: row_tiles * parts must not exceed one CTA per SM, or the extra
@@ -680,13 +727,13 @@ inline void split_tiles(uint64_t m, uint64_t n, uint64_t cols_per_tile, SplitGeo
 
 template <typename T> SplitGeom split_geom(uint64_t m, uint64_t n) {
     SplitGeom g;
-    const uint64_t mt = m < cm_single_max() ? m : cm_tile_rows();
+    const uint64_t mt = choose_tile_rows(m, 2 * uint64_t(kSplitBlock), 1); // RPT <= 2
     uint64_t rl = 32; // a power of two, so row_lanes divides the block
     while (rl < mt && rl < uint64_t(kSplitBlock)) rl *= 2;
     g.row_lanes = int(rl);
     g.col_lanes = kSplitBlock / g.row_lanes;
     g.rpt = int((mt + rl - 1) / rl);
-    split_tiles(m, n, uint64_t(g.col_lanes) * split_u<T>(), &g);
+    split_tiles(m, n, uint64_t(g.col_lanes) * split_u<T>(), mt, &g);
     // [col_lanes][rows] for the column-lane combine, >= one entry per thread for
     // split_final: <= max(kSplitBlock, mt) entries, 16 KB for fp64
     const size_t entries = size_t(g.col_lanes) * g.mt;
@@ -700,14 +747,14 @@ template <typename T> bool split_vec_ok(const T* A, uint64_t m) {
 
 template <typename T> SplitGeom split_vec_geom(uint64_t m, uint64_t n) {
     SplitGeom g;
-    const uint64_t mt = m < cm_single_max() ? m : cm_tile_rows();
+    const uint64_t mt = choose_tile_rows(m, uint64_t(kSplitBlock) * Vec<T>::N, Vec<T>::N);
     const uint64_t mv = mt / Vec<T>::N;
     uint64_t rl = 1;
     while (rl < mv) rl *= 2;
     g.row_lanes = int(rl);
     g.col_lanes = kSplitBlock / g.row_lanes;
     g.rpt = 1;
-    split_tiles(m, n, uint64_t(g.col_lanes) * 4, &g);
+    split_tiles(m, n, uint64_t(g.col_lanes) * 4, mt, &g);
     g.smem = 0;
     return g;
 }
