@@ -872,10 +872,23 @@ enum CmPath { kPathTallVec, kPathTallScalar, kPathBulk, kPathBulkScalar, kPathSp
 // (>= one 256-row-vector unit per SM, or >= 1024 rows per SM for the scalar
 // variant).  Everything else splits the columns (2-D row tiles x column
 // parts; a single bulk-streamed row tile when m < kSplitMaxRows).
+// 256-vector units from which the tall kernel runs: half the SMs.  One CTA
+// per SM with 16 column loads per thread in flight streams fast enough that
+// 74 SMs match the 2-D split on all 148 (256 MiB fp32: m = 1.5e5 51.1 vs
+// 51.2 us; 2e5 47.1 vs 59.6; 2.6e5 44.1 vs 53.3), and it is bitwise gemv_ref.
+// CABL_CM_TALL_MIN overrides (tuning only).
+inline uint64_t tall_min_units() {
+    static const long forced = [] {
+        const char* e = getenv("CABL_CM_TALL_MIN");
+        return e ? atol(e) : -1L;
+    }();
+    return forced > 0 ? uint64_t(forced) : uint64_t(sm_count()) / 2;
+}
+
 template <typename T> CmPath cm_path(const T* A, const T* c, uint64_t m) {
     const uint64_t sms = uint64_t(sm_count());
     if (tall_vec_ok(A, c, m)) {
-        if (m / Vec<T>::N >= sms * kTallBlock) return kPathTallVec;
+        if (m / Vec<T>::N >= tall_min_units() * kTallBlock) return kPathTallVec;
     } else if (m >= sms * 1024) {
         return kPathTallScalar;
     }

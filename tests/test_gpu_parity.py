@@ -177,7 +177,9 @@ CM_SHAPES = [(3, 3), (8, 8), (257, 259), (1000, 1000), (256, 65536), (2047, 300)
              # short-wide with few rows: tiles wider than the ring's x slot
              (1, 1 << 20), (3, 300_000), (8, 400_000), (64, 100_000), (100, 50_000),
              # tall and narrow (n < 16): several row vectors per thread, bitwise
-             (303_104, 4), (1 << 20, 5), (1 << 20, 15), (1 << 21, 1), (1 << 20, 8)]
+             (303_104, 4), (1 << 20, 5), (1 << 20, 15), (1 << 21, 1), (1 << 20, 8),
+             # tall from half the SMs' worth of 256-vector units up (bitwise)
+             (151_552, 33), (200_000, 20), (151_544, 7)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)

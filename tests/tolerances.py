@@ -93,12 +93,12 @@ def rm_is_lane(m: int, n: int, dtype) -> bool:
 
 
 def cm_is_tall(m: int, dtype, aligned: bool = True) -> bool:
-    """csrc/gemv_cm.cu cm_path: the bit-exact tall kernels run when m/V >= 148
-    units of 256 row vectors (V = 32/s, aligned, m % V == 0) or, otherwise,
-    m >= 148 * 1024."""
+    """csrc/gemv_cm.cu cm_path: the bit-exact tall kernels run when m/V >= 74
+    units of 256 row vectors (half the SMs; V = 32/s, aligned, m % V == 0) or,
+    otherwise, m >= 148 * 1024."""
     V = 32 // np.dtype(dtype).itemsize
     if aligned and m % V == 0:
-        return m // V >= SMS * 256
+        return m // V >= (SMS // 2) * 256
     return m >= SMS * 1024
 
 

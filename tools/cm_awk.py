@@ -18,7 +18,9 @@ def timeit(fn, reps=7):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(); fn(); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
     return sorted(ts)[len(ts)//2] * 1e3
-for m in (520, 1000, 5000, 20000, 50000, 100000, 200000, 300000, 303104, 400000, 1000000):
+import os
+MS = [int(v) for v in os.environ.get('CM_MS', '520,1000,5000,20000,50000,100000,200000,300000,303104,400000,1000000').split(',')]
+for m in MS:
     n = (1 << 26) // m
     A = cb.fill_uniform(torch.empty(m * n, device=dev), 1, 3)
     x = cb.fill_uniform(torch.empty(n, device=dev), 1, 1)
