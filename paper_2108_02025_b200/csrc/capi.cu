@@ -213,7 +213,7 @@ int gemv_impl(const T* A, int layout, uint64_t m, uint64_t n, const T* x, T* c,
     if (touched <= cutoff) {
         CABL_TRY_CUDA(gemv_ordered_launch<T>(A, layout, m, n, x, c, s, &info), "gemv kernel");
     } else if (layout == CABL_ROW_MAJOR && rm_reference_order() &&
-               !gemv_rm_is_lane(m, n, sizeof(T)) && gemv_rm_ordered_ok<T>(A, x, m, n)) {
+               !gemv_rm_is_lane(A, x, m, n, sizeof(T)) && gemv_rm_ordered_ok<T>(A, x, m, n)) {
         CABL_TRY_CUDA(gemv_rm_ordered_launch<T>(A, m, n, x, c, s, &info), "gemv_rm kernel");
     } else if (layout == CABL_ROW_MAJOR) {
         WsLease lease;

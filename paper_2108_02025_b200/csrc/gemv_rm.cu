@@ -242,40 +242,41 @@ __global__ void __launch_bounds__(kRmBlock, MINB)
     }
 }
 
-// Generic path: one warp per row (balanced row ranges), scalar coalesced loads.
-template <typename T>
+// Generic path (unaligned operands or n % V != 0): G lanes per row (G = 32 /
+// 16 / 8 / 4 by row length, so short rows do not idle most of a warp),
+// groups own balanced row ranges, scalar coalesced loads.  Each lane's chain
+// runs j = lane, lane + G, ... in order, the loads of kScalarU steps issued
+// before they are consumed; then a fixed butterfly over the G lanes.  (One
+// load in flight at a time ran odd-width rows at ~2.1 TB/s; 8192 x 8193 fp32
+// now 56 us, 4.8 TB/s.)
+template <typename T, int G>
 __global__ void __launch_bounds__(kRmBlock)
     gemv_rm_scalar_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
-                          uint64_t m, uint64_t n, uint64_t warps) {
+                          uint64_t m, uint64_t n, uint64_t groups) {
     pdl_enter();
-    const int lane = threadIdx.x & 31;
-    const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (gw >= warps) return;
-    const Partition part(m, warps);
-    // Each lane's chain runs j = lane, lane + 32, ... in order; the loads of
-    // kScalarU consecutive steps are issued before they are consumed, so a
-    // warp keeps kScalarU coalesced 128-byte requests per operand in flight
-    // (one at a time ran odd-width rows at ~2.1 TB/s; 8192 x 8193 fp32 now
-    // 56 us, 4.8 TB/s — 32 in flight is no faster: the scalar LSU issue is
-    // the limit there).
+    const int lg = threadIdx.x & (G - 1);
+    const uint64_t gg = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+    if (gg >= groups) return; // whole groups leave together (G divides 32)
+    const Partition part(m, groups);
     constexpr int kScalarU = 16;
-    for (uint64_t i = part.begin(gw); i < part.begin(gw + 1); ++i) {
+    for (uint64_t i = part.begin(gg); i < part.begin(gg + 1); ++i) {
         const T* row = A + i * n;
         T acc = T(0);
-        uint64_t j = lane;
-        for (; j + uint64_t(kScalarU - 1) * kWarp < n; j += uint64_t(kScalarU) * kWarp) {
+        uint64_t j = lg;
+        for (; j + uint64_t(kScalarU - 1) * G < n; j += uint64_t(kScalarU) * G) {
             T a[kScalarU], b[kScalarU];
 #pragma unroll
             for (int u = 0; u < kScalarU; ++u) {
-                a[u] = __ldcs(row + j + u * kWarp);
-                b[u] = __ldg(x + j + u * kWarp);
+                a[u] = __ldcs(row + j + u * G);
+                b[u] = __ldg(x + j + u * G);
             }
 #pragma unroll
             for (int u = 0; u < kScalarU; ++u) acc = fma_rn(a[u], b[u], acc);
         }
-        for (; j < n; j += kWarp) acc = fma_rn(row[j], x[j], acc);
-        acc = warp_sum(acc);
-        if (lane == 0) c[i] = add_rn(c[i], acc);
+        for (; j < n; j += G) acc = fma_rn(row[j], x[j], acc);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) acc = add_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o, G));
+        if (lg == 0) c[i] = add_rn(c[i], acc);
     }
 }
 
@@ -369,7 +370,7 @@ template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n
     }();
     // one thread per row (3 vector loads, 4 scalar loads): short rows, and
     // enough of them to give every SM a few warps
-    const bool lane = gemv_rm_is_lane(m, n, sizeof(T));
+    const bool lane = gemv_rm_is_lane(A, x, m, n, sizeof(T));
     if (forced == 3 || (forced < 0 && lane)) return vec ? 3 : 4;
     if (!vec) return -1;
     if (forced >= 0 && forced <= 2) return forced;
@@ -466,8 +467,17 @@ unsigned sweep_launch(const T* A, const T* x, T* c, uint64_t m, uint64_t n, int 
 
 } // namespace
 
-bool gemv_rm_is_lane(uint64_t m, uint64_t n, size_t elem) {
-    return n * elem <= rm_lane_max_bytes() && m >= uint64_t(sm_count()) * 64;
+// Scalar-load rows (odd n or misaligned) take the lane kernel only while a
+// row is at most kLaneScalarMaxN long: a warp's scalar loads touch 32 rows'
+// sectors per instruction, and the G-lanes-per-row scalar kernel wins above
+// (256 MiB fp32: n = 17 lane 75.8 / 4 lanes 96.3 us; n = 33 118.8 / 92.2;
+// n = 63 166.8 / 79.9 before the 4..16-lane groups existed).
+constexpr uint64_t kLaneScalarMaxN = 24;
+
+bool gemv_rm_is_lane(const void* A, const void* x, uint64_t m, uint64_t n, size_t elem) {
+    const bool vec = aligned32(A) && aligned32(x) && n % (32 / elem) == 0;
+    return n * elem <= rm_lane_max_bytes() && m >= uint64_t(sm_count()) * 64 &&
+           (vec || n <= kLaneScalarMaxN);
 }
 
 template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n) {
@@ -511,10 +521,19 @@ cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
             A, x, c, m, n, g, static_cast<T*>(ws.scratch), ws.counters);
         if (info) info->ctas = grid;
     } else {
-        const uint64_t max_warps = uint64_t(sm_count()) * 8 * (kRmBlock / kWarp);
-        const uint64_t warps = m < max_warps ? m : max_warps;
-        const unsigned grid = unsigned((warps * kWarp + kRmBlock - 1) / kRmBlock);
-        launch(gemv_rm_scalar_kernel<T>, grid, kRmBlock, 0, s, A, x, c, m, n, warps);
+        // lanes per row: about 8 elements per lane, 4..32 lanes
+        const int G = n > 128 ? 32 : (n > 64 ? 16 : (n > 32 ? 8 : 4));
+        const uint64_t max_groups = uint64_t(sm_count()) * 8 * (kRmBlock / G);
+        const uint64_t groups = m < max_groups ? m : max_groups;
+        const unsigned grid = unsigned((groups * G + kRmBlock - 1) / kRmBlock);
+        if (G == 32)
+            launch(gemv_rm_scalar_kernel<T, 32>, grid, kRmBlock, 0, s, A, x, c, m, n, groups);
+        else if (G == 16)
+            launch(gemv_rm_scalar_kernel<T, 16>, grid, kRmBlock, 0, s, A, x, c, m, n, groups);
+        else if (G == 8)
+            launch(gemv_rm_scalar_kernel<T, 8>, grid, kRmBlock, 0, s, A, x, c, m, n, groups);
+        else
+            launch(gemv_rm_scalar_kernel<T, 4>, grid, kRmBlock, 0, s, A, x, c, m, n, groups);
         if (info) info->ctas = grid;
     }
     return cudaGetLastError();

@@ -44,7 +44,7 @@ cudaError_t combine_partials_launch(const T* p, uint32_t count, T alpha0, T* out
 template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n);
 // short rows, many of them: the one-thread-per-row kernel (reference order,
 // bitwise gemv_ref) handles the shape on any alignment
-bool gemv_rm_is_lane(uint64_t m, uint64_t n, size_t elem);
+bool gemv_rm_is_lane(const void* A, const void* x, uint64_t m, uint64_t n, size_t elem);
 template <typename T>
 cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
                            const Workspace& ws, cudaStream_t s, LaunchInfo* info);

@@ -85,11 +85,14 @@ def rm_is_ordered(m: int, n: int, dtype, aligned: bool = True) -> bool:
     return os.environ.get("CABL_GEMV_RM_ORDER") == "reference" and aligned and (n * np.dtype(dtype).itemsize) % 16 == 0 and m >= SMS * 32
 
 
-def rm_is_lane(m: int, n: int, dtype) -> bool:
+def rm_is_lane(m: int, n: int, dtype, aligned: bool = True) -> bool:
     """csrc/gemv_rm.cu gemv_rm_is_lane: rows of <= 4 KiB and >= 148 * 64 of
     them take the one-thread-per-row kernel — the reference's order and
-    rounding, so bitwise gemv_ref at any alignment."""
-    return n * np.dtype(dtype).itemsize <= 4096 and m >= SMS * 64
+    rounding, so bitwise gemv_ref — when the rows are whole 32-byte vectors,
+    or (scalar loads) at most 24 elements long."""
+    s = np.dtype(dtype).itemsize
+    vec = aligned and n % (32 // s) == 0
+    return n * s <= 4096 and m >= SMS * 64 and (vec or n <= 24)
 
 
 def cm_is_tall(m: int, dtype, aligned: bool = True) -> bool:
