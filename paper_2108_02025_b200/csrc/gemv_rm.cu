@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kRmBlock)
     }
 }
 
-// Short rows (n*s <= rm_lane_max_bytes() = 4 KiB, e.g. 2^20 x 64): one THREAD per
+// Short rows (n*s <= rm_lane_max_bytes() = 256 B, e.g. 2^20 x 64): one THREAD per
 // row, in the reference's order and rounding — acc = c_i, then for j
 // ascending a separately rounded multiply and add (an FMA for the trailing
 // n mod 16/s terms), exactly gemv_ref (reference kernels.hpp:171-181): bit
@@ -351,9 +351,48 @@ __global__ void __launch_bounds__(kRmBlock)
 inline uint64_t rm_lane_max_bytes() {
     static const uint64_t v = [] {
         const char* e = getenv("CABL_RM_LANE_MAX");
-        return e ? uint64_t(atoll(e)) : uint64_t(4096);
+        return e ? uint64_t(atoll(e)) : uint64_t(256);
     }();
     return v;
+}
+
+// Rows of 256 B .. 4 KiB of whole 32-byte vectors (mode 7): G lanes per row,
+// each lane 32-byte vectors j = lg, lg + G, ... with kGVecU in flight, then a
+// fixed butterfly over the G lanes.  Coalesced G * 32-byte runs per row
+// where the one-thread-per-row kernel's warps touch 32 rows per load.
+constexpr int kGVecU = 4;
+constexpr uint64_t kGVecMaxBytes = 4096;
+
+template <typename T, int G>
+__global__ void __launch_bounds__(kRmBlock)
+    gemv_rm_gvec_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
+                        uint64_t m, uint64_t n, uint64_t groups) {
+    pdl_enter();
+    const int lg = threadIdx.x & (G - 1);
+    const uint64_t gg = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+    if (gg >= groups) return;
+    const Partition part(m, groups);
+    const uint64_t nv = n / Vec<T>::N;
+    const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
+    for (uint64_t i = part.begin(gg); i < part.begin(gg + 1); ++i) {
+        const Vec<T>* row = reinterpret_cast<const Vec<T>*>(A + i * n);
+        T acc = T(0);
+        uint64_t j = lg;
+        for (; j + uint64_t(kGVecU - 1) * G < nv; j += uint64_t(kGVecU) * G) {
+            Vec<T> a[kGVecU], b[kGVecU];
+#pragma unroll
+            for (int u = 0; u < kGVecU; ++u) {
+                a[u] = ld_stream(row + j + u * G);
+                b[u] = ld_reuse(X + j + u * G);
+            }
+#pragma unroll
+            for (int u = 0; u < kGVecU; ++u) acc = dot_vec(a[u], b[u], acc);
+        }
+        for (; j < nv; j += G) acc = dot_vec(ld_stream(row + j), ld_reuse(X + j), acc);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) acc = add_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o, G));
+        if (lg == 0) c[i] = add_rn(c[i], acc);
+    }
 }
 
 template <typename T> bool rm_vec_ok(const T* A, const T* x, uint64_t n) {
@@ -372,6 +411,13 @@ template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n
     // enough of them to give every SM a few warps
     const bool lane = gemv_rm_is_lane(A, x, m, n, sizeof(T));
     if (forced == 3 || (forced < 0 && lane)) return vec ? 3 : 4;
+    // rows of 256 B .. 4 KiB: G lanes per row with 32-byte vectors (256 MiB
+    // fp32, n = 256 / 1024: 51.2 / 51.2 us; the bitwise lane kernel 63.5 /
+    // 62.5, the sweeps worse still)
+    if (forced == 7 ||
+        (forced < 0 && n * sizeof(T) <= kGVecMaxBytes && m >= uint64_t(sm_count()) * 64)) {
+        if (vec) return 7;
+    }
     if (!vec) return -1;
     if (forced >= 0 && forced <= 2) return forced;
     // measured (tools/tune.py, 8192^2 and 65536^2 fp32): 4 rows x 2 vectors
@@ -502,7 +548,22 @@ cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
     if (info) info->ctas = 0;
     if (m == 0 || n == 0) return cudaSuccess; // c += 0
     const int mode = rm_mode<T>(A, x, m, n);
-    if (mode >= 3) {
+    if (mode == 7) {
+        const uint64_t nv = n / Vec<T>::N;
+        const int G = nv > 96 ? 32 : (nv > 48 ? 16 : (nv > 24 ? 8 : 4));
+        const uint64_t max_groups = uint64_t(sm_count()) * 8 * (kRmBlock / G);
+        const uint64_t groups = m < max_groups ? m : max_groups;
+        const unsigned grid = unsigned((groups * G + kRmBlock - 1) / kRmBlock);
+        if (G == 32)
+            launch(gemv_rm_gvec_kernel<T, 32>, grid, kRmBlock, 0, s, A, x, c, m, n, groups);
+        else if (G == 16)
+            launch(gemv_rm_gvec_kernel<T, 16>, grid, kRmBlock, 0, s, A, x, c, m, n, groups);
+        else if (G == 8)
+            launch(gemv_rm_gvec_kernel<T, 8>, grid, kRmBlock, 0, s, A, x, c, m, n, groups);
+        else
+            launch(gemv_rm_gvec_kernel<T, 4>, grid, kRmBlock, 0, s, A, x, c, m, n, groups);
+        if (info) info->ctas = grid;
+    } else if (mode >= 3) {
         const uint64_t cap = uint64_t(sm_count()) * 8;
         const uint64_t need = (m + kRmBlock - 1) / kRmBlock;
         const unsigned grid = unsigned(need < cap ? need : cap);

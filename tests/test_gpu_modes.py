@@ -72,9 +72,10 @@ def test_scheduling_variants_are_bitwise_identical(cuda):
 
 
 def test_row_major_gemv_modes_agree_with_oracle_tolerance(cuda):
-    """The segment kernel (mode 0), the sweep (1, 2) and the one-thread-per-row
-    kernel (3, forced here on 8 KB rows) sum a row in different orders: not
-    bitwise equal to each other, each within the contract bound."""
+    """The segment kernel (mode 0), the sweep (1, 2), the one-thread-per-row
+    kernel (3) and the G-lanes-per-row vector kernel (7), both forced here on
+    8 KB rows, sum a row in different orders: not bitwise equal to each other,
+    each within the contract bound."""
     import numpy as np
     from oracle import oracle as O
     script = r"""
@@ -93,7 +94,7 @@ print(json.dumps(c.cpu().numpy().astype(float).tolist()))
     x = O.gen_uniform(n, np.float32, 42, 1)
     c0 = O.gen_uniform(m, np.float32, 42, 4)
     truth, rowabs = O.gemv_truth(A, 0, x, c0)
-    for mode in ("0", "1", "2", "3"):
+    for mode in ("0", "1", "2", "3", "7"):
         r = subprocess.run([sys.executable, "-c", script % {"root": str(ROOT)}],
                            env=dict(os.environ, CABL_GEMV_RM_MODE=mode), capture_output=True,
                            text=True, timeout=600)

@@ -86,13 +86,13 @@ def rm_is_ordered(m: int, n: int, dtype, aligned: bool = True) -> bool:
 
 
 def rm_is_lane(m: int, n: int, dtype, aligned: bool = True) -> bool:
-    """csrc/gemv_rm.cu gemv_rm_is_lane: rows of <= 4 KiB and >= 148 * 64 of
+    """csrc/gemv_rm.cu gemv_rm_is_lane: rows of <= 256 B and >= 148 * 64 of
     them take the one-thread-per-row kernel — the reference's order and
     rounding, so bitwise gemv_ref — when the rows are whole 32-byte vectors,
     or (scalar loads) at most 24 elements long."""
     s = np.dtype(dtype).itemsize
     vec = aligned and n % (32 // s) == 0
-    return n * s <= 4096 and m >= SMS * 64 and (vec or n <= 24)
+    return n * s <= 256 and m >= SMS * 64 and (vec or n <= 24)
 
 
 def cm_is_tall(m: int, dtype, aligned: bool = True) -> bool:
