@@ -241,8 +241,9 @@ def l2_mode(step_bytes: int) -> str:
     """'stream' when a step's inputs exceed the L2: the front-to-back sweep of
     step k+1 misses on everything step k left behind.  Checked with ncu
     (--cache-control none) on back-to-back launches of the two smallest
-    configs: every D1 launch (134.2 MB alg.) reads 133.95 MB from DRAM and
-    every G1 launch (268.5 MB) 268.5 MB (profiles/r01_ncu_b2b_{D1,G1}.csv).
+    configs: every G1 launch (268.5 MB alg.) reads 268.5 MB from DRAM; a D1
+    launch (134.2 MB) reads 131.2 MB, i.e. ~2% of it still hits in L2
+    (profiles/r01_ncu_b2b_{D1,G1}.csv).
     'flush' otherwise (inputs that fit in L2)."""
     return "stream" if step_bytes > L2_BYTES else "flush"
 
