@@ -142,6 +142,40 @@ void sharded_gemv_rows(Group& g, const std::vector<const DeviceMatrix<T>*>& A,
     g.synchronize();
 }
 
+// The same, then every device assembles the full c ("output
+// slices optionally all-gathered"): c_full[r] (length sum of the slices, on
+// g.device(r)) receives slice q at offset sum_{p<q} |c[p]| through one
+// ncclBroadcast per source rank, grouped — unequal slices need no padding.
+template <typename T>
+void sharded_gemv_rows_gather(Group& g, const std::vector<const DeviceMatrix<T>*>& A,
+                              const std::vector<const DeviceVector<T>*>& x,
+                              const std::vector<DeviceVector<T>*>& c,
+                              const std::vector<DeviceVector<T>*>& c_full,
+                              const ExecPolicy& policy) {
+    const int G = g.size();
+    cabl::detail::require(int(c_full.size()) == G, "sharded_gemv_rows_gather: one c_full per device");
+    std::vector<std::size_t> off(std::size_t(G) + 1, 0);
+    for (int q = 0; q < G; ++q) off[q + 1] = off[q] + c[q]->len();
+    for (int r = 0; r < G; ++r)
+        cabl::detail::require(c_full[r]->len() == off[G], "sharded_gemv_rows_gather: c_full length");
+    for (int r = 0; r < G; ++r) {
+        cabl::detail::cuda_check(cudaSetDevice(g.device(r)), "cudaSetDevice");
+        if (A[r]->layout() == Layout::RowMajor)
+            gemv_row_major(*A[r], *x[r], *c[r], policy, g.stream(r));
+        else
+            gemv_col_major(*A[r], *x[r], *c[r], policy, g.stream(r));
+    }
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    for (int q = 0; q < G; ++q)
+        for (int r = 0; r < G; ++r)
+            nccl_check(ncclBroadcast(r == q ? c[q]->data() : nullptr, c_full[r]->data() + off[q],
+                                     c[q]->len(), detail::nccl_type<T>(), q, g.comm(r),
+                                     g.stream(r)),
+                       "ncclBroadcast");
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    g.synchronize();
+}
+
 // C[r] += x[r] (x) y[r] on every device's row block (no communication).
 template <typename T>
 void sharded_ger_rows(Group& g, const std::vector<const DeviceVector<T>*>& x,

@@ -121,5 +121,32 @@ int main() {
         std::printf("rank %d: gemv rows %s, ger rows %s\n", r, gemv_ok ? "ok" : "MISMATCH",
                     ger_ok ? "ok" : "MISMATCH");
     }
+    // the gathered variant: a second step on the same shards, then every
+    // device holds all of c (the concatenation of the per-rank results)
+    std::vector<DeviceVector<float>> full;
+    std::vector<DeviceVector<float>*> fullq;
+    std::vector<Vector<float>> c2_expect;
+    for (int r = 0; r < G; ++r) {
+        cudaSetDevice(0);
+        {
+            DeviceMatrix<float> dA(Ab[r].download());
+            DeviceVector<float> dx(xv), dc(c_expect[r]);
+            gemv_row_major(dA, dx, dc, pol);
+            c2_expect.push_back(dc.download());
+        }
+        cudaSetDevice(g.device(r));
+        full.emplace_back(m);
+    }
+    for (int r = 0; r < G; ++r) fullq.push_back(&full[r]);
+    nccl::sharded_gemv_rows_gather(g, Ap, xq, cq, fullq, pol);
+    Vector<float> want_full(m);
+    for (int r = 0, o = 0; r < G; o += int(c2_expect[r].len()), ++r)
+        std::copy(c2_expect[r].begin(), c2_expect[r].end(), want_full.begin() + o);
+    for (int r = 0; r < G; ++r) {
+        cudaSetDevice(g.device(r));
+        const bool full_ok = full[r].download() == want_full;
+        ok &= full_ok;
+        std::printf("rank %d: gathered c %s\n", r, full_ok ? "ok" : "MISMATCH");
+    }
     return ok ? 0 : 1;
 }
