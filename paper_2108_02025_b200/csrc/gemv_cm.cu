@@ -2,9 +2,10 @@
 // reference cabl::gemv_col_major (proj/include/cabl/kernels.hpp:187-224,
 // Algorithm 1 of the paper: row blocks x column blocks x m_r register panels).
 //
-// Two shapes, three kernels:
+// Two shapes (cm_path picks; the numbers below are the defaults):
 //
-// (1) TALL (m >= kSplitMaxRows, e.g. 2^20 x 256).  The CPU panel keeps m_r
+// (1) TALL (m/V >= 74 units of 256 row vectors, e.g. 2^20 x 256; n < 16 takes
+//     the narrow variant with several row vectors per thread).  The CPU panel keeps m_r
 //     rows of c in registers across a column block.  Here a THREAD keeps one
 //     32-byte vector of rows (4 doubles / 8 floats) of c in registers across
 //     ALL columns, and a CTA owns BLOCK consecutive row vectors, so every
@@ -17,8 +18,11 @@
 //     If m is not a multiple of the vector (columns misaligned), the same
 //     order runs with one row per lane (gemv_cm_rows_kernel).
 //
-// (2) SPLIT (short-wide: m < kSplitMaxRows, e.g. 256 x 2^20).  The reference
-//     runs this shape on ONE thread (a single m_c row block).
+// (2) SPLIT (everything else, e.g. 256 x 2^20).  The reference runs the
+//     short-wide shape on ONE thread (a single m_c row block).
+//     Below 512 rows (odd m: 1024) the column tiles are contiguous and stream
+//     through a cp.async.bulk ring (the bulk kernels); above, row tiles of
+//     choose_tile_rows() rows x column parts (2-D split).
 //     Here one CTA per SM sweeps column tiles in grid-stride order (the whole
 //     GPU reads one contiguous window at a time); threads are (row lane,
 //     column lane) pairs accumulating with FMA; column lanes combine in

@@ -22,8 +22,17 @@
 // Every per-element order is a function of (m, n, grid) only: bitwise
 // reproducible run to run.
 //
-// Unaligned operands or n % (32/sizeof(T)) != 0 take a scalar warp-per-row
-// kernel (same ordering guarantees).
+// Kernels by shape (rm_mode):
+//   * rows <= 256 B, many of them: one thread per row in the reference's
+//     order and rounding — bitwise gemv_ref (gemv_rm_lane_kernel, mode 3/4);
+//   * rows of 256 B .. 4 KiB: G lanes per row, 32-byte vectors (mode 7);
+//   * longer rows, enough of them: the CTA-wide SWEEP (modes 1, 2; a row
+//     shape with mostly empty last passes switches to 8 x 1 groups);
+//   * few rows: the unit kernel described above (mode 0);
+//   * unaligned operands or n % (32/sizeof(T)) != 0: G lanes per row with
+//     scalar loads (mode -1).
+// CABL_GEMV_RM_ORDER=reference routes to gemv_rm_ordered.cu instead where it
+// applies.  Every kernel is bitwise reproducible run to run.
 //
 // Algorithmic bytes per launch: m*n*s + n*s + 2*m*s.
 #include "common.cuh"
