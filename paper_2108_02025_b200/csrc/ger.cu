@@ -238,6 +238,106 @@ __global__ void __launch_bounds__(kGerBlock, 2)
     }
 }
 
+// Rows of whole 16-byte (not 32-byte) vectors — n = 4 mod 8 floats, or C / y
+// only 16-byte aligned: the same flat sweep with 16-byte vectors.
+struct alignas(16) F4 {
+    float v[4];
+};
+struct alignas(16) D2 {
+    double v[2];
+};
+template <typename T> struct H16;
+template <> struct H16<float> {
+    using type = F4;
+    static constexpr int N = 4;
+};
+template <> struct H16<double> {
+    using type = D2;
+    static constexpr int N = 2;
+};
+__device__ __forceinline__ F4 ld_rmw16(const F4* p) {
+    F4 r;
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ D2 ld_rmw16(const D2* p) {
+    D2 r;
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                 : "=d"(r.v[0]), "=d"(r.v[1])
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ F4 ld_reuse16(const F4* p) {
+    F4 r;
+    asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ D2 ld_reuse16(const D2* p) {
+    D2 r;
+    asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_stream16(F4* p, const F4& r) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(r.v[0]),
+                 "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3])
+                 : "memory");
+}
+__device__ __forceinline__ void st_stream16(D2* p, const D2& r) {
+    asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(r.v[0]),
+                 "d"(r.v[1])
+                 : "memory");
+}
+
+constexpr int kGerFlatHU = 8; // 16-byte vectors in flight per thread
+
+template <typename T>
+__global__ void __launch_bounds__(kGerBlock, 2)
+    ger_flat_hvec_kernel(const T* __restrict__ u, const T* __restrict__ v, T* __restrict__ C,
+                         uint64_t outer, uint64_t ivec, uint64_t step_o, uint64_t step_i) {
+    pdl_enter();
+    using HV = typename H16<T>::type;
+    constexpr uint64_t kSlab = uint64_t(kGerBlock) * kGerFlatHU;
+    const uint64_t total = outer * ivec;
+    const HV* V_ = reinterpret_cast<const HV*>(v);
+    HV* Cv = reinterpret_cast<HV*>(C);
+    for (uint64_t s0 = uint64_t(blockIdx.x) * kSlab; s0 < total; s0 += uint64_t(gridDim.x) * kSlab) {
+        const uint64_t q0 = s0 + threadIdx.x;
+        uint64_t o = q0 / ivec, i = q0 - o * ivec;
+        HV cv[kGerFlatHU], vv[kGerFlatHU];
+        T uo[kGerFlatHU];
+#pragma unroll
+        for (int k = 0; k < kGerFlatHU; ++k) {
+            const uint64_t q = q0 + uint64_t(k) * kGerBlock;
+            if (q < total) {
+                cv[k] = ld_rmw16(Cv + q);
+                vv[k] = ld_reuse16(V_ + i);
+                uo[k] = __ldg(u + o);
+            }
+            o += step_o;
+            i += step_i;
+            if (i >= ivec) {
+                i -= ivec;
+                ++o;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kGerFlatHU; ++k) {
+            const uint64_t q = q0 + uint64_t(k) * kGerBlock;
+            if (q < total) {
+#pragma unroll
+                for (int e = 0; e < H16<T>::N; ++e) cv[k].v[e] = fma_rn(uo[k], vv[k].v[e], cv[k].v[e]);
+                st_stream16(Cv + q, cv[k]);
+            }
+        }
+    }
+}
+
 } // namespace
 
 // CABL_GER_MODE (tuning only): 0 static row ranges, 1 tiles in grid-stride
@@ -297,6 +397,17 @@ cudaError_t ger_launch(const T* u, const T* v, T* C, uint64_t outer, uint64_t in
         const uint64_t cap = uint64_t(sm_count()) * 8;
         const unsigned grid = unsigned(slabs < cap ? slabs : cap);
         launch(ger_flat_vec_kernel<T>, grid, kGerBlock, 0, s, u, v, C, outer, ivec,
+               uint64_t(kGerBlock) / ivec, uint64_t(kGerBlock) % ivec);
+        if (info) info->ctas = grid;
+    } else if (!small && (reinterpret_cast<uintptr_t>(C) & 15u) == 0 &&
+               (reinterpret_cast<uintptr_t>(v) & 15u) == 0 && inner % (16 / sizeof(T)) == 0) {
+        // rows of whole 16-byte vectors: flat sweep in 16-byte vectors
+        constexpr uint64_t kSlab = uint64_t(kGerBlock) * kGerFlatHU;
+        const uint64_t ivec = inner / (16 / sizeof(T));
+        const uint64_t slabs = (outer * ivec + kSlab - 1) / kSlab;
+        const uint64_t cap = uint64_t(sm_count()) * 8;
+        const unsigned grid = unsigned(slabs < cap ? slabs : cap);
+        launch(ger_flat_hvec_kernel<T>, grid, kGerBlock, 0, s, u, v, C, outer, ivec,
                uint64_t(kGerBlock) / ivec, uint64_t(kGerBlock) % ivec);
         if (info) info->ctas = grid;
     } else {

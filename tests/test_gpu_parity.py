@@ -264,7 +264,9 @@ def test_gemv_single_row_equals_dot_ref_bitwise(cuda):
 GER_SHAPES = [(1, 1), (2, 3), (3, 3), (500, 500), (777, 1001), (1000, 8), (8, 1000),
               (1024, 1024), (3000, 4096), (8192, 8192),
               # short aligned rows (flat vector sweep) and short odd rows (flat scalar)
-              (20_000, 64), (64, 20_000), (100_000, 8), (50_000, 5), (5, 50_000), (1, 300_000)]
+              (20_000, 64), (64, 20_000), (100_000, 8), (50_000, 5), (5, 50_000), (1, 300_000),
+              # rows of whole 16-byte vectors (flat 16-byte sweep)
+              (3000, 4100), (12, 100_004), (40_000, 12)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)

@@ -49,7 +49,7 @@ for m, n, off in ((8192, 8192, 0), (8193, 8192, 0), (8192, 8192, 1), (256, 1 << 
     A, x, c = buf(m * n, off), buf(n, off), buf(m, off)
     M = cb.DenseMatrix.wrap(A, m, n, cb.Layout.ColMajor)
     report(f"gemv_cm {m}x{n} off={off}", timeit(lambda: cb.gemv_col_major(M, x, c, pol)), m * n * s)
-for m, n, off in ((8192, 8192, 0), (8192, 8193, 0), (8192, 8192, 1)):
+for m, n, off in ((8192, 8192, 0), (8192, 8193, 0), (8192, 8192, 1), (8192, 8196, 0), (8192, 8192, 4)):
     C, x, y = buf(m * n, off), buf(m, off), buf(n, off)
     M = cb.DenseMatrix.wrap(C, m, n, cb.Layout.RowMajor)
     report(f"ger_rm {m}x{n} off={off}", timeit(lambda: cb.ger(x, y, M, pol)), 2 * m * n * s)
