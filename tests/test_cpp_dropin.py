@@ -63,3 +63,38 @@ def test_multi_gpu_nccl_example(cuda):
     r = subprocess.run([str(CPP / "mgpu_example")], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "MISMATCH" not in r.stdout
+
+
+def _cmake_consumer(tmp_path):
+    """a reference-shaped consumer switched to the drop-in
+    by CMake target alone (tests/cpp/cmake_consumer)."""
+    import shutil
+    if shutil.which("cmake") is None:
+        pytest.skip("cmake not available")
+    if not LIB.exists():
+        pytest.fail("libcabl_cuda.so is not built")
+    build = tmp_path / "build"
+    gen = ["-G", "Ninja"] if shutil.which("ninja") else []
+    r = subprocess.run(["cmake", "-S", str(CPP / "cmake_consumer"), "-B", str(build), *gen],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    r = subprocess.run(["cmake", "--build", str(build)], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    return build / "consumer"
+
+
+def test_cmake_consumer_builds(tmp_path):
+    import torch
+    exe = _cmake_consumer(tmp_path)
+    assert exe.exists()
+    if not torch.cuda.is_available():
+        r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+        assert r.returncode == 3 and "no CUDA device available" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cmake_consumer_runs(cuda, tmp_path):
+    exe = _cmake_consumer(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
