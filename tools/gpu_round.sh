@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_cpp_dropin.py -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+python tools/sanitize_driver.py > gpurun_out/san_plain.log 2>&1; echo "rc=$?" >> gpurun_out/san_plain.log
+CABL_GEMV_RM_ORDER=reference python tools/sanitize_driver.py >> gpurun_out/san_plain.log 2>&1; echo "rc=$?" >> gpurun_out/san_plain.log

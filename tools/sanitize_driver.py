@@ -37,20 +37,23 @@ def main():
             ok &= bool(torch.isfinite(torch.tensor(cb.dot(x[:n], y[:n], 0.5, pol))))
             ok &= bool(torch.isfinite(torch.tensor(cb.dot(x[1:n + 1], y[2:n + 2], 0.5, pol))))
         # GEMV row-major: ordered, segment, sweep, scalar
-        for m, n in ((3, 5), (40, 1024), (2, 65536), (7200, 256), (3000, 999), (5000, 1028)):
+        for m, n in ((3, 5), (40, 1024), (2, 65536), (7200, 256), (3000, 999), (5000, 1028),
+                     (20000, 16), (20000, 256), (20000, 33), (20001, 5), (9000, 8200)):
             A = cb.DenseMatrix.wrap(f(m * n, dt, 3), m, n, cb.Layout.RowMajor)
             c = f(m, dt, 4)
             cb.gemv_row_major(A, f(n, dt, 1), c, pol)
             ok &= bool(torch.isfinite(c).all())
         # GEMV col-major: ordered, 2-D split vec/scalar, bulk, tall vec, tall scalar
         for m, n in ((3, 5), (256, 4096), (4096, 300), (2000 + V, 77), (1001, 300),
-                     (148 * 256 * V, 4), (148 * 1024 + 1, 3)):
+                     (148 * 256 * V, 4), (148 * 1024 + 1, 3), (1, 100000), (257, 20000),
+                     (74 * 256 * V, 20), (300000 // V * V, 9), (8193, 300)):
             A = cb.DenseMatrix.wrap(f(m * n, dt, 3), m, n, cb.Layout.ColMajor)
             c = f(m, dt, 4)
             cb.gemv_col_major(A, f(n, dt, 1), c, pol)
             ok &= bool(torch.isfinite(c).all())
         # GER: generic, tile queue, both layouts
-        for m, n in ((3, 5), (37, 1000), (300, 2048), (1000, 4096)):
+        for m, n in ((3, 5), (37, 1000), (300, 2048), (1000, 4096), (20000, 64), (3000, 4100),
+                     (50000, 5)):
             for lay in (cb.Layout.RowMajor, cb.Layout.ColMajor):
                 C = cb.DenseMatrix.wrap(f(m * n, dt, 5), m, n, lay)
                 cb.ger(f(m, dt, 1), f(n, dt, 2), C, pol)
