@@ -62,9 +62,10 @@ def test_dot_guard_bands(cuda, dtype, off):
         out.check(f"dot n={n} off={off}")
 
 
-RM = [(3, 5), (40, 1024), (2, 65536), (7200, 256), (3000, 999), (5000, 1028), (4736, 100)]
+RM = [(3, 5), (40, 1024), (2, 65536), (7200, 256), (3000, 999), (5000, 1028), (4736, 100),
+      (20_000, 16), (20_000, 256), (20_000, 33), (9000, 8200)]
 CM = [(3, 5), (256, 4096), (4096, 300), (2008, 77), (1001, 300), (148 * 256 * 8, 4),
-      (148 * 1024 + 1, 3)]
+      (148 * 1024 + 1, 3), (1, 100_000), (257, 20_000), (74 * 256 * 8, 20), (8193, 300)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -90,7 +91,8 @@ def test_ger_guard_bands(cuda, dtype, off, layout):
     import paper_2108_02025_b200 as cb
     pol = cb.default_policy(1)
     lay = cb.Layout.RowMajor if layout == "row" else cb.Layout.ColMajor
-    for m, n in ((3, 5), (37, 1000), (300, 2048), (1000, 4096), (8, 8193)):
+    for m, n in ((3, 5), (37, 1000), (300, 2048), (1000, 4096), (8, 8193), (20_000, 64),
+                 (3000, 4100), (50_000, 5)):
         x, y = framed_input(m, dtype, 1, off, cuda), framed_input(n, dtype, 2, off, cuda)
         C = FramedOutput(m * n, dtype, 5, off, cuda)
         cb.ger(x, y, cb.DenseMatrix.wrap(C.view, m, n, lay), pol)

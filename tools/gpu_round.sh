@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-python tools/sanitize_driver.py > gpurun_out/san_plain.log 2>&1; echo "rc=$?" >> gpurun_out/san_plain.log
-CABL_GEMV_RM_ORDER=reference python tools/sanitize_driver.py >> gpurun_out/san_plain.log 2>&1; echo "rc=$?" >> gpurun_out/san_plain.log
+timeout 900 python -m pytest tests/test_gpu_bounds.py -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
