@@ -131,6 +131,16 @@ CABL_API int cabl_cuda_combine_partials_f32(const float* partials, uint32_t coun
 CABL_API int cabl_cuda_combine_partials_f64(const double* partials, uint32_t count, double alpha0,
                                    double* out, void* stream);
 
+/* Rank-ordered combine of `count` partial c vectors (column-sharded
+ * col-major GEMV: each rank computes A[:, cols_r] x[cols_r] from zero; the
+ * partials are all-gathered as parts[g*m + i]):
+ *   c[i] += ((parts[0*m+i] + parts[1*m+i]) + ...)   in rank order,
+ * bitwise identical on every rank whatever the collective's algorithm. */
+CABL_API int cabl_cuda_combine_rows_f32(const float* parts, uint32_t count, uint64_t m, float* c,
+                                        void* stream);
+CABL_API int cabl_cuda_combine_rows_f64(const double* parts, uint32_t count, uint64_t m,
+                                        double* c, void* stream);
+
 /* --------------------------------------------------------------- GEMV ---
  * c[0..m) += A x, A is m x n.  `small_cutoff`: when m*n + m + n <= cutoff the
  * call runs the ordered single-CTA path, which reproduces the compiled

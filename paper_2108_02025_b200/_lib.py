@@ -56,6 +56,8 @@ SIGNATURES: dict[str, list] = {
     "cabl_cuda_dot_f64": [vp, vp, u64, f64, vp, u64, _P, vp],
     "cabl_cuda_combine_partials_f32": [vp, u32, f32, vp, vp],
     "cabl_cuda_combine_partials_f64": [vp, u32, f64, vp, vp],
+    "cabl_cuda_combine_rows_f32": [vp, u32, u64, vp, vp],
+    "cabl_cuda_combine_rows_f64": [vp, u32, u64, vp, vp],
     "cabl_cuda_gemv_rm_f32": [vp, u64, u64, vp, vp, u64, _P, vp],
     "cabl_cuda_gemv_rm_f64": [vp, u64, u64, vp, vp, u64, _P, vp],
     "cabl_cuda_gemv_cm_f32": [vp, u64, u64, vp, vp, u64, _P, vp],

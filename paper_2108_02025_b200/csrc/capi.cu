@@ -183,6 +183,16 @@ int combine_impl(const T* p, uint32_t count, T alpha0, T* out, void* stream) {
     return CABL_OK;
 }
 
+template <typename T>
+int combine_rows_impl(const T* parts, uint32_t count, uint64_t m, T* c, void* stream) {
+    if (m > 0 && (!c || (count > 0 && !parts))) return fail(CABL_EINVAL, "combine_rows: null pointer");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    CABL_TRY_CUDA(combine_rows_launch<T>(parts, count, m, c, as_stream(stream)),
+                  "combine_rows kernel");
+    return CABL_OK;
+}
+
 // ------------------------------------------------------------------ GEMV
 // Row-major GEMV runs the deterministic sweep kernels (BASELINE tolerance,
 // bitwise run to run) by default; CABL_GEMV_RM_ORDER=reference selects the
@@ -599,6 +609,15 @@ int cabl_cuda_combine_partials_f32(const float* p, uint32_t count, float alpha0,
 int cabl_cuda_combine_partials_f64(const double* p, uint32_t count, double alpha0,
                                    double* out, void* stream) {
     return combine_impl<double>(p, count, alpha0, out, stream);
+}
+
+int cabl_cuda_combine_rows_f32(const float* parts, uint32_t count, uint64_t m, float* c,
+                               void* stream) {
+    return combine_rows_impl<float>(parts, count, m, c, stream);
+}
+int cabl_cuda_combine_rows_f64(const double* parts, uint32_t count, uint64_t m, double* c,
+                               void* stream) {
+    return combine_rows_impl<double>(parts, count, m, c, stream);
 }
 
 int cabl_cuda_gemv_rm_f32(const float* A, uint64_t m, uint64_t n, const float* x, float* c,

@@ -374,6 +374,39 @@ cudaError_t combine_partials_launch(const T* p, uint32_t count, T alpha0, T* out
     return cudaGetLastError();
 }
 
+namespace {
+// c[i] += ((parts[0][i] + parts[1][i]) + ...) in index order: the combine of
+// a column-sharded col-major GEMV (each rank's partial c over its column block,
+// all-gathered), bitwise the same on every rank and for any reduction order
+// of the collective.
+template <typename T>
+__global__ void combine_rows_kernel(const T* __restrict__ parts, uint32_t count, uint64_t m,
+                                    T* __restrict__ c) {
+    pdl_enter();
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
+        T total = T(0);
+        for (uint32_t g = 0; g < count; ++g) total = add_rn(total, parts[uint64_t(g) * m + i]);
+        c[i] = add_rn(c[i], total);
+    }
+}
+} // namespace
+
+template <typename T>
+cudaError_t combine_rows_launch(const T* parts, uint32_t count, uint64_t m, T* c,
+                                cudaStream_t s) {
+    if (m == 0) return cudaSuccess;
+    const uint64_t blocks = (m + 255) / 256;
+    const uint64_t cap = uint64_t(sm_count()) * 8;
+    launch(combine_rows_kernel<T>, unsigned(blocks < cap ? blocks : cap), 256, 0, s, parts, count,
+           m, c);
+    return cudaGetLastError();
+}
+template cudaError_t combine_rows_launch<float>(const float*, uint32_t, uint64_t, float*,
+                                                cudaStream_t);
+template cudaError_t combine_rows_launch<double>(const double*, uint32_t, uint64_t, double*,
+                                                 cudaStream_t);
+
 template WorkspaceNeed dot_need<float>(uint64_t, bool);
 template WorkspaceNeed dot_need<double>(uint64_t, bool);
 template cudaError_t dot_launch<float>(const float*, const float*, uint64_t, float, float*, bool,

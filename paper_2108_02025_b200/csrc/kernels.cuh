@@ -39,6 +39,9 @@ cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, boo
 template <typename T>
 cudaError_t combine_partials_launch(const T* p, uint32_t count, T alpha0, T* out,
                                     cudaStream_t s);
+template <typename T>
+cudaError_t combine_rows_launch(const T* parts, uint32_t count, uint64_t m, T* c,
+                                cudaStream_t s);
 
 // ---- GEMV row-major (gemv_rm.cu) ----
 template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n);

@@ -16,6 +16,8 @@ The reference parallelises over CPU threads with contiguous chunks
   the full c on every rank with one all-gather (slices padded to equal size).
 * GER — rank g owns a block of rows of C and of x, y is replicated; no
   communication at all.
+* GEMV col-major by columns (short-wide, e.g. G3) — rank g owns a block of
+  columns; partial c vectors are all-gathered and added in rank order.
 
 The collective and the local compute are injectable so the partition and
 combine logic can be exercised by CPU ``gloo`` tests (tests/test_shard_gloo.py)
@@ -88,6 +90,37 @@ def sharded_gemv_rows(A_local: "cabl.DenseMatrix", x: torch.Tensor, c_local: tor
         b, e = partition(m_total, world, r)
         pieces.append(slab[r * width: r * width + (e - b)])
     return torch.cat(pieces)
+
+
+def _device_combine_rows(parts: torch.Tensor, world: int, c: torch.Tensor) -> None:
+    from . import _lib
+    sfx = cabl._suffix(parts)
+    with cabl._on_device(parts.device):
+        _lib.call(f"cabl_cuda_combine_rows_{sfx}", parts.data_ptr(), world, c.numel(),
+                  c.data_ptr(), cabl._stream_of(parts))
+
+
+def sharded_gemv_cols(A_local: "cabl.DenseMatrix", x_local: torch.Tensor, c: torch.Tensor,
+                      policy: "cabl.ExecPolicy", group=None, *,
+                      local_fn: Callable | None = None,
+                      combine_fn: Callable = _device_combine_rows) -> torch.Tensor:
+    """Column-sharded col-major GEMV ("G3 by columns"): rank g
+    owns the contiguous column block A[:, cols_g] (col-major, so one dense
+    m x |cols_g| block) and x[cols_g]; c is replicated.  Each rank computes its
+    partial A[:, cols_g] x[cols_g] from zero, the G partials are all-gathered,
+    and every rank adds them to c in rank order (cabl_cuda_combine_rows_*):
+    c is bitwise identical on every rank, independent of the collective's
+    reduction order."""
+    cabl._require(A_local.layout() == cabl.Layout.ColMajor,
+                  "sharded_gemv_cols: A must be col-major (its column blocks are contiguous)")
+    world = dist.get_world_size(group)
+    m = c.numel()
+    part = torch.zeros(m, dtype=c.dtype, device=c.device)
+    (local_fn or cabl.gemv_col_major)(A_local, x_local, part, policy)
+    gathered = torch.empty(world * m, dtype=c.dtype, device=c.device)
+    dist.all_gather_into_tensor(gathered, part, group=group)
+    combine_fn(gathered, world, c)
+    return c
 
 
 def sharded_ger_rows(x_local: torch.Tensor, y: torch.Tensor, C_local: "cabl.DenseMatrix",

@@ -37,6 +37,24 @@ c2 = c.clone()
 full = shard.sharded_gemv_rows(A, xv, c, pol, gather=True, m_total=m)
 cb.gemv_row_major(A, xv, c2, pol)
 assert torch.equal(full, c2) and torch.equal(c, c2)
+# col-major by columns (world 1): c + (0 + A x) == the direct call bitwise
+mc, nc = 256, 100_003
+Ac = cb.DenseMatrix.wrap(f(mc * nc, 6), mc, nc, cb.Layout.ColMajor)
+xc, cc = f(nc, 7), f(mc, 8)
+cc2 = cc.clone()
+shard.sharded_gemv_cols(Ac, xc, cc, pol)
+cb.gemv_col_major(Ac, xc, cc2, pol)
+assert torch.equal(cc, cc2)
+# the rank-ordered row combine itself, against an ordered sum on the host
+parts = f(3 * 1000, 9).view(3, 1000)
+c3 = f(1000, 10)
+want = c3.cpu().clone()
+acc = torch.zeros(1000)
+for g in range(3):
+    acc = acc + parts[g].cpu()
+want = want + acc
+shard._device_combine_rows(parts.reshape(-1), 3, c3)
+assert torch.equal(c3.cpu(), want)
 dist.destroy_process_group()
 print('ok')
 """

@@ -54,6 +54,20 @@ def _oracle_ger(x, y, C, policy):
     O.ger_ref(x.numpy(), y.numpy(), C.data.numpy(), int(C.layout()))
 
 
+def _oracle_gemv_cols(A, x, c, policy):
+    O.gemv_ref(A.data.numpy(), int(A.layout()), x.numpy(), c.numpy())
+
+
+def _ordered_combine_rows(parts: torch.Tensor, world: int, c: torch.Tensor) -> None:
+    P = parts.numpy().reshape(world, -1)
+    dt = P.dtype.type
+    total = np.zeros(P.shape[1], dtype=P.dtype)
+    for g in range(world):
+        total = (total + P[g]).astype(P.dtype)
+    c.copy_(torch.from_numpy((c.numpy() + total).astype(P.dtype)))
+    assert dt is not None
+
+
 def _worker(rank, world, port, results):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -92,6 +106,18 @@ def _worker(rank, world, port, results):
         shard.sharded_ger_rows(torch.from_numpy(gx[b:e].copy()), torch.from_numpy(gy), Cloc, pol,
                                local_fn=_oracle_ger)
         results[f"ger_{rank}"] = (b, e, Cloc.data.numpy().copy())
+        # ---- col-major GEMV by column blocks, all-gather + rank-ordered combine
+        mc, kc = 64, 5003
+        Ac = O.gen_uniform(mc * kc, np.float64, 42, 6)  # col-major: column j at j*mc
+        xc = O.gen_uniform(kc, np.float64, 42, 7)
+        cc = O.gen_uniform(mc, np.float64, 42, 8)
+        b, e = shard.partition(kc, world, rank)
+        Aloc = cb.DenseMatrix.wrap(torch.from_numpy(Ac[b * mc:e * mc].copy()), mc, e - b,
+                                   cb.Layout.ColMajor)
+        cl = torch.from_numpy(cc.copy())
+        shard.sharded_gemv_cols(Aloc, torch.from_numpy(xc[b:e].copy()), cl, pol,
+                                local_fn=_oracle_gemv_cols, combine_fn=_ordered_combine_rows)
+        results[f"gemvcols_{rank}"] = cl.numpy().copy()
     finally:
         dist.destroy_process_group()
 
@@ -138,6 +164,24 @@ def test_sharded_paths_over_gloo(world):
         np.testing.assert_array_equal(blk.reshape(e - b, k), C[b:e])
         covered += e - b
     assert covered == m
+
+    # col-major GEMV by columns: c + sum over ranks (rank order) of the column
+    # blocks' partials, identical on every rank
+    mc, kc = 64, 5003
+    Ac = O.gen_uniform(mc * kc, np.float64, 42, 6)
+    xc = O.gen_uniform(kc, np.float64, 42, 7)
+    cc = O.gen_uniform(mc, np.float64, 42, 8)
+    total = np.zeros(mc)
+    for r in range(world):
+        b, e = shard.partition(kc, world, r)
+        part = np.zeros(mc)
+        O.gemv_ref(Ac[b * mc:e * mc].copy(), 1, xc[b:e].copy(), part)
+        total = total + part
+    want = cc + total
+    for r in range(world):
+        np.testing.assert_array_equal(results[f"gemvcols_{r}"], want)
+    truth, rowabs = O.gemv_truth(Ac, 1, xc, cc)
+    assert np.all(np.abs(want - truth) <= 4 * kc * np.finfo(np.float64).eps * (rowabs + np.abs(cc)))
 
 
 def test_partition_is_balanced_and_contiguous():

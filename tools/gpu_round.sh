@@ -1,5 +1,2 @@
 mkdir -p gpurun_out
-rm -f gpurun_out/tune22.jsonl
-for i in 1 2; do
-for ef in 0 1; do CABL_GER_EF=$ef timeout 300 python tools/b2b.py R1 | sed "s/^/ef$ef /" >> gpurun_out/tune22.jsonl 2>&1; done
-done
+timeout 900 python -m pytest tests/test_gpu_dist.py tests/test_capi.py -m "gpu or not gpu" -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
