@@ -584,7 +584,7 @@ extern "C" int cabl_describe_device(int device, cabl_gpu_machine* out) {
 extern "C" {
 
 const char* cabl_last_error(void) { return g_err.c_str(); }
-int cabl_abi_version(void) { return 100; }
+int cabl_abi_version(void) { return 101; } // 1.01: + describe_device, combine_rows
 int cabl_device_count(void) {
     int c = 0;
     if (cudaGetDeviceCount(&c) != cudaSuccess) {
