@@ -90,6 +90,13 @@ inline int combine(const float* p, std::uint32_t k, float a, float* o, cudaStrea
 inline int combine(const double* p, std::uint32_t k, double a, double* o, cudaStream_t s) {
     return cabl_cuda_combine_partials_f64(p, k, a, o, s);
 }
+inline int combine_rows(const float* p, std::uint32_t k, std::uint64_t m, float* c, cudaStream_t s) {
+    return cabl_cuda_combine_rows_f32(p, k, m, c, s);
+}
+inline int combine_rows(const double* p, std::uint32_t k, std::uint64_t m, double* c,
+                        cudaStream_t s) {
+    return cabl_cuda_combine_rows_f64(p, k, m, c, s);
+}
 } // namespace detail
 
 // alpha0 + x.y with x, y given as per-device chunks (x[r], y[r] on
@@ -173,6 +180,43 @@ void sharded_gemv_rows_gather(Group& g, const std::vector<const DeviceMatrix<T>*
                                      g.stream(r)),
                        "ncclBroadcast");
     nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    g.synchronize();
+}
+
+// Col-major GEMV sharded by columns (short-wide shapes): A[r] is device r's
+// column block (m x n_r, col-major), x[r] the matching slice of x, c[r] a
+// replica of c.  Each device computes its partial from zero; the partials are
+// all-gathered and added to every replica in rank order (combine_rows), so
+// all devices end with the same bits.
+template <typename T>
+void sharded_gemv_cols(Group& g, const std::vector<const DeviceMatrix<T>*>& A,
+                       const std::vector<const DeviceVector<T>*>& x,
+                       const std::vector<DeviceVector<T>*>& c, const ExecPolicy& policy) {
+    const int G = g.size();
+    const std::size_t m = c[0]->len();
+    std::vector<DeviceVector<T>> part, gathered;
+    for (int r = 0; r < G; ++r) {
+        cabl::detail::require(A[r]->layout() == Layout::ColMajor && A[r]->rows() == m &&
+                                  c[r]->len() == m,
+                              "sharded_gemv_cols: col-major blocks of m rows, c replicas of length m");
+        cabl::detail::cuda_check(cudaSetDevice(g.device(r)), "cudaSetDevice");
+        part.emplace_back(m);
+        gathered.emplace_back(m * std::size_t(G));
+        cabl::detail::cuda_check(cudaMemsetAsync(part[r].data(), 0, m * sizeof(T), g.stream(r)),
+                                 "memset");
+        gemv_col_major(*A[r], *x[r], part[r], policy, g.stream(r));
+    }
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    for (int r = 0; r < G; ++r)
+        nccl_check(ncclAllGather(part[r].data(), gathered[r].data(), m, detail::nccl_type<T>(),
+                                 g.comm(r), g.stream(r)),
+                   "ncclAllGather");
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    for (int r = 0; r < G; ++r) {
+        cabl::detail::cuda_check(cudaSetDevice(g.device(r)), "cudaSetDevice");
+        cabl::detail::check(detail::combine_rows(gathered[r].data(), std::uint32_t(G), m,
+                                                 c[r]->data(), g.stream(r)));
+    }
     g.synchronize();
 }
 

@@ -148,5 +148,55 @@ int main() {
         ok &= full_ok;
         std::printf("rank %d: gathered c %s\n", r, full_ok ? "ok" : "MISMATCH");
     }
+    // col-major GEMV sharded by columns: every replica of c ends equal to
+    // c + the rank-ordered sum of the column blocks' partials
+    {
+        const std::size_t mc = 256, kc = 30001;
+        DenseMatrix<float> Ac(mc, kc, Layout::ColMajor);
+        Vector<float> xcv(kc), ccv(mc);
+        for (std::size_t i = 0; i < Ac.size(); ++i) Ac.data()[i] = U(rng);
+        for (auto& v : xcv) v = U(rng);
+        for (auto& v : ccv) v = U(rng);
+        std::vector<DeviceMatrix<float>> Acb;
+        std::vector<DeviceVector<float>> xcb, ccb;
+        Vector<float> want = ccv;
+        std::vector<float> total(mc, 0.0f);
+        for (int r = 0; r < G; ++r) {
+            const nccl::Range rg = nccl::partition(kc, G, r);
+            const std::size_t kr = rg.end - rg.begin;
+            DenseMatrix<float> Ar(mc, kr, Layout::ColMajor);
+            std::copy(Ac.data() + rg.begin * mc, Ac.data() + rg.end * mc, Ar.data());
+            Vector<float> xr(kr);
+            std::copy(xcv.begin() + rg.begin, xcv.begin() + rg.end, xr.begin());
+            cudaSetDevice(0);
+            {
+                DeviceMatrix<float> dA(Ar);
+                DeviceVector<float> dx(xr), dp(Vector<float>(mc, 0.0f));
+                gemv_col_major(dA, dx, dp, pol);
+                const Vector<float> p = dp.download();
+                for (std::size_t i = 0; i < mc; ++i) total[i] = total[i] + p[i];
+            }
+            cudaSetDevice(g.device(r));
+            Acb.emplace_back(Ar);
+            xcb.emplace_back(xr);
+            ccb.emplace_back(ccv);
+        }
+        for (std::size_t i = 0; i < mc; ++i) want[i] = want[i] + total[i];
+        std::vector<const DeviceMatrix<float>*> Acp;
+        std::vector<const DeviceVector<float>*> xcp;
+        std::vector<DeviceVector<float>*> ccp;
+        for (int r = 0; r < G; ++r) {
+            Acp.push_back(&Acb[r]);
+            xcp.push_back(&xcb[r]);
+            ccp.push_back(&ccb[r]);
+        }
+        nccl::sharded_gemv_cols(g, Acp, xcp, ccp, pol);
+        for (int r = 0; r < G; ++r) {
+            cudaSetDevice(g.device(r));
+            const bool cols_ok = ccb[r].download() == want;
+            ok &= cols_ok;
+            std::printf("rank %d: gemv by columns %s\n", r, cols_ok ? "ok" : "MISMATCH");
+        }
+    }
     return ok ? 0 : 1;
 }
