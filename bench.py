@@ -215,9 +215,16 @@ def make_inputs(w, rows: tuple[int, int], dev, layout=None):
     return {"C": cb.DenseMatrix.wrap(C, m, w.n, cb.Layout.RowMajor), "x": x, "y": y}
 
 
-def step_fn(w, ins, policy, ctx, sharded_dot: bool):
+def step_fn(w, ins, policy, ctx, sharded_dot: bool, fused: bool = False):
     import paper_2108_02025_b200 as cb
     from paper_2108_02025_b200 import shard
+    if w.op == "dot" and fused:
+        # the exchange of partials fused into the DOT kernel over peer memory
+        # (csrc/peer.cu): one launch per step at any N, no NCCL call
+        if getattr(ctx, "peer_mb", None) is None:
+            ctx.peer_mb = shard.PeerMailboxes(ctx.dev)
+        return (lambda: shard.sharded_dot_fused(ins["x"], ins["y"], 0.0, ins["out"], policy,
+                                                ctx.peer_mb)), 1
     if w.op == "dot":
         if sharded_dot and ctx.world > 1:
             import torch
@@ -588,10 +595,12 @@ def run_suite(args, ctx, flush, policy, peak):
 
     from paper_2108_02025_b200 import workloads as WL
     ids = list(WL.WORKLOADS) if ctx.world == 1 else ["R1", "G4", "D2"]
+    ids.append("D2f")  # D2 with the exchange fused into the kernel (peer memory)
     out = {}
     steps = max(3, min(args.steps, args.suite_steps))
     for wid in ids:
-        w = WL.WORKLOADS[wid]
+        fused = wid == "D2f"
+        w = WL.WORKLOADS["D2" if fused else wid]
         total = w.n if w.op == "dot" else w.m
         b, e = (0, total) if ctx.world == 1 else WL.Workload.shard_rows(w, ctx.rank, ctx.world)
         try:
@@ -602,13 +611,15 @@ def run_suite(args, ctx, flush, policy, peak):
             else:
                 import dataclasses
                 wl = dataclasses.replace(w, m=e - b)
-            fn, lps = step_fn(wl, ins, policy, ctx, sharded_dot=True)
+            fn, lps = step_fn(wl, ins, policy, ctx, sharded_dot=True, fused=fused)
             alg = w.alg_bytes(ctx.world)
             mode = l2_mode(wl.alg_bytes(1))
             times, _ = time_steps(fn, steps, args.warmup, ctx, flush, mode=mode)
             t_max = ctx.max(sum(times) / 1000.0)
             gbs = alg * steps / t_max / 1e9
-            entry = {"desc": w.desc, "gbs": round(gbs, 2),
+            desc = w.desc + (", partials exchanged inside the kernel over peer memory "
+                             "(cabl_cuda_dot_peer)" if fused else "")
+            entry = {"desc": desc, "gbs": round(gbs, 2),
                      "frac_of_peak": round(gbs / (peak * ctx.world), 4),
                      "us_per_step": round(t_max / steps * 1e6, 3),
                      "gflops": round(w.flops() * steps / t_max / 1e9, 2),

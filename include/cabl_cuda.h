@@ -141,6 +141,61 @@ CABL_API int cabl_cuda_combine_rows_f32(const float* parts, uint32_t count, uint
 CABL_API int cabl_cuda_combine_rows_f64(const double* parts, uint32_t count, uint64_t m,
                                         double* c, void* stream);
 
+/* ------------------------------------------- multi-GPU DOT, fused exchange ---
+ * The sharded DOT of SURVEY.md §8(e) (rank g owns a contiguous shard of x and
+ * y) with the exchange of partials fused into the DOT kernel over peer memory
+ * (NVLink / NVSwitch P2P stores), instead of an NCCL all-gather followed by
+ * cabl_cuda_combine_partials.  Each rank computes its shard partial with the
+ * single-GPU plan, stores it into every rank's mailbox, waits for all `world`
+ * partials and writes *out = ((p_0 + p_1) + ...) + alpha0 — bitwise the
+ * unfused path's result (cabl_cuda_dot(alpha0 = 0) per shard, then
+ * cabl_cuda_combine_partials), identical on every rank.
+ *
+ * Mailboxes: each rank creates one (cabl_peer_mailbox_create, on its device),
+ * exports an IPC handle, imports every other rank's handle, and passes the
+ * table mboxes[0..world) — its own mailbox at [rank], the peers' mappings
+ * elsewhere.  One process driving several devices passes device pointers
+ * directly after cudaDeviceEnablePeerAccess.  Calls are collective: every
+ * rank calls with the same table order, in the same sequence.  A rank that
+ * does not arrive within CABL_PEER_TIMEOUT_MS (default 30000) makes the
+ * waiting ranks write NaN and record the call in their mailbox's `fault`
+ * (cabl_peer_mailbox_state) instead of hanging.  world <= 8.
+ * Replaces cabl::dot (reference kernels.hpp:134-164) across GPUs. */
+typedef struct cabl_peer_handle {
+    unsigned char bytes[64]; /* cudaIpcMemHandle_t */
+} cabl_peer_handle;
+
+CABL_API int cabl_peer_mailbox_create(void** mbox); /* 512 B on the current device */
+CABL_API int cabl_peer_mailbox_destroy(void* mbox);
+CABL_API int cabl_peer_mailbox_export(void* mbox, cabl_peer_handle* out);
+CABL_API int cabl_peer_mailbox_import(const cabl_peer_handle* h, void** mapped);
+CABL_API int cabl_peer_mailbox_unmap(void* mapped);
+/* Synchronous read of a mailbox's completed-call count and fault epoch. */
+CABL_API int cabl_peer_mailbox_state(const void* mbox, uint64_t* epoch, uint64_t* fault);
+
+CABL_API int cabl_cuda_dot_peer_f32(const float* x, const float* y, uint64_t n, float alpha0,
+                                    float* out, void* const* mboxes, int world, int rank,
+                                    uint64_t small_cutoff, cabl_probe* probe, void* stream);
+CABL_API int cabl_cuda_dot_peer_f64(const double* x, const double* y, uint64_t n, double alpha0,
+                                    double* out, void* const* mboxes, int world, int rank,
+                                    uint64_t small_cutoff, cabl_probe* probe, void* stream);
+
+/* Every rank of a peer DOT on the CURRENT device, in one cooperative launch
+ * (blockIdx.y = rank; mailboxes all on this device): the same kernel and
+ * protocol as cabl_cuda_dot_peer_*, for testing the exchange with fewer GPUs
+ * than ranks.  xs/ys/ns/outs/mboxes have `world` entries.  CABL_EINVAL when
+ * the ranks' grids do not fit one co-resident wave. */
+CABL_API int cabl_cuda_dot_peer_emulate_f32(int world, const float* const* xs,
+                                            const float* const* ys, const uint64_t* ns,
+                                            float alpha0, float* const* outs,
+                                            void* const* mboxes, uint64_t small_cutoff,
+                                            void* stream);
+CABL_API int cabl_cuda_dot_peer_emulate_f64(int world, const double* const* xs,
+                                            const double* const* ys, const uint64_t* ns,
+                                            double alpha0, double* const* outs,
+                                            void* const* mboxes, uint64_t small_cutoff,
+                                            void* stream);
+
 /* --------------------------------------------------------------- GEMV ---
  * c[0..m) += A x, A is m x n.  `small_cutoff`: when m*n + m + n <= cutoff the
  * call runs the ordered single-CTA path, which reproduces the compiled

@@ -72,6 +72,16 @@ SIGNATURES: dict[str, list] = {
     "cabl_host_gemv_f64": [vp, i32, u64, u64, vp, vp, u64, _P, vp],
     "cabl_host_ger_f32": [vp, vp, vp, i32, u64, u64, u64, _P, vp],
     "cabl_host_ger_f64": [vp, vp, vp, i32, u64, u64, u64, _P, vp],
+    "cabl_peer_mailbox_create": [C.POINTER(vp)],
+    "cabl_peer_mailbox_destroy": [vp],
+    "cabl_peer_mailbox_export": [vp, C.c_char_p],
+    "cabl_peer_mailbox_import": [C.c_char_p, C.POINTER(vp)],
+    "cabl_peer_mailbox_unmap": [vp],
+    "cabl_peer_mailbox_state": [vp, C.POINTER(u64), C.POINTER(u64)],
+    "cabl_cuda_dot_peer_f32": [vp, vp, u64, f32, vp, vp, i32, i32, u64, _P, vp],
+    "cabl_cuda_dot_peer_f64": [vp, vp, u64, f64, vp, vp, i32, i32, u64, _P, vp],
+    "cabl_cuda_dot_peer_emulate_f32": [i32, vp, vp, vp, f32, vp, vp, u64, vp],
+    "cabl_cuda_dot_peer_emulate_f64": [i32, vp, vp, vp, f64, vp, vp, u64, vp],
     "cabl_cuda_fill_uniform_f32": [vp, u64, u64, u64, u64, vp],
     "cabl_cuda_fill_uniform_f64": [vp, u64, u64, u64, u64, vp],
     "cabl_cuda_fill_normal_f64": [vp, u64, u64, u64, u64, vp],

@@ -193,6 +193,125 @@ int combine_rows_impl(const T* parts, uint32_t count, uint64_t m, T* c, void* st
     return CABL_OK;
 }
 
+// ------------------------------------------------- peer-memory DOT (peer.cu)
+unsigned long long peer_timeout_ns() {
+    static const unsigned long long ns = [] {
+        const char* e = getenv("CABL_PEER_TIMEOUT_MS");
+        const unsigned long long ms = e ? strtoull(e, nullptr, 10) : 30000ull;
+        return (ms ? ms : 30000ull) * 1000000ull;
+    }();
+    return ns;
+}
+
+template <typename T>
+int peer_common_checks(int world, void* const* mboxes) {
+    if (world < 1 || world > kMaxPeers)
+        return fail(CABL_EINVAL, "dot_peer: world must be in [1, 8] (one NVLink domain)");
+    if (!mboxes) return fail(CABL_EINVAL, "dot_peer: mailbox table must not be null");
+    for (int g = 0; g < world; ++g)
+        if (!mboxes[g]) return fail(CABL_EINVAL, "dot_peer: null mailbox in the table");
+    return CABL_OK;
+}
+
+// Fill local slot lr of the argument block from the rank's operands and the
+// single-GPU plan; `ws` provides its partials and counters.
+template <typename T>
+void peer_slot(PeerDotArgs<T>& a, int lr, const T* x, const T* y, uint64_t n, T* out,
+               const DotPlan& p, T* partials, unsigned* counters) {
+    a.x[lr] = x;
+    a.y[lr] = y;
+    a.out[lr] = out;
+    a.n[lr] = n;
+    a.head[lr] = p.head;
+    a.chunk[lr] = p.chunk;
+    a.partials[lr] = partials;
+    a.counters[lr] = counters;
+    a.grid[lr] = p.grid;
+    a.vec_ok[lr] = p.vec_ok;
+}
+
+template <typename T>
+int dot_peer_impl(const T* x, const T* y, uint64_t n, T alpha0, T* out, void* const* mboxes,
+                  int world, int rank, uint64_t cutoff, cabl_probe* probe, void* stream) {
+    if (!out) return fail(CABL_EINVAL, "dot_peer: out must not be null");
+    if (n > 0 && (!x || !y)) return fail(CABL_EINVAL, "dot_peer: x and y must not be null");
+    if (int rc = peer_common_checks<T>(world, mboxes)) return rc;
+    if (rank < 0 || rank >= world) return fail(CABL_EINVAL, "dot_peer: rank must be in [0, world)");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    const bool small = n <= cutoff;
+    cudaStream_t s = as_stream(stream);
+    WsLease lease;
+    if (int rc = get_workspace(dev, s, dot_need<T>(n, small), &lease)) return rc;
+    const DotPlan p = dot_plan<T>(x, y, n, small);
+    PeerDotArgs<T> a{};
+    peer_slot(a, 0, x, y, n, out, p, static_cast<T*>(lease.ws.scratch), lease.ws.counters);
+    for (int g = 0; g < world; ++g) a.mbox[g] = mboxes[g];
+    a.world = world;
+    a.rank0 = rank;
+    a.timeout_ns = peer_timeout_ns();
+    a.prefetch = pdl_prefetch_enabled();
+    a.alpha0 = alpha0;
+    CABL_TRY_CUDA(dot_peer_launch<T>(a, 1, p.chunked, p.head != 0, false, s), "dot_peer kernel");
+    set_probe(probe, small ? CABL_VARIANT_DOT_SMALL : CABL_VARIANT_DOT_BLOCKED, p.grid);
+    return CABL_OK;
+}
+
+template <typename T>
+int dot_peer_emulate_impl(int world, const T* const* xs, const T* const* ys, const uint64_t* ns,
+                          T alpha0, T* const* outs, void* const* mboxes, uint64_t cutoff,
+                          void* stream) {
+    if (int rc = peer_common_checks<T>(world, mboxes)) return rc;
+    if (!xs || !ys || !ns || !outs) return fail(CABL_EINVAL, "dot_peer_emulate: null table");
+    for (int r = 0; r < world; ++r) {
+        if (!outs[r]) return fail(CABL_EINVAL, "dot_peer_emulate: out must not be null");
+        if (ns[r] > 0 && (!xs[r] || !ys[r]))
+            return fail(CABL_EINVAL, "dot_peer_emulate: x and y must not be null");
+    }
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    DotPlan plan[kMaxPeers];
+    size_t per_rank = 256;
+    bool chunked = false, peel = false;
+    unsigned gx = 1;
+    for (int r = 0; r < world; ++r) {
+        const bool small = ns[r] <= cutoff;
+        plan[r] = dot_plan<T>(xs[r], ys[r], ns[r], small);
+        const WorkspaceNeed w = dot_need<T>(ns[r], small);
+        per_rank = w.scratch_bytes > per_rank ? w.scratch_bytes : per_rank;
+        if (r > 0 && plan[r].chunked != chunked)
+            return fail(CABL_EINVAL, "dot_peer_emulate: every rank must take the same DOT kernel");
+        chunked = plan[r].chunked;
+        peel = peel || plan[r].head != 0;
+        gx = plan[r].grid > gx ? plan[r].grid : gx;
+    }
+    per_rank = (per_rank + 255) / 256 * 256;
+    // every waiting CTA must be co-resident: one cooperative wave
+    const int per_sm = dot_peer_ctas_per_sm(chunked, sizeof(T));
+    if (uint64_t(gx) * uint64_t(world) > uint64_t(per_sm) * uint64_t(sm_count()))
+        return fail(CABL_EINVAL, "dot_peer_emulate: the emulated ranks' grids do not fit one "
+                                 "co-resident wave (use smaller shards)");
+    cudaStream_t s = as_stream(stream);
+    WorkspaceNeed need;
+    need.counters = 2 * size_t(world);
+    need.scratch_bytes = per_rank * size_t(world);
+    WsLease lease;
+    if (int rc = get_workspace(dev, s, need, &lease)) return rc;
+    PeerDotArgs<T> a{};
+    for (int r = 0; r < world; ++r)
+        peer_slot(a, r, xs[r], ys[r], ns[r], outs[r], plan[r],
+                  reinterpret_cast<T*>(static_cast<char*>(lease.ws.scratch) + per_rank * r),
+                  lease.ws.counters + 2 * r);
+    for (int g = 0; g < world; ++g) a.mbox[g] = mboxes[g];
+    a.world = world;
+    a.rank0 = 0;
+    a.timeout_ns = peer_timeout_ns();
+    a.prefetch = pdl_prefetch_enabled();
+    a.alpha0 = alpha0;
+    CABL_TRY_CUDA(dot_peer_launch<T>(a, world, chunked, peel, true, s), "dot_peer_emulate kernel");
+    return CABL_OK;
+}
+
 // ------------------------------------------------------------------ GEMV
 // Row-major GEMV runs the deterministic sweep kernels (BASELINE tolerance,
 // bitwise run to run) by default; CABL_GEMV_RM_ORDER=reference selects the
@@ -584,7 +703,7 @@ extern "C" int cabl_describe_device(int device, cabl_gpu_machine* out) {
 extern "C" {
 
 const char* cabl_last_error(void) { return g_err.c_str(); }
-int cabl_abi_version(void) { return 101; } // 1.01: + describe_device, combine_rows
+int cabl_abi_version(void) { return 102; } // 1.02: + peer-memory DOT and its mailboxes
 int cabl_device_count(void) {
     int c = 0;
     if (cudaGetDeviceCount(&c) != cudaSuccess) {
@@ -601,6 +720,82 @@ int cabl_cuda_dot_f32(const float* x, const float* y, uint64_t n, float alpha0, 
 int cabl_cuda_dot_f64(const double* x, const double* y, uint64_t n, double alpha0,
                       double* out, uint64_t small_cutoff, cabl_probe* probe, void* stream) {
     return dot_impl<double>(x, y, n, alpha0, out, small_cutoff, probe, stream);
+}
+int cabl_peer_mailbox_create(void** mbox) {
+    if (!mbox) return fail(CABL_EINVAL, "peer_mailbox_create: out must not be null");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    void* p = nullptr;
+    // cudaMalloc (not the stream-ordered pool): the allocation is exported by IPC
+    CABL_TRY_CUDA(cudaMalloc(&p, sizeof(PeerMailbox)), "peer mailbox alloc");
+    cudaError_t e = cudaMemset(p, 0, sizeof(PeerMailbox));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return cuda_fail(e, "peer mailbox init");
+    }
+    *mbox = p;
+    return CABL_OK;
+}
+int cabl_peer_mailbox_destroy(void* mbox) {
+    if (!mbox) return CABL_OK;
+    CABL_TRY_CUDA(cudaFree(mbox), "peer mailbox free");
+    return CABL_OK;
+}
+int cabl_peer_mailbox_export(void* mbox, cabl_peer_handle* out) {
+    if (!mbox || !out) return fail(CABL_EINVAL, "peer_mailbox_export: null pointer");
+    static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(out->bytes), "IPC handle size");
+    cudaIpcMemHandle_t h;
+    CABL_TRY_CUDA(cudaIpcGetMemHandle(&h, mbox), "cudaIpcGetMemHandle");
+    std::memcpy(out->bytes, &h, sizeof(h));
+    return CABL_OK;
+}
+int cabl_peer_mailbox_import(const cabl_peer_handle* h, void** mapped) {
+    if (!h || !mapped) return fail(CABL_EINVAL, "peer_mailbox_import: null pointer");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, h->bytes, sizeof(ih));
+    CABL_TRY_CUDA(cudaIpcOpenMemHandle(mapped, ih, cudaIpcMemLazyEnablePeerAccess),
+                  "cudaIpcOpenMemHandle");
+    return CABL_OK;
+}
+int cabl_peer_mailbox_unmap(void* mapped) {
+    if (!mapped) return CABL_OK;
+    CABL_TRY_CUDA(cudaIpcCloseMemHandle(mapped), "cudaIpcCloseMemHandle");
+    return CABL_OK;
+}
+int cabl_peer_mailbox_state(const void* mbox, uint64_t* epoch, uint64_t* fault) {
+    if (!mbox) return fail(CABL_EINVAL, "peer_mailbox_state: null mailbox");
+    PeerMailbox m;
+    CABL_TRY_CUDA(cudaMemcpy(&m, mbox, sizeof(m), cudaMemcpyDeviceToHost), "peer mailbox read");
+    if (epoch) *epoch = m.epoch;
+    if (fault) *fault = m.fault;
+    return CABL_OK;
+}
+int cabl_cuda_dot_peer_f32(const float* x, const float* y, uint64_t n, float alpha0, float* out,
+                           void* const* mboxes, int world, int rank, uint64_t small_cutoff,
+                           cabl_probe* probe, void* stream) {
+    return dot_peer_impl<float>(x, y, n, alpha0, out, mboxes, world, rank, small_cutoff, probe,
+                                stream);
+}
+int cabl_cuda_dot_peer_f64(const double* x, const double* y, uint64_t n, double alpha0,
+                           double* out, void* const* mboxes, int world, int rank,
+                           uint64_t small_cutoff, cabl_probe* probe, void* stream) {
+    return dot_peer_impl<double>(x, y, n, alpha0, out, mboxes, world, rank, small_cutoff, probe,
+                                 stream);
+}
+int cabl_cuda_dot_peer_emulate_f32(int world, const float* const* xs, const float* const* ys,
+                                   const uint64_t* ns, float alpha0, float* const* outs,
+                                   void* const* mboxes, uint64_t small_cutoff, void* stream) {
+    return dot_peer_emulate_impl<float>(world, xs, ys, ns, alpha0, outs, mboxes, small_cutoff,
+                                        stream);
+}
+int cabl_cuda_dot_peer_emulate_f64(int world, const double* const* xs, const double* const* ys,
+                                   const uint64_t* ns, double alpha0, double* const* outs,
+                                   void* const* mboxes, uint64_t small_cutoff, void* stream) {
+    return dot_peer_emulate_impl<double>(world, xs, ys, ns, alpha0, outs, mboxes, small_cutoff,
+                                         stream);
 }
 int cabl_cuda_combine_partials_f32(const float* p, uint32_t count, float alpha0, float* out,
                                    void* stream) {

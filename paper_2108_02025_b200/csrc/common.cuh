@@ -177,10 +177,14 @@ struct Partition {
 // CTA), so whoever draws raw value total - 1 is the counter's last user in
 // this launch and resets it to zero for the next launch on the stream.
 __device__ __forceinline__ unsigned long long dyn_next(unsigned* counter,
-                                                       unsigned long long total) {
+                                                       unsigned long long total, unsigned nblk) {
     const unsigned long long raw = atomicAdd(counter, 1u);
     if (raw == total - 1) *counter = 0u;
-    return raw + gridDim.x;
+    return raw + nblk;
+}
+__device__ __forceinline__ unsigned long long dyn_next(unsigned* counter,
+                                                       unsigned long long total) {
+    return dyn_next(counter, total, gridDim.x);
 }
 
 // ---- programmatic dependent launch (PDL) ---------------------------------

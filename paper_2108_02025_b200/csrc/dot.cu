@@ -16,6 +16,7 @@
 //
 // Algorithmic bytes per launch: 2 * n * sizeof(T).
 #include "common.cuh"
+#include "dot_body.cuh"
 #include "kernels.cuh"
 
 #include <cstdio>
@@ -25,100 +26,31 @@ namespace cabl_dev {
 
 namespace {
 
-// measured best on n = 2^24 fp32 (tools/tune.py): 512 x 2 CTAs/SM, 2 vectors
-// of x and y in flight per thread per iteration
-constexpr int kDotBlock = 512;
-constexpr int kDotUnroll = 2;
-constexpr int kDotCtasPerSm = 2;
 
 template <typename T, int BLOCK, int U, int MINB, bool PEEL = false>
 __global__ void __launch_bounds__(BLOCK, MINB)
     dot_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t n, int vec_ok,
                uint64_t head_, T alpha0, T* __restrict__ out, T* __restrict__ partials,
                unsigned* __restrict__ ticket, int pf) {
-    const uint64_t head = PEEL ? head_ : 0; // the aligned instantiation keeps its old code
     // vec_ok: x + head and y + head are 32-byte aligned (head < V elements are
     // peeled when both operands share their misalignment); the head and the
     // < V tail run in the scalar loop
     pdl_trigger();
     if (pf > 0 && vec_ok && threadIdx.x < 2 * U) { // warm L2: this CTA's first U slabs of x and y
-        const uint64_t nvec = (n - head) / Vec<T>::N;
+        const uint64_t nvec = (n - (PEEL ? head_ : 0)) / Vec<T>::N;
         const uint64_t T_all = uint64_t(gridDim.x) * BLOCK;
         const uint64_t v0 = uint64_t(blockIdx.x) * BLOCK + uint64_t(threadIdx.x >> 1) * T_all;
         if (v0 < nvec) {
             const uint64_t cnt = nvec - v0 < uint64_t(BLOCK) ? nvec - v0 : uint64_t(BLOCK);
-            const T* base = ((threadIdx.x & 1) ? y : x) + head;
+            const T* base = ((threadIdx.x & 1) ? y : x) + (PEEL ? head_ : 0);
             prefetch_l2_bulk(base + v0 * Vec<T>::N, unsigned(cnt * sizeof(Vec<T>)));
         }
     }
     pdl_wait();
     __shared__ T red[32];
     __shared__ bool am_last;
-    constexpr int V = Vec<T>::N;
     const int tid = threadIdx.x;
-
-    T acc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc[u] = T(0);
-
-    uint64_t done = 0; // elements covered by the head and the vector loop
-    if (vec_ok) {
-        const uint64_t nvec = (n - head) / V;
-        const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x + head);
-        const Vec<T>* Y = reinterpret_cast<const Vec<T>*>(y + head);
-        // thread-level grid stride: with T threads in the grid, thread t takes
-        // vectors t, t + T, t + 2T, ... (U of them in flight per iteration), so
-        // every thread's share is within one vector of every other's and the
-        // grid sweeps the operands front to back in T-vector slabs
-        const uint64_t T_all = uint64_t(gridDim.x) * BLOCK;
-        for (uint64_t k0 = uint64_t(blockIdx.x) * BLOCK + tid; k0 < nvec; k0 += U * T_all) {
-            Vec<T> xv[U], yv[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint64_t i = k0 + uint64_t(u) * T_all;
-                if (i < nvec) {
-                    xv[u] = ld_stream(X + i);
-                    yv[u] = ld_stream(Y + i);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < V; ++k) xv[u].v[k] = yv[u].v[k] = T(0);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) acc[u] = dot_vec(xv[u], yv[u], acc[u]);
-        }
-        // the peeled head: one element for each of the first `head` threads
-        if (PEEL) {
-            const uint64_t gt = uint64_t(blockIdx.x) * BLOCK + tid;
-            if (gt < head) acc[0] = fma_rn(x[gt], y[gt], acc[0]);
-        }
-        done = head + nvec * V;
-    }
-    // Scalar remainder (unaligned operands, or the < V trailing elements):
-    // one chain per thread over i = done + gt, + gs, ... in order, with the
-    // loads of kScalarU steps issued before they are consumed (coalesced
-    // 128-byte warp requests; one pair at a time ran misaligned DOT at ~2 TB/s).
-    {
-        constexpr int kScalarU = 8;
-        const uint64_t gt = uint64_t(blockIdx.x) * BLOCK + tid;
-        const uint64_t gs = uint64_t(gridDim.x) * BLOCK;
-        uint64_t i = done + gt;
-        for (; i + uint64_t(kScalarU - 1) * gs < n; i += uint64_t(kScalarU) * gs) {
-            T a[kScalarU], b[kScalarU];
-#pragma unroll
-            for (int u = 0; u < kScalarU; ++u) {
-                a[u] = __ldcs(x + i + u * gs);
-                b[u] = __ldcs(y + i + u * gs);
-            }
-#pragma unroll
-            for (int u = 0; u < kScalarU; ++u) acc[0] = fma_rn(a[u], b[u], acc[0]);
-        }
-        for (; i < n; i += gs) acc[0] = fma_rn(x[i], y[i], acc[0]);
-    }
-
-    T s = acc[0];
-#pragma unroll
-    for (int u = 1; u < U; ++u) s = add_rn(s, acc[u]);
+    const T s = dot_thread_sum<T, BLOCK, U, PEEL>(x, y, n, vec_ok, head_, blockIdx.x, gridDim.x);
     const T cta_total = block_sum(s, red);
 
     if (gridDim.x == 1) {
@@ -183,57 +115,17 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     __shared__ T red[32];
     __shared__ unsigned long long next_sh;
     __shared__ bool am_last;
-    constexpr int V = Vec<T>::N;
-    const int tid = threadIdx.x;
-    const uint64_t nvec = n / V;
-    const uint64_t nchunks = (nvec + chunk - 1) / chunk;
-    const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
-    const Vec<T>* Y = reinterpret_cast<const Vec<T>*>(y);
-
-    uint64_t ch = blockIdx.x; // first chunk static, the rest from the queue
-    while (ch < nchunks) {
-        if (tid == 0) next_sh = dyn_next(counters, nchunks); // prefetch
-        T acc[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) acc[u] = T(0);
-        const uint64_t c0 = ch * chunk;
-        const uint64_t c1 = (c0 + chunk < nvec) ? c0 + chunk : nvec;
-        for (uint64_t base = c0; base < c1; base += uint64_t(BLOCK) * U) {
-            Vec<T> xv[U], yv[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint64_t i = base + uint64_t(u) * BLOCK + tid;
-                if (i < c1) {
-                    xv[u] = ld_stream(X + i);
-                    yv[u] = ld_stream(Y + i);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < V; ++k) xv[u].v[k] = yv[u].v[k] = T(0);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) acc[u] = dot_vec(xv[u], yv[u], acc[u]);
-        }
-        T v = acc[0];
-#pragma unroll
-        for (int u = 1; u < U; ++u) v = add_rn(v, acc[u]);
-        const T chunk_total = block_sum(v, red); // its barriers publish next_sh
-        if (tid == 0) partials[ch] = chunk_total;
-        ch = next_sh;
-        __syncthreads(); // next_sh is rewritten at the top of the next chunk
-    }
-    if (tid == 0) {
+    dot_chunk_sweep<T, BLOCK, U>(x, y, n, partials, counters, chunk, blockIdx.x, gridDim.x, red,
+                                 &next_sh);
+    if (threadIdx.x == 0) {
         __threadfence();
         am_last = atomicAdd(counters + 1, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!am_last) return;
     __threadfence();
-    T v = T(0);
-    for (uint64_t i = tid; i < nchunks; i += BLOCK) v = add_rn(v, ld_cg(partials + i));
-    T total = block_sum(v, red);
-    if (tid == 0) {
-        for (uint64_t i = nvec * V; i < n; ++i) total = fma_rn(x[i], y[i], total);
+    const T total = dot_chunk_total<T, BLOCK>(x, y, n, partials, chunk, red);
+    if (threadIdx.x == 0) {
         *out = add_rn(total, alpha0);
         counters[1] = 0u;
     }
@@ -334,37 +226,45 @@ template <typename T> WorkspaceNeed dot_need(uint64_t n, bool small) {
     return w;
 }
 
-template <typename T>
-cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, bool small,
-                       const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
+template <typename T> DotPlan dot_plan(const T* x, const T* y, uint64_t n, bool small) {
+    DotPlan p;
     const int vec_ok = aligned32(x) && aligned32(y);
     if (dot_chunked(n, sizeof(T), small, vec_ok)) {
-        const uint64_t cv = chunk_vecs(n / Vec<T>::N);
-    const uint64_t chunks = (n / Vec<T>::N + cv - 1) / cv;
+        p.chunked = true;
+        p.vec_ok = 1;
+        p.chunk = chunk_vecs(n / Vec<T>::N);
+        const uint64_t chunks = (n / Vec<T>::N + p.chunk - 1) / p.chunk;
         const uint64_t cap = uint64_t(sm_count()) * kDotCtasPerSm;
-        const unsigned grid = unsigned(chunks < cap ? chunks : cap);
-        launch(dot_chunk_kernel<T, kDotBlock, kDotUnroll, kDotCtasPerSm>, grid, kDotBlock, 0, s, 
-            x, y, n, alpha0, out, static_cast<T*>(ws.scratch), ws.counters, cv);
-        if (info) info->ctas = grid;
-        return cudaGetLastError();
+        p.grid = unsigned(chunks < cap ? chunks : cap);
+        return p;
     }
     // operands that share their misalignment: peel head < V elements so the
     // rest is 32-byte aligned (x[k:], y[k:] slices of aligned buffers)
-    uint64_t head = 0;
-    int peeled_ok = vec_ok;
+    p.vec_ok = vec_ok;
     if (!vec_ok) {
         const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
         if (xa % 32 == ya % 32 && xa % sizeof(T) == 0) {
-            head = ((32 - xa % 32) % 32) / sizeof(T);
-            peeled_ok = head < n ? 1 : 0;
-            if (!peeled_ok) head = 0;
+            p.head = ((32 - xa % 32) % 32) / sizeof(T);
+            p.vec_ok = p.head < n ? 1 : 0;
+            if (!p.vec_ok) p.head = 0;
         }
     }
-    const unsigned grid = dot_grid<T>(n, small);
-    const cudaError_t e = dot_dispatch<T>(grid, x, y, n, peeled_ok, head, alpha0, out,
-                                          static_cast<T*>(ws.scratch), ws.counters + 1, s);
-    if (info) info->ctas = grid;
-    return e;
+    p.grid = dot_grid<T>(n, small);
+    return p;
+}
+
+template <typename T>
+cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, bool small,
+                       const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
+    const DotPlan p = dot_plan<T>(x, y, n, small);
+    if (info) info->ctas = p.grid;
+    if (p.chunked) {
+        launch(dot_chunk_kernel<T, kDotBlock, kDotUnroll, kDotCtasPerSm>, p.grid, kDotBlock, 0, s,
+               x, y, n, alpha0, out, static_cast<T*>(ws.scratch), ws.counters, p.chunk);
+        return cudaGetLastError();
+    }
+    return dot_dispatch<T>(p.grid, x, y, n, p.vec_ok, p.head, alpha0, out,
+                           static_cast<T*>(ws.scratch), ws.counters + 1, s);
 }
 
 template <typename T>
@@ -407,6 +307,8 @@ template cudaError_t combine_rows_launch<float>(const float*, uint32_t, uint64_t
 template cudaError_t combine_rows_launch<double>(const double*, uint32_t, uint64_t, double*,
                                                  cudaStream_t);
 
+template DotPlan dot_plan<float>(const float*, const float*, uint64_t, bool);
+template DotPlan dot_plan<double>(const double*, const double*, uint64_t, bool);
 template WorkspaceNeed dot_need<float>(uint64_t, bool);
 template WorkspaceNeed dot_need<double>(uint64_t, bool);
 template cudaError_t dot_launch<float>(const float*, const float*, uint64_t, float, float*, bool,

@@ -32,6 +32,18 @@ int sm_count(); // of the current device (cached per device)
 uint64_t queue_threshold_bytes(); // work-queue size rule, from the device L2 (capi.cu)
 
 // ---- DOT (dot.cu) ----
+// Launch plan of the single-GPU DOT for (x, y, n): which kernel, its grid,
+// the aligned-vector path and peeled head, and the chunk size of the chunked
+// kernel.  The peer-memory DOT (peer.cu) runs each rank's shard with exactly
+// this plan, so its per-rank partial is the bits dot_launch(alpha0 = 0) gives.
+struct DotPlan {
+    bool chunked = false;
+    unsigned grid = 1;
+    int vec_ok = 0;
+    uint64_t head = 0;
+    uint64_t chunk = 0; // vectors per chunk (chunked kernel)
+};
+template <typename T> DotPlan dot_plan(const T* x, const T* y, uint64_t n, bool small);
 template <typename T> WorkspaceNeed dot_need(uint64_t n, bool small);
 template <typename T>
 cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, bool small,
@@ -42,6 +54,45 @@ cudaError_t combine_partials_launch(const T* p, uint32_t count, T alpha0, T* out
 template <typename T>
 cudaError_t combine_rows_launch(const T* parts, uint32_t count, uint64_t m, T* c,
                                 cudaStream_t s);
+
+// ---- peer-memory DOT (peer.cu) ----
+constexpr int kMaxPeers = 8; // ranks of one NVLink / NVSwitch domain (one node)
+
+// One rank's mailbox (512 B, zeroed at creation; layout shared by every rank).
+// word[p][g][h] = (epoch << 32) | 32-bit half h of rank g's partial for the
+// last epoch of parity p (fp32 uses h = 0 only): the tag and the data are one
+// single-copy-atomic 8-byte store, so neither side needs a fence.
+struct PeerMailbox {
+    unsigned long long word[2][kMaxPeers][2];
+    unsigned long long epoch; // this rank's completed calls (owner-written)
+    unsigned long long fault; // epoch of a call whose wait timed out (0 = none)
+    unsigned long long reserved[30];
+};
+
+// Kernel argument block.  Local slot lr (blockIdx.y) is rank rank0 + lr; a
+// real multi-GPU call has one local slot, the emulation has `world`.
+template <typename T> struct PeerDotArgs {
+    const T* x[kMaxPeers];
+    const T* y[kMaxPeers];
+    T* out[kMaxPeers];
+    uint64_t n[kMaxPeers];
+    uint64_t head[kMaxPeers];
+    uint64_t chunk[kMaxPeers];
+    T* partials[kMaxPeers];
+    unsigned* counters[kMaxPeers]; // [0] chunk queue, [1] ticket; zero on entry and exit
+    unsigned grid[kMaxPeers];
+    int vec_ok[kMaxPeers];
+    void* mbox[kMaxPeers]; // every rank's mailbox, as addressable from this device
+    int world;
+    int rank0;
+    unsigned long long timeout_ns;
+    int prefetch; // pre-wait L2 prefetch (dot_kernel's; CABL_PDL_PREFETCH)
+    T alpha0;
+};
+template <typename T>
+cudaError_t dot_peer_launch(const PeerDotArgs<T>& a, int local_ranks, bool chunked, bool peel,
+                            bool cooperative, cudaStream_t s);
+int dot_peer_ctas_per_sm(bool chunked, size_t elem);
 
 // ---- GEMV row-major (gemv_rm.cu) ----
 template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n);

@@ -10,7 +10,10 @@ The reference parallelises over CPU threads with contiguous chunks
   NCCL; every rank then sums them IN RANK ORDER on the device and adds
   alpha0 last (``cabl_cuda_combine_partials_*``), so the result does not
   depend on NCCL's reduction algorithm: bitwise reproducible, and identical
-  on every rank.
+  on every rank.  ``sharded_dot_fused`` gives the same bits from ONE kernel
+  per rank: the partials are exchanged over peer memory (NVLink P2P stores
+  into every rank's mailbox, csrc/peer.cu) inside the DOT kernel, with no
+  NCCL call and no combine launch.
 * GEMV (row-major or col-major tall) — rank g owns a block of rows of A and
   of c, x is replicated; no exchange is needed.  ``gather=True`` assembles
   the full c on every rank with one all-gather (slices padded to equal size).
@@ -25,6 +28,7 @@ without a GPU; the defaults are the CUDA kernels and nothing else.
 """
 from __future__ import annotations
 
+import ctypes as C
 from typing import Callable
 
 import torch
@@ -127,3 +131,101 @@ def sharded_ger_rows(x_local: torch.Tensor, y: torch.Tensor, C_local: "cabl.Dens
                      policy: "cabl.ExecPolicy", *, local_fn: Callable | None = None) -> None:
     """C_local += x_local (x) y on this rank's row block — no communication."""
     (local_fn or cabl.ger)(x_local, y, C_local, policy)
+
+
+# --------------------------------------------------------------------------
+# DOT with the exchange fused into the kernel (csrc/peer.cu)
+
+class PeerMailboxes:
+    """This rank's peer-DOT mailbox and every other rank's, mapped here.
+
+    Each rank creates a 512-byte mailbox on its device and exports a CUDA IPC
+    handle; the handles are all-gathered over the process group (any backend:
+    this is setup, not data path) and every peer's is imported.  ``table`` is
+    the mailbox pointer table of ``cabl_cuda_dot_peer_*`` in rank order.  At
+    world size 1 nothing is exchanged.  ``create``/``export``/``import_``
+    are injectable so the exchange can be tested on CPU over gloo.
+    """
+
+    def __init__(self, device: torch.device, group=None, *, create=None, export=None,
+                 import_=None):
+        from . import _lib
+        grouped = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if grouped else 1
+        self.rank = dist.get_rank(group) if grouped else 0
+        self.device = device
+        if self.world > 8:
+            raise ValueError("peer DOT: at most 8 ranks (one NVLink domain)")
+        create = create or self._create
+        export = export or self._export
+        import_ = import_ or self._import
+        with cabl._on_device(device):
+            self.own = create()
+            handles: list = [b""]
+            if self.world > 1:
+                handles = [None] * self.world
+                dist.all_gather_object(handles, export(self.own), group=group)
+            self.mapped = {}
+            for g, h in enumerate(handles):
+                if g != self.rank:
+                    self.mapped[g] = import_(h)
+        ptrs = [self.own if g == self.rank else self.mapped[g] for g in range(self.world)]
+        self.table = (C.c_void_p * self.world)(*ptrs)
+        self._lib = _lib
+
+    @staticmethod
+    def _create() -> int:
+        from . import _lib
+        p = C.c_void_p()
+        _lib.call("cabl_peer_mailbox_create", C.byref(p))
+        return p.value
+
+    @staticmethod
+    def _export(ptr: int) -> bytes:
+        from . import _lib
+        buf = C.create_string_buffer(64)
+        _lib.call("cabl_peer_mailbox_export", C.c_void_p(ptr), buf)
+        return buf.raw
+
+    @staticmethod
+    def _import(handle: bytes) -> int:
+        from . import _lib
+        p = C.c_void_p()
+        _lib.call("cabl_peer_mailbox_import", C.c_char_p(handle), C.byref(p))
+        return p.value
+
+    def state(self) -> tuple[int, int]:
+        """(completed calls, epoch of a timed-out call or 0) of this rank's mailbox."""
+        e, f = C.c_uint64(), C.c_uint64()
+        with cabl._on_device(self.device):
+            self._lib.call("cabl_peer_mailbox_state", C.c_void_p(self.own), C.byref(e), C.byref(f))
+        return e.value, f.value
+
+    def close(self) -> None:
+        if self.own is None:
+            return
+        with cabl._on_device(self.device):
+            for p in self.mapped.values():
+                self._lib.call("cabl_peer_mailbox_unmap", C.c_void_p(p))
+            self._lib.call("cabl_peer_mailbox_destroy", C.c_void_p(self.own))
+        self.own, self.mapped = None, {}
+
+
+def sharded_dot_fused(x_local: torch.Tensor, y_local: torch.Tensor, alpha0: float,
+                      out: torch.Tensor, policy: "cabl.ExecPolicy",
+                      mailboxes: PeerMailboxes) -> torch.Tensor:
+    """out[0] = alpha0 + sum over ranks (rank order) of each rank's shard partial,
+    in one kernel per rank (``cabl_cuda_dot_peer_*``): bitwise ``sharded_dot``'s
+    result.  Collective: every rank of the mailboxes' group must call it."""
+    from . import _lib
+    cabl._require(x_local.numel() == y_local.numel(), "dot: x and y lengths differ")
+    sfx, cuda = cabl._check_same([x_local, y_local, out], "dot")
+    cabl._require(cuda, "sharded_dot_fused: operands must be CUDA tensors")
+    p = cabl.Probe()
+    with cabl._on_device(x_local.device):
+        _lib.call(f"cabl_cuda_dot_peer_{sfx}", cabl._ptr(x_local), cabl._ptr(y_local),
+                  x_local.numel(), float(alpha0), out.data_ptr(), mailboxes.table,
+                  mailboxes.world, mailboxes.rank, policy.plan.dot_cutoff, C.byref(p),
+                  cabl._stream_of(x_local))
+    cabl._record(p)
+    return out

@@ -8,7 +8,9 @@ Checks: balanced contiguous partition; sharded DOT = rank-ordered sum of the
 shard partials + alpha0 (bitwise, identical on every rank, independent of
 which rank finishes first); row-sharded GEMV with gather reproduces the
 single-process oracle bitwise (rows are independent); row-sharded GER needs no
-communication and reproduces the oracle bitwise.
+communication and reproduces the oracle bitwise; the peer-DOT mailbox exchange
+(IPC handles all-gathered, peers imported) builds every rank's pointer table
+in rank order.
 """
 from __future__ import annotations
 
@@ -118,6 +120,12 @@ def _worker(rank, world, port, results):
         shard.sharded_gemv_cols(Aloc, torch.from_numpy(xc[b:e].copy()), cl, pol,
                                 local_fn=_oracle_gemv_cols, combine_fn=_ordered_combine_rows)
         results[f"gemvcols_{rank}"] = cl.numpy().copy()
+        # ---- peer-DOT mailboxes: IPC handles all-gathered, peers imported,
+        # the pointer table in rank order with this rank's own mailbox at [rank]
+        mb = shard.PeerMailboxes(torch.device("cpu"), create=lambda: 1000 + rank,
+                                 export=lambda p: f"h{p}".encode().ljust(64, b"\0"),
+                                 import_=lambda h: 2000 + int(h.rstrip(b"\0")[1:]))
+        results[f"peer_{rank}"] = (mb.world, mb.rank, [mb.table[g] for g in range(world)])
     finally:
         dist.destroy_process_group()
 
@@ -182,6 +190,13 @@ def test_sharded_paths_over_gloo(world):
         np.testing.assert_array_equal(results[f"gemvcols_{r}"], want)
     truth, rowabs = O.gemv_truth(Ac, 1, xc, cc)
     assert np.all(np.abs(want - truth) <= 4 * kc * np.finfo(np.float64).eps * (rowabs + np.abs(cc)))
+
+
+    # peer-DOT mailbox tables: own mailbox at [rank], rank g's import elsewhere
+    for r in range(world):
+        w, rk, table = results[f"peer_{r}"]
+        assert (w, rk) == (world, r)
+        assert table == [1000 + r if g == r else 2000 + 1000 + g for g in range(world)]
 
 
 def test_partition_is_balanced_and_contiguous():

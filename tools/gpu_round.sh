@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-LD_LIBRARY_PATH=paper_2108_02025_b200 ./tests/cpp/mgpu_example > gpurun_out/mgpu.log 2>&1; echo "rc=$?" >> gpurun_out/mgpu.log
+timeout 900 python -m pytest tests/test_gpu_peer.py -q -x --timeout 600 -p no:cacheprovider > gpurun_out/pytest_peer.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_peer.log
+python tools/peer_cost.py > gpurun_out/peer_cost.jsonl 2>&1
