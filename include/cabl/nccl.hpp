@@ -12,6 +12,10 @@
 //         result is independent of NCCL's algorithm and identical everywhere.
 //   GEMV  row blocks of A and c, x replicated, no exchange needed.
 //   GER   row blocks of C and x, y replicated, no exchange at all.
+//   sharded_dot_fused: DOT with the exchange inside the kernel — every device
+//         stores its partial into every device's mailbox over NVLink P2P and
+//         sums the G partials in device order itself (cabl_cuda_dot_peer_*,
+//         csrc/peer.cu); same bits as sharded_dot, one kernel, no NCCL call.
 //
 // Needs nccl.h and -lnccl in addition to cabl/device.hpp's requirements.
 #pragma once
@@ -57,6 +61,10 @@ public:
     Group(const Group&) = delete;
     Group& operator=(const Group&) = delete;
     ~Group() {
+        for (std::size_t i = 0; i < mboxes_.size(); ++i) {
+            cudaSetDevice(devs_[i]);
+            cabl_peer_mailbox_destroy(mboxes_[i]);
+        }
         for (std::size_t i = 0; i < devs_.size(); ++i) {
             cudaSetDevice(devs_[i]);
             cudaStreamDestroy(streams_[i]);
@@ -74,10 +82,37 @@ public:
         }
     }
 
+    // Peer-DOT mailboxes, one per device, created on first use; every device
+    // gets P2P access to every other (NVLink), so the table holds plain
+    // device pointers (no IPC inside one process).
+    void* const* mailboxes() {
+        if (mboxes_.empty()) {
+            const int G = size();
+            for (int r = 0; r < G; ++r) {
+                detail::cuda_check(cudaSetDevice(devs_[r]), "cudaSetDevice");
+                for (int q = 0; q < G; ++q) {
+                    if (q == r) continue;
+                    int can = 0;
+                    detail::cuda_check(cudaDeviceCanAccessPeer(&can, devs_[r], devs_[q]),
+                                       "cudaDeviceCanAccessPeer");
+                    if (!can) throw std::runtime_error("sharded_dot_fused: no P2P path between devices");
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(devs_[q], 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                    else detail::cuda_check(e, "cudaDeviceEnablePeerAccess");
+                }
+                void* mb = nullptr;
+                detail::check(cabl_peer_mailbox_create(&mb));
+                mboxes_.push_back(mb);
+            }
+        }
+        return mboxes_.data();
+    }
+
 private:
     std::vector<int> devs_;
     std::vector<ncclComm_t> comms_;
     std::vector<cudaStream_t> streams_;
+    std::vector<void*> mboxes_;
 };
 
 namespace detail {
@@ -96,6 +131,14 @@ inline int combine_rows(const float* p, std::uint32_t k, std::uint64_t m, float*
 inline int combine_rows(const double* p, std::uint32_t k, std::uint64_t m, double* c,
                         cudaStream_t s) {
     return cabl_cuda_combine_rows_f64(p, k, m, c, s);
+}
+inline int dot_peer(const float* x, const float* y, std::uint64_t n, float a, float* o,
+                    void* const* mb, int G, int r, std::uint64_t cut, cudaStream_t s) {
+    return cabl_cuda_dot_peer_f32(x, y, n, a, o, mb, G, r, cut, nullptr, s);
+}
+inline int dot_peer(const double* x, const double* y, std::uint64_t n, double a, double* o,
+                    void* const* mb, int G, int r, std::uint64_t cut, cudaStream_t s) {
+    return cabl_cuda_dot_peer_f64(x, y, n, a, o, mb, G, r, cut, nullptr, s);
 }
 } // namespace detail
 
@@ -125,6 +168,34 @@ T sharded_dot(Group& g, const std::vector<const DeviceVector<T>*>& x,
         cabl::detail::cuda_check(cudaSetDevice(g.device(r)), "cudaSetDevice");
         cabl::detail::check(detail::combine(gathered[r].data(), std::uint32_t(G), alpha0,
                                             out[r].data(), g.stream(r)));
+    }
+    T result{};
+    cabl::detail::cuda_check(cudaSetDevice(g.device(0)), "cudaSetDevice");
+    cabl::detail::cuda_check(cudaMemcpyAsync(&result, out[0].data(), sizeof(T),
+                                             cudaMemcpyDeviceToHost, g.stream(0)), "D2H");
+    g.synchronize();
+    return result;
+}
+
+// sharded_dot with the exchange fused into the DOT kernel (peer memory, no
+// NCCL): same arguments, same bits.  All G kernels are enqueued before any
+// is waited on; each spins only for its peers' partials.
+template <typename T>
+T sharded_dot_fused(Group& g, const std::vector<const DeviceVector<T>*>& x,
+                    const std::vector<const DeviceVector<T>*>& y, T alpha0,
+                    const ExecPolicy& policy) {
+    const int G = g.size();
+    cabl::detail::require(int(x.size()) == G && int(y.size()) == G,
+                          "sharded_dot_fused: one chunk per device");
+    void* const* mb = g.mailboxes();
+    std::vector<DeviceVector<T>> out;
+    for (int r = 0; r < G; ++r) {
+        cabl::detail::require(x[r]->len() == y[r]->len(), "Vectors must have equal length");
+        cabl::detail::cuda_check(cudaSetDevice(g.device(r)), "cudaSetDevice");
+        out.emplace_back(1);
+        cabl::detail::check(detail::dot_peer(x[r]->data(), y[r]->data(), x[r]->len(), alpha0,
+                                             out[r].data(), mb, G, r, policy.plan.dot_cutoff,
+                                             g.stream(r)));
     }
     T result{};
     cabl::detail::cuda_check(cudaSetDevice(g.device(0)), "cudaSetDevice");

@@ -1,7 +1,8 @@
 // Multi-GPU drop-in use (cabl/nccl.hpp): one process drives every visible
 // device through an NCCL clique.  Checks the sharded results bit for bit
 // against the same per-shard computations run one by one on device 0:
-//   DOT  = rank-ordered sum of the per-shard partials + alpha0,
+//   DOT  = rank-ordered sum of the per-shard partials + alpha0 (NCCL all-gather
+//          path and the fused peer-memory path),
 //   GEMV = each row block, GER = each row block.
 // With one GPU (this run's boxes) the clique has one member and the path
 // still goes through ncclCommInitAll / ncclAllGather / the ordered combine.
@@ -57,6 +58,12 @@ int main() {
     ok &= got == expect;
     std::printf("sharded dot over %d GPU(s): %.9g (expected %.9g) %s\n", G, double(got),
                 double(expect), got == expect ? "ok" : "MISMATCH");
+    for (int call = 0; call < 3; ++call) { // the fused (peer-memory) exchange: same bits
+        const float fused = nccl::sharded_dot_fused(g, xp, yp, 0.75f, pol);
+        ok &= fused == expect;
+        std::printf("fused sharded dot over %d GPU(s), call %d: %.9g %s\n", G, call,
+                    double(fused), fused == expect ? "ok" : "MISMATCH");
+    }
 
     // ---- GEMV (row blocks) and GER (row blocks)
     const std::size_t m = 8192, k = 4096;
