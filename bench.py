@@ -218,6 +218,7 @@ def make_inputs(w, rows: tuple[int, int], dev, layout=None):
 def step_fn(w, ins, policy, ctx, sharded_dot: bool, fused: bool = False):
     import paper_2108_02025_b200 as cb
     from paper_2108_02025_b200 import shard
+    from paper_2108_02025_b200 import workloads as WL
     if w.op == "dot" and fused:
         # the exchange of partials fused into the DOT kernel over peer memory
         # (csrc/peer.cu): one launch per step at any N, no NCCL call
@@ -232,6 +233,11 @@ def step_fn(w, ins, policy, ctx, sharded_dot: bool, fused: bool = False):
             return (lambda: shard.sharded_dot(ins["x"], ins["y"], 0.0, ins["out"], policy,
                                               gathered=gathered)), 2  # dot + combine (+ NCCL all-gather)
         return (lambda: cb.dot_into(ins["x"], ins["y"], 0.0, ins["out"], policy)), 1
+    if w.op == "gemv-row" and sharded_dot and ctx.world > 1 and w.id == "G4":
+        # BASELINE config 5: "c slices all-gathered" (NCCL) after the row blocks
+        m_total = WL.WORKLOADS["G4"].m
+        return (lambda: shard.sharded_gemv_rows(ins["A"], ins["x"], ins["c"], policy,
+                                                gather=True, m_total=m_total)), 1
     if w.op == "gemv-row":
         return (lambda: cb.gemv_row_major(ins["A"], ins["x"], ins["c"], policy)), 1
     if w.op == "gemv-col":
