@@ -29,6 +29,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <cstdio>
 #include <cstdlib>
 
 namespace cabl_dev {
@@ -338,6 +339,153 @@ __global__ void __launch_bounds__(kGerBlock, 2)
     }
 }
 
+// Any row width >= V and any element-aligned C (odd n, x[k:]-style offsets):
+// C flattened and cut into 32-byte vectors at C's first 32-byte boundary.  A
+// vector may straddle a row boundary (at most once, since inner >= V); its
+// elements take y[i..] and y[0..] and x[o], x[o+1] accordingly — scalar y
+// reads (shared memory when y fits and YS, else L1), while C moves in 256-bit
+// loads and stores with U vectors in flight per thread (EARLY: the y / x reads
+// of all U vectors issued with the C loads).  The < V elements before the
+// boundary and after the last whole vector run in CTA 0's scalar prologue.
+// The flat scalar sweep it replaces ran 8192 x 8193 fp32 at 4.2 TB/s
+// (129 us flushed); this kernel 92 us (5.8 TB/s); fp64 4096 x 8193 119 -> 82 us.
+constexpr size_t kGerYsMax = 96 * 1024; // y staged in shared memory up to this size
+
+template <typename T, bool YS, int U, bool EARLY>
+__global__ void __launch_bounds__(kGerBlock, 2)
+    ger_flat_any_kernel(const T* __restrict__ u, const T* __restrict__ v, T* __restrict__ C,
+                        uint64_t outer, uint64_t inner, uint64_t head, uint64_t nvec,
+                        uint64_t step_o, uint64_t step_i) {
+    pdl_enter();
+    constexpr int V = Vec<T>::N;
+    const uint64_t total = outer * inner;
+    extern __shared__ unsigned char ger_smem[];
+    T* ys = reinterpret_cast<T*>(ger_smem);
+    if (YS) { // y staged in shared memory (rows that fit): LDS instead of L1 LDG
+        for (uint64_t j = threadIdx.x; j < inner; j += kGerBlock) ys[j] = __ldg(v + j);
+        __syncthreads();
+    }
+    if (blockIdx.x == 0) { // head and tail elements
+        const uint64_t tail0 = head + nvec * V;
+        for (uint64_t e = threadIdx.x; e < head + (total - tail0); e += kGerBlock) {
+            const uint64_t f = e < head ? e : tail0 + (e - head);
+            const uint64_t o = f / inner, i = f - o * inner;
+            C[f] = fma_rn(u[o], v[i], C[f]);
+        }
+    }
+    constexpr uint64_t kSlab = uint64_t(kGerBlock) * U;
+    constexpr int UE = EARLY ? U : 1; // vectors whose y / x are held in registers
+    Vec<T>* Cv = reinterpret_cast<Vec<T>*>(C + head);
+    for (uint64_t s0 = uint64_t(blockIdx.x) * kSlab; s0 < nvec; s0 += uint64_t(gridDim.x) * kSlab) {
+        const uint64_t q0 = s0 + threadIdx.x;
+        const uint64_t f0 = head + q0 * V; // flat index of the vector's first element
+        uint64_t o0;
+        if ((f0 >> 32) == 0 && (inner >> 32) == 0) { // 32-bit division when it fits
+            o0 = unsigned(f0) / unsigned(inner);
+        } else {
+            o0 = f0 / inner;
+        }
+        const uint64_t i0 = f0 - o0 * inner;
+        // EARLY: every load (C, y, x) of the U vectors issued before any FMA;
+        // otherwise the C loads first and y / x per vector when it is consumed
+        Vec<T> cv[U];
+        T yv[UE][V], ua[UE], ub[UE];
+        uint64_t o = o0, i = i0;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const uint64_t q = q0 + uint64_t(k) * kGerBlock;
+            if (q < nvec) {
+                cv[k] = ld_rmw(Cv + q);
+                if (EARLY) {
+                    ua[k % UE] = __ldg(u + o);
+                    ub[k % UE] = (i + V > inner) ? __ldg(u + o + 1) : ua[k % UE];
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        const uint64_t ie = i + e;
+                        const uint64_t j = ie < inner ? ie : ie - inner;
+                        yv[k % UE][e] = YS ? ys[j] : __ldg(v + j);
+                    }
+                }
+            }
+            o += step_o; // advance (o, i) by kGerBlock vectors
+            i += step_i;
+            if (i >= inner) {
+                i -= inner;
+                ++o;
+            }
+        }
+        o = o0;
+        i = i0;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const uint64_t q = q0 + uint64_t(k) * kGerBlock;
+            if (q < nvec) {
+                if (!EARLY) {
+                    ua[0] = __ldg(u + o);
+                    ub[0] = (i + V > inner) ? __ldg(u + o + 1) : ua[0];
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        const uint64_t ie = i + e;
+                        const uint64_t j = ie < inner ? ie : ie - inner;
+                        yv[0][e] = YS ? ys[j] : __ldg(v + j);
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < V; ++e)
+                    cv[k].v[e] = fma_rn(i + e < inner ? ua[k % UE] : ub[k % UE], yv[k % UE][e],
+                                        cv[k].v[e]);
+                st_stream(Cv + q, cv[k]);
+            }
+            o += step_o;
+            i += step_i;
+            if (i >= inner) {
+                i -= inner;
+                ++o;
+            }
+        }
+    }
+}
+
+struct GerAnyCfg {
+    int ys, u, early, per_sm;
+};
+// CABL_GER_ANY_CFG="ys,u,early,ctas_per_sm" (tuning only)
+inline GerAnyCfg ger_any_cfg(size_t elem) {
+    static const GerAnyCfg forced = [] {
+        GerAnyCfg c{-1, 0, 0, 0};
+        if (const char* e = getenv("CABL_GER_ANY_CFG"))
+            sscanf(e, "%d,%d,%d,%d", &c.ys, &c.u, &c.early, &c.per_sm);
+        return c;
+    }();
+    if (forced.ys >= 0) return forced;
+    // measured (tools/ger_odd.py, 10 shapes per dtype, flushed): fp32 y in shared
+    // memory, fp64 y from L1 with a second wave of CTAs
+    return elem == 4 ? GerAnyCfg{1, 4, 1, 2} : GerAnyCfg{0, 4, 1, 4};
+}
+
+template <typename T, bool YS, int U, bool EARLY>
+void ger_any_go(unsigned per_sm, const T* u, const T* v, T* C, uint64_t outer, uint64_t inner,
+                uint64_t head, uint64_t nvec, cudaStream_t s, LaunchInfo* info) {
+    constexpr int V = Vec<T>::N;
+    constexpr uint64_t kSlab = uint64_t(kGerBlock) * U;
+    const uint64_t slabs = (nvec + kSlab - 1) / kSlab;
+    const uint64_t cap = uint64_t(sm_count()) * per_sm;
+    const unsigned grid = unsigned(slabs < cap ? slabs : cap);
+    const uint64_t stepv = uint64_t(kGerBlock) * V; // elements between a thread's vectors
+    const size_t ysz = YS ? size_t(inner) * sizeof(T) : 0;
+    if (YS && ysz > 48 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(ger_flat_any_kernel<T, YS, U, EARLY>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGerYsMax));
+            attr = true;
+        }
+    }
+    launch(ger_flat_any_kernel<T, YS, U, EARLY>, grid, kGerBlock, ysz, s, u, v, C, outer, inner,
+           head, nvec, stepv / inner, stepv % inner);
+    if (info) info->ctas = grid;
+}
+
 } // namespace
 
 // CABL_GER_MODE (tuning only): 0 static row ranges, 1 tiles in grid-stride
@@ -348,6 +496,15 @@ inline int ger_mode() {
         return e ? atoi(e) : kGerDefaultMode;
     }();
     return m;
+}
+
+// CABL_GER_ANY=0 sends odd / misaligned rows back to the scalar flat sweep (A/B only).
+inline bool ger_any_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("CABL_GER_ANY");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
 }
 
 template <typename T>
@@ -410,6 +567,24 @@ cudaError_t ger_launch(const T* u, const T* v, T* C, uint64_t outer, uint64_t in
         launch(ger_flat_hvec_kernel<T>, grid, kGerBlock, 0, s, u, v, C, outer, ivec,
                uint64_t(kGerBlock) / ivec, uint64_t(kGerBlock) % ivec);
         if (info) info->ctas = grid;
+    } else if (!small && inner >= uint64_t(V) && ger_any_enabled() &&
+               reinterpret_cast<uintptr_t>(C) % sizeof(T) == 0 &&
+               outer * inner >= uint64_t(sm_count()) * kGerBlock * V) {
+        // any width >= V, element-aligned C: flat sweep in 32-byte vectors of C
+        const uint64_t mis = (reinterpret_cast<uintptr_t>(C) & 31u) / sizeof(T);
+        const uint64_t head = mis ? uint64_t(V) - mis : 0;
+        const uint64_t nvec = (outer * inner - head) / V;
+        GerAnyCfg c = ger_any_cfg(sizeof(T));
+        if (size_t(inner) * sizeof(T) > kGerYsMax) c.ys = 0;
+        const unsigned ps = unsigned(c.per_sm);
+#define CABL_GER_ANY(YS_, U_, E_)                                                                 \
+    if (c.ys == YS_ && c.u == U_ && c.early == E_)                                                \
+        ger_any_go<T, YS_, U_, E_>(ps, u, v, C, outer, inner, head, nvec, s, info);              \
+    else
+        CABL_GER_ANY(1, 8, 0) CABL_GER_ANY(0, 8, 0) CABL_GER_ANY(1, 4, 1) CABL_GER_ANY(0, 4, 1)
+        CABL_GER_ANY(1, 4, 0) CABL_GER_ANY(0, 4, 0)
+        ger_any_go<T, false, 4, true>(ps, u, v, C, outer, inner, head, nvec, s, info);
+#undef CABL_GER_ANY
     } else {
         constexpr uint64_t kSlab = uint64_t(kGerBlock) * kGerFlatU;
         const uint64_t slabs = (outer * inner + kSlab - 1) / kSlab;

@@ -266,7 +266,9 @@ GER_SHAPES = [(1, 1), (2, 3), (3, 3), (500, 500), (777, 1001), (1000, 8), (8, 10
               # short aligned rows (flat vector sweep) and short odd rows (flat scalar)
               (20_000, 64), (64, 20_000), (100_000, 8), (50_000, 5), (5, 50_000), (1, 300_000),
               # rows of whole 16-byte vectors (flat 16-byte sweep)
-              (3000, 4100), (12, 100_004), (40_000, 12)]
+              (3000, 4100), (12, 100_004), (40_000, 12),
+              # odd rows of >= 8 elements (flat 32-byte sweep of C, rows straddling vectors)
+              (1001, 777), (400, 1003), (3, 200_001), (200_001, 9), (8192, 8193)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -285,6 +287,24 @@ def test_ger_bitwise_equals_oracle(cuda, dtype, layout, m, n):
     want = np_of(C0)
     O.ger_ref(np_of(x), np_of(y), want, int(lay))
     np.testing.assert_array_equal(np_of(Cm.data), want)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("off", [1, 2, 3, 5])
+@pytest.mark.parametrize("m,n", [(1000, 4096), (777, 1001), (2048, 2048)])
+def test_ger_misaligned_c_bitwise(cuda, dtype, off, m, n):
+    """C (and x, y) starting off elements past a 32-byte boundary: the flat
+    sweep's scalar head/tail plus 32-byte body, still one FMA per element."""
+    import paper_2108_02025_b200 as cb
+    x = dev_uniform(m + off, dtype, 1, cuda)[off:]
+    y = dev_uniform(n + off, dtype, 2, cuda)[off:]
+    big = dev_uniform(m * n + off, dtype, 5, cuda)
+    C0 = big[off:].clone()
+    view = big[off:]
+    cb.ger(x, y, cb.DenseMatrix.wrap(view, m, n, cb.Layout.RowMajor), plan_for(dtype))
+    want = np_of(C0)
+    O.ger_ref(np_of(x), np_of(y), want, 0)
+    np.testing.assert_array_equal(np_of(view), want)
 
 
 def test_ger_hand_values(cuda):
