@@ -32,11 +32,25 @@ def main():
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
-    w = WL.WORKLOADS[args.config]
-    span = w.n if w.op == "dot" else w.m
-    ins = bench.make_inputs(w, (0, span), dev)
     ctx = bench.Ctx(1, 0, 0, dev)
-    fn, _ = bench.step_fn(w, ins, cb.default_policy(1), ctx, sharded_dot=False)
+    pol = cb.default_policy(1)
+    if args.config == "R1x":  # GER fp32 8192 x 8193: odd rows (ger_flat_any_kernel)
+        m, n = 8192, 8193
+        x = cb.fill_uniform(torch.empty(m, device=dev), WL.SEED, WL.STREAM_X)
+        y = cb.fill_uniform(torch.empty(n, device=dev), WL.SEED, WL.STREAM_Y)
+        C = cb.DenseMatrix.wrap(cb.fill_uniform(torch.empty(m * n, device=dev), WL.SEED,
+                                                WL.STREAM_CC), m, n, cb.Layout.RowMajor)
+        fn = lambda: cb.ger(x, y, C, pol)  # noqa: E731
+
+        class w:  # noqa: N801
+            id = "R1x"
+    else:
+        # D1f: D1 through the fused peer-memory DOT at world 1 (dot_peer_kernel)
+        fused = args.config == "D1f"
+        w = WL.WORKLOADS["D1" if fused else args.config]
+        span = w.n if w.op == "dot" else w.m
+        ins = bench.make_inputs(w, (0, span), dev)
+        fn, _ = bench.step_fn(w, ins, pol, ctx, sharded_dot=False, fused=fused)
     flush = bench.L2Flush(dev)
     for _ in range(args.reps):
         if not args.no_flush:

@@ -80,12 +80,13 @@ def main():
     for rep in a.reps:
         rep = Path(rep)
         cfg = rep.stem.split("_")[-1]
-        cfg = cfg[:2]
         d = raw(rep)
-        w = WL.WORKLOADS[cfg]
         dur = num(d, "gpu__time_duration.sum")
         rd, wr = num(d, "dram__bytes_read.sum"), num(d, "dram__bytes_write.sum")
-        alg = w.alg_bytes(1)
+        if cfg == "R1x":  # GER fp32 8192 x 8193 (tools/ncu_runner.py)
+            alg = (2 * 8192 * 8193 + 8192 + 8193) * 4
+        else:  # D1f: D1 through the fused peer DOT
+            alg = WL.WORKLOADS[cfg[:2]].alg_bytes(1)
         el = num(d, "sm__cycles_elapsed.max")
         act = [num(d, f"sm__cycles_active.{s}") / el for s in ("min", "avg", "max")]
         kname = d["Kernel Name"][0].split("(")[0].replace("void ", "")
