@@ -629,6 +629,128 @@ __global__ void __launch_bounds__(kSplitBlock, 1)
     if (tid == 0) tickets[blockIdx.y] = 0u;
 }
 
+// Realigning split kernel: col-major A whose columns are not 32-byte aligned
+// (odd m, or A offset from a 32-byte boundary), m >= 1024.  Same 2-D split
+// as gemv_cm_split_vec_kernel, but a column segment of a warp starts at an
+// arbitrary element: the warp loads the 32 ALIGNED 32-byte vectors that cover
+// it (one 256-bit load per lane), takes its right neighbour's vector with
+// V shuffles, and every lane < 31 extracts its V rows at the column's shift
+// (warp-uniform, a switch over V cases).  A warp therefore owns 31 * V rows
+// (lane 31 only feeds lane 30; its vector is re-read by the next warp from
+// L2), and every DRAM byte still moves once in a 256-bit load.  The 2-D
+// scalar split it replaces read 4 bytes per load (8192^2 fp32 offset by one
+// element: 87 us, 3.1 TB/s).  Thread layout: warp w = (column lane cl, row
+// warp rw), RW row warps x CL = 32 / RW column lanes; U columns in flight.
+constexpr int kRealignBlock = 512; // 1 CTA per SM: 128 registers per thread
+constexpr int kRealignU = 8;      // 256-bit column loads in flight per thread (128 KB per SM)
+
+// acc[e] += x * (element SH + e of the 2V-element window own ++ nb), for the
+// lane's first `valid` rows (all V when valid >= V)
+template <typename T, int SH>
+__device__ __forceinline__ void realign_fma(const Vec<T>& own, const Vec<T>& nb, T xv, int64_t valid,
+                                            Vec<T>& acc) {
+    constexpr int V = Vec<T>::N;
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+        const T a = (SH + e < V) ? own.v[(SH + e) % V] : nb.v[(SH + e) % V];
+        if (valid >= V || e < valid) acc.v[e] = fma_rn(a, xv, acc.v[e]);
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void realign_fma(const Vec<T>& own, const Vec<T>& nb, int sh, T xv,
+                                            int64_t valid, Vec<T>& acc) {
+    switch (sh) {
+    case 0: realign_fma<T, 0>(own, nb, xv, valid, acc); break;
+    case 1: realign_fma<T, 1>(own, nb, xv, valid, acc); break;
+    case 2: realign_fma<T, 2>(own, nb, xv, valid, acc); break;
+    case 3: realign_fma<T, 3>(own, nb, xv, valid, acc); break;
+    case 4: if constexpr (Vec<T>::N > 4) realign_fma<T, 4 % Vec<T>::N>(own, nb, xv, valid, acc); break;
+    case 5: if constexpr (Vec<T>::N > 5) realign_fma<T, 5 % Vec<T>::N>(own, nb, xv, valid, acc); break;
+    case 6: if constexpr (Vec<T>::N > 6) realign_fma<T, 6 % Vec<T>::N>(own, nb, xv, valid, acc); break;
+    default: if constexpr (Vec<T>::N > 7) realign_fma<T, 7 % Vec<T>::N>(own, nb, xv, valid, acc); break;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRealignBlock, 1)
+    gemv_cm_split_realign_kernel(const T* __restrict__ A, const T* __restrict__ x,
+                                 T* __restrict__ c, uint64_t m, uint64_t n, uint64_t mt, int RW,
+                                 T* __restrict__ partials, unsigned* __restrict__ tickets) {
+    pdl_enter();
+    constexpr int V = Vec<T>::N;
+    constexpr int U = kRealignU;
+    constexpr int LR = 31 * V; // rows per warp
+    extern __shared__ unsigned char smem_raw[];
+    T* sm = reinterpret_cast<T*>(smem_raw); // [CL][rows]
+    __shared__ bool am_last;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int CL = (kRealignBlock / 32) / RW;
+    const int rw = wid % RW, cl = wid / RW;
+    const uint64_t r0 = uint64_t(blockIdx.y) * mt;
+    const uint64_t rows = (m - r0 < mt) ? m - r0 : mt;
+    const uint64_t wr0 = uint64_t(rw) * LR; // the warp's first row in the tile
+    const bool warp_live = wr0 < rows;
+    // rows of this lane: wr0 + lane*V + e, valid when < rows (lane < 31)
+    const int64_t my_rows = lane < 31 ? int64_t(rows) - int64_t(wr0 + uint64_t(lane) * V) : 0;
+    const uintptr_t abase = reinterpret_cast<uintptr_t>(A);
+    const uint64_t a0 = (abase & 31u) / sizeof(T); // A's element offset from a 32-byte boundary
+    const Vec<T>* Av = reinterpret_cast<const Vec<T>*>(abase - a0 * sizeof(T));
+    const uint64_t total_v = (a0 + m * n + V - 1) / V; // aligned vectors touching A
+    const uint64_t tile = uint64_t(CL) * U;
+    const uint64_t tiles = (n + tile - 1) / tile;
+
+    Vec<T> acc;
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc.v[e] = T(0);
+    if (warp_live) {
+        for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+            const uint64_t j0 = t * tile + cl;
+            const uint64_t g0 = a0 + j0 * m + r0 + wr0; // element index from the aligned base
+            Vec<T> own[U];
+            T xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t j = j0 + uint64_t(u) * CL;
+                const uint64_t v = (g0 + uint64_t(u) * CL * m) / V + uint64_t(lane);
+                xv[u] = j < n ? __ldg(x + j) : T(0);
+                if (j < n && v < total_v) own[u] = ld_stream(Av + v);
+                else
+#pragma unroll
+                    for (int e = 0; e < V; ++e) own[u].v[e] = T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                Vec<T> nb;
+#pragma unroll
+                for (int e = 0; e < V; ++e) nb.v[e] = __shfl_down_sync(0xffffffffu, own[u].v[e], 1);
+                const int sh = int((g0 + uint64_t(u) * CL * m) % V); // warp-uniform
+                realign_fma(own[u], nb, sh, xv[u], my_rows, acc);
+            }
+        }
+    }
+    // column lanes -> partial of this (row tile, column part), fixed order
+    if (warp_live && lane < 31)
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+            if (e < my_rows) sm[uint64_t(cl) * rows + wr0 + uint64_t(lane) * V + e] = acc.v[e];
+    __syncthreads();
+    T* tile_partials = partials + uint64_t(blockIdx.y) * gridDim.x * mt;
+    for (uint64_t r = tid; r < rows; r += kRealignBlock) {
+        T v = sm[r];
+        for (int q = 1; q < CL; ++q) v = add_rn(v, sm[uint64_t(q) * rows + r]);
+        tile_partials[uint64_t(blockIdx.x) * mt + r] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) am_last = atomicAdd(tickets + blockIdx.y, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    split_final(tile_partials, c + r0, rows, mt, gridDim.x, sm);
+    if (tid == 0) tickets[blockIdx.y] = 0u;
+}
+
 struct SplitGeom {
     int row_lanes, col_lanes, rpt;
     unsigned grid;       // column parts (gridDim.x)
@@ -763,6 +885,49 @@ template <typename T> SplitGeom split_vec_geom(uint64_t m, uint64_t n) {
     return g;
 }
 
+// Realign geometry: tiles of RW * 31 * V rows (RW row warps, a power of two
+// <= 32), column parts filling one wave; RW scored like choose_tile_rows
+// (useful SM slots x useful tile rows, bounded final sum).  smem: [CL][rows]
+// for the column-lane combine, >= kSplitBlock entries for split_final.
+// best row-warp count for m and its score
+template <typename T> int realign_rw(uint64_t m, double* score_out) {
+    constexpr uint64_t LR = 31 * Vec<T>::N;
+    const uint64_t sms = uint64_t(sm_count());
+    int best_rw = 1;
+    double best_score = -1.0;
+    for (int rw = 1; rw <= kRealignBlock / 32; rw *= 2) {
+        const uint64_t mt = uint64_t(rw) * LR;
+        const uint64_t tiles = (m + mt - 1) / mt;
+        uint64_t parts = sms / tiles;
+        if (parts < 1) parts = 1;
+        const uint64_t ctas = tiles * parts;
+        const uint64_t waves = (ctas + sms - 1) / sms;
+        double score = double(ctas) / double(waves * sms) * double(m) / double(tiles * mt) /
+                       (1.0 + 0.15 * double(waves - 1));
+        if (parts * mt > kFinalBudget) score *= double(kFinalBudget) / double(parts * mt);
+        if (score > best_score + 1e-9) {
+            best_score = score;
+            best_rw = rw;
+        }
+        if (tiles == 1) break;
+    }
+    if (score_out) *score_out = best_score;
+    return best_rw;
+}
+
+template <typename T> SplitGeom split_realign_geom(uint64_t m, uint64_t n) {
+    constexpr uint64_t LR = 31 * Vec<T>::N;
+    const int best_rw = realign_rw<T>(m, nullptr);
+    SplitGeom g;
+    g.row_lanes = best_rw; // row warps
+    g.col_lanes = (kRealignBlock / 32) / best_rw;
+    g.rpt = 1;
+    split_tiles(m, n, uint64_t(g.col_lanes) * kRealignU, uint64_t(best_rw) * LR, &g);
+    const size_t entries = size_t(g.col_lanes) * g.mt;
+    g.smem = (entries > size_t(kRealignBlock) ? entries : size_t(kRealignBlock)) * sizeof(T);
+    return g;
+}
+
 struct BulkCfg {
     int stages;
     unsigned stage_bytes;
@@ -869,7 +1034,16 @@ template <typename T> bool tall_vec_ok(const T* A, const T* c, uint64_t m) {
 }
 
 enum CmPath { kPathTallVec, kPathTallScalar, kPathBulk, kPathBulkScalar, kPathSplitVec,
-              kPathSplitScalar };
+              kPathSplitScalar, kPathSplitRealign };
+
+// CABL_CM_REALIGN=0 keeps misaligned columns on the scalar 2-D split (A/B only).
+inline bool realign_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("CABL_CM_REALIGN");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
+}
 
 // The bit-exact tall kernels keep each row's sum on one thread, so their
 // parallelism is m/V threads: they are used only when that fills the GPU
@@ -899,6 +1073,13 @@ template <typename T> CmPath cm_path(const T* A, const T* c, uint64_t m) {
     if (split_vec_ok(A, m)) return (m < cm_single_max() && split_mode() == 1) ? kPathBulk : kPathSplitVec;
     if (m < kBulkScalarMaxRows && split_mode() == 1 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0)
         return kPathBulkScalar;
+    // the realigning split when its tiling keeps most SM slots and tile rows
+    // busy (score >= 0.8: 8193 rows 0.89); a poor tiling (m = 100003: 0.70,
+    // 74 us against the scalar split's 61) stays on the scalar split
+    double score = 0.0;
+    if (m >= kBulkScalarMaxRows && realign_enabled() &&
+        reinterpret_cast<uintptr_t>(A) % sizeof(T) == 0 && (realign_rw<T>(m, &score), score >= 0.8))
+        return kPathSplitRealign;
     return kPathSplitScalar;
 }
 
@@ -912,6 +1093,7 @@ template <typename T> SplitGeom cm_split_geom(CmPath p, uint64_t m, uint64_t n, 
         return g;
     }
     if (p == kPathSplitVec) return split_vec_geom<T>(m, n);
+    if (p == kPathSplitRealign) return split_realign_geom<T>(m, n);
     return split_geom<T>(m, n);
 }
 
@@ -1007,6 +1189,16 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
                 bulk_scalar_go<T, 2>(A, x, c, m, n, g, tc, x_bulk, partials, ws.counters, s);
             else
                 bulk_scalar_go<T, 4>(A, x, c, m, n, g, tc, x_bulk, partials, ws.counters, s);
+        } else if (path == kPathSplitRealign) {
+            static bool configured = [] {
+                cudaFuncSetAttribute(gemv_cm_split_realign_kernel<T>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(16 * 31 * Vec<T>::N * sizeof(T)));
+                return true;
+            }();
+            (void)configured;
+            launch(gemv_cm_split_realign_kernel<T>, grid, kRealignBlock, g.smem, s, A, x, c, m, n,
+                   g.mt, g.row_lanes, partials, ws.counters);
         } else if (path == kPathSplitVec) {
             launch(gemv_cm_split_vec_kernel<T>, grid, kSplitBlock, 0, s, 
                 A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);

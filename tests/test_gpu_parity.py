@@ -179,7 +179,9 @@ CM_SHAPES = [(3, 3), (8, 8), (257, 259), (1000, 1000), (256, 65536), (2047, 300)
              # tall and narrow (n < 16): several row vectors per thread, bitwise
              (303_104, 4), (1 << 20, 5), (1 << 20, 15), (1 << 21, 1), (1 << 20, 8),
              # tall from half the SMs' worth of 256-vector units up (bitwise)
-             (151_552, 33), (200_000, 20), (151_544, 7)]
+             (151_552, 33), (200_000, 20), (151_544, 7),
+             # odd m >= 1024: the realigning split (aligned 256-bit loads + warp shuffles)
+             (1025, 3000), (8193, 2000), (3001, 5003), (12_345, 777), (100_003, 64)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -195,6 +197,33 @@ def test_gemv_col_major_matches_oracle(cuda, dtype, m, n):
     tol_c = T.contract_tol(n, rowabs, np.abs(c0), dt)
     assert np.all(np.abs(got.astype(np.float64) - want) <= tol_c)
     tol_t = T.truth_tol(T.gemv_cm_chain(m, n, dt), rowabs, np.abs(c0), dt)
+    assert np.all(np.abs(got.astype(np.float64) - truth) <= tol_t)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("off", [1, 3])
+@pytest.mark.parametrize("m,n", [(4096, 2048), (2048, 4096), (1024, 1000), (5000, 300)])
+def test_gemv_col_major_misaligned_a(cuda, dtype, off, m, n):
+    """A starting `off` elements past a 32-byte boundary (every column
+    misaligned): the realigning split, within the contract and truth bounds,
+    and bitwise run to run."""
+    import paper_2108_02025_b200 as cb
+    A = dev_uniform(m * n + off, dtype, 3, cuda)[off:]
+    x = dev_uniform(n, dtype, 1, cuda)
+    c0 = dev_uniform(m, dtype, 4, cuda)
+    Am = cb.DenseMatrix.wrap(A, m, n, cb.Layout.ColMajor)
+    c, c2 = c0.clone(), c0.clone()
+    cb.gemv_col_major(Am, x, c, plan_for(dtype))
+    cb.gemv_col_major(Am, x, c2, plan_for(dtype))
+    assert torch.equal(c, c2)
+    An, xn, c0n = np_of(A), np_of(x), np_of(c0)
+    want = c0n.copy()
+    O.gemv_ref(An, 1, xn, want)
+    truth, rowabs = O.gemv_truth(An, 1, xn, c0n)
+    got = np_of(c)
+    dt = got.dtype
+    assert np.all(np.abs(got.astype(np.float64) - want) <= T.contract_tol(n, rowabs, np.abs(c0n), dt))
+    tol_t = T.truth_tol(T.gemv_cm_chain(m, n, dt), rowabs, np.abs(c0n), dt)
     assert np.all(np.abs(got.astype(np.float64) - truth) <= tol_t)
 
 

@@ -38,17 +38,22 @@ def buf(n, off, dt):
     return t[off:]
 
 
-for dt in (torch.float32, torch.float64):
-    s = torch.tensor([], dtype=dt).element_size()
-    for m, n, off in ((8192, 8192, 0), (8192, 8193, 0), (8192, 8192, 1), (8192, 8196, 0),
-                      (8192, 8192, 4), (4096, 16383, 0), (65536, 1001, 0), (1001, 65536, 3),
-                      (262144, 255, 0), (2_000_000, 33, 0)):
-        if dt == torch.float64:
-            m //= 2
-        x, y, C = buf(m, off, dt), buf(n, off, dt), buf(m * n, off, dt)
-        Cm = cb.DenseMatrix.wrap(C, m, n, cb.Layout.RowMajor)
-        us = timeit(lambda: cb.ger(x, y, Cm, pol))
-        nbytes = (2 * m * n + m + n) * s
-        print(json.dumps({"dtype": str(dt)[6:], "m": m, "n": n, "off": off, "us": round(us, 2),
-                          "gbs": round(nbytes / us / 1e3, 1)}), flush=True)
-        del x, y, C, Cm
+def main():
+    for dt in (torch.float32, torch.float64):
+        s = torch.tensor([], dtype=dt).element_size()
+        for m, n, off in ((8192, 8192, 0), (8192, 8193, 0), (8192, 8192, 1), (8192, 8196, 0),
+                          (8192, 8192, 4), (4096, 16383, 0), (65536, 1001, 0), (1001, 65536, 3),
+                          (262144, 255, 0), (2_000_000, 33, 0)):
+            if dt == torch.float64:
+                m //= 2
+            x, y, C = buf(m, off, dt), buf(n, off, dt), buf(m * n, off, dt)
+            Cm = cb.DenseMatrix.wrap(C, m, n, cb.Layout.RowMajor)
+            us = timeit(lambda: cb.ger(x, y, Cm, pol))
+            nbytes = (2 * m * n + m + n) * s
+            print(json.dumps({"dtype": str(dt)[6:], "m": m, "n": n, "off": off, "us": round(us, 2),
+                              "gbs": round(nbytes / us / 1e3, 1)}), flush=True)
+            del x, y, C, Cm
+
+
+if __name__ == "__main__":
+    main()
