@@ -125,7 +125,9 @@ RM_SHAPES = [(1, 777), (3, 3), (8, 8), (40, 200), (257, 259), (1000, 1000), (200
              (9472, 64), (100_000, 16), (20_001, 5), (9472, 256), (30_000, 255), (1 << 18, 1),
              (9472, 1024), (12_000, 999),
              # rows of whole 16-byte (not 32-byte) vectors: the scalar-load kernel
-             (20_000, 2052), (3000, 20_002), (1800, 65_540)]
+             (20_000, 2052), (3000, 20_002), (1800, 65_540),
+             # odd rows, long and short: the G-lanes scalar kernel
+             (8192, 8193), (7200, 1001), (8000, 249)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
