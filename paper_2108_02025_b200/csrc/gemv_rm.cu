@@ -36,6 +36,7 @@
 //
 // Algorithmic bytes per launch: m*n*s + n*s + 2*m*s.
 #include "common.cuh"
+#include "dot_body.cuh"
 #include "kernels.cuh"
 
 #include <cstdio>
@@ -251,6 +252,80 @@ __global__ void __launch_bounds__(kRmBlock, MINB)
     }
 }
 
+// CHUNKED FEW-ROWS kernel (aligned rows, few of them: a row is a long DOT
+// with x).  Units are (row, chunk of `chunk` 32-byte vectors), numbered chunk-
+// major so the m units that read the same x chunk run together (x comes from
+// L2 after the first row).  CTAs take units from an atomic queue (the first
+// one static), as the chunked DOT does (dot_body.cuh); a unit's partial is a
+// fixed function of its data and goes to partials[row][chunk]; the CTA that
+// finishes a row's last unit (per-row acq_rel ticket) sums the row's partials
+// in chunk order and adds them to c.  Bitwise reproducible (depends on m, n
+// only).  The unit kernel below keeps 4 loads in flight per lane at 512
+// threads per SM (1 x 2^26 fp32: 127 us, 4.2 TB/s).
+constexpr int kChunkBlock = 512;
+constexpr int kChunkU = 2;
+
+template <typename T>
+__global__ void __launch_bounds__(kChunkBlock, 2)
+    gemv_rm_chunk_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
+                         uint64_t m, uint64_t n, uint64_t chunk, uint64_t nchunks,
+                         T* __restrict__ partials, unsigned* __restrict__ counters) {
+    pdl_enter();
+    constexpr int V = Vec<T>::N;
+    constexpr int U = kChunkU;
+    __shared__ T red[32];
+    __shared__ unsigned long long next_sh;
+    __shared__ bool last_sh;
+    const int tid = threadIdx.x;
+    const uint64_t nvec = n / V;
+    const uint64_t units = m * nchunks;
+    const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
+    uint64_t u = blockIdx.x;
+    while (u < units) {
+        if (tid == 0) next_sh = dyn_next(counters, units); // prefetch
+        const uint64_t ch = u / m, row = u - ch * m;
+        const Vec<T>* Ar = reinterpret_cast<const Vec<T>*>(A + row * n);
+        const uint64_t c0 = ch * chunk;
+        const uint64_t c1 = (c0 + chunk < nvec) ? c0 + chunk : nvec;
+        T acc[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) acc[k] = T(0);
+        for (uint64_t base = c0; base < c1; base += uint64_t(kChunkBlock) * U) {
+            Vec<T> av[U], xv[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const uint64_t i = base + uint64_t(k) * kChunkBlock + tid;
+                if (i < c1) {
+                    av[k] = ld_stream(Ar + i);
+                    xv[k] = ld_stream(X + i);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) av[k].v[e] = xv[k].v[e] = T(0);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) acc[k] = dot_vec(av[k], xv[k], acc[k]);
+        }
+        T v = acc[0];
+#pragma unroll
+        for (int k = 1; k < U; ++k) v = add_rn(v, acc[k]);
+        const T unit_total = block_sum(v, red); // its barriers publish next_sh
+        if (tid == 0) partials[row * nchunks + ch] = unit_total;
+        if (last_arriver(counters + 1 + row, unsigned(nchunks), &last_sh)) {
+            T w = T(0);
+            for (uint64_t i = tid; i < nchunks; i += kChunkBlock)
+                w = add_rn(w, ld_cg(partials + row * nchunks + i));
+            const T total = block_sum(w, red);
+            if (tid == 0) {
+                c[row] = add_rn(c[row], total);
+                counters[1 + row] = 0u;
+            }
+        }
+        u = next_sh;
+        __syncthreads(); // next_sh is rewritten at the top of the next unit
+    }
+}
+
 // Generic path (unaligned operands or n % V != 0): G lanes per row (G = 32 /
 // 16 / 8 / 4 by row length, so short rows do not idle most of a warp),
 // groups own balanced row ranges, scalar coalesced loads.  Each lane's chain
@@ -408,8 +483,20 @@ template <typename T> bool rm_vec_ok(const T* A, const T* x, uint64_t n) {
     return aligned32(A) && aligned32(x) && (n % Vec<T>::N == 0);
 }
 
+// Few long rows take the chunked kernel (mode 9).  256 MiB of A, flushed
+// (tools/rm_few.py), unit kernel -> chunked: m = 1 / 2 / 4 fp32 129 / 129 / 96
+// -> 84 / 74 / 68 us; m = 16 ties (61.4); from m = 64 up the sweeps win
+// (51 vs 61).  CABL_RM_FEW_MAX overrides the row limit (tuning only).
+inline bool rm_few_rows(uint64_t m, uint64_t n, size_t elem) {
+    static const uint64_t max_rows = [] {
+        const char* e = getenv("CABL_RM_FEW_MAX");
+        return e ? uint64_t(atoll(e)) : uint64_t(8);
+    }();
+    return m <= max_rows && n * elem >= 65536;
+}
+
 // -1 scalar, 0 segment-balanced warps, 1 sweep for short rows, 2 sweep for
-// long rows.  CABL_GEMV_RM_MODE overrides (tuning / tests only).
+// long rows, 9 chunked few rows.  CABL_GEMV_RM_MODE overrides (tuning / tests only).
 template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n) {
     const bool vec = rm_vec_ok(A, x, n);
     static const int forced = [] {
@@ -429,6 +516,7 @@ template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n
     }
     if (!vec) return -1;
     if (forced >= 0 && forced <= 2) return forced;
+    if (forced == 9 || (forced < 0 && rm_few_rows(m, n, sizeof(T)))) return 9;
     // measured (tools/tune.py, 8192^2 and 65536^2 fp32): 4 rows x 2 vectors
     // per thread at 2 CTAs/SM for rows of <= 2 CTA passes, 2 rows x 8 vectors
     // at 1 CTA/SM for long rows.  The sweep must see >= 6 row groups per CTA
@@ -438,6 +526,16 @@ template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n
     if (short_rows && (m + 3) / 4 >= 6 * 2 * sms) return 1;
     if (!short_rows && (m + 1) / 2 >= 6 * 1 * sms) return 2;
     return 0;
+}
+
+// Few-rows chunk size (vectors): the largest power of two giving >= 8 units
+// per CTA slot, in [256, 65536], and no more than a row.
+template <typename T> uint64_t rm_chunk_vecs(uint64_t m, uint64_t n) {
+    const uint64_t nvec = n / Vec<T>::N;
+    const uint64_t slots = uint64_t(sm_count()) * 2 * 8;
+    uint64_t cv = 256;
+    while (cv * 2 <= 65536 && m * ((nvec + cv * 2 - 1) / (cv * 2)) >= slots && cv * 2 <= nvec) cv *= 2;
+    return cv;
 }
 
 template <typename T> RmGeom rm_geom(uint64_t m, uint64_t n) {
@@ -539,6 +637,13 @@ template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_
     WorkspaceNeed w;
     if (m == 0 || n == 0) return w;
     const int mode = rm_mode<T>(A, x, m, n);
+    if (mode == 9) {
+        const uint64_t cv = rm_chunk_vecs<T>(m, n);
+        const uint64_t nch = (n / Vec<T>::N + cv - 1) / cv;
+        w.counters = 1 + m; // queue + per-row tickets
+        w.scratch_bytes = m * nch * sizeof(T);
+        return w;
+    }
     if (mode >= 3) return w; // lane-per-row kernels: no scratch
     if (mode >= 1) {
         w.counters = 1; // group counter of the dynamic sweep
@@ -571,6 +676,15 @@ cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
             launch(gemv_rm_gvec_kernel<T, 8>, grid, kRmBlock, 0, s, A, x, c, m, n, groups);
         else
             launch(gemv_rm_gvec_kernel<T, 4>, grid, kRmBlock, 0, s, A, x, c, m, n, groups);
+        if (info) info->ctas = grid;
+    } else if (mode == 9) {
+        const uint64_t cv = rm_chunk_vecs<T>(m, n);
+        const uint64_t nch = (n / Vec<T>::N + cv - 1) / cv;
+        const uint64_t units = m * nch;
+        const uint64_t cap = uint64_t(sm_count()) * 2;
+        const unsigned grid = unsigned(units < cap ? units : cap); // grid <= units (dyn_next)
+        launch(gemv_rm_chunk_kernel<T>, grid, kChunkBlock, 0, s, A, x, c, m, n, cv, nch,
+               static_cast<T*>(ws.scratch), ws.counters);
         if (info) info->ctas = grid;
     } else if (mode >= 3) {
         const uint64_t cap = uint64_t(sm_count()) * 8;

@@ -127,7 +127,9 @@ RM_SHAPES = [(1, 777), (3, 3), (8, 8), (40, 200), (257, 259), (1000, 1000), (200
              # rows of whole 16-byte (not 32-byte) vectors: the scalar-load kernel
              (20_000, 2052), (3000, 20_002), (1800, 65_540),
              # odd rows, long and short: the G-lanes scalar kernel
-             (8192, 8193), (7200, 1001), (8000, 249)]
+             (8192, 8193), (7200, 1001), (8000, 249),
+             # few long rows: the chunked kernel (units of row x chunk, queue, row tickets)
+             (1, 1 << 20), (3, 300_000), (8, 65_536), (2, 1_000_000)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
