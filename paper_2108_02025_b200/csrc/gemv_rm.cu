@@ -265,8 +265,9 @@ __global__ void __launch_bounds__(kRmBlock, MINB)
 constexpr int kChunkBlock = 512;
 constexpr int kChunkU = 2;
 
-template <typename T>
-__global__ void __launch_bounds__(kChunkBlock, 2)
+// R rows per unit share each x vector load (R = 1 for a single row).
+template <typename T, int R, int MINB>
+__global__ void __launch_bounds__(kChunkBlock, MINB)
     gemv_rm_chunk_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                          uint64_t m, uint64_t n, uint64_t chunk, uint64_t nchunks,
                          T* __restrict__ partials, unsigned* __restrict__ counters) {
@@ -278,48 +279,62 @@ __global__ void __launch_bounds__(kChunkBlock, 2)
     __shared__ bool last_sh;
     const int tid = threadIdx.x;
     const uint64_t nvec = n / V;
-    const uint64_t units = m * nchunks;
+    const uint64_t groups = (m + R - 1) / R;
+    const uint64_t units = groups * nchunks;
     const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
     uint64_t u = blockIdx.x;
     while (u < units) {
         if (tid == 0) next_sh = dyn_next(counters, units); // prefetch
-        const uint64_t ch = u / m, row = u - ch * m;
-        const Vec<T>* Ar = reinterpret_cast<const Vec<T>*>(A + row * n);
+        const uint64_t ch = u / groups, grp = u - ch * groups;
+        const uint64_t row0 = grp * R;
+        const int rows = (m - row0 < uint64_t(R)) ? int(m - row0) : R;
         const uint64_t c0 = ch * chunk;
         const uint64_t c1 = (c0 + chunk < nvec) ? c0 + chunk : nvec;
-        T acc[U];
+        T acc[R][U];
 #pragma unroll
-        for (int k = 0; k < U; ++k) acc[k] = T(0);
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int k = 0; k < U; ++k) acc[r][k] = T(0);
         for (uint64_t base = c0; base < c1; base += uint64_t(kChunkBlock) * U) {
-            Vec<T> av[U], xv[U];
+            Vec<T> av[R][U], xv[U];
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 const uint64_t i = base + uint64_t(k) * kChunkBlock + tid;
-                if (i < c1) {
-                    av[k] = ld_stream(Ar + i);
-                    xv[k] = ld_stream(X + i);
-                } else {
+                const bool ok = i < c1;
+                if (ok) xv[k] = ld_stream(X + i);
+                else
 #pragma unroll
-                    for (int e = 0; e < V; ++e) av[k].v[e] = xv[k].v[e] = T(0);
+                    for (int e = 0; e < V; ++e) xv[k].v[e] = T(0);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (ok && r < rows) av[r][k] = ld_stream(reinterpret_cast<const Vec<T>*>(A + (row0 + r) * n) + i);
+                    else
+#pragma unroll
+                        for (int e = 0; e < V; ++e) av[r][k].v[e] = T(0);
                 }
             }
 #pragma unroll
-            for (int k = 0; k < U; ++k) acc[k] = dot_vec(av[k], xv[k], acc[k]);
-        }
-        T v = acc[0];
+            for (int k = 0; k < U; ++k)
 #pragma unroll
-        for (int k = 1; k < U; ++k) v = add_rn(v, acc[k]);
-        const T unit_total = block_sum(v, red); // its barriers publish next_sh
-        if (tid == 0) partials[row * nchunks + ch] = unit_total;
-        if (last_arriver(counters + 1 + row, unsigned(nchunks), &last_sh)) {
-            T w = T(0);
-            for (uint64_t i = tid; i < nchunks; i += kChunkBlock)
-                w = add_rn(w, ld_cg(partials + row * nchunks + i));
-            const T total = block_sum(w, red);
-            if (tid == 0) {
-                c[row] = add_rn(c[row], total);
-                counters[1 + row] = 0u;
+                for (int r = 0; r < R; ++r) acc[r][k] = dot_vec(av[r][k], xv[k], acc[r][k]);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            T v = acc[r][0];
+#pragma unroll
+            for (int k = 1; k < U; ++k) v = add_rn(v, acc[r][k]);
+            const T unit_total = block_sum(v, red); // its barriers publish next_sh
+            if (tid == 0 && r < rows) partials[(row0 + r) * nchunks + ch] = unit_total;
+        }
+        if (last_arriver(counters + 1 + grp, unsigned(nchunks), &last_sh)) {
+            for (int r = 0; r < rows; ++r) {
+                T w = T(0);
+                for (uint64_t i = tid; i < nchunks; i += kChunkBlock)
+                    w = add_rn(w, ld_cg(partials + (row0 + r) * nchunks + i));
+                const T total = block_sum(w, red);
+                if (tid == 0) c[row0 + r] = add_rn(c[row0 + r], total);
             }
+            if (tid == 0) counters[1 + grp] = 0u;
         }
         u = next_sh;
         __syncthreads(); // next_sh is rewritten at the top of the next unit
@@ -484,13 +499,14 @@ template <typename T> bool rm_vec_ok(const T* A, const T* x, uint64_t n) {
 }
 
 // Few long rows take the chunked kernel (mode 9).  256 MiB of A, flushed
-// (tools/rm_few.py), unit kernel -> chunked: m = 1 / 2 / 4 fp32 129 / 129 / 96
-// -> 84 / 74 / 68 us; m = 16 ties (61.4); from m = 64 up the sweeps win
-// (51 vs 61).  CABL_RM_FEW_MAX overrides the row limit (tuning only).
+// (tools/rm_few.py), unit kernel -> chunked (R = 1 for one row, else 2 rows per
+// unit): m = 1 / 2 / 4 / 16 fp32 129 / 129 / 96 / 61.4 -> 84 / 67.6 / 59.4 /
+// 55.3 us; from m = 64 up the other kernels win (51 vs 53; 4 rows per unit
+// was slower everywhere).  CABL_RM_FEW_MAX overrides the row limit (tuning).
 inline bool rm_few_rows(uint64_t m, uint64_t n, size_t elem) {
     static const uint64_t max_rows = [] {
         const char* e = getenv("CABL_RM_FEW_MAX");
-        return e ? uint64_t(atoll(e)) : uint64_t(8);
+        return e ? uint64_t(atoll(e)) : uint64_t(16);
     }();
     return m <= max_rows && n * elem >= 65536;
 }
@@ -536,6 +552,16 @@ template <typename T> uint64_t rm_chunk_vecs(uint64_t m, uint64_t n) {
     uint64_t cv = 256;
     while (cv * 2 <= 65536 && m * ((nvec + cv * 2 - 1) / (cv * 2)) >= slots && cv * 2 <= nvec) cv *= 2;
     return cv;
+}
+
+// Rows per unit of the chunked kernel (CABL_RM_CHUNK_ROWS overrides: tuning).
+inline int rm_chunk_rows(uint64_t m) {
+    static const int forced = [] {
+        const char* e = getenv("CABL_RM_CHUNK_ROWS");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced == 1 || forced == 2) return forced;
+    return m == 1 ? 1 : 2; // measured: R = 2 beats 1 from m = 2 and 4 everywhere
 }
 
 template <typename T> RmGeom rm_geom(uint64_t m, uint64_t n) {
@@ -680,11 +706,17 @@ cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
     } else if (mode == 9) {
         const uint64_t cv = rm_chunk_vecs<T>(m, n);
         const uint64_t nch = (n / Vec<T>::N + cv - 1) / cv;
-        const uint64_t units = m * nch;
+        const int R = rm_chunk_rows(m);
+        const uint64_t units = (m + R - 1) / R * nch;
         const uint64_t cap = uint64_t(sm_count()) * 2;
         const unsigned grid = unsigned(units < cap ? units : cap); // grid <= units (dyn_next)
-        launch(gemv_rm_chunk_kernel<T>, grid, kChunkBlock, 0, s, A, x, c, m, n, cv, nch,
-               static_cast<T*>(ws.scratch), ws.counters);
+        T* part = static_cast<T*>(ws.scratch);
+        if (R == 1)
+            launch(gemv_rm_chunk_kernel<T, 1, 2>, grid, kChunkBlock, 0, s, A, x, c, m, n, cv, nch,
+                   part, ws.counters);
+        else
+            launch(gemv_rm_chunk_kernel<T, 2, 2>, grid, kChunkBlock, 0, s, A, x, c, m, n, cv, nch,
+                   part, ws.counters);
         if (info) info->ctas = grid;
     } else if (mode >= 3) {
         const uint64_t cap = uint64_t(sm_count()) * 8;
