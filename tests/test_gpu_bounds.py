@@ -93,7 +93,8 @@ def test_ger_guard_bands(cuda, dtype, off, layout):
     pol = cb.default_policy(1)
     lay = cb.Layout.RowMajor if layout == "row" else cb.Layout.ColMajor
     for m, n in ((3, 5), (37, 1000), (300, 2048), (1000, 4096), (8, 8193), (20_000, 64),
-                 (3000, 4100), (50_000, 5), (777, 1001), (1001, 777), (400, 1003)):
+                 (3000, 4100), (50_000, 5), (777, 1001), (1001, 777), (400, 1003),
+                 (400_003, 1), (1, 400_003)):
         x, y = framed_input(m, dtype, 1, off, cuda), framed_input(n, dtype, 2, off, cuda)
         C = FramedOutput(m * n, dtype, 5, off, cuda)
         cb.ger(x, y, cb.DenseMatrix.wrap(C.view, m, n, lay), pol)

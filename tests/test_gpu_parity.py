@@ -301,7 +301,9 @@ GER_SHAPES = [(1, 1), (2, 3), (3, 3), (500, 500), (777, 1001), (1000, 8), (8, 10
               # rows of whole 16-byte vectors (flat 16-byte sweep)
               (3000, 4100), (12, 100_004), (40_000, 12),
               # odd rows of >= 8 elements (flat 32-byte sweep of C, rows straddling vectors)
-              (1001, 777), (400, 1003), (3, 200_001), (200_001, 9), (8192, 8193)]
+              (1001, 777), (400, 1003), (3, 200_001), (200_001, 9), (8192, 8193),
+              # one-element rows (row-major n = 1, col-major m = 1): the AXPY kernel
+              (400_001, 1), (1, 400_003)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
