@@ -156,19 +156,34 @@ class PeerMailboxes:
         self.device = device
         if self.world > 8:
             raise ValueError("peer DOT: at most 8 ranks (one NVLink domain)")
+        real = create is None and import_ is None  # library-owned mappings to release on failure
         create = create or self._create
         export = export or self._export
         import_ = import_ or self._import
         with cabl._on_device(device):
             self.own = create()
-            handles: list = [b""]
-            if self.world > 1:
-                handles = [None] * self.world
-                dist.all_gather_object(handles, export(self.own), group=group)
             self.mapped = {}
-            for g, h in enumerate(handles):
-                if g != self.rank:
-                    self.mapped[g] = import_(h)
+            if self.world > 1:
+                handles: list = [None] * self.world
+                dist.all_gather_object(handles, export(self.own), group=group)
+                err = None
+                try:
+                    for g, h in enumerate(handles):
+                        if g != self.rank:
+                            self.mapped[g] = import_(h)
+                except Exception as e:  # noqa: BLE001 - reported collectively below
+                    err = e
+                # every rank must agree before any kernel spins on a peer
+                flag = torch.tensor([0 if err else 1], dtype=torch.int32,
+                                    device=device if device.type == "cuda" else "cpu")
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+                if int(flag.item()) == 0:
+                    if real:
+                        for p in self.mapped.values():  # return codes ignored: failing anyway
+                            _lib.lib().cabl_peer_mailbox_unmap(C.c_void_p(p))
+                        _lib.lib().cabl_peer_mailbox_destroy(C.c_void_p(self.own))
+                    raise RuntimeError(f"peer mailbox exchange failed on at least one rank"
+                                       f"{': ' + str(err) if err else ''}")
         ptrs = [self.own if g == self.rank else self.mapped[g] for g in range(self.world)]
         self.table = (C.c_void_p * self.world)(*ptrs)
         self._lib = _lib

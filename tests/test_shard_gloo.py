@@ -126,6 +126,18 @@ def _worker(rank, world, port, results):
                                  export=lambda p: f"h{p}".encode().ljust(64, b"\0"),
                                  import_=lambda h: 2000 + int(h.rstrip(b"\0")[1:]))
         results[f"peer_{rank}"] = (mb.world, mb.rank, [mb.table[g] for g in range(world)])
+        # an import failure on one rank is reported on every rank (no rank may
+        # go on to spin on a peer that never arrives)
+        def bad_import(h):
+            if rank == world - 1:
+                raise OSError("no IPC here")
+            return 1
+        try:
+            shard.PeerMailboxes(torch.device("cpu"), create=lambda: 1, export=lambda p: b"h",
+                                import_=bad_import)
+            results[f"peerfail_{rank}"] = "no error"
+        except RuntimeError as e:
+            results[f"peerfail_{rank}"] = str(e)
     finally:
         dist.destroy_process_group()
 
@@ -197,6 +209,7 @@ def test_sharded_paths_over_gloo(world):
         w, rk, table = results[f"peer_{r}"]
         assert (w, rk) == (world, r)
         assert table == [1000 + r if g == r else 2000 + 1000 + g for g in range(world)]
+        assert results[f"peerfail_{r}"].startswith("peer mailbox exchange failed")
 
 
 def test_partition_is_balanced_and_contiguous():
