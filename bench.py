@@ -233,6 +233,14 @@ def step_fn(w, ins, policy, ctx, sharded_dot: bool, fused: bool = False):
             return (lambda: shard.sharded_dot(ins["x"], ins["y"], 0.0, ins["out"], policy,
                                               gathered=gathered)), 2  # dot + combine (+ NCCL all-gather)
         return (lambda: cb.dot_into(ins["x"], ins["y"], 0.0, ins["out"], policy)), 1
+    if w.op == "gemv-row" and fused:
+        # row blocks with the c all-gather inside the GEMV kernel (csrc/peer_gemv.cu)
+        m_total = WL.WORKLOADS[w.id].m
+        row_off = WL.Workload.shard_rows(WL.WORKLOADS[w.id], ctx.rank, ctx.world)[0] \
+            if ctx.world > 1 else 0
+        if getattr(ctx, "gather_gemv", None) is None:
+            ctx.gather_gemv = shard.GatherGemv(ctx.dev, m_total, w.dtype)
+        return (lambda: ctx.gather_gemv(ins["A"], ins["x"], ins["c"], row_off)), 1
     if w.op == "gemv-row" and sharded_dot and ctx.world > 1 and w.id == "G4":
         # BASELINE config 5: "c slices all-gathered" (NCCL) after the row blocks
         m_total = WL.WORKLOADS["G4"].m
@@ -601,12 +609,12 @@ def run_suite(args, ctx, flush, policy, peak):
 
     from paper_2108_02025_b200 import workloads as WL
     ids = list(WL.WORKLOADS) if ctx.world == 1 else ["R1", "G4", "D2"]
-    ids.append("D2f")  # D2 with the exchange fused into the kernel (peer memory)
+    ids += ["D2f", "G4f"]  # D2 / G4 with the exchange fused into the kernel (peer memory)
     out = {}
     steps = max(3, min(args.steps, args.suite_steps))
     for wid in ids:
-        fused = wid == "D2f"
-        w = WL.WORKLOADS["D2" if fused else wid]
+        fused = wid in ("D2f", "G4f")
+        w = WL.WORKLOADS[wid[:2] if fused else wid]
         total = w.n if w.op == "dot" else w.m
         b, e = (0, total) if ctx.world == 1 else WL.Workload.shard_rows(w, ctx.rank, ctx.world)
         try:
@@ -623,8 +631,10 @@ def run_suite(args, ctx, flush, policy, peak):
             times, _ = time_steps(fn, steps, args.warmup, ctx, flush, mode=mode)
             t_max = ctx.max(sum(times) / 1000.0)
             gbs = alg * steps / t_max / 1e9
-            desc = w.desc + (", partials exchanged inside the kernel over peer memory "
-                             "(cabl_cuda_dot_peer)" if fused else "")
+            desc = w.desc + ((", partials exchanged inside the kernel over peer memory "
+                              "(cabl_cuda_dot_peer)" if w.op == "dot" else
+                              ", c slices all-gathered inside the GEMV kernel over peer memory "
+                              "(cabl_cuda_gemv_rm_gather)") if fused else "")
             entry = {"desc": desc, "gbs": round(gbs, 2),
                      "frac_of_peak": round(gbs / (peak * ctx.world), 4),
                      "us_per_step": round(t_max / steps * 1e6, 3),

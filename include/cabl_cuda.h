@@ -196,6 +196,50 @@ CABL_API int cabl_cuda_dot_peer_emulate_f64(int world, const double* const* xs,
                                             void* const* mboxes, uint64_t small_cutoff,
                                             void* stream);
 
+/* ------------------------------------ row-major GEMV, c all-gather fused ---
+ * BASELINE config 5 / SURVEY.md §8(e): rank g owns rows [row_off, row_off+m)
+ * of A and of c (x replicated), and every rank needs the full c.  One kernel
+ * per rank computes c_slice += A_slice x with the single-GPU sweep (same bits
+ * as cabl_cuda_gemv_rm on the slice) and stores every finished row into every
+ * rank's gathered buffer over NVLink P2P; it ends when all ranks' rows have
+ * arrived.  No NCCL call.
+ *
+ * cfull[g]: rank g's gathered buffer, 2 * m_total elements allocated with
+ * cabl_peer_alloc on rank g's device (double-buffered: the e-th call on a
+ * mailbox fills half e & 1, i.e. elements [(e & 1) * m_total, +m_total)),
+ * as mapped here (cabl_peer_mailbox_export / _import work on any
+ * cabl_peer_alloc pointer).  mboxes: a mailbox set used only by this
+ * operation.  Calls are collective.  CABL_EINVAL when the slice shape does not
+ * take the sweep kernel (few or short rows, unaligned): use cabl_cuda_gemv_rm
+ * plus a collective there.  A rank that never arrives makes the others record
+ * the epoch in their mailbox's `fault` after CABL_PEER_TIMEOUT_MS.
+ * Replaces cabl::gemv_row_major (reference kernels.hpp:230-257) across GPUs. */
+CABL_API int cabl_peer_alloc(uint64_t bytes, void** ptr); /* zeroed, exportable */
+CABL_API int cabl_peer_free(void* ptr);
+CABL_API int cabl_cuda_gemv_rm_gather_f32(const float* A, uint64_t m, uint64_t n, const float* x,
+                                          float* c, uint64_t row_off, uint64_t m_total,
+                                          void* const* cfull, void* const* mboxes, int world,
+                                          int rank, cabl_probe* probe, void* stream);
+CABL_API int cabl_cuda_gemv_rm_gather_f64(const double* A, uint64_t m, uint64_t n,
+                                          const double* x, double* c, uint64_t row_off,
+                                          uint64_t m_total, void* const* cfull,
+                                          void* const* mboxes, int world, int rank,
+                                          cabl_probe* probe, void* stream);
+/* Every rank in one cooperative launch on the current device (testing with
+ * fewer GPUs than ranks; all slices must take the same sweep shape). */
+CABL_API int cabl_cuda_gemv_rm_gather_emulate_f32(int world, const float* const* As,
+                                                  const uint64_t* ms, uint64_t n,
+                                                  const float* const* xs, float* const* cs,
+                                                  const uint64_t* row_offs, uint64_t m_total,
+                                                  void* const* cfull, void* const* mboxes,
+                                                  void* stream);
+CABL_API int cabl_cuda_gemv_rm_gather_emulate_f64(int world, const double* const* As,
+                                                  const uint64_t* ms, uint64_t n,
+                                                  const double* const* xs, double* const* cs,
+                                                  const uint64_t* row_offs, uint64_t m_total,
+                                                  void* const* cfull, void* const* mboxes,
+                                                  void* stream);
+
 /* --------------------------------------------------------------- GEMV ---
  * c[0..m) += A x, A is m x n.  `small_cutoff`: when m*n + m + n <= cutoff the
  * call runs the ordered single-CTA path, which reproduces the compiled

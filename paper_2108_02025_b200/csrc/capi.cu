@@ -312,6 +312,134 @@ int dot_peer_emulate_impl(int world, const T* const* xs, const T* const* ys, con
     return CABL_OK;
 }
 
+// ------------------------------------- row-major GEMV + fused all-gather
+// Fence between the pushes and the completion words: none at world 1 (no
+// peer reads the buffers), else fence.acq_rel.sys; CABL_GATHER_FENCE=0|1|2
+// overrides (A/B only; 2 = fence.sc.sys).
+int gather_fence(int world) {
+    static const int forced = [] {
+        const char* e = getenv("CABL_GATHER_FENCE");
+        return e ? atoi(e) : -1;
+    }();
+    if (forced >= 0) return forced;
+    return world > 1 ? 1 : 0;
+}
+
+template <typename T>
+int gather_common_checks(int world, void* const* cfull, void* const* mboxes, uint64_t n,
+                         uint64_t m_total) {
+    if (world < 1 || world > kMaxPeers)
+        return fail(CABL_EINVAL, "gemv_rm_gather: world must be in [1, 8] (one NVLink domain)");
+    if (!cfull || !mboxes) return fail(CABL_EINVAL, "gemv_rm_gather: null peer table");
+    for (int g = 0; g < world; ++g)
+        if (!cfull[g] || !mboxes[g]) return fail(CABL_EINVAL, "gemv_rm_gather: null entry in a peer table");
+    if (n == 0 || m_total == 0) return fail(CABL_EINVAL, "gemv_rm_gather: empty matrix");
+    return CABL_OK;
+}
+
+template <typename T>
+int gemv_gather_impl(const T* A, uint64_t m, uint64_t n, const T* x, T* c, uint64_t row_off,
+                     uint64_t m_total, void* const* cfull, void* const* mboxes, int world, int rank,
+                     cabl_probe* probe, void* stream) {
+    if (int rc = gather_common_checks<T>(world, cfull, mboxes, n, m_total)) return rc;
+    if (rank < 0 || rank >= world) return fail(CABL_EINVAL, "gemv_rm_gather: rank must be in [0, world)");
+    if (!A || !x || !c || m == 0) return fail(CABL_EINVAL, "gemv_rm_gather: null operand or empty slice");
+    if (row_off + m > m_total) return fail(CABL_EINVAL, "gemv_rm_gather: slice outside the gathered c");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    int R, KV, mb;
+    if (!gemv_rm_sweep_cfg<T>(A, x, m, n, &R, &KV, &mb) || gemv_rm_gather_ctas_per_sm(R, KV, mb, sizeof(T)) == 0)
+        return fail(CABL_EINVAL, "gemv_rm_gather: this slice shape does not take the sweep kernel "
+                                 "(use gemv_rm + a collective)");
+    cudaStream_t s = as_stream(stream);
+    WorkspaceNeed need;
+    need.counters = 2;
+    WsLease lease;
+    if (int rc = get_workspace(dev, s, need, &lease)) return rc;
+    PeerGemvArgs<T> a{};
+    const uint64_t groups = (m + R - 1) / R;
+    const uint64_t cap = uint64_t(sm_count()) * mb;
+    a.A[0] = A;
+    a.x[0] = x;
+    a.c[0] = c;
+    a.m[0] = m;
+    a.row_off[0] = row_off;
+    a.grid[0] = unsigned(groups < cap ? groups : cap);
+    a.counters[0] = lease.ws.counters;
+    for (int g = 0; g < world; ++g) {
+        a.cfull[g] = static_cast<T*>(cfull[g]);
+        a.mbox[g] = mboxes[g];
+    }
+    a.n = n;
+    a.m_total = m_total;
+    a.world = world;
+    a.rank0 = rank;
+    a.timeout_ns = peer_timeout_ns();
+    a.fence = gather_fence(world);
+    const bool dyn = gemv_rm_use_dyn(m * n * sizeof(T));
+    CABL_TRY_CUDA(gemv_rm_gather_launch<T>(a, 1, R, KV, mb, dyn, false, s), "gemv_rm_gather kernel");
+    set_probe(probe, CABL_VARIANT_GEMV_ROW, a.grid[0]);
+    return CABL_OK;
+}
+
+template <typename T>
+int gemv_gather_emulate_impl(int world, const T* const* As, const uint64_t* ms, uint64_t n,
+                             const T* const* xs, T* const* cs, const uint64_t* row_offs,
+                             uint64_t m_total, void* const* cfull, void* const* mboxes,
+                             void* stream) {
+    if (int rc = gather_common_checks<T>(world, cfull, mboxes, n, m_total)) return rc;
+    if (!As || !ms || !xs || !cs || !row_offs) return fail(CABL_EINVAL, "gemv_rm_gather_emulate: null table");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    int R = 0, KV = 0, mb = 0;
+    for (int r = 0; r < world; ++r) {
+        if (!As[r] || !xs[r] || !cs[r] || ms[r] == 0 || row_offs[r] + ms[r] > m_total)
+            return fail(CABL_EINVAL, "gemv_rm_gather_emulate: bad slice");
+        int r_, kv_, mb_;
+        if (!gemv_rm_sweep_cfg<T>(As[r], xs[r], ms[r], n, &r_, &kv_, &mb_))
+            return fail(CABL_EINVAL, "gemv_rm_gather_emulate: a slice does not take the sweep kernel");
+        if (r > 0 && (r_ != R || kv_ != KV || mb_ != mb))
+            return fail(CABL_EINVAL, "gemv_rm_gather_emulate: every slice must take the same sweep shape");
+        R = r_, KV = kv_, mb = mb_;
+    }
+    const int per_sm = gemv_rm_gather_ctas_per_sm(R, KV, mb, sizeof(T));
+    if (per_sm == 0) return fail(CABL_EINVAL, "gemv_rm_gather_emulate: unsupported sweep shape");
+    // every rank's grid in one co-resident wave
+    const uint64_t share = uint64_t(sm_count()) * uint64_t(per_sm) / uint64_t(world);
+    if (share == 0) return fail(CABL_EINVAL, "gemv_rm_gather_emulate: too many ranks for one wave");
+    cudaStream_t s = as_stream(stream);
+    WorkspaceNeed need;
+    need.counters = 2 * size_t(world);
+    WsLease lease;
+    if (int rc = get_workspace(dev, s, need, &lease)) return rc;
+    PeerGemvArgs<T> a{};
+    bool dyn = false;
+    for (int r = 0; r < world; ++r) {
+        const uint64_t groups = (ms[r] + R - 1) / R;
+        a.A[r] = As[r];
+        a.x[r] = xs[r];
+        a.c[r] = cs[r];
+        a.m[r] = ms[r];
+        a.row_off[r] = row_offs[r];
+        a.grid[r] = unsigned(groups < share ? groups : share);
+        a.counters[r] = lease.ws.counters + 2 * r;
+        dyn = dyn || gemv_rm_use_dyn(ms[r] * n * sizeof(T));
+    }
+    for (int g = 0; g < world; ++g) {
+        a.cfull[g] = static_cast<T*>(cfull[g]);
+        a.mbox[g] = mboxes[g];
+    }
+    a.n = n;
+    a.m_total = m_total;
+    a.world = world;
+    a.rank0 = 0;
+    a.timeout_ns = peer_timeout_ns();
+    a.fence = gather_fence(world);
+    CABL_TRY_CUDA(gemv_rm_gather_launch<T>(a, world, R, KV, mb, dyn, true, s),
+                  "gemv_rm_gather_emulate kernel");
+    return CABL_OK;
+}
+
 // ------------------------------------------------------------------ GEMV
 // Row-major GEMV runs the deterministic sweep kernels (BASELINE tolerance,
 // bitwise run to run) by default; CABL_GEMV_RM_ORDER=reference selects the
@@ -703,7 +831,7 @@ extern "C" int cabl_describe_device(int device, cabl_gpu_machine* out) {
 extern "C" {
 
 const char* cabl_last_error(void) { return g_err.c_str(); }
-int cabl_abi_version(void) { return 102; } // 1.02: + peer-memory DOT and its mailboxes
+int cabl_abi_version(void) { return 103; } // 1.03: + GEMV with the c all-gather fused (peer memory)
 int cabl_device_count(void) {
     int c = 0;
     if (cudaGetDeviceCount(&c) != cudaSuccess) {
@@ -796,6 +924,54 @@ int cabl_cuda_dot_peer_emulate_f64(int world, const double* const* xs, const dou
                                    void* const* mboxes, uint64_t small_cutoff, void* stream) {
     return dot_peer_emulate_impl<double>(world, xs, ys, ns, alpha0, outs, mboxes, small_cutoff,
                                          stream);
+}
+int cabl_peer_alloc(uint64_t bytes, void** ptr) {
+    if (!ptr || bytes == 0) return fail(CABL_EINVAL, "peer_alloc: null out or zero bytes");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    void* p = nullptr;
+    CABL_TRY_CUDA(cudaMalloc(&p, bytes), "peer buffer alloc"); // exportable by IPC
+    cudaError_t e = cudaMemset(p, 0, bytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return cuda_fail(e, "peer buffer init");
+    }
+    *ptr = p;
+    return CABL_OK;
+}
+int cabl_peer_free(void* ptr) {
+    if (!ptr) return CABL_OK;
+    CABL_TRY_CUDA(cudaFree(ptr), "peer buffer free");
+    return CABL_OK;
+}
+int cabl_cuda_gemv_rm_gather_f32(const float* A, uint64_t m, uint64_t n, const float* x, float* c,
+                                 uint64_t row_off, uint64_t m_total, void* const* cfull,
+                                 void* const* mboxes, int world, int rank, cabl_probe* probe,
+                                 void* stream) {
+    return gemv_gather_impl<float>(A, m, n, x, c, row_off, m_total, cfull, mboxes, world, rank,
+                                   probe, stream);
+}
+int cabl_cuda_gemv_rm_gather_f64(const double* A, uint64_t m, uint64_t n, const double* x,
+                                 double* c, uint64_t row_off, uint64_t m_total,
+                                 void* const* cfull, void* const* mboxes, int world, int rank,
+                                 cabl_probe* probe, void* stream) {
+    return gemv_gather_impl<double>(A, m, n, x, c, row_off, m_total, cfull, mboxes, world, rank,
+                                    probe, stream);
+}
+int cabl_cuda_gemv_rm_gather_emulate_f32(int world, const float* const* As, const uint64_t* ms,
+                                         uint64_t n, const float* const* xs, float* const* cs,
+                                         const uint64_t* row_offs, uint64_t m_total,
+                                         void* const* cfull, void* const* mboxes, void* stream) {
+    return gemv_gather_emulate_impl<float>(world, As, ms, n, xs, cs, row_offs, m_total, cfull,
+                                           mboxes, stream);
+}
+int cabl_cuda_gemv_rm_gather_emulate_f64(int world, const double* const* As, const uint64_t* ms,
+                                         uint64_t n, const double* const* xs, double* const* cs,
+                                         const uint64_t* row_offs, uint64_t m_total,
+                                         void* const* cfull, void* const* mboxes, void* stream) {
+    return gemv_gather_emulate_impl<double>(world, As, ms, n, xs, cs, row_offs, m_total, cfull,
+                                            mboxes, stream);
 }
 int cabl_cuda_combine_partials_f32(const float* p, uint32_t count, float alpha0, float* out,
                                    void* stream) {

@@ -187,6 +187,21 @@ __device__ __forceinline__ unsigned long long dyn_next(unsigned* counter,
     return dyn_next(counter, total, gridDim.x);
 }
 
+// Acq_rel ticket: true in the CTA that arrives last (every earlier CTA's
+// partial is visible to it).  Contains one __syncthreads().
+__device__ __forceinline__ bool last_arriver(unsigned* ticket, unsigned nblk, bool* am_last_sh) {
+    if (threadIdx.x == 0) {
+        unsigned t;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                     : "=r"(t)
+                     : "l"(ticket)
+                     : "memory");
+        *am_last_sh = (t == nblk - 1);
+    }
+    __syncthreads();
+    return *am_last_sh;
+}
+
 // ---- programmatic dependent launch (PDL) ---------------------------------
 // Every kernel of the library starts with pdl_enter(): it lets the NEXT
 // kernel on the stream begin launching (its CTAs take SMs as this grid's

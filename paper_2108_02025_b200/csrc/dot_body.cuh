@@ -158,19 +158,4 @@ __device__ __forceinline__ T dot_chunk_total(const T* __restrict__ x, const T* _
     return total;
 }
 
-// Acq_rel ticket: true in the CTA that arrives last (every earlier CTA's
-// partial is visible to it).  Contains one __syncthreads().
-__device__ __forceinline__ bool last_arriver(unsigned* ticket, unsigned nblk, bool* am_last_sh) {
-    if (threadIdx.x == 0) {
-        unsigned t;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
-                     : "=r"(t)
-                     : "l"(ticket)
-                     : "memory");
-        *am_last_sh = (t == nblk - 1);
-    }
-    __syncthreads();
-    return *am_last_sh;
-}
-
 } // namespace cabl_dev

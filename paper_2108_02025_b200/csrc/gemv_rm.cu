@@ -37,6 +37,7 @@
 // Algorithmic bytes per launch: m*n*s + n*s + 2*m*s.
 #include "common.cuh"
 #include "dot_body.cuh"
+#include "gemv_rm_body.cuh"
 #include "kernels.cuh"
 
 #include <cstdio>
@@ -46,7 +47,6 @@ namespace cabl_dev {
 
 namespace {
 
-constexpr int kRmBlock = 256;
 constexpr int kRmCtasPerSm = 2;
 constexpr int kRmRows = 2; // R
 constexpr int kRmSeg = 2;  // SEG warp-vectors per unit
@@ -194,62 +194,8 @@ __global__ void __launch_bounds__(kRmBlock, MINB)
             prefetch_l2_bulk(A + row * n, unsigned(n * sizeof(T) < pass ? n * sizeof(T) : pass));
     }
     pdl_wait();
-    constexpr int NW = kRmBlock / kWarp;
-    __shared__ T red[2][R][NW];
-    __shared__ unsigned long long next_sh[2];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint64_t nvec_row = n / Vec<T>::N;
-    const uint64_t groups = (m + R - 1) / R;
-    const Vec<T>* X = reinterpret_cast<const Vec<T>*>(x);
-    uint64_t g = blockIdx.x; // first group static, the rest from the queue (DYN)
-    int parity = 0;
-    while (g < groups) {
-        if (DYN && tid == 0) next_sh[parity ^ 1] = dyn_next(counter, groups); // prefetch
-        const uint64_t row0 = g * R;
-        const int rows = (m - row0 < uint64_t(R)) ? int(m - row0) : R;
-        T acc[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) acc[r] = T(0);
-        for (uint64_t base = 0; base < nvec_row; base += uint64_t(kRmBlock) * KV) {
-            Vec<T> av[R][KV];
-            Vec<T> xv[KV];
-#pragma unroll
-            for (int k = 0; k < KV; ++k) {
-                const uint64_t j = base + uint64_t(tid) + uint64_t(k) * kRmBlock;
-                const bool ok = j < nvec_row;
-                if (ok) xv[k] = ld_reuse(X + j);
-                else
-#pragma unroll
-                    for (int e = 0; e < Vec<T>::N; ++e) xv[k].v[e] = T(0);
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    if (ok && r < rows)
-                        av[r][k] = ld_stream(reinterpret_cast<const Vec<T>*>(A + (row0 + r) * n) + j);
-                    else
-#pragma unroll
-                        for (int e = 0; e < Vec<T>::N; ++e) av[r][k].v[e] = T(0);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < KV; ++k)
-#pragma unroll
-                for (int r = 0; r < R; ++r) acc[r] = dot_vec(av[r][k], xv[k], acc[r]);
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const T v = warp_sum(acc[r]);
-            if (lane == 0) red[parity][r][wid] = v;
-        }
-        __syncthreads(); // also publishes next_sh[parity ^ 1]
-        if (tid < rows) {
-            T sum = red[parity][tid][0];
-#pragma unroll
-            for (int w = 1; w < NW; ++w) sum = add_rn(sum, red[parity][tid][w]);
-            c[row0 + tid] = add_rn(c[row0 + tid], sum);
-        }
-        parity ^= 1;
-        g = DYN ? next_sh[parity] : g + gridDim.x;
-    }
+    sweep_groups<T, R, KV, DYN>(A, x, m, n, counter, blockIdx.x, gridDim.x,
+                                [&](uint64_t row, T sum) { c[row] = add_rn(c[row], sum); });
 }
 
 // CHUNKED FEW-ROWS kernel (aligned rows, few of them: a row is a long DOT
@@ -610,17 +556,36 @@ unsigned sweep_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, unsigned
     return grid;
 }
 
-// Tuning table (CABL_RM_SWEEP="R,KV,MINB" selects an entry; tools/tune.py).
-template <typename T>
-unsigned sweep_launch(const T* A, const T* x, T* c, uint64_t m, uint64_t n, int mode,
-                      unsigned* counter, cudaStream_t s) {
+// The sweep shape for (m, n, mode): the CABL_RM_SWEEP="R,KV,MINB" tuning entry
+// if set (tools/tune.py), else the measured rule.
+//   A row whose vectors leave the last pass of the chosen shape mostly empty
+// pays a whole pass of latency for it (fp32 8192 x 8200 under (2,8,1): 59.6
+// us against 44.1 for 8192 x 8192).  When the passes would be more than
+// 25% empty, take 8 rows x 1 vector (256-vector passes): 8200 -> 47.1,
+// 10000 -> 45.1, 2048 -> 46.1 (was 53.3), 5000 -> 46.1 (was 49.2) us.
+template <typename T> SweepCfg sweep_choice(uint64_t m, uint64_t n, int mode) {
     static const SweepCfg forced = [] {
         SweepCfg f{0, 0, 0};
         if (const char* e = getenv("CABL_RM_SWEEP")) sscanf(e, "%d,%d,%d", &f.R, &f.KV, &f.minb);
         return f;
     }();
+    const SweepCfg table[] = {{2, 4, 2}, {2, 8, 1}, {4, 1, 4}, {4, 2, 2}, {4, 4, 1}, {8, 1, 2}, {8, 2, 1}};
+    for (const SweepCfg& t : table)
+        if (forced.R == t.R && forced.KV == t.KV && forced.minb == t.minb) return t;
+    const uint64_t nvec = n / Vec<T>::N;
+    const uint64_t pass = uint64_t(kRmBlock) * (mode == 1 ? 2 : 8);
+    const uint64_t used = (nvec + pass - 1) / pass * pass;
+    if (used * 4 > nvec * 5 && (m + 7) / 8 >= uint64_t(sm_count()) * 2) return SweepCfg{8, 1, 2};
+    if (mode == 1) return SweepCfg{4, 2, 2}; // rows <= 2 passes
+    return SweepCfg{2, 8, 1};                // long rows
+}
+
+template <typename T>
+unsigned sweep_launch(const T* A, const T* x, T* c, uint64_t m, uint64_t n, int mode,
+                      unsigned* counter, cudaStream_t s) {
+    const SweepCfg cfg = sweep_choice<T>(m, n, mode);
 #define CABL_SWEEP_CASE(R_, KV_, MB_)                                                          \
-    if (forced.R == R_ && forced.KV == KV_ && forced.minb == MB_)                             \
+    if (cfg.R == R_ && cfg.KV == KV_ && cfg.minb == MB_)                                       \
         return sweep_go<T, R_, KV_, MB_>(A, x, c, m, n, counter, s);
     CABL_SWEEP_CASE(2, 4, 2)
     CABL_SWEEP_CASE(2, 8, 1)
@@ -630,18 +595,7 @@ unsigned sweep_launch(const T* A, const T* x, T* c, uint64_t m, uint64_t n, int 
     CABL_SWEEP_CASE(8, 1, 2)
     CABL_SWEEP_CASE(8, 2, 1)
 #undef CABL_SWEEP_CASE
-    // A row whose vectors leave the last pass of the chosen shape mostly empty
-    // pays a whole pass of latency for it (fp32 8192 x 8200 under (2,8,1): 59.6
-    // us against 44.1 for 8192 x 8192).  When the passes would be more than
-    // 25% empty, take 8 rows x 1 vector (256-vector passes): 8200 -> 47.1,
-    // 10000 -> 45.1, 2048 -> 46.1 (was 53.3), 5000 -> 46.1 (was 49.2) us.
-    const uint64_t nvec = n / Vec<T>::N;
-    const uint64_t pass = uint64_t(kRmBlock) * (mode == 1 ? 2 : 8);
-    const uint64_t used = (nvec + pass - 1) / pass * pass;
-    if (used * 4 > nvec * 5 && (m + 7) / 8 >= uint64_t(sm_count()) * 2)
-        return sweep_go<T, 8, 1, 2>(A, x, c, m, n, counter, s);
-    if (mode == 1) return sweep_go<T, 4, 2, 2>(A, x, c, m, n, counter, s); // rows <= 2 passes
-    return sweep_go<T, 2, 8, 1>(A, x, c, m, n, counter, s);                  // long rows
+    return sweep_go<T, 2, 8, 1>(A, x, c, m, n, counter, s);
 }
 
 } // namespace
@@ -658,6 +612,23 @@ bool gemv_rm_is_lane(const void* A, const void* x, uint64_t m, uint64_t n, size_
     return n * elem <= rm_lane_max_bytes() && m >= uint64_t(sm_count()) * 64 &&
            (vec || n <= kLaneScalarMaxN);
 }
+
+bool gemv_rm_use_dyn(uint64_t bytes) { return use_dyn_queue(bytes); }
+
+template <typename T>
+bool gemv_rm_sweep_cfg(const T* A, const T* x, uint64_t m, uint64_t n, int* R, int* KV, int* minb) {
+    if (m == 0 || n == 0) return false;
+    const int mode = rm_mode<T>(A, x, m, n);
+    if (mode != 1 && mode != 2) return false;
+    const SweepCfg c = sweep_choice<T>(m, n, mode);
+    *R = c.R;
+    *KV = c.KV;
+    *minb = c.minb;
+    return true;
+}
+template bool gemv_rm_sweep_cfg<float>(const float*, const float*, uint64_t, uint64_t, int*, int*, int*);
+template bool gemv_rm_sweep_cfg<double>(const double*, const double*, uint64_t, uint64_t, int*, int*,
+                                        int*);
 
 template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n) {
     WorkspaceNeed w;

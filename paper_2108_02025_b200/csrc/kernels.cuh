@@ -94,6 +94,27 @@ cudaError_t dot_peer_launch(const PeerDotArgs<T>& a, int local_ranks, bool chunk
                             bool cooperative, cudaStream_t s);
 int dot_peer_ctas_per_sm(bool chunked, size_t elem);
 
+// ---- row-major GEMV with the c all-gather fused (peer_gemv.cu) ----
+template <typename T> struct PeerGemvArgs {
+    const T* A[kMaxPeers];
+    const T* x[kMaxPeers];
+    T* c[kMaxPeers];                // the rank's own c slice (c += A x in place)
+    uint64_t m[kMaxPeers];          // rows of the rank's slice
+    uint64_t row_off[kMaxPeers];    // first global row of the slice
+    unsigned grid[kMaxPeers];
+    unsigned* counters[kMaxPeers];  // [0] group queue, [1] ticket; zero on entry and exit
+    T* cfull[kMaxPeers];            // rank g's double buffer (2 x m_total), as mapped here
+    void* mbox[kMaxPeers];          // rank g's gather mailbox, as mapped here
+    uint64_t n, m_total;
+    int world, rank0;
+    unsigned long long timeout_ns;
+    int fence; // 0 none (world 1), 1 acq_rel.sys, 2 sc.sys
+};
+template <typename T>
+cudaError_t gemv_rm_gather_launch(const PeerGemvArgs<T>& a, int local_ranks, int R, int KV,
+                                  int minb, bool dyn, bool cooperative, cudaStream_t s);
+int gemv_rm_gather_ctas_per_sm(int R, int KV, int minb, size_t elem);
+
 // ---- GEMV row-major (gemv_rm.cu) ----
 template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n);
 // short rows, many of them: the one-thread-per-row kernel (reference order,
@@ -102,6 +123,13 @@ bool gemv_rm_is_lane(const void* A, const void* x, uint64_t m, uint64_t n, size_
 template <typename T>
 cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
                            const Workspace& ws, cudaStream_t s, LaunchInfo* info);
+
+// The sweep shape (rows per group, vectors per pass, CTAs per SM) plain
+// gemv_rm_launch uses for this shape; false when the shape takes another
+// kernel.  The gathering sweep (peer_gemv.cu) runs exactly this shape.
+template <typename T>
+bool gemv_rm_sweep_cfg(const T* A, const T* x, uint64_t m, uint64_t n, int* R, int* KV, int* minb);
+bool gemv_rm_use_dyn(uint64_t bytes); // the sweep's queue rule
 
 // ---- GEMV row-major in the reference's order (gemv_rm_ordered.cu): bit for
 // bit the compiled reference gemv_row_major / gemv_ref ----

@@ -49,6 +49,7 @@
 #include "common.cuh"
 #include "dot_body.cuh"
 #include "kernels.cuh"
+#include "peer.cuh"
 
 namespace cabl_dev {
 
@@ -56,14 +57,6 @@ static_assert(sizeof(PeerMailbox) == 512, "mailbox layout is part of the ABI");
 
 namespace {
 
-__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 // the partial's bits as (up to) two 32-bit halves, and back
 __device__ __forceinline__ void halves(float v, unsigned* h) { h[0] = __float_as_uint(v); }
 __device__ __forceinline__ void halves(double v, unsigned* h) {
@@ -75,12 +68,6 @@ __device__ __forceinline__ float from_halves(const unsigned* h, float*) { return
 __device__ __forceinline__ double from_halves(const unsigned* h, double*) {
     return __longlong_as_double((long long)((unsigned long long)h[1] << 32 | h[0]));
 }
-__device__ __forceinline__ unsigned long long globaltimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
 template <typename T> __device__ __forceinline__ T quiet_nan();
 template <> __device__ __forceinline__ float quiet_nan<float>() { return __int_as_float(0x7fc00000); }
 template <> __device__ __forceinline__ double quiet_nan<double>() {

@@ -21,6 +21,9 @@ The reference parallelises over CPU threads with contiguous chunks
   communication at all.
 * GEMV col-major by columns (short-wide, e.g. G3) — rank g owns a block of
   columns; partial c vectors are all-gathered and added in rank order.
+* ``GatherGemv`` — row-block GEMV whose c all-gather runs inside the GEMV
+  kernel: every finished row is stored into every rank's (double-buffered)
+  gathered c over peer memory (csrc/peer_gemv.cu), no NCCL call.
 
 The collective and the local compute are injectable so the partition and
 combine logic can be exercised by CPU ``gloo`` tests (tests/test_shard_gloo.py)
@@ -244,3 +247,121 @@ def sharded_dot_fused(x_local: torch.Tensor, y_local: torch.Tensor, alpha0: floa
                   cabl._stream_of(x_local))
     cabl._record(p)
     return out
+
+
+# --------------------------------------------------------------------------
+# Row-major GEMV with the c all-gather fused into the kernel (csrc/peer_gemv.cu)
+
+class _CudaArray:
+    """Zero-copy view of library-owned device memory for torch.as_tensor."""
+
+    def __init__(self, ptr: int, n: int, dtype: torch.dtype):
+        self.__cuda_array_interface__ = {
+            "shape": (n,), "typestr": "<f4" if dtype == torch.float32 else "<f8",
+            "data": (ptr, False), "version": 3, "strides": None}
+
+
+class GatherGemv:
+    """c_slice += A_slice x on every rank, with the full c assembled on every
+    rank by the same kernel (``cabl_cuda_gemv_rm_gather_*``): each finished row
+    is stored into every rank's gathered buffer over NVLink P2P, no NCCL call.
+
+    Rank g owns rows ``row_off[g] .. row_off[g] + m_g`` of A and c (x
+    replicated), like ``sharded_gemv_rows``.  The gathered buffer is library
+    memory, double-buffered: call k returns the view of half k & 1, valid
+    until call k + 2 (``cabl_cuda_gemv_rm_gather_*`` in include/cabl_cuda.h).
+    Collective: every rank of the group calls, in the same order.  The slice
+    shape must take the sweep kernel (long aligned rows, enough of them); other
+    shapes raise ValueError — use ``sharded_gemv_rows(gather=True)`` there.
+    ``alloc``/``create``/``export``/``import_`` are injectable for CPU tests.
+    """
+
+    def __init__(self, device: torch.device, m_total: int, dtype: torch.dtype, group=None, *,
+                 alloc=None, create=None, export=None, import_=None):
+        from . import _lib
+        self._lib = _lib
+        self.device, self.m_total, self.dtype = device, m_total, dtype
+        real = alloc is None and import_ is None
+        s = torch.tensor([], dtype=dtype).element_size()
+        alloc = alloc or (lambda nbytes: GatherGemv._alloc(nbytes))
+        create = create or PeerMailboxes._create
+        export = export or PeerMailboxes._export
+        import_ = import_ or PeerMailboxes._import
+        grouped = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if grouped else 1
+        self.rank = dist.get_rank(group) if grouped else 0
+        if self.world > 8:
+            raise ValueError("gather GEMV: at most 8 ranks (one NVLink domain)")
+        with cabl._on_device(device):
+            self.buf = alloc(2 * m_total * s)
+            self.mbox = create()
+            self.mapped: dict[int, tuple[int, int]] = {}
+            if self.world > 1:
+                handles: list = [None] * self.world
+                dist.all_gather_object(handles, (export(self.buf), export(self.mbox)), group=group)
+                err = None
+                try:
+                    for g, (hb, hm) in enumerate(handles):
+                        if g != self.rank:
+                            self.mapped[g] = (import_(hb), import_(hm))
+                except Exception as e:  # noqa: BLE001 - reported collectively below
+                    err = e
+                flag = torch.tensor([0 if err else 1], dtype=torch.int32,
+                                    device=device if device.type == "cuda" else "cpu")
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+                if int(flag.item()) == 0:
+                    if real:
+                        self.close()
+                    raise RuntimeError(f"gather buffer exchange failed on at least one rank"
+                                       f"{': ' + str(err) if err else ''}")
+        bufs = [self.buf if g == self.rank else self.mapped[g][0] for g in range(self.world)]
+        mbs = [self.mbox if g == self.rank else self.mapped[g][1] for g in range(self.world)]
+        self.cfull_table = (C.c_void_p * self.world)(*bufs)
+        self.mbox_table = (C.c_void_p * self.world)(*mbs)
+        self.calls = 0
+        self._views = None
+        if device.type == "cuda":
+            self._views = [torch.as_tensor(_CudaArray(self.buf + h * m_total * s, m_total, dtype),
+                                           device=device) for h in (0, 1)]
+
+    @staticmethod
+    def _alloc(nbytes: int) -> int:
+        from . import _lib
+        p = C.c_void_p()
+        _lib.call("cabl_peer_alloc", nbytes, C.byref(p))
+        return p.value
+
+    def __call__(self, A_local: "cabl.DenseMatrix", x: torch.Tensor, c_local: torch.Tensor,
+                 row_off: int) -> torch.Tensor:
+        cabl._require(A_local.layout() == cabl.Layout.RowMajor, "gemv_row_major: A must be row-major")
+        sfx = cabl._suffix(c_local)
+        m, n = A_local.rows(), A_local.cols()
+        cabl._require(x.numel() == n and c_local.numel() == m, "gemv_row_major: shape mismatch")
+        p = cabl.Probe()
+        with cabl._on_device(self.device):
+            self._lib.call(f"cabl_cuda_gemv_rm_gather_{sfx}", A_local.data.data_ptr(), m, n,
+                           x.data_ptr(), c_local.data_ptr(), row_off, self.m_total,
+                           self.cfull_table, self.mbox_table, self.world, self.rank, C.byref(p),
+                           cabl._stream_of(c_local))
+        cabl._record(p)
+        self.calls += 1
+        return self._views[self.calls & 1]
+
+    def state(self) -> tuple[int, int]:
+        """(completed calls, epoch of a timed-out call or 0) of this rank's mailbox."""
+        e, f = C.c_uint64(), C.c_uint64()
+        with cabl._on_device(self.device):
+            self._lib.call("cabl_peer_mailbox_state", C.c_void_p(self.mbox), C.byref(e), C.byref(f))
+        return e.value, f.value
+
+    def close(self) -> None:
+        if getattr(self, "buf", None) is None:
+            return
+        L = self._lib.lib()
+        with cabl._on_device(self.device):
+            for pb, pm in self.mapped.values():  # return codes ignored on teardown
+                L.cabl_peer_mailbox_unmap(C.c_void_p(pb))
+                L.cabl_peer_mailbox_unmap(C.c_void_p(pm))
+            L.cabl_peer_free(C.c_void_p(self.buf))
+            L.cabl_peer_mailbox_destroy(C.c_void_p(self.mbox))
+        self.buf, self.mapped, self._views = None, {}, None

@@ -126,6 +126,14 @@ def _worker(rank, world, port, results):
                                  export=lambda p: f"h{p}".encode().ljust(64, b"\0"),
                                  import_=lambda h: 2000 + int(h.rstrip(b"\0")[1:]))
         results[f"peer_{rank}"] = (mb.world, mb.rank, [mb.table[g] for g in range(world)])
+        # gathered-GEMV buffers: (buffer, mailbox) handles exchanged in one
+        # all-gather, both tables in rank order
+        gg = shard.GatherGemv(torch.device("cpu"), 100, torch.float32,
+                              alloc=lambda nb: 5000 + rank, create=lambda: 6000 + rank,
+                              export=lambda p: f"h{p}".encode().ljust(64, b"\0"),
+                              import_=lambda h: 10000 + int(h.rstrip(b"\0")[1:]))
+        results[f"gg_{rank}"] = ([gg.cfull_table[g] for g in range(world)],
+                                 [gg.mbox_table[g] for g in range(world)])
         # an import failure on one rank is reported on every rank (no rank may
         # go on to spin on a peer that never arrives)
         def bad_import(h):
@@ -210,6 +218,9 @@ def test_sharded_paths_over_gloo(world):
         assert (w, rk) == (world, r)
         assert table == [1000 + r if g == r else 2000 + 1000 + g for g in range(world)]
         assert results[f"peerfail_{r}"].startswith("peer mailbox exchange failed")
+        bufs, mbs = results[f"gg_{r}"]
+        assert bufs == [5000 + r if g == r else 15000 + g for g in range(world)]
+        assert mbs == [6000 + r if g == r else 16000 + g for g in range(world)]
 
 
 def test_partition_is_balanced_and_contiguous():

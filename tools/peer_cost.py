@@ -1,4 +1,4 @@
-"""Cost of the fused peer-memory exchange (csrc/peer.cu) on one GPU.
+"""Cost of the fused peer-memory exchanges (csrc/peer.cu, peer_gemv.cu) on one GPU.
 
 Times, back to back with CUDA events (K launches per event pair):
   plain   cabl_cuda_dot                      (one kernel, no exchange)
@@ -60,6 +60,28 @@ def main():
         del x, y
         torch.cuda.empty_cache()
     _lib.call("cabl_peer_mailbox_destroy", mb)
+
+    # row-major GEMV: plain vs the gathering kernel at world 1 (c slice also
+    # stored into the gathered buffer, completion words, epoch)
+    for m, n in ((8192, 8192), (8192, 65536)):
+        A = cb.fill_uniform(torch.empty(m * n, device="cuda"), 1, 3)
+        x = cb.fill_uniform(torch.empty(n, device="cuda"), 1, 1)
+        c = cb.fill_uniform(torch.empty(m, device="cuda"), 1, 4)
+        buf, gmb = C.c_void_p(), C.c_void_p()
+        _lib.call("cabl_peer_alloc", 2 * m * 4, C.byref(buf))
+        _lib.call("cabl_peer_mailbox_create", C.byref(gmb))
+        bt, mt = (C.c_void_p * 1)(buf.value), (C.c_void_p * 1)(gmb.value)
+        plain = lambda: L.cabl_cuda_gemv_rm_f32(A.data_ptr(), m, n, x.data_ptr(), c.data_ptr(),  # noqa: E731
+                                                8192, None, st)
+        gath = lambda: L.cabl_cuda_gemv_rm_gather_f32(A.data_ptr(), m, n, x.data_ptr(),  # noqa: E731
+                                                      c.data_ptr(), 0, m, bt, mt, 1, 0, None, st)
+        r = {"gemv_m": m, "gemv_n": n, "plain_us": round(timed(plain), 2),
+             "gather_us": round(timed(gath), 2)}
+        print(json.dumps(r), flush=True)
+        _lib.call("cabl_peer_free", buf)
+        _lib.call("cabl_peer_mailbox_destroy", gmb)
+        del A
+        torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":
