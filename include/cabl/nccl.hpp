@@ -12,6 +12,8 @@
 //         result is independent of NCCL's algorithm and identical everywhere.
 //   GEMV  row blocks of A and c, x replicated, no exchange needed.
 //   GER   row blocks of C and x, y replicated, no exchange at all.
+//   sharded_gemv_rows_gather_fused: the c all-gather inside the GEMV kernel —
+//         rows stored into every device's double-buffered gathered c over P2P.
 //   sharded_dot_fused: DOT with the exchange inside the kernel — every device
 //         stores its partial into every device's mailbox over NVLink P2P and
 //         sums the G partials in device order itself (cabl_cuda_dot_peer_*,
@@ -61,6 +63,7 @@ public:
     Group(const Group&) = delete;
     Group& operator=(const Group&) = delete;
     ~Group() {
+        free_gather();
         for (std::size_t i = 0; i < mboxes_.size(); ++i) {
             cudaSetDevice(devs_[i]);
             cabl_peer_mailbox_destroy(mboxes_[i]);
@@ -87,19 +90,9 @@ public:
     // device pointers (no IPC inside one process).
     void* const* mailboxes() {
         if (mboxes_.empty()) {
-            const int G = size();
-            for (int r = 0; r < G; ++r) {
+            enable_peer_access();
+            for (int r = 0; r < size(); ++r) {
                 detail::cuda_check(cudaSetDevice(devs_[r]), "cudaSetDevice");
-                for (int q = 0; q < G; ++q) {
-                    if (q == r) continue;
-                    int can = 0;
-                    detail::cuda_check(cudaDeviceCanAccessPeer(&can, devs_[r], devs_[q]),
-                                       "cudaDeviceCanAccessPeer");
-                    if (!can) throw std::runtime_error("sharded_dot_fused: no P2P path between devices");
-                    const cudaError_t e = cudaDeviceEnablePeerAccess(devs_[q], 0);
-                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-                    else detail::cuda_check(e, "cudaDeviceEnablePeerAccess");
-                }
                 void* mb = nullptr;
                 detail::check(cabl_peer_mailbox_create(&mb));
                 mboxes_.push_back(mb);
@@ -108,11 +101,66 @@ public:
         return mboxes_.data();
     }
 
+    // Gathered-c buffers (2 x bytes_half each, one per device) and their own
+    // mailboxes for the fused GEMV gather; reallocated when the size changes.
+    struct Gather {
+        std::vector<void*> bufs, mboxes;
+        std::size_t bytes_half = 0;
+        std::uint64_t calls = 0;
+    };
+    Gather& gather(std::size_t bytes_half) {
+        if (gather_.bytes_half != bytes_half) {
+            free_gather();
+            enable_peer_access();
+            for (int r = 0; r < size(); ++r) {
+                detail::cuda_check(cudaSetDevice(devs_[r]), "cudaSetDevice");
+                void* b = nullptr;
+                void* mb = nullptr;
+                detail::check(cabl_peer_alloc(2 * bytes_half, &b));
+                detail::check(cabl_peer_mailbox_create(&mb));
+                gather_.bufs.push_back(b);
+                gather_.mboxes.push_back(mb);
+            }
+            gather_.bytes_half = bytes_half;
+            gather_.calls = 0;
+        }
+        return gather_;
+    }
+
 private:
+    void enable_peer_access() {
+        if (peer_enabled_) return;
+        const int G = size();
+        for (int r = 0; r < G; ++r) {
+            detail::cuda_check(cudaSetDevice(devs_[r]), "cudaSetDevice");
+            for (int q = 0; q < G; ++q) {
+                if (q == r) continue;
+                int can = 0;
+                detail::cuda_check(cudaDeviceCanAccessPeer(&can, devs_[r], devs_[q]),
+                                   "cudaDeviceCanAccessPeer");
+                if (!can) throw std::runtime_error("peer-memory path: no P2P path between devices");
+                const cudaError_t e = cudaDeviceEnablePeerAccess(devs_[q], 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else detail::cuda_check(e, "cudaDeviceEnablePeerAccess");
+            }
+        }
+        peer_enabled_ = true;
+    }
+    void free_gather() {
+        for (std::size_t i = 0; i < gather_.bufs.size(); ++i) {
+            cudaSetDevice(devs_[i]);
+            cabl_peer_free(gather_.bufs[i]);
+            cabl_peer_mailbox_destroy(gather_.mboxes[i]);
+        }
+        gather_ = Gather{};
+    }
+
     std::vector<int> devs_;
     std::vector<ncclComm_t> comms_;
     std::vector<cudaStream_t> streams_;
     std::vector<void*> mboxes_;
+    Gather gather_;
+    bool peer_enabled_ = false;
 };
 
 namespace detail {
@@ -139,6 +187,16 @@ inline int dot_peer(const float* x, const float* y, std::uint64_t n, float a, fl
 inline int dot_peer(const double* x, const double* y, std::uint64_t n, double a, double* o,
                     void* const* mb, int G, int r, std::uint64_t cut, cudaStream_t s) {
     return cabl_cuda_dot_peer_f64(x, y, n, a, o, mb, G, r, cut, nullptr, s);
+}
+inline int gemv_gather(const float* A, std::uint64_t m, std::uint64_t n, const float* x, float* c,
+                       std::uint64_t off, std::uint64_t mt, void* const* b, void* const* mb, int G,
+                       int r, cudaStream_t s) {
+    return cabl_cuda_gemv_rm_gather_f32(A, m, n, x, c, off, mt, b, mb, G, r, nullptr, s);
+}
+inline int gemv_gather(const double* A, std::uint64_t m, std::uint64_t n, const double* x,
+                       double* c, std::uint64_t off, std::uint64_t mt, void* const* b,
+                       void* const* mb, int G, int r, cudaStream_t s) {
+    return cabl_cuda_gemv_rm_gather_f64(A, m, n, x, c, off, mt, b, mb, G, r, nullptr, s);
 }
 } // namespace detail
 
@@ -252,6 +310,40 @@ void sharded_gemv_rows_gather(Group& g, const std::vector<const DeviceMatrix<T>*
                        "ncclBroadcast");
     nccl_check(ncclGroupEnd(), "ncclGroupEnd");
     g.synchronize();
+}
+
+// sharded_gemv_rows_gather with the gather fused into the GEMV kernel (peer
+// memory, no NCCL): every device's slice update is stored into every device's
+// gathered buffer as its rows finish.  Returns, per device, a device pointer
+// to the full c (sum of the slice lengths), valid until the call after next
+// on this Group.  Row-major slices that take the sweep kernel only (long
+// aligned rows, enough of them); others throw std::invalid_argument — use
+// sharded_gemv_rows_gather there.
+template <typename T>
+std::vector<const T*> sharded_gemv_rows_gather_fused(Group& g,
+                                                     const std::vector<const DeviceMatrix<T>*>& A,
+                                                     const std::vector<const DeviceVector<T>*>& x,
+                                                     const std::vector<DeviceVector<T>*>& c,
+                                                     const ExecPolicy&) {
+    const int G = g.size();
+    std::vector<std::uint64_t> off(std::size_t(G) + 1, 0);
+    for (int q = 0; q < G; ++q) off[q + 1] = off[q] + c[q]->len();
+    Group::Gather& st = g.gather(off[G] * sizeof(T));
+    for (int r = 0; r < G; ++r) {
+        cabl::detail::require(A[r]->layout() == Layout::RowMajor,
+                              "gemv_row_major: A must be RowMajor");
+        cabl::detail::cuda_check(cudaSetDevice(g.device(r)), "cudaSetDevice");
+        cabl::detail::check(detail::gemv_gather(A[r]->data(), A[r]->rows(), A[r]->cols(),
+                                                x[r]->data(), c[r]->data(), off[r], off[G],
+                                                st.bufs.data(), st.mboxes.data(), G, r,
+                                                g.stream(r)));
+    }
+    g.synchronize();
+    st.calls += 1;
+    std::vector<const T*> full;
+    for (int r = 0; r < G; ++r)
+        full.push_back(static_cast<const T*>(st.bufs[r]) + (st.calls & 1) * off[G]);
+    return full;
 }
 
 // Col-major GEMV sharded by columns (short-wide shapes): A[r] is device r's

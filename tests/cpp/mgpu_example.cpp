@@ -155,6 +155,37 @@ int main() {
         ok &= full_ok;
         std::printf("rank %d: gathered c %s\n", r, full_ok ? "ok" : "MISMATCH");
     }
+    // the same with the gather fused into the GEMV kernel (peer memory): a third
+    // step, then every device's gathered buffer is the concatenation of the
+    // per-rank results (slices that do not take the sweep kernel are rejected)
+    {
+        std::vector<Vector<float>> c3_expect;
+        for (int r = 0; r < G; ++r) {
+            cudaSetDevice(0);
+            DeviceMatrix<float> dA(Ab[r].download());
+            DeviceVector<float> dx(xv), dc(c2_expect[r]);
+            gemv_row_major(dA, dx, dc, pol);
+            c3_expect.push_back(dc.download());
+        }
+        Vector<float> want3(m);
+        for (int r = 0, o = 0; r < G; o += int(c3_expect[r].len()), ++r)
+            std::copy(c3_expect[r].begin(), c3_expect[r].end(), want3.begin() + o);
+        try {
+            const std::vector<const float*> full3 =
+                nccl::sharded_gemv_rows_gather_fused(g, Ap, xq, cq, pol);
+            for (int r = 0; r < G; ++r) {
+                cudaSetDevice(g.device(r));
+                Vector<float> got(m);
+                cudaMemcpy(got.data(), full3[r], m * sizeof(float), cudaMemcpyDeviceToHost);
+                const bool f_ok = got == want3 && cb[r].download() == c3_expect[r];
+                ok &= f_ok;
+                std::printf("rank %d: gathered c, gather fused into the kernel %s\n", r,
+                            f_ok ? "ok" : "MISMATCH");
+            }
+        } catch (const std::invalid_argument& e) {
+            std::printf("fused gather skipped: %s\n", e.what());
+        }
+    }
     // col-major GEMV sharded by columns: every replica of c ends equal to
     // c + the rank-ordered sum of the column blocks' partials
     {
