@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
-for f in 0 1; do CABL_GATHER_FENCE=$f python tools/peer_cost.py 2>&1 | grep gemv > gpurun_out/peer_cost_f$f.jsonl; done
-timeout 900 python -m pytest tests/test_gpu_peer_gemv.py -q -x --timeout 600 -p no:cacheprovider > gpurun_out/pytest_pgemv.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_pgemv.log
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+./tests/cpp/mgpu_example > gpurun_out/mgpu_example.log 2>&1; echo "rc=$?" >> gpurun_out/mgpu_example.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
