@@ -521,6 +521,23 @@ def _time_host_loop(fn, steps, warmup, ctx):
 E2E_DEPTH = 4
 
 
+def _h2d_seconds(nbytes: int, dev) -> float:
+    """Median wall time of a pinned host -> device copy of nbytes (the PCIe bound)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    ts = []
+    for i in range(7):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d.copy_(h, non_blocking=True)
+        torch.cuda.synchronize()
+        if i >= 2:
+            ts.append(time.perf_counter() - t0)
+    del h, d
+    return sorted(ts)[len(ts) // 2]
+
+
 def run_e2e(w, ins, policy, ctx, args):
     """End-to-end through the public API, host<->device copies inside the
     timed loop, wall clock (max over ranks).  Returns (resident, host):
@@ -560,6 +577,14 @@ def run_e2e(w, ins, policy, ctx, args):
             "ms_per_step": round(t_max / steps * 1e3, 4), "api": api_host}
     full["pattern"] = ("drop-in call on host buffers: every operand copied H2D from pinned "
                        "memory and the result D2H inside every call")
+    # the link that bounds it: a plain pinned H2D copy of the same bytes, timed here
+    link_s = _h2d_seconds(h2d, ctx.dev)
+    h2d_gbs = h2d / link_s / 1e9
+    full["link"] = {"h2d_gbs_measured": round(h2d_gbs, 2),
+                    "h2d_bound_ms_per_step": round(link_s * 1e3, 4),
+                    "frac_of_link": round(link_s / (t_max / steps), 4),
+                    "what": "torch pinned-host -> device copy of the step's H2D bytes, median "
+                            "of 5; frac_of_link = that copy's time / the e2e step time"}
     if not w.op.startswith("gemv"):
         return full, None
 
