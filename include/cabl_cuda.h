@@ -196,6 +196,32 @@ CABL_API int cabl_cuda_dot_peer_emulate_f64(int world, const double* const* xs,
                                             void* const* mboxes, uint64_t small_cutoff,
                                             void* stream);
 
+/* -------------------------------- column-sharded GEMV combine, peer memory ---
+ * SURVEY.md §8(e) "G3 by columns": rank g computes part_g = A[:, cols_g] x[cols_g]
+ * (m values, from zero) with cabl_cuda_gemv_cm; then every rank needs
+ * c += ((part_0 + part_1) + ...) in rank order.  This single kernel per rank
+ * pushes part into slot (epoch parity, rank) of every rank's slot buffer over
+ * P2P, exchanges epoch-tagged mailbox words and adds the world partials in
+ * rank order: bitwise the all-gather + cabl_cuda_combine_rows path, with no
+ * collective call.  slots[g]: rank g's buffer of 2 * 8 * m elements from
+ * cabl_peer_alloc (as mapped here); mboxes: a mailbox set used only by this
+ * operation.  Collective; a missing rank records a fault and leaves c as is.
+ * The rank-ordered combine follows reference kernels.hpp:160-163. */
+CABL_API int cabl_cuda_combine_rows_peer_f32(const float* part, uint64_t m, float* c,
+                                             void* const* slots, void* const* mboxes, int world,
+                                             int rank, void* stream);
+CABL_API int cabl_cuda_combine_rows_peer_f64(const double* part, uint64_t m, double* c,
+                                             void* const* slots, void* const* mboxes, int world,
+                                             int rank, void* stream);
+CABL_API int cabl_cuda_combine_rows_peer_emulate_f32(int world, const float* const* parts,
+                                                     uint64_t m, float* const* cs,
+                                                     void* const* slots, void* const* mboxes,
+                                                     void* stream);
+CABL_API int cabl_cuda_combine_rows_peer_emulate_f64(int world, const double* const* parts,
+                                                     uint64_t m, double* const* cs,
+                                                     void* const* slots, void* const* mboxes,
+                                                     void* stream);
+
 /* ------------------------------------ row-major GEMV, c all-gather fused ---
  * BASELINE config 5 / SURVEY.md §8(e): rank g owns rows [row_off, row_off+m)
  * of A and of c (x replicated), and every rank needs the full c.  One kernel

@@ -88,6 +88,10 @@ SIGNATURES: dict[str, list] = {
     "cabl_cuda_gemv_rm_gather_f64": [vp, u64, u64, vp, vp, u64, u64, vp, vp, i32, i32, _P, vp],
     "cabl_cuda_gemv_rm_gather_emulate_f32": [i32, vp, vp, u64, vp, vp, vp, u64, vp, vp, vp],
     "cabl_cuda_gemv_rm_gather_emulate_f64": [i32, vp, vp, u64, vp, vp, vp, u64, vp, vp, vp],
+    "cabl_cuda_combine_rows_peer_f32": [vp, u64, vp, vp, vp, i32, i32, vp],
+    "cabl_cuda_combine_rows_peer_f64": [vp, u64, vp, vp, vp, i32, i32, vp],
+    "cabl_cuda_combine_rows_peer_emulate_f32": [i32, vp, u64, vp, vp, vp, vp],
+    "cabl_cuda_combine_rows_peer_emulate_f64": [i32, vp, u64, vp, vp, vp, vp],
     "cabl_cuda_fill_uniform_f32": [vp, u64, u64, u64, u64, vp],
     "cabl_cuda_fill_uniform_f64": [vp, u64, u64, u64, u64, vp],
     "cabl_cuda_fill_normal_f64": [vp, u64, u64, u64, u64, vp],

@@ -312,6 +312,61 @@ int dot_peer_emulate_impl(int world, const T* const* xs, const T* const* ys, con
     return CABL_OK;
 }
 
+// ------------------------------------ rank-ordered row combine, peer memory
+template <typename T>
+int rows_peer_fill(PeerRowsArgs<T>& a, int world, uint64_t m, void* const* slots,
+                   void* const* mboxes) {
+    if (world < 1 || world > kMaxPeers)
+        return fail(CABL_EINVAL, "combine_rows_peer: world must be in [1, 8] (one NVLink domain)");
+    if (!slots || !mboxes) return fail(CABL_EINVAL, "combine_rows_peer: null peer table");
+    for (int g = 0; g < world; ++g) {
+        if (!slots[g] || !mboxes[g]) return fail(CABL_EINVAL, "combine_rows_peer: null entry in a peer table");
+        a.slots[g] = static_cast<T*>(slots[g]);
+        a.mbox[g] = mboxes[g];
+    }
+    a.m = m;
+    a.world = world;
+    a.timeout_ns = peer_timeout_ns();
+    return CABL_OK;
+}
+
+template <typename T>
+int combine_rows_peer_impl(const T* part, uint64_t m, T* c, void* const* slots,
+                           void* const* mboxes, int world, int rank, void* stream) {
+    PeerRowsArgs<T> a{};
+    if (int rc = rows_peer_fill<T>(a, world, m, slots, mboxes)) return rc;
+    if (rank < 0 || rank >= world) return fail(CABL_EINVAL, "combine_rows_peer: rank must be in [0, world)");
+    if (m == 0) return CABL_OK;
+    if (!part || !c) return fail(CABL_EINVAL, "combine_rows_peer: null pointer");
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    a.part[0] = part;
+    a.c[0] = c;
+    a.rank0 = rank;
+    CABL_TRY_CUDA(combine_rows_peer_launch<T>(a, 1, false, as_stream(stream)), "combine_rows_peer kernel");
+    return CABL_OK;
+}
+
+template <typename T>
+int combine_rows_peer_emulate_impl(int world, const T* const* parts, uint64_t m, T* const* cs,
+                                   void* const* slots, void* const* mboxes, void* stream) {
+    PeerRowsArgs<T> a{};
+    if (int rc = rows_peer_fill<T>(a, world, m, slots, mboxes)) return rc;
+    if (m == 0) return CABL_OK;
+    if (!parts || !cs) return fail(CABL_EINVAL, "combine_rows_peer_emulate: null table");
+    for (int r = 0; r < world; ++r) {
+        if (!parts[r] || !cs[r]) return fail(CABL_EINVAL, "combine_rows_peer_emulate: null pointer");
+        a.part[r] = parts[r];
+        a.c[r] = cs[r];
+    }
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    a.rank0 = 0;
+    CABL_TRY_CUDA(combine_rows_peer_launch<T>(a, world, true, as_stream(stream)),
+                  "combine_rows_peer_emulate kernel");
+    return CABL_OK;
+}
+
 // ------------------------------------- row-major GEMV + fused all-gather
 // Fence between the pushes and the completion words: none at world 1 (no
 // peer reads the buffers), else fence.acq_rel.sys; CABL_GATHER_FENCE=0|1|2
@@ -831,7 +886,7 @@ extern "C" int cabl_describe_device(int device, cabl_gpu_machine* out) {
 extern "C" {
 
 const char* cabl_last_error(void) { return g_err.c_str(); }
-int cabl_abi_version(void) { return 103; } // 1.03: + GEMV with the c all-gather fused (peer memory)
+int cabl_abi_version(void) { return 104; } // 1.04: + rank-ordered row combine over peer memory
 int cabl_device_count(void) {
     int c = 0;
     if (cudaGetDeviceCount(&c) != cudaSuccess) {
@@ -972,6 +1027,24 @@ int cabl_cuda_gemv_rm_gather_emulate_f64(int world, const double* const* As, con
                                          void* const* cfull, void* const* mboxes, void* stream) {
     return gemv_gather_emulate_impl<double>(world, As, ms, n, xs, cs, row_offs, m_total, cfull,
                                             mboxes, stream);
+}
+int cabl_cuda_combine_rows_peer_f32(const float* part, uint64_t m, float* c, void* const* slots,
+                                    void* const* mboxes, int world, int rank, void* stream) {
+    return combine_rows_peer_impl<float>(part, m, c, slots, mboxes, world, rank, stream);
+}
+int cabl_cuda_combine_rows_peer_f64(const double* part, uint64_t m, double* c, void* const* slots,
+                                    void* const* mboxes, int world, int rank, void* stream) {
+    return combine_rows_peer_impl<double>(part, m, c, slots, mboxes, world, rank, stream);
+}
+int cabl_cuda_combine_rows_peer_emulate_f32(int world, const float* const* parts, uint64_t m,
+                                            float* const* cs, void* const* slots,
+                                            void* const* mboxes, void* stream) {
+    return combine_rows_peer_emulate_impl<float>(world, parts, m, cs, slots, mboxes, stream);
+}
+int cabl_cuda_combine_rows_peer_emulate_f64(int world, const double* const* parts, uint64_t m,
+                                            double* const* cs, void* const* slots,
+                                            void* const* mboxes, void* stream) {
+    return combine_rows_peer_emulate_impl<double>(world, parts, m, cs, slots, mboxes, stream);
 }
 int cabl_cuda_combine_partials_f32(const float* p, uint32_t count, float alpha0, float* out,
                                    void* stream) {

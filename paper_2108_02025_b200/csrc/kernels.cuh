@@ -94,6 +94,20 @@ cudaError_t dot_peer_launch(const PeerDotArgs<T>& a, int local_ranks, bool chunk
                             bool cooperative, cudaStream_t s);
 int dot_peer_ctas_per_sm(bool chunked, size_t elem);
 
+// ---- rank-ordered combine of partial c vectors over peer memory (peer.cu) ----
+template <typename T> struct PeerRowsArgs {
+    const T* part[kMaxPeers]; // the rank's partial c (m values)
+    T* c[kMaxPeers];          // the rank's replica of c (c += sum of partials)
+    T* slots[kMaxPeers];      // rank g's slot buffer (2 x kMaxPeers x m), as mapped here
+    void* mbox[kMaxPeers];
+    uint64_t m;
+    int world, rank0;
+    unsigned long long timeout_ns;
+};
+template <typename T>
+cudaError_t combine_rows_peer_launch(const PeerRowsArgs<T>& a, int local_ranks, bool cooperative,
+                                     cudaStream_t s);
+
 // ---- row-major GEMV with the c all-gather fused (peer_gemv.cu) ----
 template <typename T> struct PeerGemvArgs {
     const T* A[kMaxPeers];

@@ -204,6 +204,70 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     peer_finish(total, a, lr, prev_epoch);
 }
 
+// Column-sharded col-major GEMV combine (shard.sharded_gemv_cols without the
+// all-gather): every rank pushes its partial c (m values, from zero) into
+// slot [epoch parity][rank] of every rank's slot buffer, fences, publishes an
+// epoch-tagged mailbox word, waits for every peer's word, and adds the world
+// partials to its replica of c in rank order — bitwise the all-gather +
+// cabl_cuda_combine_rows path, in one single-CTA kernel per rank with no
+// collective call.  Parity double-buffering as for the DOT slots.
+template <typename T>
+__global__ void __launch_bounds__(1024) combine_rows_peer_kernel(const __grid_constant__ PeerRowsArgs<T> a) {
+    pdl_enter();
+    __shared__ unsigned epoch_sh;
+    const int lr = blockIdx.y;
+    const int rank = a.rank0 + lr;
+    const uint64_t m = a.m;
+    PeerMailbox* mine = static_cast<PeerMailbox*>(a.mbox[rank]);
+    if (threadIdx.x == 0)
+        epoch_sh = unsigned(*reinterpret_cast<volatile unsigned long long*>(&mine->epoch) + 1);
+    __syncthreads();
+    const unsigned e = epoch_sh;
+    const int p = e & 1;
+    const T* part = a.part[lr];
+    const uint64_t my_slot = (uint64_t(p) * kMaxPeers + uint64_t(rank)) * m;
+    for (uint64_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const T v = part[i];
+        for (int g = 0; g < a.world; ++g)
+            if (g != rank) a.slots[g][my_slot + i] = v;
+    }
+    if (a.world > 1) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    __syncthreads();
+    if (int(threadIdx.x) < a.world && int(threadIdx.x) != rank) {
+        PeerMailbox* peer = static_cast<PeerMailbox*>(a.mbox[threadIdx.x]);
+        st_relaxed_sys(&peer->word[p][rank][0], (unsigned long long)e << 32);
+    }
+    __shared__ bool ok_sh;
+    if (threadIdx.x == 0) {
+        const unsigned long long t0 = globaltimer();
+        bool ok = true;
+        for (int g = 0; g < a.world && ok; ++g) {
+            if (g == rank) continue;
+            while (unsigned(ld_relaxed_sys(&mine->word[p][g][0]) >> 32) != e) {
+                if (globaltimer() - t0 > a.timeout_ns) {
+                    ok = false;
+                    break;
+                }
+                __nanosleep(64);
+            }
+        }
+        if (a.world > 1) asm volatile("fence.acq_rel.sys;" ::: "memory");
+        ok_sh = ok;
+        if (!ok) mine->fault = e;
+        mine->epoch = e;
+    }
+    __syncthreads();
+    if (!ok_sh) return; // c untouched; the fault is recorded
+    const T* own = a.slots[rank] + uint64_t(p) * kMaxPeers * m;
+    T* c = a.c[lr];
+    for (uint64_t i = threadIdx.x; i < m; i += blockDim.x) {
+        T total = T(0);
+        for (int g = 0; g < a.world; ++g)
+            total = add_rn(total, g == rank ? part[i] : ld_cg(own + uint64_t(g) * m + i));
+        c[i] = add_rn(c[i], total);
+    }
+}
+
 } // namespace
 
 template <typename T>
@@ -253,6 +317,30 @@ int dot_peer_ctas_per_sm(bool chunked, size_t elem) {
     }
     return b;
 }
+
+template <typename T>
+cudaError_t combine_rows_peer_launch(const PeerRowsArgs<T>& a, int local_ranks, bool cooperative,
+                                     cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1, unsigned(local_ranks));
+    cfg.blockDim = dim3(1024);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    if (cooperative) {
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+    } else {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = (cooperative || pdl_enabled()) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, combine_rows_peer_kernel<T>, a);
+}
+template cudaError_t combine_rows_peer_launch<float>(const PeerRowsArgs<float>&, int, bool,
+                                                     cudaStream_t);
+template cudaError_t combine_rows_peer_launch<double>(const PeerRowsArgs<double>&, int, bool,
+                                                      cudaStream_t);
 
 template cudaError_t dot_peer_launch<float>(const PeerDotArgs<float>&, int, bool, bool, bool,
                                             cudaStream_t);

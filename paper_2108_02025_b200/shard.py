@@ -21,6 +21,9 @@ The reference parallelises over CPU threads with contiguous chunks
   communication at all.
 * GEMV col-major by columns (short-wide, e.g. G3) — rank g owns a block of
   columns; partial c vectors are all-gathered and added in rank order.
+* ``sharded_gemv_cols_fused`` — the column-sharded GEMV with its combine as one
+  peer-memory kernel (partials pushed into every rank's slots, rank-ordered
+  sum), no collective call.
 * ``GatherGemv`` — row-block GEMV whose c all-gather runs inside the GEMV
   kernel: every finished row is stored into every rank's (double-buffered)
   gathered c over peer memory (csrc/peer_gemv.cu), no NCCL call.
@@ -365,3 +368,93 @@ class GatherGemv:
             L.cabl_peer_free(C.c_void_p(self.buf))
             L.cabl_peer_mailbox_destroy(C.c_void_p(self.mbox))
         self.buf, self.mapped, self._views = None, {}, None
+
+
+# --------------------------------------------------------------------------
+# Column-sharded col-major GEMV with the combine over peer memory (csrc/peer.cu)
+
+class PeerRows:
+    """Slot buffer (2 x 8 x m values) and mailbox of this rank, and every
+    peer's, mapped here: the tables ``cabl_cuda_combine_rows_peer_*`` takes.
+    Exchange and failure agreement as in ``GatherGemv``."""
+
+    def __init__(self, device: torch.device, m: int, dtype: torch.dtype, group=None, *,
+                 alloc=None, create=None, export=None, import_=None):
+        from . import _lib
+        self._lib = _lib
+        self.device, self.m, self.dtype = device, m, dtype
+        real = alloc is None and import_ is None
+        s = torch.tensor([], dtype=dtype).element_size()
+        alloc = alloc or GatherGemv._alloc
+        create = create or PeerMailboxes._create
+        export = export or PeerMailboxes._export
+        import_ = import_ or PeerMailboxes._import
+        grouped = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if grouped else 1
+        self.rank = dist.get_rank(group) if grouped else 0
+        if self.world > 8:
+            raise ValueError("peer combine: at most 8 ranks (one NVLink domain)")
+        with cabl._on_device(device):
+            self.buf = alloc(2 * 8 * max(m, 1) * s)
+            self.mbox = create()
+            self.mapped: dict[int, tuple[int, int]] = {}
+            if self.world > 1:
+                handles: list = [None] * self.world
+                dist.all_gather_object(handles, (export(self.buf), export(self.mbox)), group=group)
+                err = None
+                try:
+                    for g, (hb, hm) in enumerate(handles):
+                        if g != self.rank:
+                            self.mapped[g] = (import_(hb), import_(hm))
+                except Exception as e:  # noqa: BLE001 - reported collectively below
+                    err = e
+                flag = torch.tensor([0 if err else 1], dtype=torch.int32,
+                                    device=device if device.type == "cuda" else "cpu")
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+                if int(flag.item()) == 0:
+                    if real:
+                        self.close()
+                    raise RuntimeError(f"peer slot exchange failed on at least one rank"
+                                       f"{': ' + str(err) if err else ''}")
+        self.slot_table = (C.c_void_p * self.world)(
+            *[self.buf if g == self.rank else self.mapped[g][0] for g in range(self.world)])
+        self.mbox_table = (C.c_void_p * self.world)(
+            *[self.mbox if g == self.rank else self.mapped[g][1] for g in range(self.world)])
+
+    def state(self) -> tuple[int, int]:
+        e, f = C.c_uint64(), C.c_uint64()
+        with cabl._on_device(self.device):
+            self._lib.call("cabl_peer_mailbox_state", C.c_void_p(self.mbox), C.byref(e), C.byref(f))
+        return e.value, f.value
+
+    def close(self) -> None:
+        if getattr(self, "buf", None) is None:
+            return
+        L = self._lib.lib()
+        with cabl._on_device(self.device):
+            for pb, pm in self.mapped.values():  # return codes ignored on teardown
+                L.cabl_peer_mailbox_unmap(C.c_void_p(pb))
+                L.cabl_peer_mailbox_unmap(C.c_void_p(pm))
+            L.cabl_peer_free(C.c_void_p(self.buf))
+            L.cabl_peer_mailbox_destroy(C.c_void_p(self.mbox))
+        self.buf, self.mapped = None, {}
+
+
+def sharded_gemv_cols_fused(A_local: "cabl.DenseMatrix", x_local: torch.Tensor, c: torch.Tensor,
+                            policy: "cabl.ExecPolicy", peers: PeerRows) -> torch.Tensor:
+    """``sharded_gemv_cols`` with the all-gather + rank-ordered combine replaced by
+    one peer-memory kernel (``cabl_cuda_combine_rows_peer_*``): bitwise the same
+    c on every rank, no collective call.  Collective over ``peers``' group."""
+    from . import _lib
+    cabl._require(A_local.layout() == cabl.Layout.ColMajor,
+                  "sharded_gemv_cols: A must be col-major (its column blocks are contiguous)")
+    m = c.numel()
+    cabl._require(m == peers.m, "sharded_gemv_cols_fused: c length differs from the slot size")
+    part = torch.zeros(m, dtype=c.dtype, device=c.device)
+    cabl.gemv_col_major(A_local, x_local, part, policy)
+    sfx = cabl._suffix(c)
+    with cabl._on_device(c.device):
+        _lib.call(f"cabl_cuda_combine_rows_peer_{sfx}", part.data_ptr(), m, c.data_ptr(),
+                  peers.slot_table, peers.mbox_table, peers.world, peers.rank,
+                  cabl._stream_of(c))
+    return c

@@ -310,3 +310,86 @@ def test_sharded_dot_fused_under_nccl_world1(cuda):
     r = subprocess.run([sys.executable, "-c", NCCL_SCRIPT % {"root": str(ROOT)}], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-3000:]
+
+
+# ---------------------------------------------------------------------------
+# Column-sharded GEMV combine over peer memory (cabl_cuda_combine_rows_peer_*)
+
+def _unfused_rows(parts, c0):
+    """The all-gather + cabl_cuda_combine_rows arithmetic on one device."""
+    L = _lib()
+    sfx = "f32" if c0.dtype == torch.float32 else "f64"
+    c = c0.clone()
+    stacked = torch.stack(parts).reshape(-1).contiguous()
+    L.call(f"cabl_cuda_combine_rows_{sfx}", stacked.data_ptr(), len(parts), c.numel(),
+           c.data_ptr(), _stream())
+    return c
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("world,m", [(1, 256), (2, 256), (3, 1000), (8, 4097), (5, 1)])
+def test_emulated_row_combine_equals_unfused_bitwise(cuda, dtype, world, m):
+    import paper_2108_02025_b200 as cb
+    L = _lib()
+    sfx = "f32" if dtype == torch.float32 else "f64"
+    s = torch.tensor([], dtype=dtype).element_size()
+    parts = [cb.fill_uniform(torch.empty(m, dtype=dtype, device="cuda"), 3, 10 + r)
+             for r in range(world)]
+    c0 = cb.fill_uniform(torch.empty(m, dtype=dtype, device="cuda"), 3, 9)
+    bufs = []
+    for _ in range(world):
+        p = C.c_void_p()
+        L.call("cabl_peer_alloc", 2 * 8 * m * s, C.byref(p))
+        bufs.append(p.value)
+    mb = _mailboxes(world)
+    cs = [c0.clone() for _ in range(world)]
+    want = c0.clone()
+    P = C.c_void_p * world
+    try:
+        for call in range(3):
+            L.call(f"cabl_cuda_combine_rows_peer_emulate_{sfx}", world,
+                   P(*[t.data_ptr() for t in parts]), m, P(*[t.data_ptr() for t in cs]),
+                   P(*bufs), P(*mb), _stream())
+            want = _unfused_rows(parts, want)
+            torch.cuda.synchronize()
+            for r in range(world):
+                assert torch.equal(cs[r], want), (call, r)
+        for p in mb:
+            assert _state(p) == (3, 0)
+    finally:
+        for p in bufs:
+            L.lib().cabl_peer_free(C.c_void_p(p))
+        _destroy(mb)
+
+
+COLS_SCRIPT = r"""
+import sys, torch, torch.distributed as dist
+sys.path.insert(0, %(root)r)
+import paper_2108_02025_b200 as cb
+from paper_2108_02025_b200 import shard
+dev = torch.device('cuda:0'); torch.cuda.set_device(dev)
+dist.init_process_group('nccl', rank=0, world_size=1, device_id=dev)
+pol = cb.default_policy(1)
+m, n = 256, 300_007
+f = lambda k, st: cb.fill_uniform(torch.empty(k, dtype=torch.float64, device=dev), 6, st)
+A = cb.DenseMatrix.wrap(f(m * n, 3), m, n, cb.Layout.ColMajor)
+x, c = f(n, 1), f(m, 4)
+c2 = c.clone()
+peers = shard.PeerRows(dev, m, torch.float64)
+for _ in range(3):
+    shard.sharded_gemv_cols_fused(A, x, c, pol, peers)
+    shard.sharded_gemv_cols(A, x, c2, pol)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c2)
+assert peers.state() == (3, 0)
+peers.close()
+dist.destroy_process_group()
+print('ok')
+"""
+
+
+def test_sharded_gemv_cols_fused_under_nccl_world1(cuda):
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29565")
+    r = subprocess.run([sys.executable, "-c", COLS_SCRIPT % {"root": str(ROOT)}], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-3000:]

@@ -134,6 +134,12 @@ def _worker(rank, world, port, results):
                               import_=lambda h: 10000 + int(h.rstrip(b"\0")[1:]))
         results[f"gg_{rank}"] = ([gg.cfull_table[g] for g in range(world)],
                                  [gg.mbox_table[g] for g in range(world)])
+        pr = shard.PeerRows(torch.device("cpu"), 64, torch.float64,
+                            alloc=lambda nb: 7000 + rank, create=lambda: 8000 + rank,
+                            export=lambda p: f"h{p}".encode().ljust(64, b"\0"),
+                            import_=lambda h: 10000 + int(h.rstrip(b"\0")[1:]))
+        results[f"pr_{rank}"] = ([pr.slot_table[g] for g in range(world)],
+                                 [pr.mbox_table[g] for g in range(world)])
         # an import failure on one rank is reported on every rank (no rank may
         # go on to spin on a peer that never arrives)
         def bad_import(h):
@@ -221,6 +227,9 @@ def test_sharded_paths_over_gloo(world):
         bufs, mbs = results[f"gg_{r}"]
         assert bufs == [5000 + r if g == r else 15000 + g for g in range(world)]
         assert mbs == [6000 + r if g == r else 16000 + g for g in range(world)]
+        slots, mbs = results[f"pr_{r}"]
+        assert slots == [7000 + r if g == r else 17000 + g for g in range(world)]
+        assert mbs == [8000 + r if g == r else 18000 + g for g in range(world)]
 
 
 def test_partition_is_balanced_and_contiguous():
