@@ -12,6 +12,8 @@
 //         result is independent of NCCL's algorithm and identical everywhere.
 //   GEMV  row blocks of A and c, x replicated, no exchange needed.
 //   GER   row blocks of C and x, y replicated, no exchange at all.
+//   sharded_gemv_cols_fused: the column-block partials combined by one
+//         peer-memory kernel per device instead of all-gather + combine_rows.
 //   sharded_gemv_rows_gather_fused: the c all-gather inside the GEMV kernel —
 //         rows stored into every device's double-buffered gathered c over P2P.
 //   sharded_dot_fused: DOT with the exchange inside the kernel — every device
@@ -127,7 +129,35 @@ public:
         return gather_;
     }
 
+    // Slot buffers (2 x 8 x m values each, one per device) and mailboxes for
+    // the peer-memory row combine; reallocated when the size changes.
+    Gather& rows(std::size_t bytes_slots) {
+        if (rows_.bytes_half != bytes_slots) {
+            free_set(rows_);
+            enable_peer_access();
+            for (int r = 0; r < size(); ++r) {
+                detail::cuda_check(cudaSetDevice(devs_[r]), "cudaSetDevice");
+                void* b = nullptr;
+                void* mb = nullptr;
+                detail::check(cabl_peer_alloc(bytes_slots, &b));
+                detail::check(cabl_peer_mailbox_create(&mb));
+                rows_.bufs.push_back(b);
+                rows_.mboxes.push_back(mb);
+            }
+            rows_.bytes_half = bytes_slots;
+        }
+        return rows_;
+    }
+
 private:
+    void free_set(Gather& st) {
+        for (std::size_t i = 0; i < st.bufs.size(); ++i) {
+            cudaSetDevice(devs_[i]);
+            cabl_peer_free(st.bufs[i]);
+            cabl_peer_mailbox_destroy(st.mboxes[i]);
+        }
+        st = Gather{};
+    }
     void enable_peer_access() {
         if (peer_enabled_) return;
         const int G = size();
@@ -147,19 +177,15 @@ private:
         peer_enabled_ = true;
     }
     void free_gather() {
-        for (std::size_t i = 0; i < gather_.bufs.size(); ++i) {
-            cudaSetDevice(devs_[i]);
-            cabl_peer_free(gather_.bufs[i]);
-            cabl_peer_mailbox_destroy(gather_.mboxes[i]);
-        }
-        gather_ = Gather{};
+        free_set(gather_);
+        free_set(rows_);
     }
 
     std::vector<int> devs_;
     std::vector<ncclComm_t> comms_;
     std::vector<cudaStream_t> streams_;
     std::vector<void*> mboxes_;
-    Gather gather_;
+    Gather gather_, rows_;
     bool peer_enabled_ = false;
 };
 
@@ -197,6 +223,14 @@ inline int gemv_gather(const double* A, std::uint64_t m, std::uint64_t n, const 
                        double* c, std::uint64_t off, std::uint64_t mt, void* const* b,
                        void* const* mb, int G, int r, cudaStream_t s) {
     return cabl_cuda_gemv_rm_gather_f64(A, m, n, x, c, off, mt, b, mb, G, r, nullptr, s);
+}
+inline int rows_peer(const float* p, std::uint64_t m, float* c, void* const* b, void* const* mb,
+                     int G, int r, cudaStream_t s) {
+    return cabl_cuda_combine_rows_peer_f32(p, m, c, b, mb, G, r, s);
+}
+inline int rows_peer(const double* p, std::uint64_t m, double* c, void* const* b,
+                     void* const* mb, int G, int r, cudaStream_t s) {
+    return cabl_cuda_combine_rows_peer_f64(p, m, c, b, mb, G, r, s);
 }
 } // namespace detail
 
@@ -379,6 +413,31 @@ void sharded_gemv_cols(Group& g, const std::vector<const DeviceMatrix<T>*>& A,
         cabl::detail::cuda_check(cudaSetDevice(g.device(r)), "cudaSetDevice");
         cabl::detail::check(detail::combine_rows(gathered[r].data(), std::uint32_t(G), m,
                                                  c[r]->data(), g.stream(r)));
+    }
+    g.synchronize();
+}
+
+// sharded_gemv_cols with the all-gather + combine replaced by one peer-memory
+// kernel per device (cabl_cuda_combine_rows_peer_*): same bits, no NCCL call.
+template <typename T>
+void sharded_gemv_cols_fused(Group& g, const std::vector<const DeviceMatrix<T>*>& A,
+                             const std::vector<const DeviceVector<T>*>& x,
+                             const std::vector<DeviceVector<T>*>& c, const ExecPolicy& policy) {
+    const int G = g.size();
+    const std::size_t m = c[0]->len();
+    Group::Gather& st = g.rows(2 * 8 * (m ? m : 1) * sizeof(T));
+    std::vector<DeviceVector<T>> part;
+    for (int r = 0; r < G; ++r) {
+        cabl::detail::require(A[r]->layout() == Layout::ColMajor && A[r]->rows() == m &&
+                                  c[r]->len() == m,
+                              "sharded_gemv_cols: col-major blocks of m rows, c replicas of length m");
+        cabl::detail::cuda_check(cudaSetDevice(g.device(r)), "cudaSetDevice");
+        part.emplace_back(m);
+        cabl::detail::cuda_check(cudaMemsetAsync(part[r].data(), 0, m * sizeof(T), g.stream(r)),
+                                 "memset");
+        gemv_col_major(*A[r], *x[r], part[r], policy, g.stream(r));
+        cabl::detail::check(detail::rows_peer(part[r].data(), m, c[r]->data(), st.bufs.data(),
+                                              st.mboxes.data(), G, r, g.stream(r)));
     }
     g.synchronize();
 }

@@ -235,6 +235,17 @@ int main() {
             ok &= cols_ok;
             std::printf("rank %d: gemv by columns %s\n", r, cols_ok ? "ok" : "MISMATCH");
         }
+        // again with the combine over peer memory: every replica gets the same
+        // rank-ordered sum once more (want += total, in the same order)
+        for (std::size_t i = 0; i < mc; ++i) want[i] = want[i] + total[i];
+        nccl::sharded_gemv_cols_fused(g, Acp, xcp, ccp, pol);
+        for (int r = 0; r < G; ++r) {
+            cudaSetDevice(g.device(r));
+            const bool cols_ok = ccb[r].download() == want;
+            ok &= cols_ok;
+            std::printf("rank %d: gemv by columns, combine over peer memory %s\n", r,
+                        cols_ok ? "ok" : "MISMATCH");
+        }
     }
     return ok ? 0 : 1;
 }

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_peer.py -q -x --timeout 600 -p no:cacheprovider > gpurun_out/pytest_peer.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_peer.log
+./tests/cpp/mgpu_example > gpurun_out/mgpu_example.log 2>&1; echo "rc=$?" >> gpurun_out/mgpu_example.log
