@@ -44,6 +44,12 @@ def main():
 
         class w:  # noqa: N801
             id = "R1x"
+    elif args.config == "G1g":  # G1 through the gathering GEMV at world 1 (gemv_rm_gather_kernel)
+        from paper_2108_02025_b200 import shard
+        w = WL.WORKLOADS["G1"]
+        ins = bench.make_inputs(w, (0, w.m), dev)
+        gg = shard.GatherGemv(dev, w.m, w.dtype)
+        fn = lambda: gg(ins["A"], ins["x"], ins["c"], 0)  # noqa: E731
     else:
         # D1f: D1 through the fused peer-memory DOT at world 1 (dot_peer_kernel)
         fused = args.config == "D1f"

@@ -85,7 +85,7 @@ def main():
         rd, wr = num(d, "dram__bytes_read.sum"), num(d, "dram__bytes_write.sum")
         if cfg == "R1x":  # GER fp32 8192 x 8193 (tools/ncu_runner.py)
             alg = (2 * 8192 * 8193 + 8192 + 8193) * 4
-        else:  # D1f: D1 through the fused peer DOT
+        else:  # D1f / G1g: D1 / G1 through the fused peer-memory paths
             alg = WL.WORKLOADS[cfg[:2]].alg_bytes(1)
         el = num(d, "sm__cycles_elapsed.max")
         act = [num(d, f"sm__cycles_active.{s}") / el for s in ("min", "avg", "max")]
