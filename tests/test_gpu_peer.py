@@ -393,3 +393,24 @@ def test_sharded_gemv_cols_fused_under_nccl_world1(cuda):
     r = subprocess.run([sys.executable, "-c", COLS_SCRIPT % {"root": str(ROOT)}], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-3000:]
+
+
+def test_emulated_protocol_stress(cuda):
+    """Many back-to-back collective calls on reused mailboxes, 8 emulated
+    ranks with uneven shards (ranks finish at different times): every call's
+    result on every rank equals the unfused path, no fault, epochs in step."""
+    xs, ys = _shards([40_000, 3, 70_000, 0, 12_345, 65_536, 1, 50_000], torch.float32, 17)
+    want = unfused(xs, ys, -0.5, 8192)
+    mb = _mailboxes(8)
+    try:
+        outs_all = []
+        for _ in range(200):
+            outs_all.append(emulate(xs, ys, -0.5, mb, 8192))
+        torch.cuda.synchronize()
+        for k, outs in enumerate(outs_all):
+            for r, o in enumerate(outs):
+                assert torch.equal(o, want), (k, r)
+        for p in mb:
+            assert _state(p) == (200, 0)
+    finally:
+        _destroy(mb)
