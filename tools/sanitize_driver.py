@@ -8,8 +8,10 @@ Paths: DOT small / main / chunked (forced) / unaligned; GEMV row-major
 (with CABL_GEMV_RM_ORDER=reference also the reference-order kernel)
 ordered / segment / sweep (static and queue) / scalar; col-major ordered /
 tall vec (static and queue) / tall scalar / 2-D split vec / 2-D split scalar /
-bulk-copy split; GER tile queue / static / generic; the fills and the
-partial combine.  Exits non-zero if any result is non-finite.
+bulk-copy split / realigning split; GER tile queue / static / generic /
+flat any-width / one-element rows; row-major few long rows; the peer-memory
+DOT, gathering GEMV and row combine at world 1; the fills and the partial
+combine.  Exits non-zero if any result is non-finite.
 """
 from __future__ import annotations
 
@@ -58,6 +60,51 @@ def main():
                 C = cb.DenseMatrix.wrap(f(m * n, dt, 5), m, n, lay)
                 cb.ger(f(m, dt, 1), f(n, dt, 2), C, pol)
                 ok &= bool(torch.isfinite(C.data).all())
+        # this round's paths: few long rows (chunked RM), realigning CM split
+        # (odd m and an offset A), flat any-width GER, one-element-row GER
+        for m, n, lay, off in ((3, 300_000, cb.Layout.RowMajor, 0), (1, 1 << 18, cb.Layout.RowMajor, 0),
+                               (8193, 300, cb.Layout.ColMajor, 0), (4096, 100, cb.Layout.ColMajor, 1),
+                               (1025, 777, cb.Layout.ColMajor, 3)):
+            A = cb.DenseMatrix.wrap(f(m * n + off, dt, 3)[off:], m, n, lay)
+            c = f(m, dt, 4)
+            (cb.gemv_row_major if lay == cb.Layout.RowMajor else cb.gemv_col_major)(A, f(n, dt, 1), c, pol)
+            ok &= bool(torch.isfinite(c).all())
+        for m, n, off in ((777, 1001, 0), (1000, 4096, 1), (400_003, 1, 0), (1, 400_003, 1)):
+            for lay in (cb.Layout.RowMajor, cb.Layout.ColMajor):
+                C = cb.DenseMatrix.wrap(f(m * n + off, dt, 5)[off:], m, n, lay)
+                cb.ger(f(m + off, dt, 1)[off:], f(n + off, dt, 2)[off:], C, pol)
+                ok &= bool(torch.isfinite(C.data).all())
+        # peer-memory paths at world 1 (DOT, gathering GEMV, row combine)
+        import ctypes as C_
+        sfx = "f32" if dt == torch.float32 else "f64"
+        s = torch.tensor([], dtype=dt).element_size()
+        mb, buf, slots = C_.c_void_p(), C_.c_void_p(), C_.c_void_p()
+        _lib.call("cabl_peer_mailbox_create", C_.byref(mb))
+        x, y = f(100_003, dt, 1), f(100_003, dt, 2)
+        out = torch.empty(1, dtype=dt, device=dev)
+        _lib.call(f"cabl_cuda_dot_peer_{sfx}", x.data_ptr(), y.data_ptr(), 100_003, 0.5,
+                  out.data_ptr(), (C_.c_void_p * 1)(mb.value), 1, 0, 8192, None, None)
+        ok &= bool(torch.isfinite(out).all())
+        m, n = 3000, 16384 if dt == torch.float32 else 8192
+        gmb = C_.c_void_p()
+        _lib.call("cabl_peer_mailbox_create", C_.byref(gmb))
+        _lib.call("cabl_peer_alloc", 2 * m * s, C_.byref(buf))
+        A, xv, c = f(m * n, dt, 3), f(n, dt, 1), f(m, dt, 4)
+        _lib.call(f"cabl_cuda_gemv_rm_gather_{sfx}", A.data_ptr(), m, n, xv.data_ptr(), c.data_ptr(),
+                  0, m, (C_.c_void_p * 1)(buf.value), (C_.c_void_p * 1)(gmb.value), 1, 0, None, None)
+        ok &= bool(torch.isfinite(c).all())
+        rmb = C_.c_void_p()
+        _lib.call("cabl_peer_mailbox_create", C_.byref(rmb))
+        _lib.call("cabl_peer_alloc", 2 * 8 * 256 * s, C_.byref(slots))
+        part, cc = f(256, dt, 6), f(256, dt, 7)
+        _lib.call(f"cabl_cuda_combine_rows_peer_{sfx}", part.data_ptr(), 256, cc.data_ptr(),
+                  (C_.c_void_p * 1)(slots.value), (C_.c_void_p * 1)(rmb.value), 1, 0, None)
+        ok &= bool(torch.isfinite(cc).all())
+        torch.cuda.synchronize()
+        for p_ in (mb, gmb, rmb):
+            _lib.call("cabl_peer_mailbox_destroy", p_)
+        for p_ in (buf, slots):
+            _lib.call("cabl_peer_free", p_)
         # rank-ordered combine
         p = f(8, dt, 9)
         out = torch.empty(1, dtype=dt, device=dev)
