@@ -142,3 +142,30 @@ def test_product_never_touches_the_oracle():
     syms = subprocess.run(["nm", "-D", "--defined-only", str(pkg / "libcabl_cuda.so")],
                           capture_output=True, text=True).stdout
     assert "dot_ref" not in syms and "gemv_ref" not in syms and "ger_ref" not in syms
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_peer_entry_points_without_a_gpu():
+    """The peer-memory entry points validate their arguments the reference way
+    (EINVAL + message) and otherwise fail loudly without a device (ECUDA)."""
+    from paper_2108_02025_b200 import _lib
+    L = _lib.lib()
+    p = C.c_void_p()
+    assert L.cabl_peer_mailbox_create(C.byref(p)) == _lib.CABL_ECUDA
+    assert L.cabl_peer_alloc(1024, C.byref(p)) == _lib.CABL_ECUDA
+    x = np.ones(16, np.float32)
+    fake = (C.c_void_p * 2)(x.ctypes.data, x.ctypes.data)
+    rc = L.cabl_cuda_dot_peer_f32(x.ctypes.data, x.ctypes.data, 16, C.c_float(0), x.ctypes.data,
+                                  fake, 9, 0, 8192, None, None)
+    assert rc == _lib.CABL_EINVAL and "world" in L.cabl_last_error().decode()
+    rc = L.cabl_cuda_dot_peer_f32(x.ctypes.data, x.ctypes.data, 16, C.c_float(0), x.ctypes.data,
+                                  fake, 2, 0, 8192, None, None)
+    assert rc == _lib.CABL_ECUDA
+    rc = L.cabl_cuda_gemv_rm_gather_f32(x.ctypes.data, 4, 4, x.ctypes.data, x.ctypes.data, 0, 4,
+                                        fake, fake, 2, 0, None, None)
+    assert rc == _lib.CABL_ECUDA
+    rc = L.cabl_cuda_combine_rows_peer_f32(x.ctypes.data, 4, x.ctypes.data, fake, fake, 2, 5, None)
+    assert rc == _lib.CABL_EINVAL and "rank" in L.cabl_last_error().decode()
+    rc = L.cabl_cuda_combine_rows_peer_f32(x.ctypes.data, 4, x.ctypes.data, fake, fake, 2, 1, None)
+    assert rc == _lib.CABL_ECUDA
+    assert x[0] == 1.0  # nothing was written
