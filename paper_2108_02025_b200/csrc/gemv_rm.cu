@@ -459,6 +459,10 @@ inline bool rm_few_rows(uint64_t m, uint64_t n, size_t elem) {
 
 // -1 scalar, 0 segment-balanced warps, 1 sweep for short rows, 2 sweep for
 // long rows, 9 chunked few rows.  CABL_GEMV_RM_MODE overrides (tuning / tests only).
+// Row groups from which the sweeps run (see rm_mode).
+constexpr uint64_t kRmShortMinGroups = 256; // 4-row groups: m >= 1021
+constexpr uint64_t kRmLongMinGroups = 128;  // 2-row groups: m >= 255
+
 template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n) {
     const bool vec = rm_vec_ok(A, x, n);
     static const int forced = [] {
@@ -483,10 +487,20 @@ template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n
     // per thread at 2 CTAs/SM for rows of <= 2 CTA passes, 2 rows x 8 vectors
     // at 1 CTA/SM for long rows.  The sweep must see >= 6 row groups per CTA
     // to keep the single wave balanced; otherwise the segment kernel.
+    // Few groups per CTA still beat the unit kernel (256 MiB fp32, flushed,
+    // tools/rm_mid.py): 2048 x 8192 22.5 -> 16.4 us at 1.7 groups per CTA,
+    // 512 x 131072 49.2 -> 44.1 us at 0.9 (CABL_RM_FEW_GROUPS=0: the old
+    // >= 6 groups per CTA rule, tuning only).
     const uint64_t sms = uint64_t(sm_count());
     const bool short_rows = n / Vec<T>::N <= uint64_t(kRmBlock) * 2 * 2;
-    if (short_rows && (m + 3) / 4 >= 6 * 2 * sms) return 1;
-    if (!short_rows && (m + 1) / 2 >= 6 * 1 * sms) return 2;
+    static const bool few = [] {
+        const char* e = getenv("CABL_RM_FEW_GROUPS");
+        return e ? atoi(e) != 0 : true;
+    }();
+    const uint64_t short_min = few ? kRmShortMinGroups : 6 * 2 * sms;
+    const uint64_t long_min = few ? kRmLongMinGroups : 6 * 1 * sms;
+    if (short_rows && (m + 3) / 4 >= short_min) return 1;
+    if (!short_rows && (m + 1) / 2 >= long_min) return 2;
     return 0;
 }
 
@@ -569,15 +583,20 @@ template <typename T> SweepCfg sweep_choice(uint64_t m, uint64_t n, int mode) {
         if (const char* e = getenv("CABL_RM_SWEEP")) sscanf(e, "%d,%d,%d", &f.R, &f.KV, &f.minb);
         return f;
     }();
-    const SweepCfg table[] = {{2, 4, 2}, {2, 8, 1}, {4, 1, 4}, {4, 2, 2}, {4, 4, 1}, {8, 1, 2}, {8, 2, 1}};
+    const SweepCfg table[] = {{2, 4, 2}, {2, 8, 1}, {4, 1, 4}, {4, 2, 2}, {4, 4, 1}, {8, 1, 2}, {8, 2, 1},
+                              {1, 8, 2}, {1, 16, 1}, {2, 4, 1}};
     for (const SweepCfg& t : table)
         if (forced.R == t.R && forced.KV == t.KV && forced.minb == t.minb) return t;
+    // long rows below the queue threshold: 2 rows x 4 vectors at 2 CTAs/SM
+    // (256 MiB fp32: 512 x 131072 / 2048 x 32768 / 4096 x 16384 44.1 / 45.1 /
+    // 45.1 us against 47.1-49.2 for 2 x 8 at 1 CTA/SM); above it (G4) 2 x 8.
+    const bool big = m * n * sizeof(T) >= queue_threshold_bytes();
+    const SweepCfg base = mode == 1 ? SweepCfg{4, 2, 2} : (big ? SweepCfg{2, 8, 1} : SweepCfg{2, 4, 2});
     const uint64_t nvec = n / Vec<T>::N;
-    const uint64_t pass = uint64_t(kRmBlock) * (mode == 1 ? 2 : 8);
+    const uint64_t pass = uint64_t(kRmBlock) * base.KV;
     const uint64_t used = (nvec + pass - 1) / pass * pass;
     if (used * 4 > nvec * 5 && (m + 7) / 8 >= uint64_t(sm_count()) * 2) return SweepCfg{8, 1, 2};
-    if (mode == 1) return SweepCfg{4, 2, 2}; // rows <= 2 passes
-    return SweepCfg{2, 8, 1};                // long rows
+    return base;
 }
 
 template <typename T>
@@ -594,6 +613,9 @@ unsigned sweep_launch(const T* A, const T* x, T* c, uint64_t m, uint64_t n, int 
     CABL_SWEEP_CASE(4, 4, 1)
     CABL_SWEEP_CASE(8, 1, 2)
     CABL_SWEEP_CASE(8, 2, 1)
+    CABL_SWEEP_CASE(1, 8, 2)
+    CABL_SWEEP_CASE(1, 16, 1)
+    CABL_SWEEP_CASE(2, 4, 1)
 #undef CABL_SWEEP_CASE
     return sweep_go<T, 2, 8, 1>(A, x, c, m, n, counter, s);
 }

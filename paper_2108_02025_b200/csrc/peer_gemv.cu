@@ -150,7 +150,7 @@ template <typename T, int R, int KV, int MINB> int occupancy() {
 
 // The sweep shapes gemv_rm_launch uses by default (gemv_rm.cu sweep_choice);
 // a CABL_RM_SWEEP tuning entry outside them is rejected by the caller.
-#define CABL_GATHER_SHAPES(X) X(4, 2, 2) X(2, 8, 1) X(8, 1, 2)
+#define CABL_GATHER_SHAPES(X) X(4, 2, 2) X(2, 8, 1) X(2, 4, 2) X(8, 1, 2)
 
 template <typename T>
 cudaError_t gemv_rm_gather_launch(const PeerGemvArgs<T>& a, int local_ranks, int R, int KV,

@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_bounds.py -q -x -k "col_major or gemv_guard" --timeout 600 -p no:cacheprovider > gpurun_out/pytest_cm.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_cm.log
-python tools/cm_realign.py > gpurun_out/cm_realign_after.jsonl 2>&1
+python tools/rm_mid.py > gpurun_out/rm_mid_new.jsonl 2>&1
+CABL_RM_FEW_GROUPS=0 python tools/rm_mid.py > gpurun_out/rm_mid_old.jsonl 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+python tools/b2b.py G1 G4 > gpurun_out/b2b_g.jsonl 2>&1
