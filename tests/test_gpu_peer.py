@@ -414,3 +414,25 @@ def test_emulated_protocol_stress(cuda):
             assert _state(p) == (200, 0)
     finally:
         _destroy(mb)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_emulated_dots(cuda, seed):
+    """Random world sizes, shard lengths (incl. empty and tiny), dtypes, alpha0."""
+    rng = np.random.default_rng(100 + seed)
+    world = int(rng.integers(1, 9))
+    dtype = torch.float32 if rng.integers(0, 2) == 0 else torch.float64
+    # shards small enough that every rank's grid fits one co-resident wave
+    shards = [int(rng.choice([0, rng.integers(1, 50), rng.integers(50, 20_000),
+                              rng.integers(20_000, 60_000)])) for _ in range(world)]
+    alpha = float(rng.uniform(-2, 2))
+    xs, ys = _shards(shards, dtype, 40 + seed, int(rng.choice([0, 0, 2])))
+    want = unfused(xs, ys, alpha, 8192)
+    mb = _mailboxes(world)
+    try:
+        for _ in range(3):
+            outs = emulate(xs, ys, alpha, mb, 8192)
+            torch.cuda.synchronize()
+            assert all(torch.equal(o, want) for o in outs), (seed, shards)
+    finally:
+        _destroy(mb)

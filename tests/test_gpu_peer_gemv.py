@@ -201,3 +201,45 @@ def test_gather_gemv_under_nccl_world1(cuda):
     r = subprocess.run([sys.executable, "-c", NCCL_SCRIPT % {"root": str(ROOT)}], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_emulated_gathers(cuda, seed):
+    """Random world sizes, ragged slices, dtypes and offsets into the gathered
+    buffer: every rank's half equals the concatenation of the plain slices."""
+    import numpy as np
+    L = _lib()
+    rng = np.random.default_rng(seed)
+    world = int(rng.integers(1, 9))
+    dtype = torch.float32 if rng.integers(0, 2) == 0 else torch.float64
+    n = 9216 if dtype == torch.float32 else 4608  # long rows (> 1024 vectors)
+    ms = [int(v) for v in rng.integers(300, 1500, size=world)]
+    m_total = sum(ms)
+    offs = [sum(ms[:r]) for r in range(world)]
+    A, x, c0 = _inputs(m_total, n, dtype, seed)
+    s = torch.tensor([], dtype=dtype).element_size()
+    sfx = "f32" if dtype == torch.float32 else "f64"
+    bufs = [_alloc(2 * m_total * s) for _ in range(world)]
+    mbs = [_mbox() for _ in range(world)]
+    cs = [c0[o:o + m].clone() for o, m in zip(offs, ms)]
+    want = [c0[o:o + m].clone() for o, m in zip(offs, ms)]
+    P = C.c_void_p * world
+    try:
+        for call in range(1, 3):
+            L.call(f"cabl_cuda_gemv_rm_gather_emulate_{sfx}", world,
+                   P(*[A[o * n:(o + m) * n].data_ptr() for o, m in zip(offs, ms)]),
+                   (C.c_uint64 * world)(*ms), n, P(*[x.data_ptr()] * world),
+                   P(*[t.data_ptr() for t in cs]), (C.c_uint64 * world)(*offs), m_total,
+                   P(*bufs), P(*mbs), _stream())
+            for r, (o, m) in enumerate(zip(offs, ms)):
+                _plain(A[o * n:(o + m) * n], x, want[r], n)
+            torch.cuda.synchronize()
+            full = torch.cat(want)
+            for r in range(world):
+                assert torch.equal(cs[r], want[r]), (seed, call, r)
+                assert torch.equal(_view(bufs[r] + (call & 1) * m_total * s, m_total, dtype), full)
+    finally:
+        for p in bufs:
+            L.lib().cabl_peer_free(C.c_void_p(p))
+        for p in mbs:
+            L.lib().cabl_peer_mailbox_destroy(C.c_void_p(p))
