@@ -325,6 +325,38 @@ __global__ void __launch_bounds__(kRmBlock)
     }
 }
 
+// Long scalar rows, few of them (odd n or unaligned operands; fewer rows than
+// the G-lanes kernel needs to keep the SMs' memory pipes full): one CTA per
+// row, all kRmBlock threads on the row — thread t chains j = t, t + BLOCK, ...
+// with kScalarU loads in flight, then a fixed-order block sum.  (2400 x 27961
+// fp32 on one warp per row kept ~32 KB per SM in flight: 113 us.)
+template <typename T>
+__global__ void __launch_bounds__(kRmBlock)
+    gemv_rm_scalar_cta_kernel(const T* __restrict__ A, const T* __restrict__ x,
+                              T* __restrict__ c, uint64_t m, uint64_t n) {
+    pdl_enter();
+    __shared__ T red[32];
+    constexpr int kScalarU = 16;
+    for (uint64_t i = blockIdx.x; i < m; i += gridDim.x) {
+        const T* row = A + i * n;
+        T acc = T(0);
+        uint64_t j = threadIdx.x;
+        for (; j + uint64_t(kScalarU - 1) * kRmBlock < n; j += uint64_t(kScalarU) * kRmBlock) {
+            T a[kScalarU], b[kScalarU];
+#pragma unroll
+            for (int u = 0; u < kScalarU; ++u) {
+                a[u] = __ldcs(row + j + u * kRmBlock);
+                b[u] = __ldg(x + j + u * kRmBlock);
+            }
+#pragma unroll
+            for (int u = 0; u < kScalarU; ++u) acc = fma_rn(a[u], b[u], acc);
+        }
+        for (; j < n; j += kRmBlock) acc = fma_rn(row[j], x[j], acc);
+        const T total = block_sum(acc, red);
+        if (threadIdx.x == 0) c[i] = add_rn(c[i], total);
+    }
+}
+
 // Short rows (n*s <= rm_lane_max_bytes() = 256 B, e.g. 2^20 x 64): one THREAD per
 // row, in the reference's order and rounding — acc = c_i, then for j
 // ascending a separately rounded multiply and add (an FMA for the trailing
@@ -629,6 +661,18 @@ unsigned sweep_launch(const T* A, const T* x, T* c, uint64_t m, uint64_t n, int 
 // n = 63 166.8 / 79.9 before the 4..16-lane groups existed).
 constexpr uint64_t kLaneScalarMaxN = 24;
 
+// Scalar rows long enough for a CTA each (>= 16 loads per thread) and too few
+// for one warp per row to keep 4+ warps' loads per SM scheduler busy.
+// CABL_RM_SCALAR_CTA=0|1 overrides (A/B only).
+inline bool rm_scalar_cta(uint64_t m, uint64_t n) {
+    static const int forced = [] {
+        const char* e = getenv("CABL_RM_SCALAR_CTA");
+        return e ? atoi(e) : -1;
+    }();
+    if (forced >= 0) return forced != 0;
+    return n >= uint64_t(kRmBlock) * 16 && m < uint64_t(sm_count()) * 32;
+}
+
 bool gemv_rm_is_lane(const void* A, const void* x, uint64_t m, uint64_t n, size_t elem) {
     const bool vec = aligned32(A) && aligned32(x) && n % (32 / elem) == 0;
     return n * elem <= rm_lane_max_bytes() && m >= uint64_t(sm_count()) * 64 &&
@@ -728,6 +772,11 @@ cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         const unsigned grid = unsigned((g.warps * kWarp + kRmBlock - 1) / kRmBlock);
         launch(gemv_rm_vec_kernel<T, kRmRows, kRmSeg>, grid, kRmBlock, 0, s, 
             A, x, c, m, n, g, static_cast<T*>(ws.scratch), ws.counters);
+        if (info) info->ctas = grid;
+    } else if (rm_scalar_cta(m, n)) {
+        const uint64_t cap = uint64_t(sm_count()) * 8;
+        const unsigned grid = unsigned(m < cap ? m : cap);
+        launch(gemv_rm_scalar_cta_kernel<T>, grid, kRmBlock, 0, s, A, x, c, m, n);
         if (info) info->ctas = grid;
     } else {
         // lanes per row: about 8 elements per lane, 4..32 lanes

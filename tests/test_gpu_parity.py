@@ -129,7 +129,9 @@ RM_SHAPES = [(1, 777), (3, 3), (8, 8), (40, 200), (257, 259), (1000, 1000), (200
              # odd rows, long and short: the G-lanes scalar kernel
              (8192, 8193), (7200, 1001), (8000, 249),
              # few long rows: the chunked kernel (units of row x chunk, queue, row tickets)
-             (1, 1 << 20), (3, 300_000), (8, 65_536), (2, 1_000_000)]
+             (1, 1 << 20), (3, 300_000), (8, 65_536), (2, 1_000_000),
+             # few long odd rows: one CTA per row (scalar loads, block sum)
+             (1000, 65_537), (37, 100_001), (4096, 16_385)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
