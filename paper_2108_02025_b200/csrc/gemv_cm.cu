@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     gemv_cm_split_bulk_scalar_kernel(const T* __restrict__ A, const T* __restrict__ x,
                                      T* __restrict__ c, uint64_t m, uint64_t n, int row_lanes,
                                      int tc, uint64_t x_off, int x_bulk, T* __restrict__ partials,
-                                     unsigned* __restrict__ ticket) {
+                                     unsigned* __restrict__ ticket, int a_off) {
     pdl_enter();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* stages = reinterpret_cast<T*>(smem_raw);
@@ -480,11 +480,17 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
                 if (use > 0) mbar_wait(&empty[st], (use - 1) & 1u);
                 const uint64_t col0 = t * tc;
                 const uint64_t cols = (n - col0 < uint64_t(tc)) ? n - col0 : uint64_t(tc);
-                const unsigned bytes = unsigned(cols * m * sizeof(T)) & ~15u;
+                // a_off > 0 (A not 16-byte aligned): copy from the 16-byte boundary
+                // a_off elements before the tile; a full tile is rounded up to
+                // whole 16-byte units, so a copy may start / end inside a 16-byte
+                // segment of A's neighbours (bytes never read by the consumers)
+                const uint64_t span = (cols * m + uint64_t(a_off)) * sizeof(T);
+                const unsigned bytes = cols == uint64_t(tc) ? unsigned((span + 15) & ~uint64_t(15))
+                                                            : unsigned(span & ~uint64_t(15));
                 const unsigned xbytes =
                     (x_bulk && cols == uint64_t(tc)) ? unsigned(cols * sizeof(T)) : 0u;
                 mbar_arrive_expect_tx(&full[st], bytes + xbytes);
-                if (bytes) bulk_g2s(stages + st * stage_elems, A + col0 * m, bytes, &full[st], pol);
+                if (bytes) bulk_g2s(stages + st * stage_elems, A + col0 * m - a_off, bytes, &full[st], pol);
                 if (xbytes) bulk_g2s(stages + st * stage_elems + x_off, x + col0, xbytes, &full[st], pol);
             }
         }
@@ -504,10 +510,10 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
             mbar_wait(&full[st], unsigned(it / kBulkStages) & 1u);
             const uint64_t col0 = t * tc;
             const int cols = int((n - col0 < uint64_t(tc)) ? n - col0 : uint64_t(tc));
-            const T* sb = stages + st * stage_elems;
+            const T* sb = stages + st * stage_elems + a_off;
             if (live) {
                 if (cols == tc) { // full tile: everything is in the stage
-                    const T* xs = x_bulk ? sb + x_off : nullptr;
+                    const T* xs = x_bulk ? stages + st * stage_elems + x_off : nullptr;
                     unsigned e = unsigned(cl) * mm + unsigned(rl);
                     const unsigned step = unsigned(col_lanes) * mm;
 #pragma unroll 4
@@ -519,7 +525,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
                     }
                 } else { // ragged last tile: its odd tail was not bulk-copied
                     const uint64_t in_smem =
-                        (uint64_t(cols) * m * sizeof(T) & ~uint64_t(15)) / sizeof(T);
+                        ((uint64_t(cols) * m + uint64_t(a_off)) * sizeof(T) & ~uint64_t(15)) /
+                            sizeof(T) - uint64_t(a_off);
                     for (int j = cl; j < cols; j += col_lanes) {
                         const T xj = __ldg(x + col0 + j);
 #pragma unroll
@@ -1016,6 +1023,11 @@ inline int bulk_scalar_rpt(uint64_t m) {
 template <typename T, int RPT>
 void bulk_scalar_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const SplitGeom& g,
                     int tc, int x_bulk, T* partials, unsigned* ticket, cudaStream_t s) {
+    // A's element offset from a 16-byte boundary; the x slice goes after the
+    // tile rounded up to 16 bytes (its bulk destination must be aligned)
+    const int a_off = int((reinterpret_cast<uintptr_t>(A) & 15u) / sizeof(T));
+    const uint64_t q = 16 / sizeof(T);
+    const uint64_t x_off = a_off ? (uint64_t(tc) * m + a_off + q - 1) / q * q : uint64_t(tc) * m;
     static bool configured = [] {
         cudaFuncSetAttribute(gemv_cm_split_bulk_scalar_kernel<T, 3, 49152, RPT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(bulk_smem(3, 49152)));
@@ -1023,8 +1035,8 @@ void bulk_scalar_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const 
     }();
     (void)configured;
     launch(gemv_cm_split_bulk_scalar_kernel<T, 3, 49152, RPT>, g.grid, kBulkThreads,
-           bulk_smem(3, 49152), s, A, x, c, m, n, g.row_lanes, tc, uint64_t(tc) * m, x_bulk,
-           partials, ticket);
+           bulk_smem(3, 49152), s, A, x, c, m, n, g.row_lanes, tc, x_off, x_bulk, partials,
+           ticket, a_off);
 }
 
 inline int split_mode() {
@@ -1037,6 +1049,16 @@ inline int split_mode() {
 
 template <typename T> bool tall_vec_ok(const T* A, const T* c, uint64_t m) {
     return aligned32(A) && aligned32(c) && m % Vec<T>::N == 0;
+}
+
+// CABL_CM_BULK_ANY=0: A off a 16-byte boundary (m < 1024) back on the scalar
+// 2-D split (A/B only).
+inline bool bulk_any_align() {
+    static const bool on = [] {
+        const char* e = getenv("CABL_CM_BULK_ANY");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
 }
 
 enum CmPath { kPathTallVec, kPathTallScalar, kPathBulk, kPathBulkScalar, kPathSplitVec,
@@ -1077,6 +1099,13 @@ template <typename T> CmPath cm_path(const T* A, const T* c, uint64_t m) {
         return kPathTallScalar;
     }
     if (split_vec_ok(A, m)) return (m < cm_single_max() && split_mode() == 1) ? kPathBulk : kPathSplitVec;
+    // A off a 16-byte boundary: the bulk ring from the boundary below A (256 MiB
+    // fp32 flushed, tools/cm_mis.py: m = 3 / 257 / 1000 680 / 137 / 78 -> 70 /
+    // 55 / 66 us against the scalar 2-D split); fp64 from 768 rows stays on the
+    // split (1000 rows: 59 against 63.5)
+    if (m < kBulkScalarMaxRows && split_mode() == 1 && reinterpret_cast<uintptr_t>(A) % sizeof(T) == 0 &&
+        bulk_any_align() && !(sizeof(T) == 8 && m >= 768))
+        return kPathBulkScalar;
     if (m < kBulkScalarMaxRows && split_mode() == 1 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0)
         return kPathBulkScalar;
     // the realigning split when its tiling keeps most SM slots and tile rows
@@ -1089,10 +1118,14 @@ template <typename T> CmPath cm_path(const T* A, const T* c, uint64_t m) {
     return kPathSplitScalar;
 }
 
-template <typename T> SplitGeom cm_split_geom(CmPath p, uint64_t m, uint64_t n, int* tc) {
+template <typename T> SplitGeom cm_split_geom(CmPath p, const T* A, uint64_t m, uint64_t n, int* tc) {
     if (p == kPathBulk) return split_bulk_geom<T>(m, n, tc);
     if (p == kPathBulkScalar) {
-        SplitGeom g = split_bulk_geom<T>(m, n, tc, BulkCfg{3, 49152}); // tc, grid, smem
+        // an A off a 16-byte boundary needs up to 2 x 16 bytes more per stage
+        // (the copy's leading pad and the rounded-up x slot): shrink the budget
+        const bool mis = (reinterpret_cast<uintptr_t>(A) & 15u) != 0;
+        SplitGeom g = split_bulk_geom<T>(m, n, tc, BulkCfg{3, mis ? 49152u - 32u : 49152u});
+        g.smem = bulk_smem(3, 49152);
         g.rpt = bulk_scalar_rpt(m);
         g.row_lanes = int((m + g.rpt - 1) / g.rpt);
         g.col_lanes = kBulkConsumers / g.row_lanes;
@@ -1115,7 +1148,7 @@ template <typename T> WorkspaceNeed gemv_cm_need(const T* A, const T*, uint64_t 
         return w;
     }
     int tc = 1;
-    const SplitGeom g = cm_split_geom<T>(p, m, n, &tc);
+    const SplitGeom g = cm_split_geom<T>(p, A, m, n, &tc);
     w.counters = g.row_tiles;
     w.scratch_bytes = size_t(g.row_tiles) * g.grid * g.mt * sizeof(T);
     return w;
@@ -1170,7 +1203,7 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         if (info) info->ctas = grid;
     } else {
         int tc = 1;
-        const SplitGeom g = cm_split_geom<T>(path, m, n, &tc);
+        const SplitGeom g = cm_split_geom<T>(path, A, m, n, &tc);
         T* partials = static_cast<T*>(ws.scratch);
         const dim3 grid(g.grid, g.row_tiles);
         if (path == kPathBulk) {

@@ -208,7 +208,8 @@ def test_gemv_col_major_matches_oracle(cuda, dtype, m, n):
 
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("off", [1, 3])
-@pytest.mark.parametrize("m,n", [(4096, 2048), (2048, 4096), (1024, 1000), (5000, 300)])
+@pytest.mark.parametrize("m,n", [(4096, 2048), (2048, 4096), (1024, 1000), (5000, 300),
+                                 (257, 20_000), (100, 65_536), (3, 300_000), (1000, 3000)])
 def test_gemv_col_major_misaligned_a(cuda, dtype, off, m, n):
     """A starting `off` elements past a 32-byte boundary (every column
     misaligned): the realigning split, within the contract and truth bounds,

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-python tools/rm_odd.py > gpurun_out/rm_odd_now.jsonl 2>&1
+python tools/cm_mis.py > gpurun_out/cm_mis_after.jsonl 2>&1
