@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     gemv_cm_split_bulk_kernel(const T* __restrict__ A, const T* __restrict__ x,
                               T* __restrict__ c, uint64_t m, uint64_t n, int row_lanes, int tc,
                               uint64_t x_off, T* __restrict__ partials,
-                              unsigned* __restrict__ ticket) {
+                              unsigned* __restrict__ ticket, int x_bulk) {
     pdl_enter();
     constexpr int V = Vec<T>::N;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -381,7 +381,10 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
                 // x slice: a full tile's is a multiple of 16 B (tc is) and rides
                 // in the stage when it fits the slot (tc * s <= kBulkXBytes); a
                 // ragged last tile's, or a wider one's, is read with plain loads
-                const unsigned xbytes = cols == uint64_t(tc) ? unsigned(cols * sizeof(T)) : 0u;
+                // (an x that is not 16-byte aligned cannot be bulk-copied: its
+                // slices are read with plain loads, x_bulk = 0)
+                const unsigned xbytes =
+                    (x_bulk && cols == uint64_t(tc)) ? unsigned(cols * sizeof(T)) : 0u;
                 mbar_arrive_expect_tx(&full[st], bytes + xbytes);
                 bulk_g2s(stages + st * stage_elems, A + col0 * m, bytes, &full[st], pol);
                 if (xbytes) bulk_g2s(stages + st * stage_elems + x_off, x + col0, xbytes, &full[st], pol);
@@ -403,7 +406,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
             if (live) {
                 for (int j = cl; j < cols; j += col_lanes) {
                     const Vec<T> a = *reinterpret_cast<const Vec<T>*>(sb + uint64_t(j) * m + uint64_t(rl) * V);
-                    const T xj = cols == tc ? sb[x_off + j] : __ldg(x + col0 + j);
+                    const T xj = (x_bulk && cols == tc) ? sb[x_off + j] : __ldg(x + col0 + j);
 #pragma unroll
                     for (int e = 0; e < V; ++e) acc.v[e] = fma_rn(a.v[e], xj, acc.v[e]);
                 }
@@ -998,7 +1001,8 @@ void bulk_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const SplitGe
     }();
     (void)configured;
     launch(gemv_cm_split_bulk_kernel<T, NS, SB>, g.grid, kBulkThreads, bulk_smem(NS, SB), s, 
-        A, x, c, m, n, g.row_lanes, tc, uint64_t(tc) * m, partials, ticket);
+        A, x, c, m, n, g.row_lanes, tc, uint64_t(tc) * m, partials, ticket,
+        int((reinterpret_cast<uintptr_t>(x) & 15u) == 0));
 }
 
 // Rows per consumer thread for the scalar bulk kernel: with row_lanes =

@@ -696,7 +696,8 @@ template bool gemv_rm_sweep_cfg<float>(const float*, const float*, uint64_t, uin
 template bool gemv_rm_sweep_cfg<double>(const double*, const double*, uint64_t, uint64_t, int*, int*,
                                         int*);
 
-template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n) {
+namespace {
+template <typename T> WorkspaceNeed rm_need_impl(const T* A, const T* x, uint64_t m, uint64_t n) {
     WorkspaceNeed w;
     if (m == 0 || n == 0) return w;
     const int mode = rm_mode<T>(A, x, m, n);
@@ -720,7 +721,7 @@ template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_
 }
 
 template <typename T>
-cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
+cudaError_t rm_launch_impl(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
                            const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
     if (info) info->ctas = 0;
     if (m == 0 || n == 0) return cudaSuccess; // c += 0
@@ -795,6 +796,34 @@ cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         if (info) info->ctas = grid;
     }
     return cudaGetLastError();
+}
+
+// x not 32-byte aligned while A's rows are whole aligned vectors (x = v[k:] of
+// a buffer, say): copy x once into aligned scratch (2 n s bytes against m n s of
+// A) and run the vector kernels; 16 x 2^22 fp32 took 1915 us on the scalar
+// path.  Few rows only pay it when m >= 4.
+template <typename T> bool rm_xcopy(const T* A, const T* x, uint64_t m, uint64_t n) {
+    return aligned32(A) && !aligned32(x) && n % Vec<T>::N == 0 && m >= 4 &&
+           reinterpret_cast<uintptr_t>(x) % sizeof(T) == 0;
+}
+} // namespace
+
+template <typename T> WorkspaceNeed gemv_rm_need(const T* A, const T* x, uint64_t m, uint64_t n) {
+    if (!rm_xcopy(A, x, m, n)) return rm_need_impl<T>(A, x, m, n);
+    WorkspaceNeed w = rm_need_impl<T>(A, A, m, n); // A stands in for an aligned x
+    w.scratch_bytes = (w.scratch_bytes + 255) / 256 * 256 + n * sizeof(T);
+    return w;
+}
+
+template <typename T>
+cudaError_t gemv_rm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
+                           const Workspace& ws, cudaStream_t s, LaunchInfo* info) {
+    if (!rm_xcopy(A, x, m, n)) return rm_launch_impl<T>(A, m, n, x, c, ws, s, info);
+    const size_t off = (rm_need_impl<T>(A, A, m, n).scratch_bytes + 255) / 256 * 256;
+    T* xa = reinterpret_cast<T*>(static_cast<char*>(ws.scratch) + off);
+    const cudaError_t e = cudaMemcpyAsync(xa, x, n * sizeof(T), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return e;
+    return rm_launch_impl<T>(A, m, n, xa, c, ws, s, info);
 }
 
 template WorkspaceNeed gemv_rm_need<float>(const float*, const float*, uint64_t, uint64_t);

@@ -673,3 +673,33 @@ def test_special_values_propagate_like_the_oracle(cuda, dtype):
         want = C0.copy()
         O.ger_ref(gx, gy, want, int(lay))
         np.testing.assert_array_equal(Cm.data.cpu().numpy(), want)  # NaN == NaN positions too
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("layout", ["row", "col"])
+@pytest.mark.parametrize("m,n", [(16, 1 << 20), (256, 1 << 16), (4, 300_000), (2048, 4096)])
+def test_gemv_misaligned_x(cuda, dtype, layout, m, n):
+    """x = v[1:] of an aligned buffer with an aligned A: the row-major path
+    stages x into aligned scratch, the col-major bulk ring reads x with plain
+    loads (a bulk copy needs 16-byte alignment)."""
+    import paper_2108_02025_b200 as cb
+    lay = cb.Layout.RowMajor if layout == "row" else cb.Layout.ColMajor
+    A = dev_uniform(m * n, dtype, 3, cuda)
+    x = dev_uniform(n + 1, dtype, 1, cuda)[1:]
+    c0 = dev_uniform(m, dtype, 4, cuda)
+    c, c2 = c0.clone(), c0.clone()
+    f = cb.gemv_row_major if layout == "row" else cb.gemv_col_major
+    Am = cb.DenseMatrix.wrap(A, m, n, lay)
+    f(Am, x, c, plan_for(dtype))
+    f(Am, x, c2, plan_for(dtype))
+    torch.cuda.synchronize()
+    assert torch.equal(c, c2)
+    An, xn, c0n = np_of(A), np_of(x), np_of(c0)
+    want = c0n.copy()
+    O.gemv_ref(An, int(lay), xn, want)
+    truth, rowabs = O.gemv_truth(An, int(lay), xn, c0n)
+    got = np_of(c).astype(np.float64)
+    dt = np_of(c).dtype
+    assert np.all(np.abs(got - want) <= T.contract_tol(n, rowabs, np.abs(c0n), dt))
+    chain = T.gemv_rm_chain(n, dt) if layout == "row" else T.gemv_cm_chain(m, n, dt)
+    assert np.all(np.abs(got - truth) <= T.truth_tol(chain, rowabs, np.abs(c0n), dt))
