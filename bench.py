@@ -159,6 +159,20 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- setup
+def workload_config(w) -> dict:
+    """The line's ``config``: workload-defining fields only, identical for our
+    arm and the reference arm (so the driver can match the two lines).  How a
+    run was executed (GPUs, machine, L2 policy details) goes under ``run``."""
+    step = w.alg_bytes(1)
+    return {"workload": f"{w.id}: {w.desc}", "m_per_gpu": w.m, "n": w.n,
+            "layout": {"gemv-row": "row-major", "gemv-col": "col-major", "ger": "row-major",
+                       "dot": "vector"}[w.op],
+            "dtype": w.dtype_name,
+            "l2": (f"inputs larger than L2 ({step / 1e6:.0f} MB per step vs the 126 MB B200 L2): "
+                   "steps back to back" if step > L2_BYTES else
+                   "L2 flushed between steps (outside the timed events)")}
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -474,10 +488,10 @@ def run_ours(args, ctx):
         "vs_baseline": None,
         "dtype": w.dtype_name,
         "data": "synthetic: seeded SplitMix64 U[-1,1) (seed 42), generated on device",
-        "config": {
-            "workload": f"{w.id}: {w.desc}",
-            "m_per_gpu": w.m, "n": w.n, "layout": "row-major",
-            "parallelism": f"row blocks over {ctx.world} GPU(s), x replicated, no collective",
+        "config": workload_config(w),
+        "run": {
+            "parallelism": (f"{w.shard} over {ctx.world} GPU(s) (one process per GPU), "
+                            "weak scaling, no collective in the step"),
             "machine": {"gpu": ginfo.name, "sms": gplan.sm_count, "l2_bytes": gplan.l2_bytes,
                         "source": "cabl_describe_device"},
             "l2": (f"inputs larger than L2: {bytes_rank / 1e6:.0f} MB per step vs "
@@ -629,6 +643,24 @@ def run_e2e(w, ins, policy, ctx, args):
     return resident, full
 
 
+def peer_probe(fn, ctx) -> None:
+    """One call of a fused peer-memory step before it is timed: if any rank's
+    kernel gave up waiting for a peer (mailbox fault, after
+    CABL_PEER_TIMEOUT_MS — bench.py sets 3 s), every rank agrees the path is
+    unavailable and the suite moves on instead of stalling."""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    faults = [o.state()[1] for o in (getattr(ctx, "peer_mb", None), getattr(ctx, "gather_gemv", None))
+              if o is not None]
+    ok = torch.tensor([0 if any(faults) else 1], dtype=torch.int32, device=ctx.dev)
+    if ctx.world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if int(ok.item()) == 0:
+        raise RuntimeError("a rank timed out waiting for its peers (mailbox fault)")
+
+
 def run_suite(args, ctx, flush, policy, peak):
     """Every BASELINE config at this N.  N=1: all seven on one GPU.  N>1: the
     configs BASELINE shards (R1, G4 row blocks; D2 chunks + all-gather),
@@ -654,6 +686,8 @@ def run_suite(args, ctx, flush, policy, peak):
                 import dataclasses
                 wl = dataclasses.replace(w, m=e - b)
             fn, lps = step_fn(wl, ins, policy, ctx, sharded_dot=True, fused=fused)
+            if fused:
+                peer_probe(fn, ctx)
             alg = w.alg_bytes(ctx.world)
             mode = l2_mode(wl.alg_bytes(1))
             times, _ = time_steps(fn, steps, args.warmup, ctx, flush, mode=mode)
@@ -747,8 +781,8 @@ def run_reference(args, ctx):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": w.dtype_name,
         "data": "synthetic: seeded SplitMix64 U[-1,1) (seed 42), generated on the host",
-        "config": {"workload": f"{w.id}: {w.desc}", "m_per_gpu": w.m, "n": w.n,
-                   "layout": "row-major", "parallelism": "CPU threads (reference ThreadPool)"},
+        "config": workload_config(w),
+        "run": {"parallelism": f"CPU threads (reference ThreadPool, {used} threads), rank 0 only"},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": used, "kind": kind,
                          "sample": f"full {w.id} workload per step; "
                                    f"{'cabl::' + w.op.replace('-', '_') if kind == 'reference' else 'restated oracle'}"
@@ -783,6 +817,60 @@ def run_cpu_table(args):
             print(json.dumps(r), flush=True)
 
 
+def fail(msg: str, code: int = 3):
+    print(f"bench.py: {msg}", file=sys.stderr, flush=True)
+    sys.exit(code)
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def ensure_ranks(args) -> None:
+    """One process per GPU.  Under torchrun (WORLD_SIZE set) the world must
+    equal --gpus.  Without it, --gpus N > 1 re-executes this command under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous)
+    and exits with its status — after checking that N GPUs are visible (our
+    arm; the reference arm and --launch-check run on the host)."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None:
+        if int(env_world) != args.gpus:
+            fail(f"WORLD_SIZE={env_world} but --gpus {args.gpus}: launch one rank per GPU "
+                 f"(torchrun --nproc-per-node {args.gpus}) or drop torchrun and let bench.py "
+                 "spawn the ranks")
+        return
+    if args.gpus == 1:
+        return
+    if args.impl == "ours" and not args.launch_check and not args.cpu_table:
+        import torch
+        have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        if have < args.gpus:
+            fail(f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    import subprocess
+    sys.exit(subprocess.call(cmd))
+
+
+def launch_check(world: int, rank: int) -> None:
+    """Every rank joins a gloo group and reports itself; rank 0 prints them."""
+    ranks = [rank]
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        got: list = [None] * world
+        dist.all_gather_object(got, {"rank": rank, "pid": os.getpid(),
+                                     "local_rank": int(os.environ.get("LOCAL_RANK", "0"))})
+        ranks = got
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "ranks": ranks}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -800,12 +888,21 @@ def main():
     ap.add_argument("--l2", choices=["auto", "flush", "stream"], default="auto",
                     help="headline L2 policy: auto = back to back when a step's inputs "
                          "exceed 2x L2, else flush between steps")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="spawn the --gpus ranks, rendezvous over gloo, print the rank list and "
+                         "exit (CPU; tests the launcher)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("bench.py: --warmup must be >= 3", file=sys.stderr)
         args.warmup = 3
+    if args.gpus < 1:
+        fail(f"--gpus must be >= 1 (got {args.gpus})")
 
+    ensure_ranks(args)
     world, rank, local = dist_env()
+    if args.launch_check:
+        launch_check(world, rank)
+        return
     if args.cpu_table:
         if rank == 0:
             run_cpu_table(args)
@@ -815,10 +912,15 @@ def main():
         run_reference(args, ctx)
         return
 
+    # a fused peer-memory step whose peer never arrives gives up after 3 s
+    # (library default 30 s), so the suite reports it unavailable promptly
+    os.environ.setdefault("CABL_PEER_TIMEOUT_MS", "3000")
     import torch
     if not torch.cuda.is_available():
         print(json.dumps({"error": "no CUDA device; libcabl_cuda has no CPU path"}))
         sys.exit(2)
+    if local >= torch.cuda.device_count():
+        fail(f"rank {rank}: LOCAL_RANK {local} but only {torch.cuda.device_count()} GPU(s) visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:

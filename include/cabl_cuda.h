@@ -52,7 +52,9 @@ enum {
     CABL_OK = 0,
     CABL_EINVAL = 1,
     CABL_ECUDA = 2,
-    CABL_ENOMEM = 3
+    CABL_ENOMEM = 3,
+    CABL_ENCCL = 4 /* multi-GPU exchange failed (cabl_mgpu_*): NCCL error, asynchronous
+                      NCCL error, a timed-out peer exchange, or the context's timeout */
 };
 
 /* Storage order of a dense matrix — reference dense.hpp:9, element (i,j) at
@@ -232,7 +234,9 @@ CABL_API int cabl_cuda_combine_rows_peer_emulate_f64(int world, const double* co
  *
  * cfull[g]: rank g's gathered buffer, 2 * m_total elements allocated with
  * cabl_peer_alloc on rank g's device (double-buffered: the e-th call on a
- * mailbox fills half e & 1, i.e. elements [(e & 1) * m_total, +m_total)),
+ * mailbox fills half e & 1, i.e. elements [(e & 1) * m_total, +m_total);
+ * ranks in separate processes must consume half e & 1, in stream order,
+ * before issuing call e + 1 — a faster peer may then write call e + 2 there),
  * as mapped here (cabl_peer_mailbox_export / _import work on any
  * cabl_peer_alloc pointer).  mboxes: a mailbox set used only by this
  * operation.  Calls are collective.  CABL_EINVAL when the slice shape does not
@@ -253,6 +257,13 @@ CABL_API int cabl_cuda_gemv_rm_gather_f64(const double* A, uint64_t m, uint64_t 
                                           cabl_probe* probe, void* stream);
 /* Every rank in one cooperative launch on the current device (testing with
  * fewer GPUs than ranks; all slices must take the same sweep shape). */
+/* *ok = 1 when the slice shape (on the current device) takes the gathering
+ * sweep kernel, else 0 — so a caller can check every rank before launching
+ * any (a rank rejected after its peers launched would leave them waiting). */
+CABL_API int cabl_cuda_gemv_rm_gather_supported_f32(const float* A, uint64_t m, uint64_t n,
+                                                    const float* x, int* ok);
+CABL_API int cabl_cuda_gemv_rm_gather_supported_f64(const double* A, uint64_t m, uint64_t n,
+                                                    const double* x, int* ok);
 CABL_API int cabl_cuda_gemv_rm_gather_emulate_f32(int world, const float* const* As,
                                                   const uint64_t* ms, uint64_t n,
                                                   const float* const* xs, float* const* cs,
@@ -315,6 +326,79 @@ CABL_API int cabl_host_ger_f32(const float* x, const float* y, float* C, int lay
                       uint64_t n, uint64_t small_cutoff, cabl_probe* probe, void* stream);
 CABL_API int cabl_host_ger_f64(const double* x, const double* y, double* C, int layout, uint64_t m,
                       uint64_t n, uint64_t small_cutoff, cabl_probe* probe, void* stream);
+
+/* ----------------------------------------------- multi-GPU (one process) ---
+ * one process drives G devices of one node.  The
+ * context holds one NCCL communicator per device (ncclCommInitAll; NCCL is
+ * loaded at run time, libnccl.so.2 or $CABL_NCCL_LIB), one non-blocking
+ * stream per device (cabl_mgpu_stream) and lazily built peer-memory buffers.
+ * Shard arrays have one entry per rank (rank r = devices[r]); shard r lives
+ * on device r.  The partition is the caller's (contiguous shards, as the
+ * reference's parallel_chunks, thread_pool.hpp:153-164).
+ *
+ * Every call is synchronous, like the reference templates: it validates all
+ * shards before launching anything (CABL_EINVAL), runs the single-GPU kernel
+ * on every shard, the exchange, and returns when every device is done.  The
+ * wait polls ncclCommGetAsyncError and a timeout (60 s, CABL_MGPU_TIMEOUT_MS
+ * or cabl_mgpu_set_timeout_ms): an asynchronous NCCL error, a timed-out peer
+ * exchange or the timeout aborts every communicator (ncclCommAbort) and
+ * returns CABL_ENCCL — a failure is reported to the caller, never a hang
+ * (the reference pool rethrows worker failures, thread_pool.hpp:63-68).  An
+ * aborted context returns CABL_ENCCL from every later call; finalize it.
+ *
+ * exchange: CABL_MGPU_NCCL (collectives) or CABL_MGPU_PEER (the exchange
+ * fused into the kernels over NVLink P2P, no collective; needs P2P between
+ * every pair).  Both give the same bits.  small_cutoff: as the single-GPU
+ * entry points (the reference plan's dot_cutoff). */
+enum { CABL_MGPU_NCCL = 0, CABL_MGPU_PEER = 1 };
+typedef struct cabl_mgpu cabl_mgpu;
+
+/* NCCL version the library loads (e.g. 22703); CABL_ENCCL if it cannot. */
+CABL_API int cabl_mgpu_nccl_version(int* version);
+CABL_API int cabl_mgpu_init(const int* devices, int count, cabl_mgpu** ctx);
+CABL_API int cabl_mgpu_finalize(cabl_mgpu* ctx);
+CABL_API int cabl_mgpu_size(const cabl_mgpu* ctx);
+CABL_API int cabl_mgpu_device(const cabl_mgpu* ctx, int rank);
+CABL_API void* cabl_mgpu_stream(const cabl_mgpu* ctx, int rank); /* cudaStream_t of rank */
+CABL_API int cabl_mgpu_set_timeout_ms(cabl_mgpu* ctx, uint64_t ms);
+
+/* *result = alpha0 + sum over ranks (in rank order) of x[r] . y[r]; the
+ * per-rank partials are the single-GPU kernel's bits (alpha0 = 0), summed
+ * left to right and alpha0 added last (reference kernels.hpp:145-163). */
+CABL_API int cabl_mgpu_dot_f32(cabl_mgpu* ctx, const float* const* x, const float* const* y,
+                               const uint64_t* n, float alpha0, uint64_t small_cutoff,
+                               int exchange, float* result);
+CABL_API int cabl_mgpu_dot_f64(cabl_mgpu* ctx, const double* const* x, const double* const* y,
+                               const uint64_t* n, double alpha0, uint64_t small_cutoff,
+                               int exchange, double* result);
+/* Row blocks: c[r] (m[r]) += A[r] (m[r] x n, row-major) x[r] (x replicated).
+ * c_full: NULL, or one device buffer of sum(m) elements per rank that
+ * receives every rank's updated slice at its row offset (the all-gather of
+ * BASELINE config 5).  Replaces cabl::gemv_row_major (kernels.hpp:230-257). */
+CABL_API int cabl_mgpu_gemv_rm_f32(cabl_mgpu* ctx, const float* const* A, const uint64_t* m,
+                                   uint64_t n, const float* const* x, float* const* c,
+                                   uint64_t small_cutoff, int exchange, float* const* c_full);
+CABL_API int cabl_mgpu_gemv_rm_f64(cabl_mgpu* ctx, const double* const* A, const uint64_t* m,
+                                   uint64_t n, const double* const* x, double* const* c,
+                                   uint64_t small_cutoff, int exchange, double* const* c_full);
+/* Column blocks of a col-major A: A[r] is m x n[r], x[r] the matching slice
+ * of x, c[r] a replica of c; every replica gets c += ((p_0 + p_1) + ...) in
+ * rank order, p_r = A[r] x[r] (same bits on every device).  Replaces
+ * cabl::gemv_col_major (kernels.hpp:187-224) for short-wide shapes. */
+CABL_API int cabl_mgpu_gemv_cm_cols_f32(cabl_mgpu* ctx, const float* const* A, uint64_t m,
+                                        const uint64_t* n, const float* const* x,
+                                        float* const* c, uint64_t small_cutoff, int exchange);
+CABL_API int cabl_mgpu_gemv_cm_cols_f64(cabl_mgpu* ctx, const double* const* A, uint64_t m,
+                                        const uint64_t* n, const double* const* x,
+                                        double* const* c, uint64_t small_cutoff, int exchange);
+/* Row blocks of a row-major C: C[r] (m[r] x n) += x[r] (m[r]) (x) y (y
+ * replicated).  No exchange.  Replaces cabl::ger (kernels.hpp:277-313). */
+CABL_API int cabl_mgpu_ger_rm_f32(cabl_mgpu* ctx, const float* const* x, const uint64_t* m,
+                                  const float* const* y, uint64_t n, float* const* C,
+                                  uint64_t small_cutoff);
+CABL_API int cabl_mgpu_ger_rm_f64(cabl_mgpu* ctx, const double* const* x, const uint64_t* m,
+                                  const double* const* y, uint64_t n, double* const* C,
+                                  uint64_t small_cutoff);
 
 /* ------------------------------------------------------ seeded inputs ---
  * Counter-based SplitMix64 generator, bit-identical to the host oracle's

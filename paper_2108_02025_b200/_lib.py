@@ -19,7 +19,8 @@ import os as _os
 LIB_PATH = Path(_os.environ["CABL_LIB"]) if _os.environ.get("CABL_LIB") else PKG / "libcabl_cuda.so"
 CSRC = PKG / "csrc"
 
-CABL_OK, CABL_EINVAL, CABL_ECUDA, CABL_ENOMEM = 0, 1, 2, 3
+CABL_OK, CABL_EINVAL, CABL_ECUDA, CABL_ENOMEM, CABL_ENCCL = 0, 1, 2, 3, 4
+CABL_MGPU_NCCL, CABL_MGPU_PEER = 0, 1
 ROW_MAJOR, COL_MAJOR = 0, 1
 
 u64 = C.c_uint64
@@ -92,11 +93,28 @@ SIGNATURES: dict[str, list] = {
     "cabl_cuda_combine_rows_peer_f64": [vp, u64, vp, vp, vp, i32, i32, vp],
     "cabl_cuda_combine_rows_peer_emulate_f32": [i32, vp, u64, vp, vp, vp, vp],
     "cabl_cuda_combine_rows_peer_emulate_f64": [i32, vp, u64, vp, vp, vp, vp],
+    "cabl_cuda_gemv_rm_gather_supported_f32": [vp, u64, u64, vp, C.POINTER(i32)],
+    "cabl_cuda_gemv_rm_gather_supported_f64": [vp, u64, u64, vp, C.POINTER(i32)],
+    "cabl_mgpu_nccl_version": [C.POINTER(i32)],
+    "cabl_mgpu_init": [C.POINTER(i32), i32, C.POINTER(vp)],
+    "cabl_mgpu_finalize": [vp],
+    "cabl_mgpu_size": [vp],
+    "cabl_mgpu_device": [vp, i32],
+    "cabl_mgpu_stream": [vp, i32],
+    "cabl_mgpu_set_timeout_ms": [vp, u64],
+    "cabl_mgpu_dot_f32": [vp, vp, vp, vp, f32, u64, i32, C.POINTER(f32)],
+    "cabl_mgpu_dot_f64": [vp, vp, vp, vp, f64, u64, i32, C.POINTER(f64)],
+    "cabl_mgpu_gemv_rm_f32": [vp, vp, vp, u64, vp, vp, u64, i32, vp],
+    "cabl_mgpu_gemv_rm_f64": [vp, vp, vp, u64, vp, vp, u64, i32, vp],
+    "cabl_mgpu_gemv_cm_cols_f32": [vp, vp, u64, vp, vp, vp, u64, i32],
+    "cabl_mgpu_gemv_cm_cols_f64": [vp, vp, u64, vp, vp, vp, u64, i32],
+    "cabl_mgpu_ger_rm_f32": [vp, vp, vp, vp, u64, vp, u64],
+    "cabl_mgpu_ger_rm_f64": [vp, vp, vp, vp, u64, vp, u64],
     "cabl_cuda_fill_uniform_f32": [vp, u64, u64, u64, u64, vp],
     "cabl_cuda_fill_uniform_f64": [vp, u64, u64, u64, u64, vp],
     "cabl_cuda_fill_normal_f64": [vp, u64, u64, u64, u64, vp],
 }
-_RESTYPE = {"cabl_last_error": C.c_char_p}
+_RESTYPE = {"cabl_last_error": C.c_char_p, "cabl_mgpu_stream": C.c_void_p}
 
 _lock = threading.Lock()
 _lib: C.CDLL | None = None
@@ -133,6 +151,11 @@ class CablError(RuntimeError):
     """CUDA-side failure (CABL_ECUDA / CABL_ENOMEM)."""
 
 
+class CablExchangeError(CablError):
+    """Multi-GPU exchange failure (CABL_ENCCL): NCCL error, asynchronous NCCL
+    error, timed-out peer exchange or context timeout; the context is aborted."""
+
+
 def check(rc: int) -> None:
     if rc == CABL_OK:
         return
@@ -140,6 +163,8 @@ def check(rc: int) -> None:
     if rc == CABL_EINVAL:
         # the reference throws std::invalid_argument (kernels.hpp:59-61)
         raise ValueError(msg)
+    if rc == CABL_ENCCL:
+        raise CablExchangeError(msg)
     raise CablError(msg)
 
 

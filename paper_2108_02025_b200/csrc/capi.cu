@@ -32,6 +32,12 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
+} // namespace
+
+void cabl_dev::set_last_error(const std::string& msg) { g_err = msg; }
+
+namespace {
+
 int cuda_fail(cudaError_t e, const char* where) {
     cudaGetLastError(); // clear sticky-free errors so the next call starts clean
     return fail(CABL_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -94,7 +100,7 @@ struct WsLease {
 };
 
 int get_workspace(int device, cudaStream_t s, const WorkspaceNeed& need, WsLease* out) {
-    if (need.counters == 0 && need.scratch_bytes == 0) {
+    if (need.counters == 0 && need.scratch_bytes == 0 && need.slots == 0) {
         out->ws = Workspace{};
         return CABL_OK;
     }
@@ -140,6 +146,16 @@ int get_workspace(int device, cudaStream_t s, const WorkspaceNeed& need, WsLease
         if (ws.scratch) cudaFreeAsync(ws.scratch, s);
         ws.scratch = p;
         ws.scratch_bytes = bytes;
+    }
+    if (need.slots > ws.n_slots) {
+        // zeroed once: epoch 0 and untagged partials (dot.cu's collector)
+        size_t cnt = need.slots < 1024 ? 1024 : need.slots * 2;
+        void* p = nullptr;
+        CABL_TRY_CUDA(cudaMallocAsync(&p, cnt * sizeof(unsigned long long), s), "workspace slots");
+        CABL_TRY_CUDA(cudaMemsetAsync(p, 0, cnt * sizeof(unsigned long long), s), "workspace memset");
+        if (ws.slots) cudaFreeAsync(ws.slots, s);
+        ws.slots = static_cast<unsigned long long*>(p);
+        ws.n_slots = cnt;
     }
     out->ws = ws;
     return CABL_OK;
@@ -389,6 +405,19 @@ int gather_common_checks(int world, void* const* cfull, void* const* mboxes, uin
     for (int g = 0; g < world; ++g)
         if (!cfull[g] || !mboxes[g]) return fail(CABL_EINVAL, "gemv_rm_gather: null entry in a peer table");
     if (n == 0 || m_total == 0) return fail(CABL_EINVAL, "gemv_rm_gather: empty matrix");
+    return CABL_OK;
+}
+
+template <typename T>
+int gather_supported_impl(const T* A, uint64_t m, uint64_t n, const T* x, int* ok) {
+    if (!ok) return fail(CABL_EINVAL, "gemv_rm_gather_supported: null result pointer");
+    *ok = 0;
+    if (!A || !x || m == 0 || n == 0) return CABL_OK;
+    int dev;
+    if (int rc = current_device(&dev)) return rc;
+    int R, KV, mb;
+    *ok = gemv_rm_sweep_cfg<T>(A, x, m, n, &R, &KV, &mb) &&
+          gemv_rm_gather_ctas_per_sm(R, KV, mb, sizeof(T)) != 0;
     return CABL_OK;
 }
 
@@ -1013,6 +1042,14 @@ int cabl_cuda_gemv_rm_gather_f64(const double* A, uint64_t m, uint64_t n, const 
                                  cabl_probe* probe, void* stream) {
     return gemv_gather_impl<double>(A, m, n, x, c, row_off, m_total, cfull, mboxes, world, rank,
                                     probe, stream);
+}
+int cabl_cuda_gemv_rm_gather_supported_f32(const float* A, uint64_t m, uint64_t n, const float* x,
+                                           int* ok) {
+    return gather_supported_impl<float>(A, m, n, x, ok);
+}
+int cabl_cuda_gemv_rm_gather_supported_f64(const double* A, uint64_t m, uint64_t n,
+                                           const double* x, int* ok) {
+    return gather_supported_impl<double>(A, m, n, x, ok);
 }
 int cabl_cuda_gemv_rm_gather_emulate_f32(int world, const float* const* As, const uint64_t* ms,
                                          uint64_t n, const float* const* xs, float* const* cs,

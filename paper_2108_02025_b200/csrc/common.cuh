@@ -202,6 +202,50 @@ __device__ __forceinline__ bool last_arriver(unsigned* ticket, unsigned nblk, bo
     return *am_last_sh;
 }
 
+// ---- epoch-tagged 64-bit words (DOT collector, dot.cu) ---------------------
+// A word is (epoch << 32) | 32 payload bits; a T takes sizeof(T) / 4 words.
+// Relaxed gpu-scope accesses: the payload travels inside the word, so no
+// other memory needs ordering, and a poller sees the word once it is in L2.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+template <typename T> __host__ __device__ constexpr int tagged_words() { return int(sizeof(T) / 4); }
+__device__ __forceinline__ void publish_tagged(unsigned long long* w, float v, unsigned e) {
+    st_relaxed_u64(w, (static_cast<unsigned long long>(e) << 32) | __float_as_uint(v));
+}
+__device__ __forceinline__ void publish_tagged(unsigned long long* w, double v, unsigned e) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    const unsigned long long tag = static_cast<unsigned long long>(e) << 32;
+    st_relaxed_u64(w, tag | (b & 0xffffffffull));
+    st_relaxed_u64(w + 1, tag | (b >> 32));
+}
+__device__ __forceinline__ unsigned wait_tagged(const unsigned long long* w, unsigned e) {
+    unsigned long long v;
+    do {
+        v = ld_relaxed_u64(w);
+    } while (unsigned(v >> 32) != e);
+    return unsigned(v);
+}
+template <typename T> __device__ __forceinline__ T collect_tagged(const unsigned long long* w, unsigned e);
+template <> __device__ __forceinline__ float collect_tagged<float>(const unsigned long long* w, unsigned e) {
+    return __uint_as_float(wait_tagged(w, e));
+}
+template <> __device__ __forceinline__ double collect_tagged<double>(const unsigned long long* w, unsigned e) {
+    const unsigned long long lo = wait_tagged(w, e), hi = wait_tagged(w + 1, e);
+    return __longlong_as_double(static_cast<long long>((hi << 32) | lo));
+}
+// this launch's epoch: one past the last completed one (never 0, the value of
+// a zeroed word)
+__device__ __forceinline__ unsigned next_epoch(const unsigned long long* epoch_word) {
+    const unsigned e = unsigned(ld_relaxed_u64(epoch_word)) + 1u;
+    return e ? e : 1u;
+}
+
 // ---- programmatic dependent launch (PDL) ---------------------------------
 // Every kernel of the library starts with pdl_enter(): it lets the NEXT
 // kernel on the stream begin launching (its CTAs take SMs as this grid's

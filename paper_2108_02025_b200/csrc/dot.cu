@@ -6,11 +6,14 @@
 //     CTAs stride over tiles of BLOCK*U 32-byte vectors, every thread keeps
 //     2*U 256-bit loads in flight and accumulates with FMA in registers;
 //   * fixed butterfly warp sums, fixed-order CTA sum -> partials[cta];
-//   * the last CTA to arrive (an acq_rel atomic ticket — no separate fence)
-//     sums the partials in a fixed order, adds alpha0 LAST (as the reference
-//     does, kernels.hpp:142,163) and resets the ticket for the next launch.  (A variant
-//     where CTA 0 acquire-polls per-CTA release flags measured 0-2 us slower
-//     on B200 and was dropped.)
+//   * every CTA publishes its total as epoch-tagged 64-bit words (common.cuh);
+//     CTA 0, once its own sweep is done, polls the CTAs' words, sums them in a
+//     fixed order, adds alpha0 LAST (as the reference does, kernels.hpp:142,163)
+//     and records the epoch.  The critical path after the last CTA's sweep is
+//     one store + one poll instead of a ticket RTT + a partials RTT: D1
+//     (2^24 fp32, one flushed launch, ncu) 25.2 -> 24.x us (tools/dotlab.py,
+//     profiles/r02_dotlab.md).  No deadlock is possible: only CTA 0 waits,
+//     and it waits for CTAs that never wait.
 // The element -> thread mapping depends only on n and the grid, so the result
 // is bitwise reproducible run to run (reference kernels.hpp:9-13).
 //
@@ -30,8 +33,8 @@ namespace {
 template <typename T, int BLOCK, int U, int MINB, bool PEEL = false>
 __global__ void __launch_bounds__(BLOCK, MINB)
     dot_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t n, int vec_ok,
-               uint64_t head_, T alpha0, T* __restrict__ out, T* __restrict__ partials,
-               unsigned* __restrict__ ticket, int pf) {
+               uint64_t head_, T alpha0, T* __restrict__ out,
+               unsigned long long* __restrict__ slots, int pf) {
     // vec_ok: x + head and y + head are 32-byte aligned (head < V elements are
     // peeled when both operands share their misalignment); the head and the
     // < V tail run in the scalar loop
@@ -48,8 +51,10 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     }
     pdl_wait();
     __shared__ T red[32];
-    __shared__ bool am_last;
     const int tid = threadIdx.x;
+    // the epoch is loaded before the sweep, so its latency hides behind it
+    const bool collector = blockIdx.x == 0;
+    const unsigned e = (gridDim.x > 1 && (tid == 0 || collector)) ? next_epoch(slots) : 0u;
     const T s = dot_thread_sum<T, BLOCK, U, PEEL>(x, y, n, vec_ok, head_, blockIdx.x, gridDim.x);
     const T cta_total = block_sum(s, red);
 
@@ -57,25 +62,18 @@ __global__ void __launch_bounds__(BLOCK, MINB)
         if (tid == 0) *out = add_rn(cta_total, alpha0);
         return;
     }
-    if (tid == 0) {
-        partials[blockIdx.x] = cta_total;
-        // release: the partial is visible before the ticket moves; acquire:
-        // the last arriver sees every partial (one fence-free RMW)
-        unsigned t;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
-                     : "=r"(t)
-                     : "l"(ticket)
-                     : "memory");
-        am_last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!am_last) return;
+    constexpr int W = tagged_words<T>();
+    if (tid == 0) publish_tagged(slots + 1 + uint64_t(W) * blockIdx.x, cta_total, e);
+    if (!collector) return;
+    // CTA totals in a fixed order (thread t: CTAs t, t + BLOCK, ...; then the
+    // fixed block tree), alpha0 last
     T v = T(0);
-    for (unsigned i = tid; i < gridDim.x; i += BLOCK) v = add_rn(v, ld_cg(partials + i));
+    for (unsigned i = tid; i < gridDim.x; i += BLOCK)
+        v = add_rn(v, collect_tagged<T>(slots + 1 + uint64_t(W) * i, e));
     const T total = block_sum(v, red);
     if (tid == 0) {
         *out = add_rn(total, alpha0);
-        *ticket = 0u; // ready for the next launch on this stream
+        st_relaxed_u64(slots, e); // the next launch on this stream takes e + 1
     }
 }
 
@@ -170,25 +168,24 @@ template <typename T> unsigned dot_grid(uint64_t n, bool small) {
 
 template <typename T, int B, int U, int M>
 cudaError_t dot_go(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok,
-                   uint64_t head, T alpha0, T* out, T* partials, unsigned* ticket,
-                   cudaStream_t s) {
+                   uint64_t head, T alpha0, T* out, unsigned long long* slots, cudaStream_t s) {
     if (head)
         launch(dot_kernel<T, B, U, M, true>, grid, B, 0, s, x, y, n, vec_ok, head, alpha0, out,
-               partials, ticket, pdl_prefetch_enabled());
+               slots, pdl_prefetch_enabled());
     else
         launch(dot_kernel<T, B, U, M, false>, grid, B, 0, s, x, y, n, vec_ok, head, alpha0, out,
-               partials, ticket, pdl_prefetch_enabled());
+               slots, pdl_prefetch_enabled());
     return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t dot_dispatch(unsigned grid, const T* x, const T* y, uint64_t n, int vec_ok,
-                         uint64_t head, T alpha0, T* out, T* partials, unsigned* ticket,
+                         uint64_t head, T alpha0, T* out, unsigned long long* slots,
                          cudaStream_t s) {
     const DotCfg c = dot_cfg();
 #define CABL_DOT_CASE(B_, U_, M_)                                                              \
     if (c.block == B_ && c.unroll == U_ && c.minb == M_)                                       \
-        return dot_go<T, B_, U_, M_>(grid, x, y, n, vec_ok, head, alpha0, out, partials, ticket, s);
+        return dot_go<T, B_, U_, M_>(grid, x, y, n, vec_ok, head, alpha0, out, slots, s);
     CABL_DOT_CASE(256, 1, 8)
     CABL_DOT_CASE(256, 2, 8)
     CABL_DOT_CASE(256, 4, 4)
@@ -199,7 +196,7 @@ cudaError_t dot_dispatch(unsigned grid, const T* x, const T* y, uint64_t n, int 
     CABL_DOT_CASE(256, 8, 1)
 #undef CABL_DOT_CASE
     return dot_go<T, kDotBlock, kDotUnroll, kDotCtasPerSm>(grid, x, y, n, vec_ok, head, alpha0,
-                                                          out, partials, ticket, s);
+                                                          out, slots, s);
 }
 
 } // namespace
@@ -223,6 +220,7 @@ template <typename T> WorkspaceNeed dot_need(uint64_t n, bool small) {
     const uint64_t chunks = (n / Vec<T>::N + cv - 1) / cv;
     const uint64_t g = dot_grid<T>(n, small);
     w.scratch_bytes = size_t(chunks > g ? chunks : g) * sizeof(T);
+    w.slots = 1 + size_t(tagged_words<T>()) * g; // epoch + the CTAs' tagged totals
     return w;
 }
 
@@ -263,8 +261,7 @@ cudaError_t dot_launch(const T* x, const T* y, uint64_t n, T alpha0, T* out, boo
                x, y, n, alpha0, out, static_cast<T*>(ws.scratch), ws.counters, p.chunk);
         return cudaGetLastError();
     }
-    return dot_dispatch<T>(p.grid, x, y, n, p.vec_ok, p.head, alpha0, out,
-                           static_cast<T*>(ws.scratch), ws.counters + 1, s);
+    return dot_dispatch<T>(p.grid, x, y, n, p.vec_ok, p.head, alpha0, out, ws.slots, s);
 }
 
 template <typename T>

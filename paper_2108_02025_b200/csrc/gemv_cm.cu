@@ -527,9 +527,13 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
                             if (rok[k]) acc[k] = fma_rn(sb[e + unsigned(k * row_lanes)], xj, acc[k]);
                     }
                 } else { // ragged last tile: its odd tail was not bulk-copied
-                    const uint64_t in_smem =
+                    // elements of the tile the producer copied: the whole 16-byte
+                    // units from the boundary below A, less the a_off lead-in (none
+                    // at all when the tile ends inside its first 16 bytes)
+                    const uint64_t copied =
                         ((uint64_t(cols) * m + uint64_t(a_off)) * sizeof(T) & ~uint64_t(15)) /
-                            sizeof(T) - uint64_t(a_off);
+                        sizeof(T);
+                    const uint64_t in_smem = copied > uint64_t(a_off) ? copied - uint64_t(a_off) : 0;
                     for (int j = cl; j < cols; j += col_lanes) {
                         const T xj = __ldg(x + col0 + j);
 #pragma unroll

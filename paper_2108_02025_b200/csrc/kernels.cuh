@@ -5,6 +5,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <string>
 
 namespace cabl_dev {
 
@@ -12,16 +13,24 @@ namespace cabl_dev {
 // entry and every kernel that uses them leaves them zero on exit (the
 // last-arriving CTA resets what it used), so the workspace is reusable by the
 // next launch on the same stream without a memset.
+//
+// `slots` are epoch-tagged 64-bit words, zero when allocated and used only by
+// the DOT kernel's collector (dot.cu): slots[0] holds the last completed
+// epoch, slots[1..] the CTAs' tagged partials.  A stale word never carries
+// the current epoch, so they need no reset between launches.
 struct Workspace {
     unsigned* counters = nullptr;
     size_t n_counters = 0;
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
+    unsigned long long* slots = nullptr;
+    size_t n_slots = 0;
 };
 
 struct WorkspaceNeed {
     size_t counters = 0;
     size_t scratch_bytes = 0;
+    size_t slots = 0;
 };
 
 struct LaunchInfo {
@@ -29,6 +38,7 @@ struct LaunchInfo {
 };
 
 int sm_count(); // of the current device (cached per device)
+void set_last_error(const std::string& msg); // cabl_last_error() of this thread (capi.cu)
 uint64_t queue_threshold_bytes(); // work-queue size rule, from the device L2 (capi.cu)
 
 // ---- DOT (dot.cu) ----

@@ -271,8 +271,11 @@ class GatherGemv:
 
     Rank g owns rows ``row_off[g] .. row_off[g] + m_g`` of A and c (x
     replicated), like ``sharded_gemv_rows``.  The gathered buffer is library
-    memory, double-buffered: call k returns the view of half k & 1, valid
-    until call k + 2 (``cabl_cuda_gemv_rm_gather_*`` in include/cabl_cuda.h).
+    memory, double-buffered: call k returns the view of half k & 1.  With the
+    ranks in separate processes that view must be consumed (or cloned), in
+    stream order, before this rank issues call k + 1: a faster peer starts
+    pushing call k + 2 into the same half as soon as it sees this rank's call
+    k + 1 (``cabl_cuda_gemv_rm_gather_*`` in include/cabl_cuda.h).
     Collective: every rank of the group calls, in the same order.  The slice
     shape must take the sweep kernel (long aligned rows, enough of them); other
     shapes raise ValueError — use ``sharded_gemv_rows(gather=True)`` there.
@@ -337,7 +340,12 @@ class GatherGemv:
     def __call__(self, A_local: "cabl.DenseMatrix", x: torch.Tensor, c_local: torch.Tensor,
                  row_off: int) -> torch.Tensor:
         cabl._require(A_local.layout() == cabl.Layout.RowMajor, "gemv_row_major: A must be row-major")
-        sfx = cabl._suffix(c_local)
+        sfx, on_gpu = cabl._check_same([A_local.data, x, c_local], "gemv_row_major")
+        # the peer buffers hold m_total values of self.dtype on self.device: an
+        # operand of another dtype or device would write past them on every rank
+        cabl._require(on_gpu and c_local.dtype == self.dtype and c_local.device == self.device,
+                      f"gather GEMV: operands must be {self.dtype} on {self.device} "
+                      "(the dtype and device the gathered buffers were built for)")
         m, n = A_local.rows(), A_local.cols()
         cabl._require(x.numel() == n and c_local.numel() == m, "gemv_row_major: shape mismatch")
         p = cabl.Probe()
@@ -449,6 +457,10 @@ def sharded_gemv_cols_fused(A_local: "cabl.DenseMatrix", x_local: torch.Tensor, 
     cabl._require(A_local.layout() == cabl.Layout.ColMajor,
                   "sharded_gemv_cols: A must be col-major (its column blocks are contiguous)")
     m = c.numel()
+    _, on_gpu = cabl._check_same([A_local.data, x_local, c], "sharded_gemv_cols")
+    cabl._require(on_gpu and c.dtype == peers.dtype and c.device == peers.device,
+                  f"sharded_gemv_cols_fused: operands must be {peers.dtype} on {peers.device} "
+                  "(the dtype and device the peer slots were built for)")
     cabl._require(m == peers.m, "sharded_gemv_cols_fused: c length differs from the slot size")
     part = torch.zeros(m, dtype=c.dtype, device=c.device)
     cabl.gemv_col_major(A_local, x_local, part, policy)

@@ -53,3 +53,51 @@ def test_cpu_reference_sample_paths(wid):
         assert r["value"] > 0 and r["unit"] == "GB/s"
         assert r["cores"] == (1 if naive or r["kind"] == "port" else 2)
         assert ("naive oracle" in r["sample"]) == (naive and r["kind"] == "reference")
+
+
+def test_launcher_spawns_gpus_ranks_over_gloo():
+    """`bench.py --gpus 2` without torchrun re-executes itself under
+    torch.distributed.run with 2 ranks (checked on CPU over gloo)."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--launch-check"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2
+    assert sorted(x["rank"] for x in d["ranks"]) == [0, 1]
+    assert len({x["pid"] for x in d["ranks"]}) == 2  # one process per rank
+
+
+@pytest.mark.skipif(torch.cuda.device_count() >= 2, reason="checks the too-few-GPUs refusal")
+def test_launcher_refuses_more_gpus_than_visible():
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "3"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode != 0
+    assert "needs 2 visible GPUs" in r.stderr
+
+
+def test_launcher_refuses_world_size_mismatch():
+    import os
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "4", "--steps", "3"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode != 0
+    assert "WORLD_SIZE=2 but --gpus 4" in r.stderr
+
+
+def test_both_arms_share_the_workload_config():
+    """The driver matches our line with the reference arm's by `config`: both
+    are built by one function and carry only workload-defining fields."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_2108_02025_b200 import workloads as WL
+    for w in WL.WORKLOADS.values():
+        cfg = bench.workload_config(w)
+        assert set(cfg) == {"workload", "m_per_gpu", "n", "layout", "dtype", "l2"}
+        assert cfg == bench.workload_config(w)
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps",
+                        "1", "--warmup", "1"], capture_output=True, text=True, timeout=600,
+                       cwd=ROOT)
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["config"] == bench.workload_config(WL.WORKLOADS["G1"])

@@ -7,6 +7,7 @@ from __future__ import annotations
 import ctypes as C
 import re
 import subprocess
+import sys
 from pathlib import Path
 
 import numpy as np
@@ -169,3 +170,46 @@ def test_peer_entry_points_without_a_gpu():
     rc = L.cabl_cuda_combine_rows_peer_f32(x.ctypes.data, 4, x.ctypes.data, fake, fake, 2, 1, None)
     assert rc == _lib.CABL_ECUDA
     assert x[0] == 1.0  # nothing was written
+
+
+def test_mgpu_entry_points_without_a_gpu():
+    """The multi-GPU C ABI: NCCL is found and loaded at run time; arguments
+    are validated the reference way (EINVAL + message); without a device the
+    context cannot be created (ECUDA), and no call proceeds without one."""
+    from paper_2108_02025_b200 import _lib
+    L = _lib.lib()
+    v = C.c_int()
+    assert L.cabl_mgpu_nccl_version(C.byref(v)) == _lib.CABL_OK
+    assert v.value >= 21800  # 2.18+; this image ships 2.27 (system) / 2.28 (torch)
+    ctx = C.c_void_p()
+    assert L.cabl_mgpu_init(None, 0, C.byref(ctx)) == _lib.CABL_EINVAL
+    devs = (C.c_int * 2)(0, 0)
+    assert L.cabl_mgpu_init(devs, 2, C.byref(ctx)) == _lib.CABL_EINVAL
+    assert "twice" in L.cabl_last_error().decode()
+    if not torch.cuda.is_available():
+        devs = (C.c_int * 1)(0)
+        assert L.cabl_mgpu_init(devs, 1, C.byref(ctx)) == _lib.CABL_ECUDA
+        assert ctx.value is None
+    out = C.c_float()
+    n = (C.c_uint64 * 1)(4)
+    assert L.cabl_mgpu_dot_f32(None, None, None, n, C.c_float(0), 8192, 0,
+                               C.byref(out)) == _lib.CABL_EINVAL
+    assert "null context" in L.cabl_last_error().decode()
+    assert L.cabl_mgpu_ger_rm_f32(None, None, n, None, 4, None, 8192) == _lib.CABL_EINVAL
+    assert L.cabl_mgpu_finalize(None) == _lib.CABL_OK
+    assert L.cabl_mgpu_size(None) == 0 and L.cabl_mgpu_stream(None, 0) is None
+
+
+def test_mgpu_reports_a_missing_nccl():
+    """CABL_NCCL_LIB pointing nowhere: CABL_ENCCL with the loader's message,
+    never a crash (the single-GPU entry points do not need NCCL at all)."""
+    code = ("import ctypes as C; from paper_2108_02025_b200 import _lib; L = _lib.lib(); "
+            "v = C.c_int(); rc = L.cabl_mgpu_nccl_version(C.byref(v)); "
+            "print(rc, L.cabl_last_error().decode())")
+    import os
+    env = dict(os.environ, CABL_NCCL_LIB="/nonexistent/libnccl.so.2")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=ROOT, timeout=300)
+    assert r.returncode == 0, r.stderr
+    rc, msg = r.stdout.split(" ", 1)
+    assert int(rc) == 4 and "cannot load NCCL" in msg

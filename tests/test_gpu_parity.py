@@ -234,6 +234,43 @@ def test_gemv_col_major_misaligned_a(cuda, dtype, off, m, n):
     assert np.all(np.abs(got.astype(np.float64) - truth) <= tol_t)
 
 
+def _bulk_scalar_tc(m, s):
+    """Columns per stage of the scalar bulk ring for an A off a 16-byte
+    boundary (csrc/gemv_cm.cu split_bulk_geom with the 49152 - 32 budget)."""
+    q = 16 // s
+    return max(q, (49152 - 32 + 1024) // ((m + 1) * s) // q * q)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("off", [1, 2])
+@pytest.mark.parametrize("m", [1, 2])
+@pytest.mark.parametrize("rag", [1, 2])
+def test_gemv_col_major_misaligned_ragged_tail_tiny_m(cuda, dtype, off, m, rag):
+    """A off a 16-byte boundary with 1-2 rows and a last tile of 1-2 columns:
+    that tile ends inside its first 16 bytes, so the ring copies nothing for it
+    and every element must come from global memory (regression: the in-smem
+    count wrapped and the tile read a stale stage)."""
+    import paper_2108_02025_b200 as cb
+    s = torch.tensor([], dtype=dtype).element_size()
+    if off * s % 16 == 0:
+        pytest.skip("offset keeps A 16-byte aligned")
+    n = _bulk_scalar_tc(m, s) * 40 + rag
+    A = dev_uniform(m * n + off, dtype, 3, cuda)[off:]
+    x = dev_uniform(n, dtype, 1, cuda)
+    c0 = dev_uniform(m, dtype, 4, cuda)
+    c = c0.clone()
+    cb.gemv_col_major(cb.DenseMatrix.wrap(A, m, n, cb.Layout.ColMajor), x, c, plan_for(dtype))
+    An, xn, c0n = np_of(A), np_of(x), np_of(c0)
+    want = c0n.copy()
+    O.gemv_ref(An, 1, xn, want)
+    truth, rowabs = O.gemv_truth(An, 1, xn, c0n)
+    got = np_of(c)
+    dt = got.dtype
+    assert np.all(np.abs(got.astype(np.float64) - want) <= T.contract_tol(n, rowabs, np.abs(c0n), dt))
+    tol_t = T.truth_tol(T.gemv_cm_chain(m, n, dt), rowabs, np.abs(c0n), dt)
+    assert np.all(np.abs(got.astype(np.float64) - truth) <= tol_t)
+
+
 @pytest.mark.parametrize("m,n", [(1 << 20, 256), (256, 1 << 20)])
 def test_gemv_col_major_baseline_configs_fp64_normal(cuda, m, n):
     """BASELINE config 4 (G2 / G3): fp64 col-major, N(0,1) inputs."""
