@@ -65,10 +65,35 @@ class L2Flush:
         import torch
         self.w = torch.empty(nbytes // 4, dtype=torch.float32, device=dev)
         self.r = torch.zeros(nbytes // 4, dtype=torch.float32, device=dev)
+        self.e = torch.zeros(nbytes // 8, dtype=torch.float32, device=dev)
+        self._evict_ms = None
 
     def zero_(self):
         self.w.zero_()
         self.r.sum()
+
+    def evict_(self):
+        """Read a buffer of 2 x L2 that the L2 does not hold: every line the
+        step left dirty is written back during this pass."""
+        self.e.sum()
+
+    def evict_ms(self, reps: int = 15) -> float:
+        """Mean time of evict_() right after zero_() (nothing dirty in L2):
+        what a timed step that ends with evict_() subtracts."""
+        import torch
+        if self._evict_ms is None:
+            ts = []
+            for i in range(reps + 2):
+                self.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                self.evict_()
+                b.record()
+                torch.cuda.synchronize()
+                if i >= 2:
+                    ts.append(a.elapsed_time(b))
+            self._evict_ms = sum(ts) / len(ts)
+        return self._evict_ms
 
 
 def peaks():
@@ -283,10 +308,15 @@ def l2_mode(step_bytes: int) -> str:
     return "stream" if step_bytes > L2_BYTES else "flush"
 
 
-def time_steps(fn, steps, warmup, ctx, flush, sampler=None, mode="flush"):
+def time_steps(fn, steps, warmup, ctx, flush, sampler=None, mode="flush", charge_writeback=False):
     """Per-step device times (ms) on the launching stream, barrier + synchronize
     on both sides of the timed region.
     mode 'flush':  L2 flushed between steps outside per-step CUDA events.
+                   charge_writeback (GER: C is written): each step's events
+                   also enclose an eviction pass, whose clean-L2 time is
+                   subtracted — so the write-back of the lines the kernel
+                   left dirty in L2 (ncu: ~56 of R1's 268 MB of C) is charged
+                   to the step instead of to the next flush.
     mode 'stream': inputs > 2x L2 — steps back to back, one event pair around
                    all K steps (per-step time = total / K)."""
     import torch
@@ -324,13 +354,16 @@ def time_steps(fn, steps, warmup, ctx, flush, sampler=None, mode="flush"):
         flush.zero_()
         starts[k].record()
         fn()
+        if charge_writeback:
+            flush.evict_()
         ends[k].record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     if sampler:
         sampler.__exit__()
     ctx.barrier()
-    return [s.elapsed_time(e) for s, e in zip(starts, ends)], wall
+    sub = flush.evict_ms() if charge_writeback else 0.0
+    return [s.elapsed_time(e) - sub for s, e in zip(starts, ends)], wall
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -704,7 +737,8 @@ def run_suite(args, ctx, flush, policy, peak):
                      "alg_bytes": alg, "launches_per_step": lps, "l2": mode,
                      "scaling": "strong" if ctx.world > 1 else None}
             if mode == "stream":  # also the conservative flushed number
-                tf, _ = time_steps(fn, steps, args.warmup, ctx, flush, mode="flush")
+                tf, _ = time_steps(fn, steps, args.warmup, ctx, flush, mode="flush",
+                                   charge_writeback=w.op == "ger")
                 tfm = ctx.max(sum(tf) / 1000.0)
                 entry["flushed_us_per_step"] = round(tfm / steps * 1e6, 3)
                 entry["flushed_gbs"] = round(alg * steps / tfm / 1e9, 2)

@@ -349,7 +349,9 @@ CABL_API int cabl_host_ger_f64(const double* x, const double* y, double* C, int 
  * exchange: CABL_MGPU_NCCL (collectives) or CABL_MGPU_PEER (the exchange
  * fused into the kernels over NVLink P2P, no collective; needs P2P between
  * every pair).  Both give the same bits.  small_cutoff: as the single-GPU
- * entry points (the reference plan's dot_cutoff). */
+ * entry points (the reference plan's dot_cutoff).  The context's streams do
+ * not wait on the caller's: operands must be ready when a call starts (the
+ * call itself returns only after its results are). */
 enum { CABL_MGPU_NCCL = 0, CABL_MGPU_PEER = 1 };
 typedef struct cabl_mgpu cabl_mgpu;
 

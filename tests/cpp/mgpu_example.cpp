@@ -1,5 +1,5 @@
-// Multi-GPU drop-in use (cabl/nccl.hpp): one process drives every visible
-// device through an NCCL clique.  Checks the sharded results bit for bit
+// Multi-GPU drop-in use (cabl/nccl.hpp over the cabl_mgpu_* C ABI): one
+// process drives every visible device through an NCCL clique.  Checks the sharded results bit for bit
 // against the same per-shard computations run one by one on device 0:
 //   DOT  = rank-ordered sum of the per-shard partials + alpha0 (NCCL all-gather
 //          path and the fused peer-memory path),
@@ -171,13 +171,17 @@ int main() {
         for (int r = 0, o = 0; r < G; o += int(c3_expect[r].len()), ++r)
             std::copy(c3_expect[r].begin(), c3_expect[r].end(), want3.begin() + o);
         try {
-            const std::vector<const float*> full3 =
-                nccl::sharded_gemv_rows_gather_fused(g, Ap, xq, cq, pol);
+            std::vector<DeviceVector<float>> full3;
+            std::vector<DeviceVector<float>*> full3q;
             for (int r = 0; r < G; ++r) {
                 cudaSetDevice(g.device(r));
-                Vector<float> got(m);
-                cudaMemcpy(got.data(), full3[r], m * sizeof(float), cudaMemcpyDeviceToHost);
-                const bool f_ok = got == want3 && cb[r].download() == c3_expect[r];
+                full3.emplace_back(m);
+            }
+            for (int r = 0; r < G; ++r) full3q.push_back(&full3[r]);
+            nccl::sharded_gemv_rows_gather_fused(g, Ap, xq, cq, full3q, pol);
+            for (int r = 0; r < G; ++r) {
+                cudaSetDevice(g.device(r));
+                const bool f_ok = full3[r].download() == want3 && cb[r].download() == c3_expect[r];
                 ok &= f_ok;
                 std::printf("rank %d: gathered c, gather fused into the kernel %s\n", r,
                             f_ok ? "ok" : "MISMATCH");
