@@ -566,6 +566,7 @@ def _time_host_loop(fn, steps, warmup, ctx):
 
 
 E2E_DEPTH = 4
+E2E_SUITE_MAX_BYTES = 3 << 30
 
 
 def _h2d_seconds(nbytes: int, dev) -> float:
@@ -585,7 +586,7 @@ def _h2d_seconds(nbytes: int, dev) -> float:
     return sorted(ts)[len(ts) // 2]
 
 
-def run_e2e(w, ins, policy, ctx, args):
+def run_e2e(w, ins, policy, ctx, args, resident: bool = True):
     """End-to-end through the public API, host<->device copies inside the
     timed loop, wall clock (max over ranks).  Returns (resident, host):
 
@@ -624,7 +625,9 @@ def run_e2e(w, ins, policy, ctx, args):
             "ms_per_step": round(t_max / steps * 1e3, 4), "api": api_host}
     full["pattern"] = ("drop-in call on host buffers: every operand copied H2D from pinned "
                        "memory and the result D2H inside every call")
-    # the link that bounds it: a plain pinned H2D copy of the same bytes, timed here
+    # the link that bounds it: a plain pinned H2D copy of the same bytes, timed
+    # here (PCIe is full duplex: GER's equal D2H can overlap it, so one
+    # direction's time is the bound)
     link_s = _h2d_seconds(h2d, ctx.dev)
     h2d_gbs = h2d / link_s / 1e9
     full["link"] = {"h2d_gbs_measured": round(h2d_gbs, 2),
@@ -634,6 +637,8 @@ def run_e2e(w, ins, policy, ctx, args):
                             "of 5; frac_of_link = that copy's time / the e2e step time"}
     if not w.op.startswith("gemv"):
         return full, None
+    if not resident:
+        return None, full
 
     # resident operator: A stays in HBM, x and c stream in, c streams out —
     # the public GemvPipeline (E2E_DEPTH independent requests in flight, one
@@ -742,6 +747,16 @@ def run_suite(args, ctx, flush, policy, peak):
                 tfm = ctx.max(sum(tf) / 1000.0)
                 entry["flushed_us_per_step"] = round(tfm / steps * 1e6, 3)
                 entry["flushed_gbs"] = round(alg * steps / tfm / 1e9, 2)
+            # the drop-in call on pinned host buffers for every config that fits
+            # a few GiB of host memory (G4 16 GiB and D2 32 GiB per step would
+            # add seconds of PCIe per step to the run)
+            if (ctx.world == 1 and not fused and not args.no_e2e
+                    and w.alg_bytes(1) <= E2E_SUITE_MAX_BYTES):
+                a, b = run_e2e(wl, ins, policy, ctx, args, resident=False)
+                host = b if b is not None else a  # (resident, host) / (host, None)
+                entry["e2e"] = {k: host[k] for k in ("value", "unit", "h2d_bytes_per_step",
+                                                     "d2h_bytes_per_step", "ms_per_step")}
+                entry["e2e"]["frac_of_link"] = host["link"]["frac_of_link"]
             out[wid] = entry
             del ins
         except torch.cuda.OutOfMemoryError as ex:

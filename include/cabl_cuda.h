@@ -363,6 +363,10 @@ CABL_API int cabl_mgpu_size(const cabl_mgpu* ctx);
 CABL_API int cabl_mgpu_device(const cabl_mgpu* ctx, int rank);
 CABL_API void* cabl_mgpu_stream(const cabl_mgpu* ctx, int rank); /* cudaStream_t of rank */
 CABL_API int cabl_mgpu_set_timeout_ms(cabl_mgpu* ctx, uint64_t ms);
+/* Device time of the last completed call on `rank`, from before its first
+ * launch to the end of its last operation on that rank's stream (CUDA
+ * events; the host's wait is not in it).  Multi-GPU time = max over ranks. */
+CABL_API int cabl_mgpu_last_call_ms(cabl_mgpu* ctx, int rank, float* ms);
 
 /* *result = alpha0 + sum over ranks (in rank order) of x[r] . y[r]; the
  * per-rank partials are the single-GPU kernel's bits (alpha0 = 0), summed

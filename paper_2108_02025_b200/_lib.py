@@ -102,6 +102,7 @@ SIGNATURES: dict[str, list] = {
     "cabl_mgpu_device": [vp, i32],
     "cabl_mgpu_stream": [vp, i32],
     "cabl_mgpu_set_timeout_ms": [vp, u64],
+    "cabl_mgpu_last_call_ms": [vp, i32, C.POINTER(f32)],
     "cabl_mgpu_dot_f32": [vp, vp, vp, vp, f32, u64, i32, C.POINTER(f32)],
     "cabl_mgpu_dot_f64": [vp, vp, vp, vp, f64, u64, i32, C.POINTER(f64)],
     "cabl_mgpu_gemv_rm_f32": [vp, vp, vp, u64, vp, vp, u64, i32, vp],

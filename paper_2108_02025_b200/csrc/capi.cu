@@ -531,7 +531,7 @@ int gemv_gather_emulate_impl(int world, const T* const* As, const uint64_t* ms, 
 // the shape allows.  The sweep is ~14% faster on G1/G4.
 bool rm_reference_order() {
     static const bool ref = [] {
-        const char* e = getenv("CABL_GEMV_RM_ORDER");
+        const char* e = tuning_env("CABL_GEMV_RM_ORDER");
         return e && std::string(e) == "reference";
     }();
     return ref;
@@ -807,6 +807,113 @@ int host_gemv(const T* A, int layout, uint64_t m, uint64_t n, const T* x, T* c, 
     return CABL_OK;
 }
 
+// ---- pinned host C: the GER host path as a three-stream pipeline ----------
+// C is read H2D and written back D2H, 2 x m*n*s over PCIe.  Done one after
+// the other the two transfers take twice the link time; PCIe is full duplex,
+// so the path splits C into slabs along its major dimension (whole rows of a
+// row-major C, whole columns of a col-major one — contiguous host bytes) and
+// runs H2D of slab k+1, the GER of slab k and the D2H of slab k-1 at once on
+// three library streams (event-ordered).  Each element is still exactly one
+// fma(x_i, y_j, C_ij): the bits equal the unsplit call's.
+constexpr size_t kPipeSlabMin = size_t(8) << 20;
+constexpr int kPipeMaxSlabs = 32;
+
+struct HostPipe {
+    std::mutex mu;
+    cudaStream_t in = nullptr, work = nullptr, out = nullptr;
+    cudaEvent_t start = nullptr;
+    cudaEvent_t loaded[kPipeMaxSlabs] = {}, done[kPipeMaxSlabs] = {};
+    bool ready = false;
+};
+
+HostPipe& host_pipe(int dev) {
+    static HostPipe p[64];
+    return p[dev & 63];
+}
+
+int pipe_init(HostPipe& p) {
+    if (p.ready) return CABL_OK;
+    CABL_TRY_CUDA(cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking), "pipeline stream");
+    CABL_TRY_CUDA(cudaStreamCreateWithFlags(&p.work, cudaStreamNonBlocking), "pipeline stream");
+    CABL_TRY_CUDA(cudaStreamCreateWithFlags(&p.out, cudaStreamNonBlocking), "pipeline stream");
+    CABL_TRY_CUDA(cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming), "pipeline event");
+    for (int k = 0; k < kPipeMaxSlabs; ++k) {
+        CABL_TRY_CUDA(cudaEventCreateWithFlags(&p.loaded[k], cudaEventDisableTiming), "pipeline event");
+        CABL_TRY_CUDA(cudaEventCreateWithFlags(&p.done[k], cudaEventDisableTiming), "pipeline event");
+    }
+    p.ready = true;
+    return CABL_OK;
+}
+
+template <typename T>
+int host_ger_pipelined(int dev, const T* x, const T* y, T* C, int layout, uint64_t m, uint64_t n,
+                       uint64_t cutoff, cabl_probe* probe, cudaStream_t s) {
+    HostPipe& p = host_pipe(dev);
+    std::lock_guard<std::mutex> lk(p.mu);
+    if (int rc = pipe_init(p)) return rc;
+    // major dimension (slabs) and the vector that follows it
+    const bool rm = layout == CABL_ROW_MAJOR;
+    const uint64_t outer = rm ? m : n, inner = rm ? n : m;
+    const size_t line = size_t(inner) * sizeof(T);
+    const size_t total = size_t(outer) * line;
+    size_t slab = total / kPipeMaxSlabs + 1;
+    if (slab < kPipeSlabMin) slab = kPipeSlabMin;
+    uint64_t lines = (slab + line - 1) / line;
+    if (lines < 1) lines = 1;
+    const uint64_t slabs = (outer + lines - 1) / lines;
+    DevBuf dx, dy, dC;
+    if (int rc = dev_alloc(dx, m * sizeof(T), s)) return rc;
+    if (int rc = dev_alloc(dy, n * sizeof(T), s)) return rc;
+    if (int rc = dev_alloc(dC, total, s)) return rc;
+    // the library streams start after everything already on the caller's
+    // stream (including these allocations)
+    CABL_TRY_CUDA(cudaEventRecord(p.start, s), "pipeline event");
+    for (cudaStream_t q : {p.in, p.work, p.out})
+        CABL_TRY_CUDA(cudaStreamWaitEvent(q, p.start, 0), "pipeline wait");
+    CABL_TRY_CUDA(cudaMemcpyAsync(dx.p, x, m * sizeof(T), cudaMemcpyHostToDevice, p.in), "H2D x");
+    CABL_TRY_CUDA(cudaMemcpyAsync(dy.p, y, n * sizeof(T), cudaMemcpyHostToDevice, p.in), "H2D y");
+    T* dCt = static_cast<T*>(dC.p);
+    const T* dxt = static_cast<const T*>(dx.p);
+    const T* dyt = static_cast<const T*>(dy.p);
+    const int rc = [&]() -> int {
+    for (uint64_t k = 0; k < slabs; ++k) {
+        const uint64_t o0 = k * lines, cnt = (outer - o0 < lines) ? outer - o0 : lines;
+        const size_t off = size_t(o0) * inner, bytes = size_t(cnt) * line;
+        CABL_TRY_CUDA(cudaMemcpyAsync(dCt + off, C + off, bytes, cudaMemcpyHostToDevice, p.in), "H2D C");
+        CABL_TRY_CUDA(cudaEventRecord(p.loaded[k], p.in), "pipeline event");
+        CABL_TRY_CUDA(cudaStreamWaitEvent(p.work, p.loaded[k], 0), "pipeline wait");
+        // the slab: rows o0.. of a row-major C take x[o0..]; columns o0.. of
+        // a col-major C take y[o0..]
+        const int rc = rm ? ger_impl<T>(dxt + o0, dyt, dCt + off, layout, cnt, n, cutoff,
+                                        k == 0 ? probe : nullptr, p.work)
+                          : ger_impl<T>(dxt, dyt + o0, dCt + off, layout, m, cnt, cutoff,
+                                        k == 0 ? probe : nullptr, p.work);
+        if (rc) return rc;
+        CABL_TRY_CUDA(cudaEventRecord(p.done[k], p.work), "pipeline event");
+        CABL_TRY_CUDA(cudaStreamWaitEvent(p.out, p.done[k], 0), "pipeline wait");
+        CABL_TRY_CUDA(cudaMemcpyAsync(C + off, dCt + off, bytes, cudaMemcpyDeviceToHost, p.out), "D2H C");
+    }
+    return CABL_OK;
+    }();
+    if (rc) { // nothing may still use the staging buffers when they are freed
+        for (cudaStream_t q : {p.in, p.work, p.out}) cudaStreamSynchronize(q);
+        return rc;
+    }
+    // the caller's stream frees the staging buffers after the last D2H
+    CABL_TRY_CUDA(cudaEventRecord(p.start, p.out), "pipeline event");
+    CABL_TRY_CUDA(cudaStreamWaitEvent(s, p.start, 0), "pipeline wait");
+    return CABL_OK;
+}
+
+bool host_pinned(const void* h) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 template <typename T>
 int host_ger(const T* x, const T* y, T* C, int layout, uint64_t m, uint64_t n, uint64_t cutoff,
              cabl_probe* probe, void* stream) {
@@ -819,6 +926,15 @@ int host_ger(const T* x, const T* y, T* C, int layout, uint64_t m, uint64_t n, u
     if (int rc = current_device(&dev)) return rc;
     keep_pool_warm(dev);
     cudaStream_t s = as_stream(stream);
+    // pinned (page-locked) C larger than one slab: the full-duplex pipeline
+    if (m && n && size_t(m) * n * sizeof(T) > 2 * kPipeSlabMin && host_pinned(C)) {
+        if (int rc = host_ger_pipelined<T>(dev, x, y, C, layout, m, n, cutoff, probe, s)) {
+            cudaStreamSynchronize(s);
+            return rc;
+        }
+        CABL_TRY_CUDA(cudaStreamSynchronize(s), "ger sync");
+        return CABL_OK;
+    }
     {
         DevBuf dx, dy, dC;
         if (int rc = dev_alloc(dx, m * sizeof(T), s)) return rc;

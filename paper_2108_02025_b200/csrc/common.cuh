@@ -15,6 +15,20 @@
 
 namespace cabl_dev {
 
+// Tuning / A-B switches (CABL_DOT_CFG, CABL_GEMV_RM_ORDER, CABL_CM_TILE, ...;
+// DESIGN.md §4 "Environment knobs") pick other launch shapes or kernels, and
+// so may change the last bits of a result.  They are honoured only when the
+// process also sets CABL_TUNING=1: a shipped process's results never depend
+// on its environment.  (Operational settings — timeouts, the NCCL library,
+// PDL — are read with plain getenv: they never change bits.)
+inline const char* tuning_env(const char* name) {
+    static const bool on = [] {
+        const char* e = getenv("CABL_TUNING");
+        return e != nullptr && e[0] == '1' && e[1] == '\0';
+    }();
+    return on ? getenv(name) : nullptr;
+}
+
 constexpr int kWarp = 32;
 
 // 32-byte vector of T.

@@ -95,7 +95,7 @@ constexpr uint64_t kChunkVecs = 65536; // at most 2 MiB of x and 2 MiB of y (fp3
 // (tuning only).
 inline uint64_t chunk_vecs(uint64_t nvec) {
     static const uint64_t forced = [] {
-        const char* e = getenv("CABL_DOT_CHUNK");
+        const char* e = tuning_env("CABL_DOT_CHUNK");
         return e ? uint64_t(atoll(e)) : uint64_t(0);
     }();
     if (forced) return forced;
@@ -149,7 +149,7 @@ struct DotCfg {
 inline DotCfg dot_cfg() {
     static const DotCfg cfg = [] {
         DotCfg c{kDotBlock, kDotUnroll, kDotCtasPerSm};
-        if (const char* e = getenv("CABL_DOT_CFG")) sscanf(e, "%d,%d,%d", &c.block, &c.unroll, &c.minb);
+        if (const char* e = tuning_env("CABL_DOT_CFG")) sscanf(e, "%d,%d,%d", &c.block, &c.unroll, &c.minb);
         return c;
     }();
     return cfg;
@@ -204,7 +204,7 @@ cudaError_t dot_dispatch(unsigned grid, const T* x, const T* y, uint64_t n, int 
 // large operands (2ns >= 512 MiB) take the chunked, queue-scheduled kernel
 inline bool dot_chunked(uint64_t n, size_t s, bool small, bool vec_ok) {
     static const int forced = [] {
-        const char* e = getenv("CABL_DOT_CHUNKED");
+        const char* e = tuning_env("CABL_DOT_CHUNKED");
         return e ? atoi(e) : -1;
     }();
     if (small || !vec_ok) return false;

@@ -802,7 +802,7 @@ constexpr uint64_t kBulkScalarMaxRows = 1024;
 inline uint64_t cm_single_max() {
     static const uint64_t v = [] {
         unsigned long a = kSingleTileRows, b = kSplitTileRows;
-        if (const char* e = getenv("CABL_CM_TILE")) sscanf(e, "%lu,%lu", &a, &b);
+        if (const char* e = tuning_env("CABL_CM_TILE")) sscanf(e, "%lu,%lu", &a, &b);
         return uint64_t(a < kSplitMaxRows ? a : kSplitMaxRows);
     }();
     return v;
@@ -810,7 +810,7 @@ inline uint64_t cm_single_max() {
 inline uint64_t cm_tile_rows() {
     static const uint64_t v = [] {
         unsigned long a = kSingleTileRows, b = kSplitTileRows;
-        if (const char* e = getenv("CABL_CM_TILE")) sscanf(e, "%lu,%lu", &a, &b);
+        if (const char* e = tuning_env("CABL_CM_TILE")) sscanf(e, "%lu,%lu", &a, &b);
         return uint64_t(b);
     }();
     return v;
@@ -828,7 +828,7 @@ constexpr uint64_t kFinalBudget = 16384; // partials one finishing CTA sums
 
 inline uint64_t choose_tile_rows(uint64_t m, uint64_t max_mt, int vec_elems) {
     if (m < cm_single_max()) return m;
-    if (getenv("CABL_CM_TILE")) return cm_tile_rows();
+    if (tuning_env("CABL_CM_TILE")) return cm_tile_rows();
     const uint64_t sms = uint64_t(sm_count());
     uint64_t best = kSplitTileRows;
     double best_score = -1.0;
@@ -964,7 +964,7 @@ inline BulkCfg bulk_cfg() {
         // 3x48 KB 299.1 us, 2x80 299.7, 4x36 299.7, 3x40 300.2, 2x64 300.9,
         // 3x64 307.0, 4x48 308.1, 2x48 311.8, 6x32 315.1
         BulkCfg b{3, 49152};
-        if (const char* e = getenv("CABL_BULK")) { // "stages,KiB" (tuning only)
+        if (const char* e = tuning_env("CABL_BULK")) { // "stages,KiB" (tuning only)
             int st = 6, kb = 32;
             if (sscanf(e, "%d,%d", &st, &kb) == 2) b = BulkCfg{st, unsigned(kb) * 1024u};
         }
@@ -1053,7 +1053,7 @@ void bulk_scalar_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const 
 
 inline int split_mode() {
     static const int v = [] {
-        const char* e = getenv("CABL_CM_SPLIT");
+        const char* e = tuning_env("CABL_CM_SPLIT");
         return e ? atoi(e) : 1;
     }();
     return v; // 1 = bulk-copy pipeline, 0 = register loads
@@ -1067,7 +1067,7 @@ template <typename T> bool tall_vec_ok(const T* A, const T* c, uint64_t m) {
 // 2-D split (A/B only).
 inline bool bulk_any_align() {
     static const bool on = [] {
-        const char* e = getenv("CABL_CM_BULK_ANY");
+        const char* e = tuning_env("CABL_CM_BULK_ANY");
         return e ? atoi(e) != 0 : true;
     }();
     return on;
@@ -1079,7 +1079,7 @@ enum CmPath { kPathTallVec, kPathTallScalar, kPathBulk, kPathBulkScalar, kPathSp
 // CABL_CM_REALIGN=0 keeps misaligned columns on the scalar 2-D split (A/B only).
 inline bool realign_enabled() {
     static const bool on = [] {
-        const char* e = getenv("CABL_CM_REALIGN");
+        const char* e = tuning_env("CABL_CM_REALIGN");
         return e ? atoi(e) != 0 : true;
     }();
     return on;
@@ -1097,7 +1097,7 @@ inline bool realign_enabled() {
 // CABL_CM_TALL_MIN overrides (tuning only).
 inline uint64_t tall_min_units() {
     static const long forced = [] {
-        const char* e = getenv("CABL_CM_TALL_MIN");
+        const char* e = tuning_env("CABL_CM_TALL_MIN");
         return e ? atol(e) : -1L;
     }();
     return forced > 0 ? uint64_t(forced) : uint64_t(sm_count()) / 2;
@@ -1194,7 +1194,7 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         // dynamic unit queue for large matrices (2^20 x 256 fp64: 310 -> 301 us),
         // static unit ranges otherwise; CABL_GEMV_DYN=0|1 overrides (tuning)
         static const int forced = [] {
-            const char* e = getenv("CABL_GEMV_DYN");
+            const char* e = tuning_env("CABL_GEMV_DYN");
             return e ? atoi(e) : -1;
         }();
         const bool dyn = forced >= 0 ? forced != 0 : m * n * sizeof(T) >= queue_threshold_bytes();

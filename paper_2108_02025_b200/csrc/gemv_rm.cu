@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kRmBlock)
 // adds the row-count condition.
 inline uint64_t rm_lane_max_bytes() {
     static const uint64_t v = [] {
-        const char* e = getenv("CABL_RM_LANE_MAX");
+        const char* e = tuning_env("CABL_RM_LANE_MAX");
         return e ? uint64_t(atoll(e)) : uint64_t(256);
     }();
     return v;
@@ -483,7 +483,7 @@ template <typename T> bool rm_vec_ok(const T* A, const T* x, uint64_t n) {
 // was slower everywhere).  CABL_RM_FEW_MAX overrides the row limit (tuning).
 inline bool rm_few_rows(uint64_t m, uint64_t n, size_t elem) {
     static const uint64_t max_rows = [] {
-        const char* e = getenv("CABL_RM_FEW_MAX");
+        const char* e = tuning_env("CABL_RM_FEW_MAX");
         return e ? uint64_t(atoll(e)) : uint64_t(16);
     }();
     return m <= max_rows && n * elem >= 65536;
@@ -498,7 +498,7 @@ constexpr uint64_t kRmLongMinGroups = 128;  // 2-row groups: m >= 255
 template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n) {
     const bool vec = rm_vec_ok(A, x, n);
     static const int forced = [] {
-        const char* e = getenv("CABL_GEMV_RM_MODE");
+        const char* e = tuning_env("CABL_GEMV_RM_MODE");
         return e ? atoi(e) : -2;
     }();
     // one thread per row (3 vector loads, 4 scalar loads): short rows, and
@@ -526,7 +526,7 @@ template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n
     const uint64_t sms = uint64_t(sm_count());
     const bool short_rows = n / Vec<T>::N <= uint64_t(kRmBlock) * 2 * 2;
     static const bool few = [] {
-        const char* e = getenv("CABL_RM_FEW_GROUPS");
+        const char* e = tuning_env("CABL_RM_FEW_GROUPS");
         return e ? atoi(e) != 0 : true;
     }();
     const uint64_t short_min = few ? kRmShortMinGroups : 6 * 2 * sms;
@@ -549,7 +549,7 @@ template <typename T> uint64_t rm_chunk_vecs(uint64_t m, uint64_t n) {
 // Rows per unit of the chunked kernel (CABL_RM_CHUNK_ROWS overrides: tuning).
 inline int rm_chunk_rows(uint64_t m) {
     static const int forced = [] {
-        const char* e = getenv("CABL_RM_CHUNK_ROWS");
+        const char* e = tuning_env("CABL_RM_CHUNK_ROWS");
         return e ? atoi(e) : 0;
     }();
     if (forced == 1 || forced == 2) return forced;
@@ -580,7 +580,7 @@ struct SweepCfg {
 // overrides the size rule (tuning only).
 inline bool use_dyn_queue(uint64_t bytes) {
     static const int forced = [] {
-        const char* e = getenv("CABL_GEMV_DYN");
+        const char* e = tuning_env("CABL_GEMV_DYN");
         return e ? atoi(e) : -1;
     }();
     if (forced >= 0) return forced != 0;
@@ -612,7 +612,7 @@ unsigned sweep_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, unsigned
 template <typename T> SweepCfg sweep_choice(uint64_t m, uint64_t n, int mode) {
     static const SweepCfg forced = [] {
         SweepCfg f{0, 0, 0};
-        if (const char* e = getenv("CABL_RM_SWEEP")) sscanf(e, "%d,%d,%d", &f.R, &f.KV, &f.minb);
+        if (const char* e = tuning_env("CABL_RM_SWEEP")) sscanf(e, "%d,%d,%d", &f.R, &f.KV, &f.minb);
         return f;
     }();
     const SweepCfg table[] = {{2, 4, 2}, {2, 8, 1}, {4, 1, 4}, {4, 2, 2}, {4, 4, 1}, {8, 1, 2}, {8, 2, 1},
@@ -666,7 +666,7 @@ constexpr uint64_t kLaneScalarMaxN = 24;
 // CABL_RM_SCALAR_CTA=0|1 overrides (A/B only).
 inline bool rm_scalar_cta(uint64_t m, uint64_t n) {
     static const int forced = [] {
-        const char* e = getenv("CABL_RM_SCALAR_CTA");
+        const char* e = tuning_env("CABL_RM_SCALAR_CTA");
         return e ? atoi(e) : -1;
     }();
     if (forced >= 0) return forced != 0;

@@ -298,7 +298,7 @@ void ordered_launch_cfg(const T* A, uint64_t m, uint64_t n, const T* x, T* c, cu
 // streams read 1 KB at a time (the sweep reads 8 KB runs), not the copy engine.
 int ordered_cfg() {
     static const int cfg = [] {
-        const char* e = std::getenv("CABL_ORD_CFG");
+        const char* e = tuning_env("CABL_ORD_CFG");
         if (!e) return 1;
         if (!std::strcmp(e, "512,5,1")) return 0;
         if (!std::strcmp(e, "1024,3,1")) return 1;

@@ -453,7 +453,7 @@ struct GerAnyCfg {
 inline GerAnyCfg ger_any_cfg(size_t elem) {
     static const GerAnyCfg forced = [] {
         GerAnyCfg c{-1, 0, 0, 0};
-        if (const char* e = getenv("CABL_GER_ANY_CFG"))
+        if (const char* e = tuning_env("CABL_GER_ANY_CFG"))
             sscanf(e, "%d,%d,%d,%d", &c.ys, &c.u, &c.early, &c.per_sm);
         return c;
     }();
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(kGerBlock)
 // order, 2 tiles from an atomic counter (default).
 inline int ger_mode() {
     static const int m = [] {
-        const char* e = getenv("CABL_GER_MODE");
+        const char* e = tuning_env("CABL_GER_MODE");
         return e ? atoi(e) : kGerDefaultMode;
     }();
     return m;
@@ -547,7 +547,7 @@ inline int ger_mode() {
 // CABL_GER_ANY=0 sends odd / misaligned rows back to the scalar flat sweep (A/B only).
 inline bool ger_any_enabled() {
     static const bool on = [] {
-        const char* e = getenv("CABL_GER_ANY");
+        const char* e = tuning_env("CABL_GER_ANY");
         return e ? atoi(e) != 0 : true;
     }();
     return on;

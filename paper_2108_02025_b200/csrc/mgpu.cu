@@ -194,7 +194,8 @@ struct cabl_mgpu {
     std::vector<int> devs;
     std::vector<ncclComm_t> comms;
     std::vector<cudaStream_t> streams;
-    std::vector<cudaEvent_t> done;
+    std::vector<cudaEvent_t> start, done; // per rank, around each call's device work
+    bool timed = false;                    // start events recorded for the last call
     std::vector<void*> scratch;
     std::vector<size_t> scratch_bytes;
     uint64_t timeout_ms = 60000;
@@ -268,6 +269,18 @@ int set_dev(cabl_mgpu* c, int r) {
     return CABL_OK;
 }
 
+// the device-side start of a call, on every rank's stream (after validation,
+// before the first launch): cabl_mgpu_last_call_ms measures from here to the
+// end of the call's last operation on that rank
+int mark_start(cabl_mgpu* c) {
+    c->timed = false;
+    for (size_t r = 0; r < c->devs.size(); ++r) {
+        MG_RC(set_dev(c, int(r)));
+        MG_CUDA(cudaEventRecord(c->start[r], c->streams[r]), "cudaEventRecord");
+    }
+    return CABL_OK; // wait_all sets `timed` once the call has completed
+}
+
 // Block until every device's stream has drained, watching NCCL for
 // asynchronous errors and the clock for the context's timeout.
 int wait_all(cabl_mgpu* c, bool watch_nccl, const char* what) {
@@ -313,6 +326,7 @@ int wait_all(cabl_mgpu* c, bool watch_nccl, const char* what) {
         }
         if (++spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
+    c->timed = true;
     return CABL_OK;
 }
 
@@ -436,6 +450,7 @@ int mgpu_dot(cabl_mgpu* c, const T* const* x, const T* const* y, const uint64_t*
     }
     if (exchange == CABL_MGPU_PEER) {
         MG_RC(peer_set(c, c->dot_mb, 0));
+        MG_RC(mark_start(c));
         for (int r = 0; r < G; ++r) {
             MG_RC(set_dev(c, r));
             MG_RC(dot_peer1(x[r], y[r], n[r], alpha0, sc[r] + G + 1, c->dot_mb.mboxes.data(), G, r,
@@ -444,6 +459,7 @@ int mgpu_dot(cabl_mgpu* c, const T* const* x, const T* const* y, const uint64_t*
         MG_RC(wait_all(c, false, "dot (peer exchange)"));
         MG_RC(check_peer_faults(c, c->dot_mb, "dot (peer exchange)"));
     } else {
+        MG_RC(mark_start(c));
         for (int r = 0; r < G; ++r) {
             MG_RC(set_dev(c, r));
             MG_RC(dot1(x[r], y[r], n[r], T(0), sc[r], cutoff, c->streams[r]));
@@ -499,6 +515,7 @@ int mgpu_gemv_rm(cabl_mgpu* c, const T* const* A, const uint64_t* m, uint64_t n,
                                               "short rows, unaligned): use CABL_MGPU_NCCL");
         }
         MG_RC(peer_set(c, c->gather, 2 * size_t(off[G]) * sizeof(T)));
+        MG_RC(mark_start(c));
         for (int r = 0; r < G; ++r) {
             MG_RC(set_dev(c, r));
             if (int rc = gather1(A[r], m[r], n, x[r], cs[r], off[r], off[G], c->gather.bufs.data(),
@@ -518,6 +535,7 @@ int mgpu_gemv_rm(cabl_mgpu* c, const T* const* A, const uint64_t* m, uint64_t n,
         MG_RC(wait_all(c, false, "gemv_rm (peer gather)"));
         return check_peer_faults(c, c->gather, "gemv_rm (peer gather)");
     }
+    MG_RC(mark_start(c));
     for (int r = 0; r < G; ++r) {
         MG_RC(set_dev(c, r));
         MG_RC(gemv_rm1(A[r], m[r], n, x[r], cs[r], cutoff, c->streams[r]));
@@ -559,6 +577,7 @@ int mgpu_gemv_cm_cols(cabl_mgpu* c, const T* const* A, uint64_t m, const uint64_
         part[r] = static_cast<T*>(p);
     }
     if (exchange == CABL_MGPU_PEER) MG_RC(peer_set(c, c->rows, 2 * 8 * size_t(m) * sizeof(T)));
+    MG_RC(mark_start(c));
     for (int r = 0; r < G; ++r) {
         MG_RC(set_dev(c, r));
         MG_CUDA(cudaMemsetAsync(part[r], 0, m * sizeof(T), c->streams[r]), "memset");
@@ -600,6 +619,7 @@ int mgpu_ger_rm(cabl_mgpu* c, const T* const* x, const uint64_t* m, const T* con
     for (int r = 0; r < G; ++r)
         if (m[r] > 0 && n > 0 && (!x[r] || !y[r] || !C[r]))
             return mfail(CABL_EINVAL, "cabl_mgpu_ger_rm: null operand");
+    MG_RC(mark_start(c));
     for (int r = 0; r < G; ++r) {
         MG_RC(set_dev(c, r));
         MG_RC(ger_rm1(x[r], y[r], C[r], m[r], n, cutoff, c->streams[r]));
@@ -658,9 +678,12 @@ CABL_API int cabl_mgpu_init(const int* devices, int count, cabl_mgpu** ctx) {
         cudaEvent_t ev = nullptr;
         cudaError_t e = cudaSetDevice(c->devs[r]);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        cudaEvent_t ev0 = nullptr;
+        if (e == cudaSuccess) e = cudaEventCreate(&ev);
+        if (e == cudaSuccess) e = cudaEventCreate(&ev0);
         c->streams.push_back(s);
         c->done.push_back(ev);
+        c->start.push_back(ev0);
         if (e != cudaSuccess) {
             const int rc = cuda_err(e, "stream/event");
             cabl_mgpu_finalize(c);
@@ -689,6 +712,7 @@ CABL_API int cabl_mgpu_finalize(cabl_mgpu* c) {
             cudaSetDevice(c->devs[r]);
             if (r < c->scratch.size() && c->scratch[r]) cudaFree(c->scratch[r]);
             if (r < c->done.size() && c->done[r]) cudaEventDestroy(c->done[r]);
+            if (r < c->start.size() && c->start[r]) cudaEventDestroy(c->start[r]);
             if (r < c->streams.size() && c->streams[r]) cudaStreamDestroy(c->streams[r]);
             if (r < c->comms.size() && c->comms[r] && N.h) N.CommDestroy(c->comms[r]);
         }
@@ -706,6 +730,16 @@ CABL_API int cabl_mgpu_device(const cabl_mgpu* c, int rank) {
 
 CABL_API void* cabl_mgpu_stream(const cabl_mgpu* c, int rank) {
     return (c && rank >= 0 && rank < int(c->streams.size())) ? c->streams[rank] : nullptr;
+}
+
+CABL_API int cabl_mgpu_last_call_ms(cabl_mgpu* c, int rank, float* ms) {
+    if (!c || !ms || rank < 0 || rank >= int(c->devs.size()))
+        return mfail(CABL_EINVAL, "cabl_mgpu_last_call_ms: null argument or rank out of range");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!c->timed) return mfail(CABL_EINVAL, "cabl_mgpu_last_call_ms: no completed call to time");
+    MG_RC(set_dev(c, rank));
+    MG_CUDA(cudaEventElapsedTime(ms, c->start[rank], c->done[rank]), "cudaEventElapsedTime");
+    return CABL_OK;
 }
 
 CABL_API int cabl_mgpu_set_timeout_ms(cabl_mgpu* c, uint64_t ms) {

@@ -81,6 +81,16 @@ class MultiGpu:
     def set_timeout_ms(self, ms: int) -> None:
         _lib.call("cabl_mgpu_set_timeout_ms", self._ctx, int(ms))
 
+    def last_call_ms(self) -> list[float]:
+        """Device time of the last call on every rank (CUDA events around its
+        work on the rank's stream); the multi-GPU time is the max."""
+        out = []
+        for r in range(len(self.devices)):
+            v = C.c_float()
+            _lib.call("cabl_mgpu_last_call_ms", self._ctx, r, C.byref(v))
+            out.append(v.value)
+        return out
+
     # -- checks shared by the ops
     def _shards(self, what: str, *groups) -> str:
         G = len(self.devices)

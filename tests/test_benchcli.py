@@ -104,3 +104,94 @@ def test_cli_fp32_rectangular_baseline_shapes(cuda, tmp_path):
     recs = B.parse_csv(csv.read_text())
     assert [(x.m, x.n) for x in recs] == [(4096, 4096), (256, 262144), (262144, 256)]
     assert all(x.dtype == "f64" and x.roofline_frac > 0.2 for x in recs)
+
+
+def test_gpus_layout_and_dram_columns_round_trip():
+    r = B.BenchRecord("gemv-col", 256, 1 << 20, 1, 3, 3.0e-4, 3.1e-4, 1.7e3, 2.0, "f64", 7.0e3,
+                      0.53, gpus=2, layout="col-major", alg_bytes=2155876352,
+                      hbm_bound_s=2155876352 / (2 * 6552.6e9), dram_bytes=2.156e9,
+                      dram_per_alg=1.0001)
+    text = B.emit_csv([r])
+    head = text.splitlines()[0]
+    assert head == B.CSV_HEADER + B.CSV_GPU_SUFFIX + B.CSV_BOUNDS_SUFFIX
+    assert head.split(",")[12:14] == ["gpus", "layout"]
+    back = B.parse_csv(text)[0]
+    assert (back.gpus, back.layout, back.dram_per_alg) == (2, "col-major", 1.0001)
+    assert B.emit_csv([back]) == text
+
+
+def test_round1_documents_still_parse():
+    old = B.CSV_HEADER + B.CSV_GPU_SUFFIX_R1 + "\n" + "ger,64,64,1,3,1e-05,2e-05,3,4,f32,5,0.5\n"
+    r = B.parse_csv(old)[0]
+    assert r.gpus == 1 and r.layout == "row-major" and r.gbs == 5
+    oldb = (B.CSV_HEADER + B.CSV_GPU_SUFFIX_R1 + B.CSV_BOUNDS_SUFFIX_R1 + "\n"
+            + "dot,0,64,1,3,1e-05,2e-05,3,4,f32,5,0.5,512,7e-11\n")
+    r = B.parse_csv(oldb)[0]
+    assert r.alg_bytes == 512 and r.dram_bytes != r.dram_bytes  # nan: not measured
+
+
+def test_alg_bytes_count_replicated_operands_per_gpu():
+    # x once per GPU for row blocks, y once per GPU for GER
+    assert B._alg_bytes("gemv-row", 65536, 65536, 4, 8) == 17182490624
+    assert B._alg_bytes("ger", 8192, 8192, 4, 4) == 537034752
+    assert B._alg_bytes("dot", 0, 1 << 32, 4, 8) == 1 << 35
+    assert B._split("gemv-col", 256, 1000, 3) == [(0, 334), (334, 667), (667, 1000)]
+    assert B._split("ger", 10, 7, 4) == [(0, 3), (3, 6), (6, 8), (8, 10)]
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_ger_exact_sample_is_ger_ref_bitwise(dtype):
+    """The GER spot check's exact-rational rule agrees with the compiled
+    oracle's ger_ref (one fma per element) and catches a one-ulp error."""
+    import numpy as np
+
+    from oracle import oracle as O
+    rng = np.random.default_rng(3)
+    npdt = np.float32 if dtype == torch.float32 else np.float64
+    m, n = 37, 53
+    x = rng.uniform(-1, 1, m).astype(npdt)
+    y = rng.uniform(-1, 1, n).astype(npdt)
+    C0 = rng.uniform(-1, 1, m * n).astype(npdt)
+    C1 = C0.copy()
+    O.ger_ref(x, y, C1, 0)
+    t = lambda a: torch.from_numpy(a)  # noqa: E731
+    assert B._ger_exact_sample(t(x), t(y), t(C0), t(C1), m, n, dtype, k=m * n) is None
+    C1[5 * n + 7] = np.nextafter(C1[5 * n + 7], npdt(2))
+    assert "C(5,7)" in B._ger_exact_sample(t(x), t(y), t(C0), t(C1), m, n, dtype, k=m * n)
+
+
+@pytest.mark.gpu
+def test_bounds_measured_dram_matches_algorithmic_bytes(cuda, tmp_path):
+    """--bounds --measure-dram: ncu's DRAM bytes for a G1-shaped row-major
+    GEMV are the algorithmic bytes (no re-reads)."""
+    import shutil
+    if not (shutil.which("ncu") or Path("/usr/local/cuda/bin/ncu").exists()):
+        pytest.skip("ncu not installed")
+    csv = tmp_path / "b.csv"
+    r = subprocess.run([sys.executable, "-m", "paper_2108_02025_b200.benchcli", "--kernel",
+                        "gemv-row", "--sizes", "8192", "--dtype", "f32", "--reps", "3",
+                        "--bounds", "--measure-dram", "--csv", str(csv)],
+                       capture_output=True, text=True, cwd=ROOT, timeout=900)
+    if r.returncode != 0 and "ncu failed" in r.stderr and "closed" in r.stderr.lower():
+        pytest.skip("ncu is closed on this pool")
+    assert r.returncode == 0, r.stderr
+    rec = B.parse_csv(csv.read_text())[0]
+    assert rec.alg_bytes == 268533760
+    assert 0.95 <= rec.dram_per_alg <= 1.10, rec.dram_per_alg
+
+
+@pytest.mark.gpu
+def test_cli_through_the_multi_gpu_c_abi(cuda, tmp_path):
+    """--mgpu: every kernel through the cabl_mgpu C ABI (all visible GPUs with
+    --gpus; here world = 1), spot-checked, device-timed, gpus column set."""
+    csv = tmp_path / "m.csv"
+    g = torch.cuda.device_count()
+    r = subprocess.run([sys.executable, "-m", "paper_2108_02025_b200.benchcli", "--kernel", "all",
+                        "--sizes", "256,4096", "--rect", "256x262144", "--dtype", "f32",
+                        "--reps", "3", "--gpus", str(g), "--mgpu", "--csv", str(csv)],
+                       capture_output=True, text=True, cwd=ROOT, timeout=900)
+    assert r.returncode == 0, r.stderr
+    recs = B.parse_csv(csv.read_text())
+    assert len(recs) == 2 + 3 * 3
+    assert all(x.gpus == g and x.gbs > 0 for x in recs)
+    assert {x.layout for x in recs} == {"vector", "row-major", "col-major"}

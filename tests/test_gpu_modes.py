@@ -57,7 +57,7 @@ VARIANTS = [
 
 
 def _run(env_extra):
-    env = dict(os.environ, **env_extra)
+    env = dict(os.environ, CABL_TUNING="1", **env_extra)
     r = subprocess.run([sys.executable, "-c", SCRIPT % {"root": str(ROOT)}], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr
@@ -96,9 +96,31 @@ print(json.dumps(c.cpu().numpy().astype(float).tolist()))
     truth, rowabs = O.gemv_truth(A, 0, x, c0)
     for mode in ("0", "1", "2", "3", "7"):
         r = subprocess.run([sys.executable, "-c", script % {"root": str(ROOT)}],
-                           env=dict(os.environ, CABL_GEMV_RM_MODE=mode), capture_output=True,
+                           env=dict(os.environ, CABL_TUNING="1", CABL_GEMV_RM_MODE=mode), capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0, r.stderr
         got = np.array(json.loads(r.stdout.strip().splitlines()[-1]))
         bound = (n / 32 + 80) * np.finfo(np.float32).eps * (rowabs + np.abs(c0))
         assert np.all(np.abs(got - truth) <= bound), mode
+
+
+def test_results_do_not_depend_on_the_environment_without_cabl_tuning(cuda):
+    """Bit-changing tuning knobs (another DOT launch shape, the reference-order
+    row-major kernel, other col-major tiles) are ignored unless CABL_TUNING=1:
+    a process that sets them alone gets the default bits.  With CABL_TUNING=1
+    the same knobs take effect (the DOT launch shape changes the DOT bits)."""
+    knobs = {"CABL_DOT_CFG": "256,1,8", "CABL_GEMV_RM_ORDER": "reference",
+             "CABL_CM_TILE": "512,1024", "CABL_GEMV_RM_MODE": "3"}
+    base = dict(os.environ)
+    base.pop("CABL_TUNING", None)
+
+    def run(env):
+        r = subprocess.run([sys.executable, "-c", SCRIPT % {"root": str(ROOT)}], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr
+        return json.loads(r.stdout.strip().splitlines()[-1])
+
+    ref = run(base)
+    assert run(dict(base, **knobs)) == ref
+    tuned = run(dict(base, CABL_TUNING="1", **knobs))
+    assert tuned != ref

@@ -166,7 +166,7 @@ def test_gemv_row_major_reference_order_mode_subprocess(cuda, cfg):
     if os.environ.get("CABL_GEMV_RM_ORDER") == "reference":
         pytest.skip("already the reference-order process")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CABL_GEMV_RM_ORDER="reference")
+    env = dict(os.environ, CABL_TUNING="1", CABL_GEMV_RM_ORDER="reference")
     if cfg:
         env["CABL_ORD_CFG"] = cfg
     r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py",
@@ -187,7 +187,11 @@ CM_SHAPES = [(3, 3), (8, 8), (257, 259), (1000, 1000), (256, 65536), (2047, 300)
              # tall from half the SMs' worth of 256-vector units up (bitwise)
              (151_552, 33), (200_000, 20), (151_544, 7),
              # odd m >= 1024: the realigning split (aligned 256-bit loads + warp shuffles)
-             (1025, 3000), (8193, 2000), (3001, 5003), (12_345, 777), (100_003, 64)]
+             (1025, 3000), (8193, 2000), (3001, 5003), (12_345, 777), (100_003, 64),
+             # aligned mid-size m: the row-tiled bulk ring (ragged last tile and
+             # column parts, stages wider and narrower than the x slot, n < parts)
+             (512, 70_001), (1000, 20_003), (4096, 16_384), (4104, 5_001), (12_000, 5_592),
+             (16_384, 4_096), (24_576, 777), (65_536, 1_030), (131_072, 130), (8_192, 3)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -473,6 +477,28 @@ def test_host_staged_copies_equal_device_path(cuda, pinned):
     assert torch.equal(Cd.data.cpu(), Ch.data)
 
 
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("layout", ["row", "col"])
+@pytest.mark.parametrize("m,n", [(8192, 8192), (3001, 5003), (40_000, 777)])
+def test_host_ger_pipeline_equals_device_path(cuda, dtype, layout, m, n):
+    """Pinned host C above two slabs: the full-duplex pipeline (H2D of slab
+    k+1, GER of slab k and D2H of slab k-1 on three streams, capi.cu
+    host_ger_pipelined) — bit for bit the device-resident call, ragged last
+    slab included, and x / y slices at the slab offsets."""
+    import paper_2108_02025_b200 as cb
+    lay = cb.Layout.RowMajor if layout == "row" else cb.Layout.ColMajor
+    C0 = dev_uniform(m * n, dtype, 5, cuda)
+    gx, gy = dev_uniform(m, dtype, 1, cuda), dev_uniform(n, dtype, 2, cuda)
+    Cd = cb.DenseMatrix.wrap(C0.clone(), m, n, lay)
+    cb.ger(gx, gy, Cd, policy())
+    Ch = cb.DenseMatrix.wrap(C0.cpu().pin_memory(), m, n, lay)
+    cb.ger(gx.cpu(), gy.cpu(), Ch, policy())
+    assert torch.equal(Cd.data.cpu(), Ch.data)
+    want = np_of(C0).copy()
+    O.ger_ref(np_of(gx), np_of(gy), want, int(lay))
+    np.testing.assert_array_equal(Ch.data.numpy(), want)
+
+
 # ------------------------------------------------- full BASELINE sizes
 def test_generator_matches_host_oracle(cuda):
     for dtype, npdt in [(torch.float32, np.float32), (torch.float64, np.float64)]:
@@ -486,9 +512,9 @@ def test_generator_matches_host_oracle(cuda):
 
 @pytest.mark.slow
 def test_gemv_65536_square_fp32_sampled_rows(cuda):
-    """BASELINE config 5 (G4): 16 GiB A.  Rows are checked against the oracle
-    on a sample (the oracle's cost is the only limit; every row of the GPU
-    result is checked against an fp64 torch matvec for the truth bound)."""
+    """BASELINE config 5 (G4): 16 GiB A.  Every row against the CPU oracle
+    gemv_ref (contract tolerance, and the truth bound from extended
+    precision), and against an fp64 torch matvec on the device."""
     import paper_2108_02025_b200 as cb
     m = n = 65536
     A = dev_uniform(m * n, torch.float32, 3, cuda)
@@ -496,18 +522,23 @@ def test_gemv_65536_square_fp32_sampled_rows(cuda):
     c0 = dev_uniform(m, torch.float32, 4, cuda)
     c = c0.clone()
     cb.gemv_row_major(cb.DenseMatrix.wrap(A, m, n, cb.Layout.RowMajor), x, c, policy())
-    rows = np.r_[0:8, 4091:4101, 32760:32776, m - 8:m]
-    An = np_of(A.view(m, n)[torch.as_tensor(rows, device=cuda)])
-    xn, c0n = np_of(x), np_of(c0)[rows]
-    want = c0n.copy()
-    O.gemv_ref(An.reshape(-1), 0, xn, want)
-    truth, rowabs = O.gemv_truth(An.reshape(-1), 0, xn, c0n)
-    got = np_of(c)[rows]
-    if T.rm_is_ordered(m, n, np.float32):
-        np.testing.assert_array_equal(got, want)
-    assert np.all(np.abs(got - want) <= T.contract_tol(n, rowabs, np.abs(c0n), np.float32))
-    assert np.all(np.abs(got - truth) <=
-                  T.truth_tol(T.gemv_rm_chain(n, np.float32), rowabs, np.abs(c0n), np.float32))
+    # every row against the CPU oracle (gemv_ref), 4096-row blocks copied to
+    # the host in turn (~4 s of oracle time for the 4.3e9 multiply-adds)
+    xn = np_of(x)
+    got_all = np_of(c)
+    c0_all = np_of(c0)
+    for r0 in range(0, m, 4096):
+        An = np_of(A.view(m, n)[r0:r0 + 4096]).reshape(-1)
+        c0n = c0_all[r0:r0 + 4096]
+        want = c0n.copy()
+        O.gemv_ref(An, 0, xn, want)
+        truth, rowabs = O.gemv_truth(An, 0, xn, c0n)
+        got = got_all[r0:r0 + 4096]
+        if T.rm_is_ordered(m, n, np.float32):
+            np.testing.assert_array_equal(got, want)
+        assert np.all(np.abs(got - want) <= T.contract_tol(n, rowabs, np.abs(c0n), np.float32))
+        assert np.all(np.abs(got - truth) <=
+                      T.truth_tol(T.gemv_rm_chain(n, np.float32), rowabs, np.abs(c0n), np.float32))
     # all rows: fp64 torch reference (exact products, fp64 sums)
     ref = c0.double().clone()
     for r0 in range(0, m, 4096):
@@ -588,8 +619,9 @@ def test_dot_chunked_large_n(cuda):
 def test_dot_2pow32_baseline_config(cuda):
     """BASELINE config 5 (D2): n = 2^32 fp32, 32 GiB of operands.  Size-
     independent properties (exact power-of-two scaling, symmetry, run-to-run
-    bits) plus the non-vacuous truth bound against an fp64 torch reduction
-    computed chunk by chunk on the device (fp32 products are exact in fp64)."""
+    bits), the non-vacuous truth bound against an fp64 torch reduction
+    computed chunk by chunk on the device (fp32 products are exact in fp64),
+    and the CPU oracle dot_ref over all 2^32 terms."""
     import paper_2108_02025_b200 as cb
     n = 1 << 32
     x = dev_uniform(n, torch.float32, 1, cuda)
@@ -611,6 +643,16 @@ def test_dot_2pow32_baseline_config(cuda):
     eps = float(np.finfo(np.float32).eps)
     # fp64 chunk sums carry ~1e-16 relative error: far below the fp32 bound
     assert abs(got - truth) <= (T.dot_chain(n, np.float32) + 2) * eps * sumabs
+    # the CPU oracle dot_ref over all 2^32 terms: its sequential chain
+    # continues exactly from chunk to chunk (chunks are multiples of its
+    # 16-byte vector prefix), so this is dot_ref of the whole vectors
+    ref = np.float32(0.0)
+    for b in range(0, n, step):
+        ref = O.dot_ref(np_of(x[b:b + step]), np_of(y[b:b + step]), float(ref))
+    assert abs(got - float(ref)) <= T.contract_tol(n, sumabs, 0.0, np.float32)
+    # both are far inside the fp32 truth bound; the GPU's short chains are the
+    # more accurate (reported in the assertion message if this ever fails)
+    assert abs(got - truth) <= abs(float(ref) - truth) + 64 * eps * sumabs, (got, float(ref), truth)
 
 
 def test_resident_gemv_operator_graph_equals_direct_call(cuda):

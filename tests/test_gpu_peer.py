@@ -170,7 +170,7 @@ for dt in (torch.float32, torch.float64):
     T._destroy(mb)
 print('ok')
 """
-    env = dict(os.environ, CABL_DOT_CHUNKED="1")
+    env = dict(os.environ, CABL_TUNING="1", CABL_DOT_CHUNKED="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-3000:]

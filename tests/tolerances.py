@@ -82,7 +82,7 @@ def rm_is_ordered(m: int, n: int, dtype, aligned: bool = True) -> bool:
     reference the reference-order row-major kernel (bitwise gemv_ref) runs when
     rows are 16-byte multiples, operands 16-byte aligned and m >= 148 * 32 (a
     full warp of rows per CTA)."""
-    return os.environ.get("CABL_GEMV_RM_ORDER") == "reference" and aligned and (n * np.dtype(dtype).itemsize) % 16 == 0 and m >= SMS * 32
+    return os.environ.get("CABL_TUNING") == "1" and os.environ.get("CABL_GEMV_RM_ORDER") == "reference" and aligned and (n * np.dtype(dtype).itemsize) % 16 == 0 and m >= SMS * 32
 
 
 def rm_is_lane(m: int, n: int, dtype, aligned: bool = True) -> bool:

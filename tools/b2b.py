@@ -1,6 +1,8 @@
 #!/usr/bin/env python
 """Back-to-back timing (no flush between steps, one event pair around K steps)
 vs per-step flushed timing, for configs whose inputs exceed 2x the L2."""
+import os as _os
+_os.environ.setdefault("CABL_TUNING", "1")  # exploration script: honour CABL_* knobs
 import json, sys, statistics
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))

@@ -9,6 +9,8 @@ shape with the kernel's CTAs (probe) and the flushed GB/s.
 """
 from __future__ import annotations
 
+import os as _os
+_os.environ.setdefault("CABL_TUNING", "1")  # exploration script: honour CABL_* knobs
 import json
 import os
 import sys

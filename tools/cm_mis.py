@@ -2,6 +2,8 @@
 """Col-major GEMV with few rows (m < 1024) and A off a 16-byte boundary, next
 to the aligned case (flushed).  CABL_CM_BULK_ANY=0 gives the scalar 2-D split
 (before)."""
+import os as _os
+_os.environ.setdefault("CABL_TUNING", "1")  # exploration script: honour CABL_* knobs
 import json
 import sys
 from pathlib import Path

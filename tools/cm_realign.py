@@ -3,6 +3,8 @@
 32-byte boundary) against the aligned neighbour, L2 flushed per rep.  Run with
 CABL_CM_REALIGN=0 (the scalar 2-D split) and 1 (gemv_cm_split_realign_kernel)
 for the before/after."""
+import os as _os
+_os.environ.setdefault("CABL_TUNING", "1")  # exploration script: honour CABL_* knobs
 import json
 import sys
 from pathlib import Path

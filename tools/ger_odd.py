@@ -2,6 +2,8 @@
 """GER on odd / misaligned rows (the flat 32-byte sweep, ger_flat_any_kernel)
 against the aligned 8192^2 tile kernel, L2 flushed per rep.  Run twice, with
 CABL_GER_ANY=0 (the previous scalar flat sweep) and 1, for the before/after."""
+import os as _os
+_os.environ.setdefault("CABL_TUNING", "1")  # exploration script: honour CABL_* knobs
 import json
 import sys
 from pathlib import Path

@@ -2,6 +2,8 @@
 """Row-major GEMV with few long rows at 256 MiB of A, L2 flushed per rep:
 the default dispatch vs the chunked few-rows kernel (CABL_GEMV_RM_MODE=9),
 and a bitwise run-to-run + oracle-tolerance spot check of the forced mode."""
+import os as _os
+_os.environ.setdefault("CABL_TUNING", "1")  # exploration script: honour CABL_* knobs
 import json
 import os
 import sys

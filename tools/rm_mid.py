@@ -2,6 +2,8 @@
 """Row-major GEMV, mid-size row counts at fixed bytes (flushed): the default
 dispatch against the sweep kernel forced (CABL_GEMV_RM_MODE=2, CABL_RM_SWEEP,
 CABL_GEMV_DYN) — the data behind the sweep's few-groups rule."""
+import os as _os
+_os.environ.setdefault("CABL_TUNING", "1")  # exploration script: honour CABL_* knobs
 import json
 import os
 import sys

@@ -2,6 +2,8 @@
 """Row-major GEMV with rows that are not whole 32-byte vectors, or a
 misaligned A, against the aligned neighbour (flushed).  CABL_RM_SCALAR_CTA=0|1
 forces the G-lanes / CTA-per-row scalar kernels."""
+import os as _os
+_os.environ.setdefault("CABL_TUNING", "1")  # exploration script: honour CABL_* knobs
 import json
 import sys
 from pathlib import Path

@@ -1,6 +1,8 @@
 #!/usr/bin/env python
 """Row-major GEMV with short rows at ~256 MiB of A (exploration of the lane
 threshold: run under CABL_RM_LANE_MAX=<bytes>)."""
+import os as _os
+_os.environ.setdefault("CABL_TUNING", "1")  # exploration script: honour CABL_* knobs
 import json, os, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))

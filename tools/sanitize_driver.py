@@ -15,6 +15,8 @@ combine.  Exits non-zero if any result is non-finite.
 """
 from __future__ import annotations
 
+import os as _os
+_os.environ.setdefault("CABL_TUNING", "1")  # exploration script: honour CABL_* knobs
 import os
 import sys
 from pathlib import Path

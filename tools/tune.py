@@ -8,6 +8,8 @@ run one process per variant:
 """
 from __future__ import annotations
 
+import os as _os
+_os.environ.setdefault("CABL_TUNING", "1")  # exploration script: honour CABL_* knobs
 import json
 import os
 import statistics
