@@ -619,7 +619,7 @@ def measure_dram(argv: list[str], records: list[BenchRecord], workdir: Path) -> 
     if r.returncode != 0:
         raise RuntimeError(f"--measure-dram: the plain dram pass failed: {r.stderr[-400:]}")
     log = workdir / "cabl_dram_ncu.csv"
-    cmd = [ncu, "-k", "regex:spin_kernel|cabl_dev", "--metrics",
+    cmd = [ncu, "--kernel-name-base", "demangled", "-k", "regex:spin_kernel|cabl_dev", "--metrics",
            "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none", "--csv",
            "--log-file", str(log), *base]
     r = subprocess.run(cmd, capture_output=True, text=True, env=env)

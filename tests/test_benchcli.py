@@ -195,3 +195,13 @@ def test_cli_through_the_multi_gpu_c_abi(cuda, tmp_path):
     assert len(recs) == 2 + 3 * 3
     assert all(x.gpus == g and x.gbs > 0 for x in recs)
     assert {x.layout for x in recs} == {"vector", "row-major", "col-major"}
+
+
+def test_cabl_bench_executable_exit_codes():
+    """bin/cabl-bench: the reference CLI's name and exit codes (2 on an error)."""
+    exe = ROOT / "bin" / "cabl-bench"
+    r = subprocess.run([str(exe), "--sizes", "0"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2 and "sizes must be >= 1" in r.stderr
+    r = subprocess.run([str(exe), "--machine", "/nonexistent.json", "--sizes", "64"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2 and "cannot open descriptor file" in r.stderr

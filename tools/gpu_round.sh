@@ -1,6 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_full.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu_full.log
-timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "rc=$?" >> gpurun_out/bench.err
-timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 900 python -m pytest tests/test_benchcli.py -m gpu -q > gpurun_out/pytest_fix.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_fix.log
+timeout 600 python tools/e2e_depth.py > gpurun_out/e2e_depth.jsonl 2>&1
+timeout 600 python tools/e2e_depth.py --distinct >> gpurun_out/e2e_depth.jsonl 2>&1
+timeout 300 python tools/host_paths.py > gpurun_out/host_paths.jsonl 2>&1
+python bench.py --gpus 2 --steps 3 > gpurun_out/gpus2.out 2> gpurun_out/gpus2.err; echo "rc=$?" >> gpurun_out/gpus2.err
