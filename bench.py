@@ -303,7 +303,7 @@ def l2_mode(step_bytes: int) -> str:
     (--cache-control none) on back-to-back launches of the two smallest
     configs: every G1 launch (268.5 MB alg.) reads 268.5 MB from DRAM; a D1
     launch (134.2 MB) reads 131.2 MB, i.e. ~2% of it still hits in L2
-    (profiles/r01_ncu_b2b_{D1,G1}.csv).
+    (profiles/r01_ncu_b2b_{D1,G1}.csv, profiles/r02_ncu_b2b_{D1,G1}.csv).
     'flush' otherwise (inputs that fit in L2)."""
     return "stream" if step_bytes > L2_BYTES else "flush"
 
@@ -531,7 +531,7 @@ def run_ours(args, ctx):
                    f"{gplan.l2_bytes / 1e6:.0f} MB L2, "
                    "steps back to back (one event pair around the K steps); ncu shows each "
                    "back-to-back launch reads its full algorithmic bytes from DRAM "
-                   "(profiles/r01_ncu_b2b_*.csv)" if mode == "stream" else
+                   "(profiles/r02_ncu_b2b_*.csv)" if mode == "stream" else
                    f"flushed between steps outside the timed events: {gplan.l2_flush_bytes >> 20} "
                    f"MiB write, then {gplan.l2_flush_bytes >> 20} MiB read (no dirty lines left "
                    "in L2)"),

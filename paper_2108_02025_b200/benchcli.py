@@ -526,6 +526,7 @@ class _Flush:
                          torch.zeros(128 << 20, dtype=torch.float32, device=d),
                          torch.zeros(64 << 20, dtype=torch.float32, device=d)) for d in devs}
         self._evict = None
+        self.sync = False  # set for the cabl_mgpu path (its streams do not wait on torch's)
 
     def __call__(self):
         import torch
@@ -533,8 +534,13 @@ class _Flush:
             with torch.cuda.device(d):
                 w.zero_()
                 r.sum()
-        for d in self.bufs:
-            torch.cuda.synchronize(d)
+        # one device: stream order is enough, and leaving the flush running
+        # hides the host's call overhead from the next call's events (a
+        # synchronize here put ~15 us of Python + ctypes inside them); several
+        # devices: the cabl_mgpu streams do not wait on torch's
+        if len(self.bufs) > 1 or self.sync:
+            for d in self.bufs:
+                torch.cuda.synchronize(d)
 
     def evict(self, d):
         self.bufs[d][2].sum()
@@ -585,6 +591,7 @@ def run_sweep(cfg: SweepConfig, nvtx: bool = False,
         mg = MultiGpu(list(range(cfg.gpus)))
     devs = list(range(cfg.gpus)) if mg is not None else [torch.cuda.current_device()]
     flush = _Flush(devs)
+    flush.sync = mg is not None
     records, failures = [], []
     try:
         for k in cfg.kernels:

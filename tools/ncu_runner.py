@@ -44,6 +44,16 @@ def main():
 
         class w:  # noqa: N801
             id = "R1x"
+    elif args.config == "CM4096":  # col-major GEMV fp32 4096 x 16384 (the 2-D split)
+        m, n = 4096, 16384
+        A = cb.DenseMatrix.wrap(cb.fill_uniform(torch.empty(m * n, device=dev), WL.SEED,
+                                                WL.STREAM_A), m, n, cb.Layout.ColMajor)
+        x = cb.fill_uniform(torch.empty(n, device=dev), WL.SEED, WL.STREAM_X)
+        c = cb.fill_uniform(torch.empty(m, device=dev), WL.SEED, WL.STREAM_C)
+        fn = lambda: cb.gemv_col_major(A, x, c, pol)  # noqa: E731
+
+        class w:  # noqa: N801
+            id = "CM4096"
     elif args.config == "G1g":  # G1 through the gathering GEMV at world 1 (gemv_rm_gather_kernel)
         from paper_2108_02025_b200 import shard
         w = WL.WORKLOADS["G1"]

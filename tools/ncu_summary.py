@@ -85,6 +85,8 @@ def main():
         rd, wr = num(d, "dram__bytes_read.sum"), num(d, "dram__bytes_write.sum")
         if cfg == "R1x":  # GER fp32 8192 x 8193 (tools/ncu_runner.py)
             alg = (2 * 8192 * 8193 + 8192 + 8193) * 4
+        elif cfg == "CM4096":  # col-major GEMV fp32 4096 x 16384
+            alg = (4096 * 16384 + 16384 + 2 * 4096) * 4
         else:  # D1f / G1g: D1 / G1 through the fused peer-memory paths
             alg = WL.WORKLOADS[cfg[:2]].alg_bytes(1)
         el = num(d, "sm__cycles_elapsed.max")
@@ -120,7 +122,7 @@ def main():
                "(cold-cache, serialised: compare shares, not absolutes).  fill_* seed the inputs; "
                "the at:: kernels are the L2 flush (write + read of 512 MiB) that bench.py runs "
                "before timing / between flushed steps.  G1 steps run back to back (inputs 2.1x "
-               "the L2, see r01_ncu_b2b_G1.csv), so the step is one launch of the GEMV kernel.",
+               f"the L2, see {a.round}_ncu_b2b_G1.csv), so the step is one launch of the GEMV kernel.",
                "",
                "| kernel | launches | mean us | share of all GPU time |", "|---|---|---|---|"]
         for k, v in agg.items():
