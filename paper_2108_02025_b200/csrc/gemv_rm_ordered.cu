@@ -39,14 +39,13 @@ namespace {
 constexpr int kOrdConsumerWarps = 2;
 constexpr int kOrdRows = kOrdConsumerWarps * 32; // rows per block
 
-template <typename T, int SEG, int NS, int CW = kOrdConsumerWarps> struct OrdGeom {
+template <typename T, int SEG, int NS> struct OrdGeom {
     static_assert(SEG % 512 == 0, "a warp instruction moves 512 B");
     static constexpr int kStages = NS;
-    static constexpr int kRows = CW * 32;                // rows per block (one lane each)
     static constexpr int kCols = SEG / int(sizeof(T));   // SEG bytes of each row per stage
     static constexpr int kPad = 16 / int(sizeof(T));     // pitch pad: 16 B
     static constexpr int kPitch = kCols + kPad;
-    static constexpr int kStageElems = kRows * kPitch + kCols;
+    static constexpr int kStageElems = kOrdRows * kPitch + kCols;
     static constexpr unsigned kSmem = unsigned(NS * kStageElems * sizeof(T));
 };
 
@@ -58,12 +57,12 @@ template <> struct alignas(16) Vec16<double> {
     double v[2];
 };
 
-template <typename T, int SEG, int NS, int PW, int CW = kOrdConsumerWarps>
-__global__ void __launch_bounds__(CW * 32 + 32 * PW, 1)
+template <typename T, int SEG, int NS, int PW>
+__global__ void __launch_bounds__(kOrdRows + 32 * PW, 1)
     gemv_rm_ordered_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                            uint64_t m, uint64_t n) {
     pdl_enter();
-    using G = OrdGeom<T, SEG, NS, CW>;
+    using G = OrdGeom<T, SEG, NS>;
     constexpr int kOrdStages = NS;
     constexpr int E = 16 / int(sizeof(T)); // elements per 16-byte group
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -78,22 +77,22 @@ __global__ void __launch_bounds__(CW * 32 + 32 * PW, 1)
     if (tid == 0) {
         for (int s = 0; s < kOrdStages; ++s) {
             mbar_init(&full[s], 32 * PW); // one cp.async arrive per producer lane
-            mbar_init(&empty[s], CW);
+            mbar_init(&empty[s], kOrdConsumerWarps);
         }
         mbar_fence_init();
     }
     __syncthreads();
 
-    if (warp >= CW) { // producer warps: rows pw, pw + PW, ...
-        const int pw = warp - CW;
+    if (warp >= kOrdConsumerWarps) { // producer warps: rows pw, pw + PW, ...
+        const int pw = warp - kOrdConsumerWarps;
         // One LDGSTS (cp.async, 16 B per lane) moves a 512-byte row segment:
         // a stage is `rows` + 1 (x) warp instructions.  Each lane then makes
         // the stage's mbarrier track its own copies (.noinc arrive), so the
         // stage completes when all 32 lanes' copies have landed.  (Bulk TMA
         // copies of 512 B per row ran 4.8x slower: per-copy overhead.)
         uint64_t it = 0;
-        for (uint64_t rb = r_begin; rb < r_end; rb += G::kRows) {
-            const int rows = int((r_end - rb < uint64_t(G::kRows)) ? r_end - rb : G::kRows);
+        for (uint64_t rb = r_begin; rb < r_end; rb += kOrdRows) {
+            const int rows = int((r_end - rb < uint64_t(kOrdRows)) ? r_end - rb : kOrdRows);
             for (uint64_t t = 0; t < tiles; ++t, ++it) {
                 const int st = int(it % kOrdStages);
                 const unsigned use = unsigned(it / kOrdStages);
@@ -108,7 +107,7 @@ __global__ void __launch_bounds__(CW * 32 + 32 * PW, 1)
                         const T* src = A + (rb + pw) * n + j0 + e0;
                         for (int r = pw; r < rows; r += PW, src += PW * n)
                             cp_async16(sb + r * G::kPitch + e0, src);
-                        if (pw == 0) cp_async16(sb + G::kRows * G::kPitch + e0, x + j0 + e0);
+                        if (pw == 0) cp_async16(sb + kOrdRows * G::kPitch + e0, x + j0 + e0);
                     }
                 }
                 cp_async_mbar_arrive(&full[st]);
@@ -119,7 +118,7 @@ __global__ void __launch_bounds__(CW * 32 + 32 * PW, 1)
 
     // consumers: lane = one row of the current block
     uint64_t it = 0;
-    for (uint64_t rb = r_begin; rb < r_end; rb += G::kRows) {
+    for (uint64_t rb = r_begin; rb < r_end; rb += kOrdRows) {
         const int rr = warp * 32 + lane;
         const bool live = rb + rr < r_end;
         T acc = live ? c[rb + rr] : T(0);
@@ -130,7 +129,7 @@ __global__ void __launch_bounds__(CW * 32 + 32 * PW, 1)
             const int cw = int((n - j0 < uint64_t(G::kCols)) ? n - j0 : G::kCols);
             const T* sb = stages + uint64_t(st) * G::kStageElems;
             const T* row = sb + rr * G::kPitch;
-            const T* xs = sb + G::kRows * G::kPitch;
+            const T* xs = sb + kOrdRows * G::kPitch;
             if (live) {
                 for (int j = 0; j < cw; j += E) {
                     const Vec16<T> a = *reinterpret_cast<const Vec16<T>*>(row + j);
@@ -276,19 +275,19 @@ template <typename T> bool gemv_rm_ordered_ok(const T* A, const T* x, uint64_t m
 
 namespace {
 
-template <typename T, int SEG, int NS, int PW, int CW = kOrdConsumerWarps>
+template <typename T, int SEG, int NS, int PW>
 void ordered_launch_cfg(const T* A, uint64_t m, uint64_t n, const T* x, T* c, cudaStream_t s,
                         unsigned grid) {
 
-    using G = OrdGeom<T, SEG, NS, CW>;
+    using G = OrdGeom<T, SEG, NS>;
     static bool configured = [] {
-        cudaFuncSetAttribute(gemv_rm_ordered_kernel<T, SEG, NS, PW, CW>,
+        cudaFuncSetAttribute(gemv_rm_ordered_kernel<T, SEG, NS, PW>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
         return true;
     }();
     (void)configured;
-    launch(gemv_rm_ordered_kernel<T, SEG, NS, PW, CW>, grid, G::kRows + 32 * PW, G::kSmem, s, A,
-           x, c, m, n);
+    launch(gemv_rm_ordered_kernel<T, SEG, NS, PW>, grid, kOrdRows + 32 * PW, G::kSmem, s, A, x, c,
+           m, n);
 }
 
 // CABL_ORD_CFG=seg,stages,producer_warps (tuning knob).  G1 / G4 b2b:
@@ -305,8 +304,6 @@ int ordered_cfg() {
         if (!std::strcmp(e, "1024,3,1")) return 1;
         if (!std::strcmp(e, "1024,3,2")) return 2;
         if (!std::strcmp(e, "tma")) return 5;
-        if (!std::strcmp(e, "2048,3,1,1w")) return 6; // 32-row blocks, 2 KB per row per stage
-        if (!std::strcmp(e, "2048,3,2,1w")) return 7;
         return 1;
     }();
     return cfg;
@@ -378,8 +375,6 @@ cudaError_t gemv_rm_ordered_launch(const T* A, uint64_t m, uint64_t n, const T* 
     case 5:
         if (cudaError_t e = ordered_launch_tma<T>(A, m, n, x, c, s, grid)) return e;
         break;
-    case 6: ordered_launch_cfg<T, 2048, 3, 1, 1>(A, m, n, x, c, s, grid); break;
-    case 7: ordered_launch_cfg<T, 2048, 3, 2, 1>(A, m, n, x, c, s, grid); break;
     default: ordered_launch_cfg<T, 1024, 3, 1>(A, m, n, x, c, s, grid); break;
     }
     if (info) info->ctas = grid;

@@ -1,7 +1,8 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_benchcli.py -m gpu -q > gpurun_out/pytest_fix.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_fix.log
-timeout 600 python tools/e2e_depth.py > gpurun_out/e2e_depth.jsonl 2>&1
-timeout 600 python tools/e2e_depth.py --distinct >> gpurun_out/e2e_depth.jsonl 2>&1
-timeout 300 python tools/host_paths.py > gpurun_out/host_paths.jsonl 2>&1
-python bench.py --gpus 2 --steps 3 > gpurun_out/gpus2.out 2> gpurun_out/gpus2.err; echo "rc=$?" >> gpurun_out/gpus2.err
+: > gpurun_out/ord2.jsonl
+for cfg in "1024,3,1" "2048,3,1,1w" "2048,3,2,1w"; do
+  echo "cfg=$cfg" >> gpurun_out/ord2.jsonl
+  CABL_TUNING=1 CABL_GEMV_RM_ORDER=reference CABL_ORD_CFG=$cfg timeout 300 python tools/b2b.py G1 G4 >> gpurun_out/ord2.jsonl 2>&1
+done
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "reference_order_mode" > gpurun_out/pytest_ord.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_ord.log
