@@ -24,7 +24,9 @@ __device__ __forceinline__ V8 ld8(const V8* p) {
     return r;
 }
 
-template <int U, int RPT>
+// GS: columns dealt grid-stride (column j to CTA (j / col_lanes) % P), so all
+// CTAs sweep the matrix front to back together, as the row-major sweep does
+template <int U, int RPT, bool GS = false>
 __global__ void __launch_bounds__(1024, 1)
     k_full(const float* __restrict__ A, const float* __restrict__ x, uint64_t m, uint64_t n,
            float* __restrict__ partials, int row_lanes) {
@@ -43,17 +45,21 @@ __global__ void __launch_bounds__(1024, 1)
     for (int k = 0; k < RPT; ++k)
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[k].v[e] = 0.f;
-    for (uint64_t j0 = cb + cl; j0 < ce; j0 += uint64_t(col_lanes) * U) {
+    const uint64_t jb = GS ? uint64_t(blockIdx.x) * col_lanes + cl : cb + cl;
+    const uint64_t jend = GS ? n : ce;
+    const uint64_t jstep = GS ? uint64_t(gridDim.x) * col_lanes : uint64_t(col_lanes);
+    for (uint64_t j0 = jb; j0 < jend; j0 += jstep * U) {
         V8 a[U][RPT];
         float xv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t j = j0 + uint64_t(u) * col_lanes;
-            xv[u] = j < ce ? __ldg(x + j) : 0.f;
+            const uint64_t j = j0 + uint64_t(u) * jstep;
+            const bool ok = j < jend;
+            xv[u] = ok ? __ldg(x + j) : 0.f;
 #pragma unroll
             for (int k = 0; k < RPT; ++k) {
                 const uint64_t v = uint64_t(rl) + uint64_t(k) * row_lanes;
-                if (j < ce && v < mv) a[u][k] = ld8(Av + j * mv + v);
+                if (ok && v < mv) a[u][k] = ld8(Av + j * mv + v);
                 else
 #pragma unroll
                     for (int e = 0; e < 8; ++e) a[u][k].v[e] = 0.f;
@@ -118,12 +124,18 @@ __global__ void __launch_bounds__(1024, 1)
 
 extern "C" int cmlab_run(int U, const float* A, const float* x, float* c, uint64_t m, uint64_t n,
                          float* partials, int parts, int pdl, void* stream) {
+    const bool gs = U >= 100; // U + 100: grid-stride columns
+    if (gs) U -= 100;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const uint64_t mv = m / 8;
     int row_lanes = 1;
     while (uint64_t(row_lanes) < mv && row_lanes < 1024) row_lanes *= 2;
     const int rpt = int((mv + row_lanes - 1) / row_lanes);
-#define GO(U_, R_) k_full<U_, R_><<<parts, 1024, 0, s>>>(A, x, m, n, partials, row_lanes)
+#define GO(U_, R_)                                                                                \
+    do {                                                                                          \
+        if (gs) k_full<U_, R_, true><<<parts, 1024, 0, s>>>(A, x, m, n, partials, row_lanes);     \
+        else k_full<U_, R_, false><<<parts, 1024, 0, s>>>(A, x, m, n, partials, row_lanes);       \
+    } while (0)
     if (rpt == 1) { if (U == 2) GO(2, 1); else if (U == 8) GO(8, 1); else GO(4, 1); }
     else if (rpt == 2) { if (U == 2) GO(2, 2); else GO(4, 2); }
     else return -1;

@@ -88,9 +88,9 @@ def main():
         print(json.dumps({"m": m, "n": n, "variant": "product", "flushed_us": round(f, 2),
                           "flushed_gbs": round(alg / f / 1e3, 1), "b2b_us": round(b, 2),
                           "b2b_gbs": round(alg / b / 1e3, 1)}), flush=True)
-        for U in (2, 4, 8):
-            for parts in (148, 144):
-                for pdl in (1, 0):
+        for U in (2, 4, 102, 104):  # U >= 100: grid-stride columns (U - 100 in flight)
+            for parts in (148,):
+                for pdl in (1,):
                     c = c0.clone()
                     rc = L.cmlab_run(U, A.data_ptr(), x.data_ptr(), c.data_ptr(), m, n,
                                      partials.data_ptr(), parts, pdl, s)
@@ -101,7 +101,7 @@ def main():
                     fn = lambda: L.cmlab_run(U, A.data_ptr(), x.data_ptr(), c.data_ptr(), m, n,  # noqa: E731
                                              partials.data_ptr(), parts, pdl, s)
                     f, b = timed(fn)
-                    print(json.dumps({"m": m, "n": n, "variant": f"full_U{U}_P{parts}_pdl{pdl}",
+                    print(json.dumps({"m": m, "n": n, "variant": f"full_{'gs' if U >= 100 else 'contig'}_U{U % 100}_P{parts}_pdl{pdl}",
                                       "flushed_us": round(f, 2), "flushed_gbs": round(alg / f / 1e3, 1),
                                       "b2b_us": round(b, 2), "b2b_gbs": round(alg / b / 1e3, 1),
                                       "err_vs_product_1e-5rowabs": round(err, 4)}), flush=True)

@@ -1,8 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-: > gpurun_out/ord2.jsonl
-for cfg in "1024,3,1" "2048,3,1,1w" "2048,3,2,1w"; do
-  echo "cfg=$cfg" >> gpurun_out/ord2.jsonl
-  CABL_TUNING=1 CABL_GEMV_RM_ORDER=reference CABL_ORD_CFG=$cfg timeout 300 python tools/b2b.py G1 G4 >> gpurun_out/ord2.jsonl 2>&1
-done
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "reference_order_mode" > gpurun_out/pytest_ord.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_ord.log
+timeout 600 python tools/cmlab.py > gpurun_out/cmlab2.jsonl 2> gpurun_out/cmlab2.err
+python tools/ncu_runner.py --config D1 --reps 20 > gpurun_out/plain_D1s.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum,sm__cycles_active.avg,sm__cycles_elapsed.max,dram__bytes_read.sum --clock-control none -k regex:dot_kernel --csv --log-file gpurun_out/ncu_D1_series.csv python tools/ncu_runner.py --config D1 --reps 20 > gpurun_out/ncu_D1s.log 2>&1
