@@ -433,8 +433,9 @@ int check_exchange(int exchange) {
 template <typename T>
 int mgpu_dot(cabl_mgpu* c, const T* const* x, const T* const* y, const uint64_t* n, T alpha0,
              uint64_t cutoff, int exchange, T* result) {
-    MG_RC(usable(c));
+    if (!c) return mfail(CABL_EINVAL, "cabl_mgpu: null context");
     std::lock_guard<std::mutex> lk(c->mu);
+    MG_RC(usable(c));
     MG_RC(check_exchange(exchange));
     const int G = int(c->devs.size());
     if (!x || !y || !n || !result) return mfail(CABL_EINVAL, "cabl_mgpu_dot: null argument");
@@ -485,8 +486,9 @@ int mgpu_dot(cabl_mgpu* c, const T* const* x, const T* const* y, const uint64_t*
 template <typename T>
 int mgpu_gemv_rm(cabl_mgpu* c, const T* const* A, const uint64_t* m, uint64_t n,
                  const T* const* x, T* const* cs, uint64_t cutoff, int exchange, T* const* c_full) {
-    MG_RC(usable(c));
+    if (!c) return mfail(CABL_EINVAL, "cabl_mgpu: null context");
     std::lock_guard<std::mutex> lk(c->mu);
+    MG_RC(usable(c));
     MG_RC(check_exchange(exchange));
     const int G = int(c->devs.size());
     if (!A || !m || !x || !cs) return mfail(CABL_EINVAL, "cabl_mgpu_gemv_rm: null argument");
@@ -558,8 +560,9 @@ int mgpu_gemv_rm(cabl_mgpu* c, const T* const* A, const uint64_t* m, uint64_t n,
 template <typename T>
 int mgpu_gemv_cm_cols(cabl_mgpu* c, const T* const* A, uint64_t m, const uint64_t* n,
                       const T* const* x, T* const* cs, uint64_t cutoff, int exchange) {
-    MG_RC(usable(c));
+    if (!c) return mfail(CABL_EINVAL, "cabl_mgpu: null context");
     std::lock_guard<std::mutex> lk(c->mu);
+    MG_RC(usable(c));
     MG_RC(check_exchange(exchange));
     const int G = int(c->devs.size());
     if (!A || !n || !x || !cs) return mfail(CABL_EINVAL, "cabl_mgpu_gemv_cm_cols: null argument");
@@ -612,8 +615,9 @@ int mgpu_gemv_cm_cols(cabl_mgpu* c, const T* const* A, uint64_t m, const uint64_
 template <typename T>
 int mgpu_ger_rm(cabl_mgpu* c, const T* const* x, const uint64_t* m, const T* const* y, uint64_t n,
                 T* const* C, uint64_t cutoff) {
-    MG_RC(usable(c));
+    if (!c) return mfail(CABL_EINVAL, "cabl_mgpu: null context");
     std::lock_guard<std::mutex> lk(c->mu);
+    MG_RC(usable(c));
     const int G = int(c->devs.size());
     if (!x || !m || !y || !C) return mfail(CABL_EINVAL, "cabl_mgpu_ger_rm: null argument");
     for (int r = 0; r < G; ++r)
