@@ -190,3 +190,82 @@ def test_mgpu_timeout_aborts_and_poisons_the_context():
         torch.cuda.synchronize()
     del xs
     torch.cuda.empty_cache()
+
+
+def test_mgpu_randomised_shapes_equal_single_gpu_calls(mg):
+    """40 seeded cases over every op, dtype, exchange and ragged shape: each
+    multi-GPU call equals the same shards run through the single-GPU API, bit
+    for bit (world = all visible GPUs; 1 on the round's boxes)."""
+    import random
+
+    import paper_2108_02025_b200 as cb
+    from paper_2108_02025_b200.mgpu import partition
+    rng = random.Random(20261020)
+    G = mg.size
+    pol = cb.default_policy(1)
+    for case in range(40):
+        dt = rng.choice([torch.float32, torch.float64])
+        op = rng.choice(["dot", "gemv_rm", "gemv_cm", "ger"])
+        ex = rng.choice(["nccl", "peer"])
+        if op == "dot":
+            n = rng.randint(1, 3_000_000)
+            xs, ys, parts = [], [], []
+            for r in range(G):
+                b, e = partition(n, G, r)
+                xs.append(_fill(e - b, dt, 1, f"cuda:{r}", b))
+                ys.append(_fill(e - b, dt, 2, f"cuda:{r}", b))
+                with torch.cuda.device(r):
+                    parts.append(cb.dot(xs[r], ys[r], 0.0, pol) if e > b else 0.0)
+            acc = torch.zeros((), dtype=dt)
+            for p in parts:
+                acc = acc + torch.tensor(p, dtype=dt)
+            want = float(acc + torch.tensor(-0.5, dtype=dt))
+            assert mg.dot(xs, ys, -0.5, pol, exchange=ex) == want, (case, n)
+        elif op == "gemv_rm":
+            m, n = rng.randint(G, 20_000), rng.choice([1, 7, 64, 1000, 4096, 8195])
+            As, xs, cs, want = [], [], [], []
+            for r in range(G):
+                b, e = partition(m, G, r)
+                A = cb.DenseMatrix.wrap(_fill((e - b) * n, dt, 3, f"cuda:{r}", b * n), e - b, n,
+                                        cb.Layout.RowMajor)
+                x, c = _fill(n, dt, 1, f"cuda:{r}"), _fill(e - b, dt, 4, f"cuda:{r}", b)
+                w = c.clone()
+                with torch.cuda.device(r):
+                    cb.gemv_row_major(A, x, w, pol)
+                As.append(A), xs.append(x), cs.append(c), want.append(w)
+            mg.gemv_rm(As, xs, cs, pol, exchange="nccl")
+            for r in range(G):
+                assert torch.equal(cs[r], want[r]), (case, m, n)
+        elif op == "gemv_cm":
+            m, n = rng.choice([1, 8, 256, 1000, 4096]), rng.randint(G, 50_000)
+            As, xs, cs = [], [], []
+            total = torch.zeros(m, dtype=dt)
+            c0 = _fill(m, dt, 4, "cuda:0").cpu()
+            for r in range(G):
+                b, e = partition(n, G, r)
+                A = cb.DenseMatrix.wrap(_fill(m * (e - b), dt, 3, f"cuda:{r}", m * b), m, e - b,
+                                        cb.Layout.ColMajor)
+                x = _fill(e - b, dt, 1, f"cuda:{r}", b)
+                p = torch.zeros(m, dtype=dt, device=f"cuda:{r}")
+                with torch.cuda.device(r):
+                    cb.gemv_col_major(A, x, p, pol)
+                total = total + p.cpu()
+                As.append(A), xs.append(x), cs.append(c0.to(f"cuda:{r}"))
+            mg.gemv_cm_cols(As, xs, cs, pol, exchange=ex)
+            for r in range(G):
+                assert torch.equal(cs[r].cpu(), c0 + total), (case, m, n)
+        else:
+            m, n = rng.randint(G, 5000), rng.choice([1, 5, 64, 777, 4096])
+            xs, ys, Cs, want = [], [], [], []
+            for r in range(G):
+                b, e = partition(m, G, r)
+                C = cb.DenseMatrix.wrap(_fill((e - b) * n, dt, 5, f"cuda:{r}", b * n), e - b, n,
+                                        cb.Layout.RowMajor)
+                x, y = _fill(e - b, dt, 1, f"cuda:{r}", b), _fill(n, dt, 2, f"cuda:{r}")
+                W = cb.DenseMatrix.wrap(C.data.clone(), e - b, n, cb.Layout.RowMajor)
+                with torch.cuda.device(r):
+                    cb.ger(x, y, W, pol)
+                xs.append(x), ys.append(y), Cs.append(C), want.append(W)
+            mg.ger_rm(xs, ys, Cs, pol)
+            for r in range(G):
+                assert torch.equal(Cs[r].data, want[r].data), (case, m, n)

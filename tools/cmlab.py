@@ -34,6 +34,8 @@ def main():
     flush = bench.L2Flush(dev)
     s = torch.cuda.current_stream().cuda_stream
     partials = torch.zeros(296 * 16384, device=dev)
+    pdyn = torch.zeros(64 << 20, device=dev)
+    queue = torch.zeros(4, dtype=torch.int32, device=dev)
 
     def timed(fn, reps=30):
         for _ in range(3):
@@ -88,7 +90,27 @@ def main():
         print(json.dumps({"m": m, "n": n, "variant": "product", "flushed_us": round(f, 2),
                           "flushed_gbs": round(alg / f / 1e3, 1), "b2b_us": round(b, 2),
                           "b2b_gbs": round(alg / b / 1e3, 1)}), flush=True)
-        for U in (2, 4, 102, 104):  # U >= 100: grid-stride columns (U - 100 in flight)
+        L.cmlab_sk.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
+                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int,
+                               C.c_void_p]
+        if m <= 8192:
+            for frac in (0.1, 0.2, 0.3):
+                for cb_kb in (128, 256, 512):
+                    ch = max(1, (cb_kb << 10) // (m * 4))
+                    c = c0.clone()
+                    fn = lambda: L.cmlab_sk(4, A.data_ptr(), x.data_ptr(), c.data_ptr(), m, n,  # noqa: E731
+                                            partials.data_ptr(), pdyn.data_ptr(), queue.data_ptr(),
+                                            148, frac, ch, s)
+                    if fn() != 0:
+                        continue
+                    torch.cuda.synchronize()
+                    err = float(((c.double() - want.double()).abs() / (rowabs * 1e-5 + 1e-30)).max())
+                    f, b = timed(fn)
+                    print(json.dumps({"m": m, "n": n, "variant": f"streamk_dyn{frac}_chunk{cb_kb}KB",
+                                      "flushed_us": round(f, 2), "flushed_gbs": round(alg / f / 1e3, 1),
+                                      "b2b_us": round(b, 2), "b2b_gbs": round(alg / b / 1e3, 1),
+                                      "err_vs_product_1e-5rowabs": round(err, 4)}), flush=True)
+        for U in (102,):  # U >= 100: grid-stride columns (U - 100 in flight)
             for parts in (148,):
                 for pdl in (1,):
                     c = c0.clone()
