@@ -707,7 +707,12 @@ def run_suite(args, ctx, flush, policy, peak):
 
     from paper_2108_02025_b200 import workloads as WL
     ids = list(WL.WORKLOADS) if ctx.world == 1 else ["R1", "G4", "D2"]
-    ids += ["D2f", "G4f"]  # D2 / G4 with the exchange fused into the kernel (peer memory)
+    # D2 / G4 with the exchange fused into the kernel (peer memory): always at
+    # N = 1; across processes (CUDA IPC + NVLink P2P, so far only emulated on
+    # one GPU) only with --fused-suite, so the BASELINE lines of a scaling run
+    # never wait on them
+    if ctx.world == 1 or args.fused_suite:
+        ids += ["D2f", "G4f"]
     out = {}
     steps = max(3, min(args.steps, args.suite_steps))
     for wid in ids:
@@ -934,6 +939,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--suite-steps", type=int, default=30)
+    ap.add_argument("--fused-suite", action="store_true",
+                    help="at N > 1 also time D2 / G4 with the exchange fused into the kernels "
+                         "over peer memory (always on at N = 1)")
     ap.add_argument("--l2", choices=["auto", "flush", "stream"], default="auto",
                     help="headline L2 policy: auto = back to back when a step's inputs "
                          "exceed 2x L2, else flush between steps")
