@@ -569,8 +569,9 @@ E2E_DEPTH = 4
 E2E_SUITE_MAX_BYTES = 3 << 30
 
 
-def _h2d_seconds(nbytes: int, dev) -> float:
-    """Median wall time of a pinned host -> device copy of nbytes (the PCIe bound)."""
+def _h2d_seconds(nbytes: int, dev, to_host: bool = False) -> float:
+    """Median wall time of a pinned host -> device copy of nbytes (the PCIe
+    bound), or device -> host with to_host."""
     import torch
     h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
     d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
@@ -578,7 +579,10 @@ def _h2d_seconds(nbytes: int, dev) -> float:
     for i in range(7):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        d.copy_(h, non_blocking=True)
+        if to_host:
+            h.copy_(d, non_blocking=True)
+        else:
+            d.copy_(h, non_blocking=True)
         torch.cuda.synchronize()
         if i >= 2:
             ts.append(time.perf_counter() - t0)
@@ -635,6 +639,12 @@ def run_e2e(w, ins, policy, ctx, args, resident: bool = True):
                     "frac_of_link": round(link_s / (t_max / steps), 4),
                     "what": "torch pinned-host -> device copy of the step's H2D bytes, median "
                             "of 5; frac_of_link = that copy's time / the e2e step time"}
+    if d2h >= (1 << 20):  # GER: C also comes back; the duplex bound is the slower direction
+        back_s = _h2d_seconds(d2h, ctx.dev, to_host=True)
+        bound = max(link_s, back_s)
+        full["link"].update({"d2h_gbs_measured": round(d2h / back_s / 1e9, 2),
+                             "duplex_bound_ms_per_step": round(bound * 1e3, 4),
+                             "frac_of_duplex_bound": round(bound / (t_max / steps), 4)})
     if not w.op.startswith("gemv"):
         return full, None
     if not resident:
@@ -762,6 +772,9 @@ def run_suite(args, ctx, flush, policy, peak):
                 entry["e2e"] = {k: host[k] for k in ("value", "unit", "h2d_bytes_per_step",
                                                      "d2h_bytes_per_step", "ms_per_step")}
                 entry["e2e"]["frac_of_link"] = host["link"]["frac_of_link"]
+                if "frac_of_duplex_bound" in host["link"]:
+                    entry["e2e"]["frac_of_duplex_bound"] = host["link"]["frac_of_duplex_bound"]
+                    entry["e2e"]["d2h_gbs_measured"] = host["link"]["d2h_gbs_measured"]
             out[wid] = entry
             del ins
         except torch.cuda.OutOfMemoryError as ex:
