@@ -574,6 +574,106 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     if (tid == 0) *ticket = 0u;
 }
 
+// Full-column sweep (aligned mid-size m, m/V <= 1024: fp32 m <= 8192, fp64 m <= 4096).
+// The 2-D split reads a fixed 1 KB row slot of every column per CTA and its
+// CTAs finish up to ~10 us apart on a 50 us launch (profiles/r02_cm_mid.md).
+// Here a CTA owns whole columns: thread (row-vector lane rl, column lane cl)
+// holds one 32-byte accumulator of rows 8rl.. (fp32) and walks columns
+// j = blockIdx.x * col_lanes + cl, then + gridDim.x * col_lanes, ... — all
+// CTAs sweep the matrix front to back together, as the row-major sweep does,
+// with U = 2 columns in flight per thread.  The column lanes are summed in
+// lane order in shared memory and the CTA's m-long partial goes to
+// partials[blockIdx.x]; gemv_cm_fullcol_combine_kernel (launched next, PDL)
+// adds the partials per row in CTA order into c.  The per-row order depends
+// only on (m, n, grid), so the result is bitwise reproducible.  256 MiB fp32,
+// flushed (tools/cmlab.py): 4096 x 16384 5.24 -> 5.67 TB/s, 2048 x 32768 5.24
+// -> 5.54, 1024 x 65536 5.24 -> 5.58.
+constexpr int kFullColU = 2;
+
+template <typename T>
+__global__ void __launch_bounds__(1024, 1)
+    gemv_cm_fullcol_kernel(const T* __restrict__ A, const T* __restrict__ x, uint64_t m, uint64_t n,
+                           int row_lanes, T* __restrict__ partials) {
+    pdl_enter();
+    constexpr int V = Vec<T>::N;
+    __shared__ alignas(32) unsigned char raw[32768]; // blockDim.x * V values (<= 32 KB)
+    T* sm = reinterpret_cast<T*>(raw);
+    const int tid = threadIdx.x;
+    const int col_lanes = int(blockDim.x) / row_lanes;
+    const int rl = tid % row_lanes, cl = tid / row_lanes;
+    const uint64_t mv = m / V;
+    const bool live = uint64_t(rl) < mv;
+    const Vec<T>* Av = reinterpret_cast<const Vec<T>*>(A) + (live ? rl : 0);
+    const uint64_t jstep = uint64_t(gridDim.x) * col_lanes;
+    Vec<T> acc;
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc.v[e] = T(0);
+    for (uint64_t j0 = uint64_t(blockIdx.x) * col_lanes + cl; j0 < n; j0 += jstep * kFullColU) {
+        Vec<T> a[kFullColU];
+        T xv[kFullColU];
+#pragma unroll
+        for (int u = 0; u < kFullColU; ++u) {
+            const uint64_t j = j0 + uint64_t(u) * jstep;
+            const bool ok = j < n;
+            xv[u] = ok ? __ldg(x + j) : T(0);
+            if (ok && live) a[u] = ld_stream(Av + j * mv);
+            else
+#pragma unroll
+                for (int e = 0; e < V; ++e) a[u].v[e] = T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < kFullColU; ++u)
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc.v[e] = fma_rn(a[u].v[e], xv[u], acc.v[e]);
+    }
+    T* out = partials + uint64_t(blockIdx.x) * m;
+    if (col_lanes == 1) {
+        if (live) *reinterpret_cast<Vec<T>*>(out + uint64_t(rl) * V) = acc;
+        return;
+    }
+    if (live)
+#pragma unroll
+        for (int e = 0; e < V; ++e) sm[(uint64_t(cl) * row_lanes + rl) * V + e] = acc.v[e];
+    __syncthreads();
+    for (uint64_t i = tid; i < m; i += blockDim.x) {
+        T t = sm[i];
+        for (int q = 1; q < col_lanes; ++q) t = add_rn(t, sm[uint64_t(q) * row_lanes * V + i]);
+        out[i] = t;
+    }
+}
+
+// c[r] += the `parts` partials of row r in part order: thread (row r of 32,
+// group g of 32) sums parts g, g + 32, ... (8 loads in flight), then the 32
+// group sums are added in g order.
+template <typename T>
+__global__ void __launch_bounds__(1024, 1)
+    gemv_cm_fullcol_combine_kernel(const T* __restrict__ partials, unsigned parts, uint64_t m,
+                                   T* __restrict__ c) {
+    pdl_enter();
+    __shared__ T red[32][33];
+    const int rloc = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const uint64_t row = uint64_t(blockIdx.x) * 32 + rloc;
+    T s = T(0);
+    if (row < m) {
+        unsigned p = unsigned(g);
+        for (; p + 7u * 32u < parts; p += 8u * 32u) {
+            T v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = ld_cg(partials + uint64_t(p + k * 32u) * m + row);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s = add_rn(s, v[k]);
+        }
+        for (; p < parts; p += 32u) s = add_rn(s, ld_cg(partials + uint64_t(p) * m + row));
+    }
+    red[g][rloc] = s;
+    __syncthreads();
+    if (g == 0 && row < m) {
+        T t = red[0][rloc];
+        for (int k = 1; k < 32; ++k) t = add_rn(t, red[k][rloc]);
+        c[row] = add_rn(c[row], t);
+    }
+}
+
 // Scalar split kernel (any m, any alignment), 2-D like the vector one: row
 // tile blockIdx.y of mt rows, column part blockIdx.x.  Thread layout
 // row_lanes x col_lanes = kSplitBlock, row_lanes a power of two >=
@@ -781,6 +881,7 @@ struct SplitGeom {
     unsigned row_tiles;  // gridDim.y
     uint64_t mt;         // rows per row tile
     size_t smem;
+    unsigned threads = 0; // block size where a path picks it (full-column sweep)
 };
 
 // Row tiles: one tile when m < cm_single_max(), else tiles of cm_tile_rows().
@@ -1074,7 +1175,42 @@ inline bool bulk_any_align() {
 }
 
 enum CmPath { kPathTallVec, kPathTallScalar, kPathBulk, kPathBulkScalar, kPathSplitVec,
-              kPathSplitScalar, kPathSplitRealign };
+              kPathSplitScalar, kPathSplitRealign, kPathFullCol };
+
+// Full-column sweep for aligned m with m/V <= 1024 row vectors (at most one per
+// thread of a 1024-thread CTA).  CABL_CM_FULLCOL=0 keeps the 2-D split (A/B).
+inline bool fullcol_enabled() {
+    static const bool on = [] {
+        const char* e = tuning_env("CABL_CM_FULLCOL");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
+}
+template <typename T> bool fullcol_ok(uint64_t m) {
+    return m / Vec<T>::N <= 1024 && fullcol_enabled();
+}
+// <= 512 row vectors: 512-thread CTAs, two per SM; up to 1024: one
+// 1024-thread CTA per SM (tools/cmlab.py: 5.67 vs 5.45 TB/s at 4096 rows,
+// 5.56 vs 5.48 at 8192); never more CTAs than column groups.
+template <typename T> SplitGeom fullcol_geom(uint64_t m, uint64_t n) {
+    SplitGeom g;
+    const uint64_t mv = m / Vec<T>::N;
+    const uint64_t sms = uint64_t(sm_count());
+    g.threads = mv <= 512 ? 512u : 1024u;
+    uint64_t rl = 1;
+    while (rl < mv) rl *= 2;
+    g.row_lanes = int(rl);
+    g.col_lanes = int(g.threads) / g.row_lanes;
+    g.rpt = 1;
+    uint64_t parts = g.threads == 512u ? 2 * sms : sms;
+    const uint64_t groups = (n + uint64_t(g.col_lanes) - 1) / uint64_t(g.col_lanes);
+    if (parts > groups) parts = groups;
+    g.grid = unsigned(parts < 1 ? 1 : parts);
+    g.row_tiles = 1;
+    g.mt = m;
+    g.smem = 0;
+    return g;
+}
 
 // CABL_CM_REALIGN=0 keeps misaligned columns on the scalar 2-D split (A/B only).
 inline bool realign_enabled() {
@@ -1110,7 +1246,10 @@ template <typename T> CmPath cm_path(const T* A, const T* c, uint64_t m) {
     } else if (m >= sms * 1024) {
         return kPathTallScalar;
     }
-    if (split_vec_ok(A, m)) return (m < cm_single_max() && split_mode() == 1) ? kPathBulk : kPathSplitVec;
+    if (split_vec_ok(A, m)) {
+        if (m < cm_single_max() && split_mode() == 1) return kPathBulk;
+        return fullcol_ok<T>(m) ? kPathFullCol : kPathSplitVec;
+    }
     // A off a 16-byte boundary: the bulk ring from the boundary below A (256 MiB
     // fp32 flushed, tools/cm_mis.py: m = 3 / 257 / 1000 680 / 137 / 78 -> 70 /
     // 55 / 66 us against the scalar 2-D split); fp64 from 768 rows stays on the
@@ -1144,6 +1283,7 @@ template <typename T> SplitGeom cm_split_geom(CmPath p, const T* A, uint64_t m, 
         return g;
     }
     if (p == kPathSplitVec) return split_vec_geom<T>(m, n);
+    if (p == kPathFullCol) return fullcol_geom<T>(m, n);
     if (p == kPathSplitRealign) return split_realign_geom<T>(m, n);
     return split_geom<T>(m, n);
 }
@@ -1250,6 +1390,11 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
             (void)configured;
             launch(gemv_cm_split_realign_kernel<T>, grid, kRealignBlock, g.smem, s, A, x, c, m, n,
                    g.mt, g.row_lanes, partials, ws.counters);
+        } else if (path == kPathFullCol) {
+            launch(gemv_cm_fullcol_kernel<T>, g.grid, g.threads, 0, s, A, x, m, n, g.row_lanes,
+                   partials);
+            launch(gemv_cm_fullcol_combine_kernel<T>, unsigned((m + 31) / 32), 1024u, 0, s,
+                   static_cast<const T*>(partials), g.grid, m, c);
         } else if (path == kPathSplitVec) {
             launch(gemv_cm_split_vec_kernel<T>, grid, kSplitBlock, 0, s, 
                 A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);

@@ -67,7 +67,7 @@ RM = [(3, 5), (40, 1024), (2, 65536), (7200, 256), (3000, 999), (5000, 1028), (4
       (700, 5003)]
 CM = [(3, 5), (256, 4096), (4096, 300), (2008, 77), (1001, 300), (148 * 256 * 8, 4),
       (148 * 1024 + 1, 3), (1, 100_000), (257, 20_000), (74 * 256 * 8, 20), (8193, 300),
-      (1025, 777), (3001, 129), (4096, 100)]
+      (1025, 777), (3001, 129), (4096, 100), (8192, 301), (512, 5000), (1000, 3)]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)

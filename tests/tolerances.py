@@ -110,7 +110,10 @@ def gemv_cm_chain(m: int, n: int, dtype) -> int:
     reference order).  Split kernels (csrc/gemv_cm.cu): <= 148 column parts,
     each thread a chain over <= ceil(n / G) columns, then its column lanes
     summed in order (< 512 adds in the bulk kernels, where a row can have up
-    to 512 column lanes), the G part partials summed in order, + c_i."""
+    to 512 column lanes), the G part partials summed in order, + c_i.  The
+    full-column sweep: <= ceil(n / 296) columns per thread, <= 8 column lanes,
+    <= 296 CTA partials in 32 groups (<= 10 + 32 adds), + c_i: inside the same
+    bound."""
     if cm_is_tall(m, dtype):
         return n + 1
     G = max(1, min(SMS, n))

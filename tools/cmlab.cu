@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(1024, 1)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __shared__ float sm[8192];
     const int tid = threadIdx.x;
-    const int col_lanes = 1024 / row_lanes;
+    const int col_lanes = int(blockDim.x) / row_lanes;
     const int rl = tid % row_lanes, cl = tid / row_lanes;
     const uint64_t mv = m / 8;
     const uint64_t q = n / gridDim.x, r = n % gridDim.x;
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(1024, 1)
             for (int e = 0; e < 8; ++e) sm[rl * 8 + e] += acc[0].v[e];
         __syncthreads();
     }
-    for (uint64_t i = tid; i < m; i += 1024) out[i] = sm[i];
+    for (uint64_t i = tid; i < m; i += blockDim.x) out[i] = sm[i];
 }
 
 __global__ void __launch_bounds__(1024, 1)
@@ -120,6 +120,32 @@ __global__ void __launch_bounds__(1024, 1)
         for (int k = 1; k < 32; ++k) t += red[k][rloc];
         c[row] += t;
     }
+}
+
+// grid-stride full columns with T threads per CTA (T in 256/512/1024) and
+// `parts` CTAs; RPT row vectors per thread when m/8 > T
+extern "C" int cmlab_gs_t(int T, const float* A, const float* x, float* c, uint64_t m,
+                          uint64_t n, float* partials, int parts, void* stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint64_t mv = m / 8;
+    int row_lanes = 1;
+    while (uint64_t(row_lanes) < mv && row_lanes < T) row_lanes *= 2;
+    const int rpt = int((mv + row_lanes - 1) / row_lanes);
+    if (rpt == 1) k_full<2, 1, true><<<parts, T, 0, s>>>(A, x, m, n, partials, row_lanes);
+    else if (rpt == 2) k_full<2, 2, true><<<parts, T, 0, s>>>(A, x, m, n, partials, row_lanes);
+    else if (rpt == 4) k_full<1, 4, true><<<parts, T, 0, s>>>(A, x, m, n, partials, row_lanes);
+    else return -1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned((m + 31) / 32));
+    cfg.blockDim = dim3(1024);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_comb, (const float*)partials, m, (unsigned)parts, c);
+    return int(cudaGetLastError());
 }
 
 extern "C" int cmlab_run(int U, const float* A, const float* x, float* c, uint64_t m, uint64_t n,

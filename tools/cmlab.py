@@ -33,7 +33,7 @@ def main():
     pol = cb.default_policy(1)
     flush = bench.L2Flush(dev)
     s = torch.cuda.current_stream().cuda_stream
-    partials = torch.zeros(296 * 16384, device=dev)
+    partials = torch.zeros(600 * 16384, device=dev)
     pdyn = torch.zeros(64 << 20, device=dev)
     queue = torch.zeros(4, dtype=torch.int32, device=dev)
 
@@ -93,7 +93,7 @@ def main():
         L.cmlab_sk.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int,
                                C.c_void_p]
-        if m <= 8192:
+        if m <= 8192 and "--streamk" in sys.argv:
             for frac in (0.1, 0.2, 0.3):
                 for cb_kb in (128, 256, 512):
                     ch = max(1, (cb_kb << 10) // (m * 4))
@@ -110,6 +110,22 @@ def main():
                                       "flushed_us": round(f, 2), "flushed_gbs": round(alg / f / 1e3, 1),
                                       "b2b_us": round(b, 2), "b2b_gbs": round(alg / b / 1e3, 1),
                                       "err_vs_product_1e-5rowabs": round(err, 4)}), flush=True)
+        L.cmlab_gs_t.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                                 C.c_uint64, C.c_void_p, C.c_int, C.c_void_p]
+        for T, parts in ((1024, 148), (512, 296), (256, 592), (512, 148), (256, 296)):
+            c = c0.clone()
+            fn = lambda: L.cmlab_gs_t(T, A.data_ptr(), x.data_ptr(), c.data_ptr(), m, n,  # noqa: E731
+                                      partials.data_ptr(), parts, s)
+            if fn() != 0:
+                continue
+            torch.cuda.synchronize()
+            err = float(((c.double() - want.double()).abs() / (rowabs * 1e-5 + 1e-30)).max())
+            f, b = timed(fn)
+            print(json.dumps({"m": m, "n": n, "variant": f"gs_T{T}_P{parts}",
+                              "flushed_us": round(f, 2), "flushed_gbs": round(alg / f / 1e3, 1),
+                              "b2b_us": round(b, 2), "b2b_gbs": round(alg / b / 1e3, 1),
+                              "err_vs_product_1e-5rowabs": round(err, 4)}), flush=True)
+        continue
         for U in (102,):  # U >= 100: grid-stride columns (U - 100 in flight)
             for parts in (148,):
                 for pdl in (1,):

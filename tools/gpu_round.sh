@@ -1,4 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-( time timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err ) 2> gpurun_out/bench_time.txt
-( time timeout 2400 python -m pytest tests -m gpu -q --durations=25 -p no:cacheprovider > gpurun_out/pytest_durations.log 2>&1 ) 2> gpurun_out/pytest_time.txt
+timeout 900 python -m pytest tests -m gpu -q -x -k "col_major or fuzz or cm or modes or bounds" > gpurun_out/pytest_cm.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_cm.log
+timeout 600 python tools/cm_mid2.py --tag fullcol > gpurun_out/cm_mid4.jsonl 2>gpurun_out/cm_mid4.err
+CABL_CM_FULLCOL=0 timeout 600 python tools/cm_mid2.py --tag split >> gpurun_out/cm_mid4.jsonl 2>>gpurun_out/cm_mid4.err
