@@ -1,5 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x -k "col_major or fuzz or cm or modes or bounds" > gpurun_out/pytest_cm.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_cm.log
-timeout 600 python tools/cm_mid2.py --tag fullcol > gpurun_out/cm_mid4.jsonl 2>gpurun_out/cm_mid4.err
-CABL_CM_FULLCOL=0 timeout 600 python tools/cm_mid2.py --tag split >> gpurun_out/cm_mid4.jsonl 2>>gpurun_out/cm_mid4.err
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+python tools/ncu_runner.py --config CM4096 --reps 2 > gpurun_out/plain_CM4096.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv_cm_fullcol -s 2 -c 2 -o gpurun_out/prof_CM4096 -f python tools/ncu_runner.py --config CM4096 --reps 2 > gpurun_out/ncu_CM4096.log 2>&1
+python tools/shape_sweep.py > gpurun_out/shape_sweep.md 2> gpurun_out/shape_sweep.err
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
