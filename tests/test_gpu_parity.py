@@ -210,6 +210,58 @@ def test_gemv_col_major_matches_oracle(cuda, dtype, m, n):
     assert np.all(np.abs(got.astype(np.float64) - truth) <= tol_t)
 
 
+# full-column sweep (aligned 512 <= m, m/V <= 1024) with its in-kernel combine:
+# grids below the 64 combiners (several row-vector passes per combiner warp),
+# row-vector counts that do not divide by the combiners, 1 and 2 column lanes
+FULLCOL_SHAPES = [(8192, 40), (2048, 100), (4096, 65), (4104, 5001), (1536, 593), (1032, 70_001),
+                  (8192, 8192), (520, 148), (2048, 1)]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("m,n", FULLCOL_SHAPES)
+def test_gemv_col_major_fullcol_combine(cuda, dtype, m, n):
+    import paper_2108_02025_b200 as cb
+    got, want, truth, rowabs, c0, probe, pol = _gemv_case(cuda, dtype, m, n, cb.Layout.ColMajor)
+    dt = got.dtype
+    tol_c = T.contract_tol(n, rowabs, np.abs(c0), dt)
+    assert np.all(np.abs(got.astype(np.float64) - want) <= tol_c)
+    tol_t = T.truth_tol(T.gemv_cm_chain(m, n, dt), rowabs, np.abs(c0), dt)
+    assert np.all(np.abs(got.astype(np.float64) - truth) <= tol_t)
+
+
+def test_gemv_col_major_fullcol_tickets_interleaved(cuda):
+    """The full-column sweep's arrival/departure tickets live in the stream's
+    shared counters: back-to-back launches with different grids, interleaved
+    with the 2-D split and the DOT on the same stream, must each give the bits
+    of a lone call."""
+    import paper_2108_02025_b200 as cb
+    pol = policy()
+    cases = []
+    for i, (m, n, dt) in enumerate([(4096, 16_384, torch.float32), (8192, 40, torch.float32),
+                                    (16_384, 300, torch.float32), (2048, 5000, torch.float64)]):
+        A = cb.DenseMatrix.wrap(dev_uniform(m * n, dt, 3 + i, cuda), m, n, cb.Layout.ColMajor)
+        cases.append((A, dev_uniform(n, dt, 1, cuda), dev_uniform(m, dt, 4, cuda)))
+
+    def run(k):
+        A, x, c0 = cases[k]
+        c = c0.clone()
+        cb.gemv_col_major(A, x, c, pol)
+        return c
+
+    lone = [run(k).cpu() for k in range(len(cases))]
+    xd, yd = dev_uniform(1 << 22, torch.float32, 1, cuda), dev_uniform(1 << 22, torch.float32, 2, cuda)
+    d0 = cb.dot(xd, yd, 0.0, pol)
+    order = [0, 1, 0, 2, 1, 3, 0, 0, 2, 3, 1]
+    outs = []
+    for k in order:
+        outs.append((k, run(k)))
+        if k == 2:
+            assert cb.dot(xd, yd, 0.0, pol) == d0
+    torch.cuda.synchronize()
+    for k, c in outs:
+        assert torch.equal(c.cpu(), lone[k]), k
+
+
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("off", [1, 3])
 @pytest.mark.parametrize("m,n", [(4096, 2048), (2048, 4096), (1024, 1000), (5000, 300),

@@ -1,7 +1,10 @@
-#!/bin/bash
 mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-python tools/ncu_runner.py --config CM4096 --reps 2 > gpurun_out/plain_CM4096.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv_cm_fullcol -s 2 -c 2 -o gpurun_out/prof_CM4096 -f python tools/ncu_runner.py --config CM4096 --reps 2 > gpurun_out/ncu_CM4096.log 2>&1
-python tools/shape_sweep.py > gpurun_out/shape_sweep.md 2> gpurun_out/shape_sweep.err
-timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -x -k "fullcol" > gpurun_out/pytest_cm.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_cm.log
+rm -f gpurun_out/cm_ab.jsonl
+CABL_LIB=$PWD/tools/ab/libcabl_head.so timeout 600 python tools/cm_mid2.py --tag head >> gpurun_out/cm_ab.jsonl 2>&1
+CABL_CM_FC_MODE=0 timeout 600 python tools/cm_mid2.py --tag mode0 >> gpurun_out/cm_ab.jsonl 2>&1
+CABL_CM_FC_P=64 timeout 600 python tools/cm_mid2.py --tag p64 >> gpurun_out/cm_ab.jsonl 2>&1
+CABL_CM_FC_P=128 timeout 600 python tools/cm_mid2.py --tag p128 >> gpurun_out/cm_ab.jsonl 2>&1
+CABL_CM_FC_P=32 timeout 600 python tools/cm_mid2.py --tag p32 >> gpurun_out/cm_ab.jsonl 2>&1
+CABL_CM_FC_P=296 timeout 600 python tools/cm_mid2.py --tag p296 >> gpurun_out/cm_ab.jsonl 2>&1
+CABL_CM_FC_FENCE=1 timeout 600 python tools/cm_mid2.py --tag fence >> gpurun_out/cm_ab.jsonl 2>&1
