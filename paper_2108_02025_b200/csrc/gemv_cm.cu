@@ -643,35 +643,52 @@ __global__ void __launch_bounds__(1024, 1)
 }
 
 // c[r] += the `parts` partials of row r in part order: thread (row r of 32,
-// group g of 32) sums parts g, g + 32, ... (8 loads in flight), then the 32
-// group sums are added in g order.
+// group g of 32) sums parts g, g + 32, ... , then the 32 group sums of a row
+// are added by one warp in a fixed shuffle tree.  Up to 320 parts (every grid the sweep uses) all of a thread's
+// loads are issued as one batch, so the chain after the sweep is one L2 round
+// trip; c's line is prefetched into L2 before the wait.
 template <typename T>
 __global__ void __launch_bounds__(1024, 1)
     gemv_cm_fullcol_combine_kernel(const T* __restrict__ partials, unsigned parts, uint64_t m,
                                    T* __restrict__ c) {
-    pdl_enter();
-    __shared__ T red[32][33];
+    pdl_trigger();
     const int rloc = threadIdx.x & 31, g = threadIdx.x >> 5;
     const uint64_t row = uint64_t(blockIdx.x) * 32 + rloc;
+    // L2 prefetch only before the wait (common.cuh: nothing reaches the SM)
+    if (threadIdx.x < 2 && uint64_t(blockIdx.x) * 32 + threadIdx.x * 31 < m)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(c + uint64_t(blockIdx.x) * 32 + threadIdx.x * 31));
+    pdl_wait();
+    __shared__ T red[32][33];
     T s = T(0);
     if (row < m) {
+        constexpr int K = 10;
         unsigned p = unsigned(g);
-        for (; p + 7u * 32u < parts; p += 8u * 32u) {
-            T v[8];
+        for (; p + unsigned(K - 1) * 32u < parts; p += unsigned(K) * 32u) {
+            T v[K];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = ld_cg(partials + uint64_t(p + k * 32u) * m + row);
+            for (int k = 0; k < K; ++k) v[k] = ld_cg(partials + uint64_t(p + k * 32u) * m + row);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) s = add_rn(s, v[k]);
+            for (int k = 0; k < K; ++k) s = add_rn(s, v[k]);
         }
-        for (; p < parts; p += 32u) s = add_rn(s, ld_cg(partials + uint64_t(p) * m + row));
+        if (p < parts) { // the < K remaining parts of this group, one batch
+            T v[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                v[k] = p + k * 32u < parts ? ld_cg(partials + uint64_t(p + k * 32u) * m + row) : T(0);
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (p + k * 32u < parts) s = add_rn(s, v[k]);
+        }
     }
     red[g][rloc] = s;
     __syncthreads();
-    if (g == 0 && row < m) {
-        T t = red[0][rloc];
-        for (int k = 1; k < 32; ++k) t = add_rn(t, red[k][rloc]);
-        c[row] = add_rn(c[row], t);
-    }
+    // warp g finishes row g of the 32: lane k holds group k's sum, fixed
+    // shuffle-down tree, lane 0 adds it to c
+    const uint64_t row_w = uint64_t(blockIdx.x) * 32 + g;
+    T t = red[rloc][g];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t = add_rn(t, __shfl_down_sync(0xffffffffu, t, off));
+    if (rloc == 0 && row_w < m) c[row_w] = add_rn(c[row_w], t);
 }
 
 // Scalar split kernel (any m, any alignment), 2-D like the vector one: row
