@@ -454,8 +454,13 @@ int mgpu_dot(cabl_mgpu* c, const T* const* x, const T* const* y, const uint64_t*
         MG_RC(mark_start(c));
         for (int r = 0; r < G; ++r) {
             MG_RC(set_dev(c, r));
-            MG_RC(dot_peer1(x[r], y[r], n[r], alpha0, sc[r] + G + 1, c->dot_mb.mboxes.data(), G, r,
-                            cutoff, c->streams[r]));
+            if (int rc = dot_peer1(x[r], y[r], n[r], alpha0, sc[r] + G + 1, c->dot_mb.mboxes.data(),
+                                   G, r, cutoff, c->streams[r])) {
+                // ranks 0..r-1 are already waiting for this one: their
+                // mailboxes will record a timed-out exchange
+                if (r > 0) abort_all(c, "dot (peer exchange): launch failed after peers started");
+                return rc;
+            }
         }
         MG_RC(wait_all(c, false, "dot (peer exchange)"));
         MG_RC(check_peer_faults(c, c->dot_mb, "dot (peer exchange)"));

@@ -29,12 +29,26 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--no-flush", action="store_true",
                     help="back-to-back launches (for DRAM-traffic checks without a flush)")
+    ap.add_argument("--cm", default="",
+                    help="col-major GEMV of shape MxN[:f64] instead of a config (e.g. 16384x4096)")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
     ctx = bench.Ctx(1, 0, 0, dev)
     pol = cb.default_policy(1)
-    if args.config == "R1x":  # GER fp32 8192 x 8193: odd rows (ger_flat_any_kernel)
+    if args.cm:
+        shape, _, dts = args.cm.partition(":")
+        m, n = (int(v) for v in shape.split("x"))
+        dt = torch.float64 if dts == "f64" else torch.float32
+        A = cb.DenseMatrix.wrap(cb.fill_uniform(torch.empty(m * n, dtype=dt, device=dev), WL.SEED,
+                                                WL.STREAM_A), m, n, cb.Layout.ColMajor)
+        x = cb.fill_uniform(torch.empty(n, dtype=dt, device=dev), WL.SEED, WL.STREAM_X)
+        c = cb.fill_uniform(torch.empty(m, dtype=dt, device=dev), WL.SEED, WL.STREAM_C)
+        fn = lambda: cb.gemv_col_major(A, x, c, pol)  # noqa: E731
+
+        class w:  # noqa: N801
+            id = "CM" + args.cm
+    elif args.config == "R1x":  # GER fp32 8192 x 8193: odd rows (ger_flat_any_kernel)
         m, n = 8192, 8193
         x = cb.fill_uniform(torch.empty(m, device=dev), WL.SEED, WL.STREAM_X)
         y = cb.fill_uniform(torch.empty(n, device=dev), WL.SEED, WL.STREAM_Y)
