@@ -340,7 +340,9 @@ def time_steps(fn, steps, warmup, ctx, flush, sampler=None, mode="flush", charge
         # when the GPU reaches them: the K timed steps then run back to back
         # from the start event, without the host's first-launch latency in the
         # interval (driver K = 20: ~1.5 us per step of the G1 headline)
-        torch.cuda._sleep(PRIME_CYCLES)
+        prime = getattr(torch.cuda, "_sleep", None)  # private torch API: optional
+        if prime is not None:
+            prime(PRIME_CYCLES)
         a.record()
         for _ in range(steps):
             fn()
