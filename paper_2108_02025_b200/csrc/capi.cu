@@ -817,6 +817,7 @@ int host_gemv(const T* A, int layout, uint64_t m, uint64_t n, const T* x, T* c, 
 // fma(x_i, y_j, C_ij): the bits equal the unsplit call's.
 constexpr size_t kPipeSlabMin = size_t(8) << 20;
 constexpr int kPipeMaxSlabs = 32;
+constexpr int kPipeSlabs = 16;
 
 struct HostPipe {
     std::mutex mu;
@@ -856,11 +857,26 @@ int host_ger_pipelined(int dev, const T* x, const T* y, T* C, int layout, uint64
     const uint64_t outer = rm ? m : n, inner = rm ? n : m;
     const size_t line = size_t(inner) * sizeof(T);
     const size_t total = size_t(outer) * line;
-    size_t slab = total / kPipeMaxSlabs + 1;
-    if (slab < kPipeSlabMin) slab = kPipeSlabMin;
+    // About kPipeSlabs slabs of >= 8 MiB: each copy has a fixed cost, and
+    // the pipeline fills and drains in one slab's time (256 MiB fp32 pinned,
+    // tools/ger_pipe.py — 4 / 8 / 16 / 32 / 64 / 128 slabs: 6.55 / 6.10 /
+    // 5.99 / 6.24 / 6.62 / 7.75 ms; the same copy pattern without the GER
+    // kernel, tools/pcie_duplex.py: 5.74 ms at 16 slabs; both directions at
+    // once with no dependency: 5.37).  Ramping the first and last slabs
+    // (1/8, 1/4, 1/2 of a slab) changed nothing.  CABL_GER_PIPE=
+    // "slabs,min_mib" overrides (tuning only).
+    static const std::pair<int, size_t> pipe_cfg = [] {
+        int sl = kPipeSlabs;
+        unsigned long mib = kPipeSlabMin >> 20;
+        if (const char* e = tuning_env("CABL_GER_PIPE")) sscanf(e, "%d,%lu", &sl, &mib);
+        if (sl < 1 || sl > kPipeMaxSlabs) sl = kPipeSlabs;
+        return std::make_pair(sl, size_t(mib) << 20);
+    }();
+    size_t slab = total / size_t(pipe_cfg.first) + 1;
+    if (slab < pipe_cfg.second) slab = pipe_cfg.second;
     uint64_t lines = (slab + line - 1) / line;
     if (lines < 1) lines = 1;
-    const uint64_t slabs = (outer + lines - 1) / lines;
+    const uint64_t slabs = (outer + lines - 1) / lines; // <= the slab count
     DevBuf dx, dy, dC;
     if (int rc = dev_alloc(dx, m * sizeof(T), s)) return rc;
     if (int rc = dev_alloc(dy, n * sizeof(T), s)) return rc;

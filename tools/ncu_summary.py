@@ -121,7 +121,9 @@ def main():
                "`python bench.py --steps 20 --warmup 3 --no-suite --no-e2e --no-cpu-baseline` "
                "(cold-cache, serialised: compare shares, not absolutes).  fill_* seed the inputs; "
                "the at:: kernels are the L2 flush (write + read of 512 MiB) that bench.py runs "
-               "before timing / between flushed steps.  G1 steps run back to back (inputs 2.1x "
+               "before timing / between flushed steps; cuda::spin_kernel is torch.cuda._sleep, the "
+               "0.5 ms device sleep the timed steps queue behind (before the start event).  "
+               "G1 steps run back to back (inputs 2.1x "
                f"the L2, see {a.round}_ncu_b2b_G1.csv), so the step is one launch of the GEMV kernel.",
                "",
                "| kernel | launches | mean us | share of all GPU time |", "|---|---|---|---|"]
