@@ -691,6 +691,126 @@ __global__ void __launch_bounds__(1024, 1)
     if (rloc == 0 && row_w < m) c[row_w] = add_rn(c[row_w], t);
 }
 
+// Full-column sweep for 1024 < m/V <= 2048 (fp32 m <= 16384, fp64 m <= 8192):
+// 1024 threads, thread t owns row vectors t and t + 1024 of every column, one
+// column per CTA at a time (U = 2 columns in flight: 4 x 32 bytes per thread),
+// columns dealt grid-stride; the CTA's m-long partial goes to
+// partials[blockIdx.x] and gemv_cm_fullcol_combine16_kernel follows (PDL).
+// fp32 16384 x 4096 in ncu: 45.9 us, SM active min / max 73k / 79k cycles,
+// against the 2-D split's 51.1 us (profiles/r02_cm_mid.md).
+template <typename T>
+__global__ void __launch_bounds__(1024, 1)
+    gemv_cm_fullcol2_kernel(const T* __restrict__ A, const T* __restrict__ x, uint64_t m, uint64_t n,
+                            T* __restrict__ partials) {
+    pdl_enter();
+    constexpr int V = Vec<T>::N;
+    const int tid = threadIdx.x;
+    const uint64_t mv = m / V;
+    const bool live1 = uint64_t(tid) + 1024u < mv;
+    const Vec<T>* Av = reinterpret_cast<const Vec<T>*>(A) + tid;
+    const uint64_t jstep = gridDim.x;
+    Vec<T> acc0, acc1;
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc0.v[e] = acc1.v[e] = T(0);
+    for (uint64_t j0 = blockIdx.x; j0 < n; j0 += jstep * kFullColU) {
+        Vec<T> a0[kFullColU], a1[kFullColU];
+        T xv[kFullColU];
+#pragma unroll
+        for (int u = 0; u < kFullColU; ++u) {
+            const uint64_t j = j0 + uint64_t(u) * jstep;
+            const bool ok = j < n;
+            xv[u] = ok ? __ldg(x + j) : T(0);
+            if (ok) a0[u] = ld_stream(Av + j * mv);
+            else
+#pragma unroll
+                for (int e = 0; e < V; ++e) a0[u].v[e] = T(0);
+            if (ok && live1) a1[u] = ld_stream(Av + j * mv + 1024u);
+            else
+#pragma unroll
+                for (int e = 0; e < V; ++e) a1[u].v[e] = T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < kFullColU; ++u)
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                acc0.v[e] = fma_rn(a0[u].v[e], xv[u], acc0.v[e]);
+                acc1.v[e] = fma_rn(a1[u].v[e], xv[u], acc1.v[e]);
+            }
+    }
+    Vec<T>* out = reinterpret_cast<Vec<T>*>(partials + uint64_t(blockIdx.x) * m);
+    out[tid] = acc0;
+    if (live1) out[tid + 1024] = acc1;
+}
+
+// Combine for many rows (m % (16 / s) == 0): thread (16-byte row group q,
+// part group g of kC16G) sums parts g, g + kC16G, ... (up to kC16K in one
+// batch of 16-byte L2 loads), then the kC16G group sums of a row are added
+// by kC16G lanes of one warp in a fixed shuffle tree.  256-thread CTAs of 16
+// row groups: m = 16384 fp32 is 256 CTAs, one wave with room to spare (the
+// 1024-thread combine runs such m in 3.5 waves of one CTA per SM).
+constexpr int kC16G = 16;
+constexpr int kC16K = 10; // parts <= 160
+template <typename T> struct alignas(16) Q16 {
+    T v[16 / sizeof(T)];
+};
+__device__ __forceinline__ Q16<float> ld_cg16(const Q16<float>* p) {
+    const float4 t = __ldcg(reinterpret_cast<const float4*>(p));
+    return Q16<float>{{t.x, t.y, t.z, t.w}};
+}
+__device__ __forceinline__ Q16<double> ld_cg16(const Q16<double>* p) {
+    const double2 t = __ldcg(reinterpret_cast<const double2*>(p));
+    return Q16<double>{{t.x, t.y}};
+}
+template <typename T>
+__global__ void __launch_bounds__(256)
+    gemv_cm_fullcol_combine16_kernel(const T* __restrict__ partials, unsigned parts, uint64_t m,
+                                     T* __restrict__ c) {
+    pdl_trigger();
+    constexpr int E = 16 / int(sizeof(T)); // rows per 16-byte group
+    constexpr int QG = 256 / kC16G;        // row groups per CTA
+    constexpr int R = QG * E;              // rows per CTA
+    const uint64_t mq = m / E;
+    const uint64_t q0 = uint64_t(blockIdx.x) * QG;
+    if (threadIdx.x < 2) { // c's lines, before the wait (L2 prefetch only)
+        const uint64_t last = (q0 + QG < mq ? q0 + QG : mq) * E - 1;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(c + (threadIdx.x ? last : q0 * E)));
+    }
+    pdl_wait();
+    __shared__ T red[kC16G][R + 1];
+    const int ql = threadIdx.x % QG, g = threadIdx.x / QG;
+    const uint64_t q = q0 + ql;
+    T s[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) s[e] = T(0);
+    if (q < mq) {
+        const Q16<T>* src = reinterpret_cast<const Q16<T>*>(partials) + q;
+        for (unsigned p = unsigned(g); p < parts; p += unsigned(kC16K * kC16G)) {
+            Q16<T> v[kC16K];
+#pragma unroll
+            for (int k = 0; k < kC16K; ++k)
+                if (p + k * kC16G < parts) v[k] = ld_cg16(src + uint64_t(p + k * kC16G) * mq);
+#pragma unroll
+            for (int k = 0; k < kC16K; ++k)
+                if (p + k * kC16G < parts)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) s[e] = add_rn(s[e], v[k].v[e]);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) red[g][ql * E + e] = s[e];
+    __syncthreads();
+    // 8 warps x 2 half-warps: half-warp h finishes rows h, h + 16, ...; lane
+    // k of a half-warp holds group k's sum, fixed shuffle-down tree
+    const int lane = threadIdx.x & 31, hw = (threadIdx.x >> 5) * 2 + (lane >> 4), k = lane & 15;
+    for (int r = hw; r < R; r += 16) {
+        T t = red[k][r];
+#pragma unroll
+        for (int off = kC16G / 2; off > 0; off >>= 1) t = add_rn(t, __shfl_down_sync(0xffffffffu, t, off, 16));
+        const uint64_t row = q0 * E + uint64_t(r);
+        if (k == 0 && row < m) c[row] = add_rn(c[row], t);
+    }
+}
+
 // Scalar split kernel (any m, any alignment), 2-D like the vector one: row
 // tile blockIdx.y of mt rows, column part blockIdx.x.  Thread layout
 // row_lanes x col_lanes = kSplitBlock, row_lanes a power of two >=
@@ -1192,7 +1312,7 @@ inline bool bulk_any_align() {
 }
 
 enum CmPath { kPathTallVec, kPathTallScalar, kPathBulk, kPathBulkScalar, kPathSplitVec,
-              kPathSplitScalar, kPathSplitRealign, kPathFullCol };
+              kPathSplitScalar, kPathSplitRealign, kPathFullCol, kPathFullCol2 };
 
 // Full-column sweep for aligned m with m/V <= 1024 row vectors (at most one per
 // thread of a 1024-thread CTA).  CABL_CM_FULLCOL=0 keeps the 2-D split (A/B).
@@ -1205,6 +1325,25 @@ inline bool fullcol_enabled() {
 }
 template <typename T> bool fullcol_ok(uint64_t m) {
     return m / Vec<T>::N <= 1024 && fullcol_enabled();
+}
+// fp32 8192 < m <= 16384: the full-column sweep with two row vectors per
+// thread and the 16-byte combine (256 MiB, tools/cm_mid2.py: 16384 x 4096
+// flushed / back to back 52.2 / 48.6 -> 48.7 / 47.2 us, 12000 x 5592 50.6 /
+// 47.7 -> 50.7 / 46.8).  fp64 (m <= 8192) stays on the 2-D split: 8192 x 8192
+// was 87.9 / 85.1 -> 85.7 / 87.6, slower back to back.  CABL_CM_FULLCOL2=0|1
+// forces it off / on for both types (A/B).
+inline int fullcol2_forced() {
+    static const int v = [] {
+        const char* e = tuning_env("CABL_CM_FULLCOL2");
+        return e ? atoi(e) : -1;
+    }();
+    return v;
+}
+template <typename T> bool fullcol2_ok(uint64_t m) {
+    const uint64_t mv = m / Vec<T>::N;
+    if (mv <= 1024 || mv > 2048 || !fullcol_enabled()) return false;
+    const int f = fullcol2_forced();
+    return f >= 0 ? f != 0 : sizeof(T) == 4;
 }
 // <= 512 row vectors: 512-thread CTAs, two per SM; up to 1024: one
 // 1024-thread CTA per SM (tools/cmlab.py: 5.67 vs 5.45 TB/s at 4096 rows,
@@ -1265,6 +1404,7 @@ template <typename T> CmPath cm_path(const T* A, const T* c, uint64_t m) {
     }
     if (split_vec_ok(A, m)) {
         if (m < cm_single_max() && split_mode() == 1) return kPathBulk;
+        if (fullcol2_ok<T>(m)) return kPathFullCol2;
         return fullcol_ok<T>(m) ? kPathFullCol : kPathSplitVec;
     }
     // A off a 16-byte boundary: the bulk ring from the boundary below A (256 MiB
@@ -1301,6 +1441,19 @@ template <typename T> SplitGeom cm_split_geom(CmPath p, const T* A, uint64_t m, 
     }
     if (p == kPathSplitVec) return split_vec_geom<T>(m, n);
     if (p == kPathFullCol) return fullcol_geom<T>(m, n);
+    if (p == kPathFullCol2) {
+        SplitGeom g;
+        g.threads = 1024u;
+        g.row_lanes = 1024;
+        g.col_lanes = 1;
+        g.rpt = 2;
+        const uint64_t sms = uint64_t(sm_count());
+        g.grid = unsigned(n < sms ? n : sms);
+        g.row_tiles = 1;
+        g.mt = m;
+        g.smem = 0;
+        return g;
+    }
     if (p == kPathSplitRealign) return split_realign_geom<T>(m, n);
     return split_geom<T>(m, n);
 }
@@ -1412,6 +1565,19 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
                    partials);
             launch(gemv_cm_fullcol_combine_kernel<T>, unsigned((m + 31) / 32), 1024u, 0, s,
                    static_cast<const T*>(partials), g.grid, m, c);
+        } else if (path == kPathFullCol2) {
+            constexpr unsigned E = 16 / sizeof(T), R = (256 / kC16G) * E;
+            launch(gemv_cm_fullcol2_kernel<T>, g.grid, g.threads, 0, s, A, x, m, n, partials);
+            static const int comb16 = [] {
+                const char* e = tuning_env("CABL_CM_FC2_COMB16");
+                return e ? atoi(e) : 1;
+            }();
+            if (comb16)
+                launch(gemv_cm_fullcol_combine16_kernel<T>, unsigned((m + R - 1) / R), 256u, 0, s,
+                       static_cast<const T*>(partials), g.grid, m, c);
+            else
+                launch(gemv_cm_fullcol_combine_kernel<T>, unsigned((m + 31) / 32), 1024u, 0, s,
+                       static_cast<const T*>(partials), g.grid, m, c);
         } else if (path == kPathSplitVec) {
             launch(gemv_cm_split_vec_kernel<T>, grid, kSplitBlock, 0, s, 
                 A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);

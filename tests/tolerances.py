@@ -112,8 +112,9 @@ def gemv_cm_chain(m: int, n: int, dtype) -> int:
     summed in order (< 512 adds in the bulk kernels, where a row can have up
     to 512 column lanes), the G part partials summed in order, + c_i.  The
     full-column sweep: <= ceil(n / 296) columns per thread, <= 8 column lanes,
-    <= 296 CTA partials in 32 groups (<= 10 adds, then a 5-level tree), + c_i: inside the same
-    bound."""
+    <= 296 CTA partials in 32 groups (<= 10 adds, then a 5-level tree), + c_i; with two
+    row vectors per thread (fp32 8192 < m <= 16384) <= 148 partials in 16 groups (<= 10
+    adds, then a 4-level tree): inside the same bound."""
     if cm_is_tall(m, dtype):
         return n + 1
     G = max(1, min(SMS, n))
