@@ -254,7 +254,8 @@ template <typename T>
 __global__ void __launch_bounds__(kSplitBlock, 1)
     gemv_cm_split_vec_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                              uint64_t m, uint64_t n, uint64_t mt, int row_lanes,
-                             T* __restrict__ partials, unsigned* __restrict__ tickets) {
+                             T* __restrict__ partials, unsigned* __restrict__ tickets,
+                             int external_combine) {
     pdl_enter();
     constexpr int V = Vec<T>::N;
     constexpr int U = 4;
@@ -307,6 +308,7 @@ __global__ void __launch_bounds__(kSplitBlock, 1)
         for (int q = 1; q < col_lanes; ++q) v = add_rn(v, sm[uint64_t(q) * rows + r]);
         tile_partials[uint64_t(blockIdx.x) * mt + r] = v;
     }
+    if (external_combine) return; // gemv_cm_fullcol_combine16_kernel follows (PDL)
     __threadfence();
     __syncthreads();
     if (tid == 0) am_last = atomicAdd(tickets + blockIdx.y, 1u) == gridDim.x - 1;
@@ -764,12 +766,12 @@ __device__ __forceinline__ Q16<double> ld_cg16(const Q16<double>* p) {
 template <typename T>
 __global__ void __launch_bounds__(256)
     gemv_cm_fullcol_combine16_kernel(const T* __restrict__ partials, unsigned parts, uint64_t m,
-                                     T* __restrict__ c) {
+                                     uint64_t mt, T* __restrict__ c) {
     pdl_trigger();
     constexpr int E = 16 / int(sizeof(T)); // rows per 16-byte group
     constexpr int QG = 256 / kC16G;        // row groups per CTA
     constexpr int R = QG * E;              // rows per CTA
-    const uint64_t mq = m / E;
+    const uint64_t mq = (m + E - 1) / E; // the last group may run past m (rows >= m are not stored)
     const uint64_t q0 = uint64_t(blockIdx.x) * QG;
     if (threadIdx.x < 2) { // c's lines, before the wait (L2 prefetch only)
         const uint64_t last = (q0 + QG < mq ? q0 + QG : mq) * E - 1;
@@ -783,12 +785,15 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int e = 0; e < E; ++e) s[e] = T(0);
     if (q < mq) {
-        const Q16<T>* src = reinterpret_cast<const Q16<T>*>(partials) + q;
+        // row tiles of mt rows (mt % E == 0): tile t's parts at (t * parts + p) * mt
+        const uint64_t row = q * E, tile = row / mt;
+        const uint64_t mqt = mt / E; // 16-byte groups per part row
+        const Q16<T>* src = reinterpret_cast<const Q16<T>*>(partials + tile * parts * mt + (row - tile * mt));
         for (unsigned p = unsigned(g); p < parts; p += unsigned(kC16K * kC16G)) {
             Q16<T> v[kC16K];
 #pragma unroll
             for (int k = 0; k < kC16K; ++k)
-                if (p + k * kC16G < parts) v[k] = ld_cg16(src + uint64_t(p + k * kC16G) * mq);
+                if (p + k * kC16G < parts) v[k] = ld_cg16(src + uint64_t(p + k * kC16G) * mqt);
 #pragma unroll
             for (int k = 0; k < kC16K; ++k)
                 if (p + k * kC16G < parts)
@@ -820,7 +825,8 @@ template <typename T, int RPT>
 __global__ void __launch_bounds__(kSplitBlock, 1)
     gemv_cm_split_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
                          uint64_t m, uint64_t n, uint64_t mt, int row_lanes,
-                         T* __restrict__ partials, unsigned* __restrict__ tickets) {
+                         T* __restrict__ partials, unsigned* __restrict__ tickets,
+                         int external_combine) {
     pdl_enter();
     extern __shared__ unsigned char smem_raw[];
     T* sm = reinterpret_cast<T*>(smem_raw); // [col_lanes][rows], >= kSplitBlock entries
@@ -874,6 +880,7 @@ __global__ void __launch_bounds__(kSplitBlock, 1)
         for (int q = 1; q < col_lanes; ++q) v = add_rn(v, sm[uint64_t(q) * rows + r]);
         tile_partials[uint64_t(blockIdx.x) * mt + r] = v;
     }
+    if (external_combine) return; // gemv_cm_fullcol_combine16_kernel follows (PDL)
     __threadfence();
     __syncthreads();
     if (tid == 0) am_last = atomicAdd(tickets + blockIdx.y, 1u) == gridDim.x - 1;
@@ -931,7 +938,8 @@ template <typename T>
 __global__ void __launch_bounds__(kRealignBlock, 1)
     gemv_cm_split_realign_kernel(const T* __restrict__ A, const T* __restrict__ x,
                                  T* __restrict__ c, uint64_t m, uint64_t n, uint64_t mt, int RW,
-                                 T* __restrict__ partials, unsigned* __restrict__ tickets) {
+                                 T* __restrict__ partials, unsigned* __restrict__ tickets,
+                                 int external_combine) {
     pdl_enter();
     constexpr int V = Vec<T>::N;
     constexpr int U = kRealignU;
@@ -1002,6 +1010,7 @@ __global__ void __launch_bounds__(kRealignBlock, 1)
         for (int q = 1; q < CL; ++q) v = add_rn(v, sm[uint64_t(q) * rows + r]);
         tile_partials[uint64_t(blockIdx.x) * mt + r] = v;
     }
+    if (external_combine) return; // gemv_cm_fullcol_combine16_kernel follows (PDL)
     __threadfence();
     __syncthreads();
     if (tid == 0) am_last = atomicAdd(tickets + blockIdx.y, 1u) == gridDim.x - 1;
@@ -1426,6 +1435,33 @@ template <typename T> CmPath cm_path(const T* A, const T* c, uint64_t m) {
     return kPathSplitScalar;
 }
 
+// Split tiles with >= 2 column parts finish in a one-wave combine kernel
+// (PDL) instead of each tile's last CTA summing parts x mt partials alone
+// (256 MiB fp64 flushed / back to back, tools/cm_mid2.py: 8192 x 8192, 16
+// tiles x 9 parts, 88.0 / 85.1 -> 85.1 / 82.3 us; 12000 x 5592 89.4 / 86.9 ->
+// 87.2 / 84.0); single-part tiles (m >= 32768) keep the in-kernel finish, a
+// second launch only costs there (fp32 65536 x 1024 49.4 -> 52.5).  Odd m
+// (scalar and realigning splits): 12345 x 5436 fp32 59.8 -> 58.1, 40001 x
+// 1677 61.3 -> 57.6 (fp64 98.5 -> 94.6); above 65536 rows the combine's many
+// CTAs cost more than the last CTA's small sum (100003 x 671 fp64, 3 parts of
+// 2048 rows: 97.3 -> 99.2), so those keep the in-kernel finish
+// (tools/ab_shapes.py, profiles/r02_cm_split_comb16*.jsonl).
+// CABL_CM_SPLIT_COMB16=0|1 forces it off / on (A/B).
+template <typename T> bool split_external_combine(const SplitGeom& g, uint64_t m) {
+    static const int forced = [] {
+        const char* e = tuning_env("CABL_CM_SPLIT_COMB16");
+        return e ? atoi(e) : -1;
+    }();
+    constexpr unsigned E = 16 / sizeof(T);
+    return (forced < 0 ? g.grid >= 2 && m <= 65536 : forced != 0) && g.mt % E == 0;
+}
+template <typename T>
+void combine16_launch(T* partials, const SplitGeom& g, uint64_t m, T* c, cudaStream_t s) {
+    constexpr unsigned E = 16 / sizeof(T), R = (256 / kC16G) * E;
+    launch(gemv_cm_fullcol_combine16_kernel<T>, unsigned((m + R - 1) / R), 256u, 0, s,
+           static_cast<const T*>(partials), g.grid, m, uint64_t(g.mt), c);
+}
+
 template <typename T> SplitGeom cm_split_geom(CmPath p, const T* A, uint64_t m, uint64_t n, int* tc) {
     if (p == kPathBulk) return split_bulk_geom<T>(m, n, tc);
     if (p == kPathBulkScalar) {
@@ -1558,8 +1594,10 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
                 return true;
             }();
             (void)configured;
+            const bool ext = split_external_combine<T>(g, m);
             launch(gemv_cm_split_realign_kernel<T>, grid, kRealignBlock, g.smem, s, A, x, c, m, n,
-                   g.mt, g.row_lanes, partials, ws.counters);
+                   g.mt, g.row_lanes, partials, ws.counters, int(ext));
+            if (ext) combine16_launch<T>(partials, g, m, c, s);
         } else if (path == kPathFullCol) {
             launch(gemv_cm_fullcol_kernel<T>, g.grid, g.threads, 0, s, A, x, m, n, g.row_lanes,
                    partials);
@@ -1574,19 +1612,24 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
             }();
             if (comb16)
                 launch(gemv_cm_fullcol_combine16_kernel<T>, unsigned((m + R - 1) / R), 256u, 0, s,
-                       static_cast<const T*>(partials), g.grid, m, c);
+                       static_cast<const T*>(partials), g.grid, m, m, c);
             else
                 launch(gemv_cm_fullcol_combine_kernel<T>, unsigned((m + 31) / 32), 1024u, 0, s,
                        static_cast<const T*>(partials), g.grid, m, c);
         } else if (path == kPathSplitVec) {
-            launch(gemv_cm_split_vec_kernel<T>, grid, kSplitBlock, 0, s, 
-                A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);
-        } else if (g.rpt == 1) {
-            launch(gemv_cm_split_kernel<T, 1>, grid, kSplitBlock, g.smem, s, 
-                A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);
+            const bool ext = split_external_combine<T>(g, m);
+            launch(gemv_cm_split_vec_kernel<T>, grid, kSplitBlock, 0, s,
+                   A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters, int(ext));
+            if (ext) combine16_launch<T>(partials, g, m, c, s);
         } else {
-            launch(gemv_cm_split_kernel<T, 2>, grid, kSplitBlock, g.smem, s, 
-                A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters);
+            const bool ext = split_external_combine<T>(g, m);
+            if (g.rpt == 1)
+                launch(gemv_cm_split_kernel<T, 1>, grid, kSplitBlock, g.smem, s,
+                       A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters, int(ext));
+            else
+                launch(gemv_cm_split_kernel<T, 2>, grid, kSplitBlock, g.smem, s,
+                       A, x, c, m, n, g.mt, g.row_lanes, partials, ws.counters, int(ext));
+            if (ext) combine16_launch<T>(partials, g, m, c, s);
         }
         if (info) info->ctas = g.grid * g.row_tiles;
     }
