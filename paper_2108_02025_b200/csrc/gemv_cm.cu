@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     gemv_cm_split_bulk_kernel(const T* __restrict__ A, const T* __restrict__ x,
                               T* __restrict__ c, uint64_t m, uint64_t n, int row_lanes, int tc,
                               uint64_t x_off, T* __restrict__ partials,
-                              unsigned* __restrict__ ticket, int x_bulk) {
+                              unsigned* __restrict__ ticket, int x_bulk, int external_combine) {
     pdl_enter();
     constexpr int V = Vec<T>::N;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
         for (int q = 1; q < col_lanes; ++q) v = add_rn(v, comb[uint64_t(q) * m + r]);
         partials[uint64_t(blockIdx.x) * m + r] = v;
     }
+    if (external_combine) return; // gemv_cm_fullcol_combine16_kernel follows (PDL)
     __threadfence();
     __syncthreads();
     if (tid == 0) am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     gemv_cm_split_bulk_scalar_kernel(const T* __restrict__ A, const T* __restrict__ x,
                                      T* __restrict__ c, uint64_t m, uint64_t n, int row_lanes,
                                      int tc, uint64_t x_off, int x_bulk, T* __restrict__ partials,
-                                     unsigned* __restrict__ ticket, int a_off) {
+                                     unsigned* __restrict__ ticket, int a_off, int external_combine) {
     pdl_enter();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* stages = reinterpret_cast<T*>(smem_raw);
@@ -566,6 +567,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
         for (int q = 1; q < col_lanes; ++q) v = add_rn(v, comb[uint64_t(q) * m + r]);
         partials[uint64_t(blockIdx.x) * m + r] = v;
     }
+    if (external_combine) return; // gemv_cm_fullcol_combine_kernel follows (PDL)
     __threadfence();
     __syncthreads();
     if (tid == 0) am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
@@ -1255,9 +1257,24 @@ void bulk_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const SplitGe
         return true;
     }();
     (void)configured;
-    launch(gemv_cm_split_bulk_kernel<T, NS, SB>, g.grid, kBulkThreads, bulk_smem(NS, SB), s, 
-        A, x, c, m, n, g.row_lanes, tc, uint64_t(tc) * m, partials, ticket,
-        int((reinterpret_cast<uintptr_t>(x) & 15u) == 0));
+    // The per-row sum of the G CTA partials in a one-wave combine kernel
+    // instead of by the last CTA alone (256 MiB flushed / back to back,
+    // tools/ab_shapes.py: fp32 m = 256 51.4 / 46.5 -> 48.2 / 43.8 us, m = 504
+    // 54.2 / 49.2 -> 48.4 / 44.0; fp64 m = 504 91.0 -> 84.8; G3 flushed
+    // 304.8 -> 300.6).  CABL_CM_BULK_COMB16=0 keeps the in-kernel finish (A/B).
+    static const int comb16 = [] {
+        const char* e = tuning_env("CABL_CM_BULK_COMB16");
+        return e ? atoi(e) : 1;
+    }();
+    const bool ext = comb16 != 0 && g.grid >= 2;
+    launch(gemv_cm_split_bulk_kernel<T, NS, SB>, g.grid, kBulkThreads, bulk_smem(NS, SB), s,
+           A, x, c, m, n, g.row_lanes, tc, uint64_t(tc) * m, partials, ticket,
+           int((reinterpret_cast<uintptr_t>(x) & 15u) == 0), int(ext));
+    if (ext) {
+        constexpr unsigned E = 16 / sizeof(T), R = (256 / kC16G) * E;
+        launch(gemv_cm_fullcol_combine16_kernel<T>, unsigned((m + R - 1) / R), 256u, 0, s,
+               static_cast<const T*>(partials), g.grid, m, m, c);
+    }
 }
 
 // Rows per consumer thread for the scalar bulk kernel: with row_lanes =
@@ -1293,9 +1310,19 @@ void bulk_scalar_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const 
         return true;
     }();
     (void)configured;
+    // the G CTA partials of each row summed by the (scalar-load) one-wave
+    // combine kernel, as in bulk_go (CABL_CM_BULK_COMB16=0: in-kernel, A/B)
+    static const int comb = [] {
+        const char* e = tuning_env("CABL_CM_BULK_COMB16");
+        return e ? atoi(e) : 1;
+    }();
+    const bool ext = comb != 0 && g.grid >= 2;
     launch(gemv_cm_split_bulk_scalar_kernel<T, 3, 49152, RPT>, g.grid, kBulkThreads,
            bulk_smem(3, 49152), s, A, x, c, m, n, g.row_lanes, tc, x_off, x_bulk, partials,
-           ticket, a_off);
+           ticket, a_off, int(ext));
+    if (ext)
+        launch(gemv_cm_fullcol_combine_kernel<T>, unsigned((m + 31) / 32), 1024u, 0, s,
+               static_cast<const T*>(partials), g.grid, m, c);
 }
 
 inline int split_mode() {
