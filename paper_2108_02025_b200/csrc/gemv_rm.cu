@@ -761,7 +761,23 @@ cudaError_t rm_launch_impl(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         const uint64_t need = (m + kRmBlock - 1) / kRmBlock;
         const unsigned grid = unsigned(need < cap ? need : cap);
         if (mode == 3)
-            launch(gemv_rm_lane_kernel<T, true, 2>, grid, kRmBlock, 0, s, A, x, c, m, n);
+        {
+            // U = 8 vectors in flight per thread from 8 vectors per row (256
+            // MiB flushed, tools/ab_shapes.py: fp32 n = 64 / 32 56.8 / 52.6 ->
+            // 53.0 / 50.7 us, fp64 n = 32 103.0 -> 98.3); shorter rows keep
+            // U = 2 (fp32 n = 8 60.3 -> 73.1 with 8).  CABL_RM_LANE_U overrides.
+            static const int forced_u = [] {
+                const char* e = tuning_env("CABL_RM_LANE_U");
+                return e ? atoi(e) : 0;
+            }();
+            const int lane_u = forced_u ? forced_u : (n / Vec<T>::N >= 4 * (sizeof(T) / 4) ? 8 : 2);
+            if (lane_u == 4)
+                launch(gemv_rm_lane_kernel<T, true, 4>, grid, kRmBlock, 0, s, A, x, c, m, n);
+            else if (lane_u == 8)
+                launch(gemv_rm_lane_kernel<T, true, 8>, grid, kRmBlock, 0, s, A, x, c, m, n);
+            else
+                launch(gemv_rm_lane_kernel<T, true, 2>, grid, kRmBlock, 0, s, A, x, c, m, n);
+        }
         else
             launch(gemv_rm_lane_kernel<T, false, 8>, grid, kRmBlock, 0, s, A, x, c, m, n);
         if (info) info->ctas = grid;
