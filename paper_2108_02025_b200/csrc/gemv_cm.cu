@@ -141,9 +141,16 @@ __global__ void __launch_bounds__(kTallBlock, 1)
     const Partition part(units, gridDim.x);
     for (uint64_t u = part.begin(blockIdx.x); u < part.begin(blockIdx.x + 1); ++u) {
         Vec<T> a[P][NC];
+        Vec<T> cv[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             const uint64_t rv = u * per_unit + uint64_t(p) * kTallBlock + threadIdx.x;
+            // c's vector in the same batch as A's: at n = 4 c is a third of
+            // the bytes, and loading it only when the sum starts serialised a
+            // second round trip (256 MiB of A flushed, tools/ab_shapes.py:
+            // fp32 2^24 x 4 78.7 -> 65.1 us, 2^26 x 1 207 -> 123; fp64 2^24 x
+            // 4 147 -> 124)
+            if (rv < mv) cv[p] = ld_rmw(Cv + rv);
 #pragma unroll
             for (int k = 0; k < NC; ++k)
                 if (rv < mv && uint64_t(k) < n) a[p][k] = ld_stream(Av + rv + uint64_t(k) * mv);
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(kTallBlock, 1)
         for (int p = 0; p < P; ++p) {
             const uint64_t rv = u * per_unit + uint64_t(p) * kTallBlock + threadIdx.x;
             if (rv < mv) {
-                Vec<T> acc = Cv[rv];
+                Vec<T> acc = cv[p];
 #pragma unroll
                 for (int k = 0; k < NC; ++k)
                     if (uint64_t(k) < n)
