@@ -194,8 +194,8 @@ __global__ void __launch_bounds__(kRmBlock, MINB)
             prefetch_l2_bulk(A + row * n, unsigned(n * sizeof(T) < pass ? n * sizeof(T) : pass));
     }
     pdl_wait();
-    sweep_groups<T, R, KV, DYN>(A, x, m, n, counter, blockIdx.x, gridDim.x,
-                                [&](uint64_t row, T sum) { c[row] = add_rn(c[row], sum); });
+    sweep_groups<T, R, KV, DYN>(A, x, m, n, counter, blockIdx.x, gridDim.x, c,
+                                [&](uint64_t row, T sum, T c_row) { c[row] = add_rn(c_row, sum); });
 }
 
 // CHUNKED FEW-ROWS kernel (aligned rows, few of them: a row is a long DOT

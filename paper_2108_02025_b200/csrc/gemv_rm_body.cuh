@@ -12,11 +12,13 @@ constexpr int kRmBlock = 256;
 // The sweep's group loop (shared with the gathering sweep in peer_gemv.cu):
 // CTA `bid` of `nblk` takes groups bid, bid + nblk, ... (DYN: the first
 // static, the rest from the queue) and hands each row's sum (before c) to
-// `epi(row, sum)`, thread tid < rows.
+// `epi(row, sum, c_row)`, thread tid < rows, where c_row = c[row] was loaded
+// at the start of the group (its latency hides behind the group's A loads
+// instead of following the reduction).
 template <typename T, int R, int KV, bool DYN, typename Epi>
 __device__ __forceinline__ void sweep_groups(const T* __restrict__ A, const T* __restrict__ x,
                                              uint64_t m, uint64_t n, unsigned* __restrict__ counter,
-                                             unsigned bid, unsigned nblk, Epi epi) {
+                                             unsigned bid, unsigned nblk, const T* c, Epi epi) {
     constexpr int NW = kRmBlock / kWarp;
     __shared__ T red[2][R][NW];
     __shared__ unsigned long long next_sh[2];
@@ -30,6 +32,7 @@ __device__ __forceinline__ void sweep_groups(const T* __restrict__ A, const T* _
         if (DYN && tid == 0) next_sh[parity ^ 1] = dyn_next(counter, groups, nblk); // prefetch
         const uint64_t row0 = g * R;
         const int rows = (m - row0 < uint64_t(R)) ? int(m - row0) : R;
+        const T c_row = tid < rows ? c[row0 + tid] : T(0);
         T acc[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = T(0);
@@ -68,7 +71,7 @@ __device__ __forceinline__ void sweep_groups(const T* __restrict__ A, const T* _
             T sum = red[parity][tid][0];
 #pragma unroll
             for (int w = 1; w < NW; ++w) sum = add_rn(sum, red[parity][tid][w]);
-            epi(row0 + tid, sum);
+            epi(row0 + tid, sum, c_row);
         }
         parity ^= 1;
         g = DYN ? next_sh[parity] : g + nblk;

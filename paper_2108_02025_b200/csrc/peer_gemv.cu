@@ -73,9 +73,9 @@ __global__ void __launch_bounds__(kRmBlock, MINB)
     T* c = a.c[lr];
     const int world = a.world;
     const uint64_t off = a.row_off[lr];
-    sweep_groups<T, R, KV, DYN>(a.A[lr], a.x[lr], a.m[lr], a.n, a.counters[lr], blockIdx.x, nblk,
-                                [&](uint64_t row, T sum) {
-                                    const T v = add_rn(c[row], sum);
+    sweep_groups<T, R, KV, DYN>(a.A[lr], a.x[lr], a.m[lr], a.n, a.counters[lr], blockIdx.x, nblk, c,
+                                [&](uint64_t row, T sum, T c_row) {
+                                    const T v = add_rn(c_row, sum);
                                     c[row] = v;
                                     const uint64_t at = uint64_t(epoch_sh & 1) * a.m_total + off + row;
                                     for (int g = 0; g < world; ++g) a.cfull[g][at] = v;
