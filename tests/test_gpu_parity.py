@@ -229,6 +229,33 @@ def test_gemv_col_major_fullcol_combine(cuda, dtype, m, n):
     assert np.all(np.abs(got.astype(np.float64) - truth) <= tol_t)
 
 
+# fp32 8192 < m <= 16384: the two-row-vector full-column sweep and its 16-byte
+# combine (a second row vector live for 1 thread, grids below 16 parts, one
+# column); fp64 at the same m: the 2-D split finishing in the same combine
+# kernel (row tiles, >= 2 parts) or in-kernel (1 part)
+TWO_RV_SHAPES = [(8200, 300), (16384, 7), (9000, 1), (16376, 4097), (12000, 160), (8208, 148)]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("m,n", TWO_RV_SHAPES)
+def test_gemv_col_major_two_row_vectors_and_combine16(cuda, dtype, m, n):
+    import paper_2108_02025_b200 as cb
+    got, want, truth, rowabs, c0, probe, pol = _gemv_case(cuda, dtype, m, n, cb.Layout.ColMajor)
+    dt = got.dtype
+    tol_c = T.contract_tol(n, rowabs, np.abs(c0), dt)
+    assert np.all(np.abs(got.astype(np.float64) - want) <= tol_c)
+    tol_t = T.truth_tol(T.gemv_cm_chain(m, n, dt), rowabs, np.abs(c0), dt)
+    assert np.all(np.abs(got.astype(np.float64) - truth) <= tol_t)
+    # run to run: the same bits
+    A = cb.DenseMatrix.wrap(dev_uniform(m * n, dtype, 3, cuda), m, n, cb.Layout.ColMajor)
+    x, c1 = dev_uniform(n, dtype, 1, cuda), dev_uniform(m, dtype, 4, cuda)
+    c2 = c1.clone()
+    cb.gemv_col_major(A, x, c1, pol)
+    cb.gemv_col_major(A, x, c2, pol)
+    assert torch.equal(c1, c2)
+    np.testing.assert_array_equal(np_of(c1), got)
+
+
 def test_gemv_col_major_fullcol_tickets_interleaved(cuda):
     """The full-column sweep's arrival/departure tickets live in the stream's
     shared counters: back-to-back launches with different grids, interleaved
