@@ -585,6 +585,98 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     if (tid == 0) *ticket = 0u;
 }
 
+// Full-column bulk ring for columns that are not 32-byte vectors (odd m, or A
+// off a 32-byte boundary), 1024 <= m with one column per stage: a column is
+// contiguous, so the producer lane copies column j (from the 16-byte boundary
+// at or below its first element, rounded up to whole 16-byte units) into a
+// ring stage with one cp.async.bulk; CTAs take columns grid-stride (the whole
+// GPU sweeps A front to back together, as the aligned full-column sweep
+// does).  Consumer thread t owns rows t, t + 512, ... (RPT of them) across all
+// columns and reads its scalars from the stage at the column's offset, so no
+// realignment shuffles are needed; each CTA writes its partial (row stride
+// mp = m rounded up to 16 bytes) and gemv_cm_fullcol_combine16_kernel sums
+// them.  Replaces the realigning 2-D split (warp shuffles per column, 128
+// registers, one 512-thread CTA per SM, latency-bound at 4.6 TB/s fp32).
+constexpr int kColBulkStages = 3;
+constexpr unsigned kColBulkStageBytes = 49152;
+constexpr int kColBulkMaxTc = 12; // columns per stage: m >= 1024 fits <= 11 fp32 columns
+
+template <typename T, int RPT>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+    gemv_cm_colbulk_kernel(const T* __restrict__ A, const T* __restrict__ x, uint64_t m, uint64_t n,
+                           uint64_t mp, int tc, T* __restrict__ partials) {
+    pdl_enter();
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* stages = reinterpret_cast<T*>(smem_raw);
+    constexpr uint64_t kStageElems = kColBulkStageBytes / sizeof(T);
+    constexpr uint64_t q = 16 / sizeof(T); // elements per 16-byte unit
+    constexpr unsigned ns = kColBulkStages;
+    __shared__ __align__(8) uint64_t full[kColBulkStages];
+    __shared__ __align__(8) uint64_t empty[kColBulkStages];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // A's element offset from the 16-byte boundary below it
+    const uint64_t a_base = (reinterpret_cast<uintptr_t>(A) & 15u) / sizeof(T);
+    const uint64_t tiles = (n + uint64_t(tc) - 1) / uint64_t(tc); // tc consecutive columns per stage
+    if (tid == 0) {
+        for (int st = 0; st < int(ns); ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], kBulkConsumerWarps);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == kBulkConsumerWarps) {
+        if (lane == 0) { // producer: column j from the 16-byte boundary at or below it
+            const uint64_t pol = l2_evict_first_policy();
+            uint64_t it = 0;
+            for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+                const int st = int(it % unsigned(ns));
+                const unsigned use = unsigned(it / unsigned(ns));
+                if (use > 0) mbar_wait(&empty[st], (use - 1) & 1u);
+                const uint64_t j0 = t * uint64_t(tc);
+                const uint64_t cols = n - j0 < uint64_t(tc) ? n - j0 : uint64_t(tc);
+                const uint64_t off = (a_base + j0 * m) % q;
+                // whole 16-byte units; the last one may end inside the next
+                // column (or past A's end within that same 16-byte segment:
+                // bytes never read by the consumers, no page can be crossed)
+                const unsigned bytes = unsigned(((off + cols * m) * sizeof(T) + 15) & ~uint64_t(15));
+                mbar_arrive_expect_tx(&full[st], bytes);
+                bulk_g2s(stages + st * kStageElems, A + j0 * m - off, bytes, &full[st], pol);
+            }
+        }
+    } else {
+        T acc[RPT];
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) acc[k] = T(0);
+        uint64_t it = 0;
+        for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            const int st = int(it % unsigned(ns));
+            const uint64_t j0 = t * uint64_t(tc);
+            const int cols = int(n - j0 < uint64_t(tc) ? n - j0 : uint64_t(tc));
+            T xj = __ldg(x + j0); // the first column's x before the wait
+            mbar_wait(&full[st], unsigned(it / unsigned(ns)) & 1u);
+            const T* col = stages + st * kStageElems + (a_base + j0 * m) % q;
+            for (int cc = 0; cc < cols; ++cc, col += m) {
+                const T xn = cc + 1 < cols ? __ldg(x + j0 + cc + 1) : T(0); // the next one's
+#pragma unroll
+                for (int k = 0; k < RPT; ++k) {
+                    const unsigned r = unsigned(tid) + unsigned(k) * kBulkConsumers;
+                    if (r < unsigned(m)) acc[k] = fma_rn(col[r], xj, acc[k]);
+                }
+                xj = xn;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+        }
+        T* out = partials + uint64_t(blockIdx.x) * mp;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            const uint64_t r = uint64_t(tid) + uint64_t(k) * kBulkConsumers;
+            if (r < m) out[r] = acc[k];
+        }
+    }
+}
+
 // Full-column sweep (aligned mid-size m, m/V <= 1024: fp32 m <= 8192, fp64 m <= 4096).
 // The 2-D split reads a fixed 1 KB row slot of every column per CTA and its
 // CTAs finish up to ~10 us apart on a 50 us launch (profiles/r02_cm_mid.md).
@@ -1355,7 +1447,29 @@ inline bool bulk_any_align() {
 }
 
 enum CmPath { kPathTallVec, kPathTallScalar, kPathBulk, kPathBulkScalar, kPathSplitVec,
-              kPathSplitScalar, kPathSplitRealign, kPathFullCol, kPathFullCol2 };
+              kPathSplitScalar, kPathSplitRealign, kPathFullCol, kPathFullCol2, kPathColBulk };
+
+// Full-column bulk ring for unvectorisable columns (odd m or A off a 32-byte
+// boundary) from kBulkScalarMaxRows rows while one column fits a stage
+// (CABL_CM_COLBULK=0|1, A/B).
+inline int colbulk_forced() {
+    static const int v = [] {
+        const char* e = tuning_env("CABL_CM_COLBULK");
+        return e ? atoi(e) : -1;
+    }();
+    return v;
+}
+template <typename T> bool colbulk_ok(const T* A, uint64_t m) {
+    if (colbulk_forced() == 0) return false;
+    if (reinterpret_cast<uintptr_t>(A) % sizeof(T) != 0) return false;
+    constexpr uint64_t q = 16 / sizeof(T);
+    if (m < kBulkScalarMaxRows || m > (kColBulkStageBytes - 32) / sizeof(T) - q) return false;
+    // stages hold >= 2 columns, or one column fills >= 3/4 of its stage: a
+    // single column of 50-75% of a stage leaves the ring short of bytes in
+    // flight (fp32 m = 8193: 68 us against 58 on the realigning split)
+    const uint64_t tcols = (kColBulkStageBytes / sizeof(T) - 2 * q) / m;
+    return tcols >= 2 || m * sizeof(T) * 4 >= uint64_t(kColBulkStageBytes) * 3;
+}
 
 // Full-column sweep for aligned m with m/V <= 1024 row vectors (at most one per
 // thread of a 1024-thread CTA).  CABL_CM_FULLCOL=0 keeps the 2-D split (A/B).
@@ -1459,6 +1573,7 @@ template <typename T> CmPath cm_path(const T* A, const T* c, uint64_t m) {
         return kPathBulkScalar;
     if (m < kBulkScalarMaxRows && split_mode() == 1 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0)
         return kPathBulkScalar;
+    if (colbulk_ok(A, m)) return kPathColBulk;
     // the realigning split when its tiling keeps most SM slots and tile rows
     // busy (score >= 0.8: 8193 rows 0.89); a poor tiling (m = 100003: 0.70,
     // 74 us against the scalar split's 61) stays on the scalar split
@@ -1496,6 +1611,32 @@ void combine16_launch(T* partials, const SplitGeom& g, uint64_t m, T* c, cudaStr
            static_cast<const T*>(partials), g.grid, m, uint64_t(g.mt), c);
 }
 
+template <typename T, int RPT>
+void colbulk_launch(const T* A, const T* x, uint64_t m, uint64_t n, const SplitGeom& g, T* partials,
+                    cudaStream_t s) {
+    static bool configured = [] {
+        cudaFuncSetAttribute(gemv_cm_colbulk_kernel<T, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kColBulkStages * kColBulkStageBytes));
+        return true;
+    }();
+    (void)configured;
+    launch(gemv_cm_colbulk_kernel<T, RPT>, g.grid, unsigned(kBulkThreads), g.smem, s, A, x, m, n,
+           uint64_t(g.mt), g.col_lanes, partials);
+}
+template <typename T>
+void colbulk_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const SplitGeom& g, T* partials,
+                cudaStream_t s) {
+    const int rpt = g.rpt;
+    if (rpt <= 2) colbulk_launch<T, 2>(A, x, m, n, g, partials, s);
+    else if (rpt <= 4) colbulk_launch<T, 4>(A, x, m, n, g, partials, s);
+    else if (rpt <= 8) colbulk_launch<T, 8>(A, x, m, n, g, partials, s);
+    else if (rpt <= 12) colbulk_launch<T, 12>(A, x, m, n, g, partials, s);
+    else if (rpt <= 16) colbulk_launch<T, 16>(A, x, m, n, g, partials, s);
+    else if (rpt <= 20) colbulk_launch<T, 20>(A, x, m, n, g, partials, s);
+    else colbulk_launch<T, 24>(A, x, m, n, g, partials, s);
+    combine16_launch<T>(partials, g, m, c, s);
+}
+
 template <typename T> SplitGeom cm_split_geom(CmPath p, const T* A, uint64_t m, uint64_t n, int* tc) {
     if (p == kPathBulk) return split_bulk_geom<T>(m, n, tc);
     if (p == kPathBulkScalar) {
@@ -1511,6 +1652,24 @@ template <typename T> SplitGeom cm_split_geom(CmPath p, const T* A, uint64_t m, 
     }
     if (p == kPathSplitVec) return split_vec_geom<T>(m, n);
     if (p == kPathFullCol) return fullcol_geom<T>(m, n);
+    if (p == kPathColBulk) {
+        SplitGeom g;
+        constexpr uint64_t q = 16 / sizeof(T);
+        g.threads = unsigned(kBulkThreads);
+        g.row_lanes = kBulkConsumers;
+        g.rpt = int((m + kBulkConsumers - 1) / kBulkConsumers);
+        // columns per stage: as many whole columns as fit with the 16-byte lead-in
+        uint64_t tcols = (kColBulkStageBytes / sizeof(T) - 2 * q) / m;
+        if (tcols > uint64_t(kColBulkMaxTc)) tcols = kColBulkMaxTc;
+        g.col_lanes = int(tcols < 1 ? 1 : tcols); // (carries tc to the launch)
+        g.smem = size_t(kColBulkStages) * kColBulkStageBytes;
+        const uint64_t tiles = (n + uint64_t(g.col_lanes) - 1) / uint64_t(g.col_lanes);
+        const uint64_t sms = uint64_t(sm_count());
+        g.grid = unsigned(tiles < sms ? tiles : sms);
+        g.row_tiles = 1;
+        g.mt = (m + q - 1) / q * q; // partial row stride: whole 16-byte units
+        return g;
+    }
     if (p == kPathFullCol2) {
         SplitGeom g;
         g.threads = 1024u;
@@ -1637,6 +1796,8 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
                    partials);
             launch(gemv_cm_fullcol_combine_kernel<T>, unsigned((m + 31) / 32), 1024u, 0, s,
                    static_cast<const T*>(partials), g.grid, m, c);
+        } else if (path == kPathColBulk) {
+            colbulk_go<T>(A, x, c, m, n, g, partials, s);
         } else if (path == kPathFullCol2) {
             constexpr unsigned E = 16 / sizeof(T), R = (256 / kC16G) * E;
             launch(gemv_cm_fullcol2_kernel<T>, g.grid, g.threads, 0, s, A, x, m, n, partials);
