@@ -598,17 +598,19 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
 // them.  Replaces the realigning 2-D split (warp shuffles per column, 128
 // registers, one 512-thread CTA per SM, latency-bound at 4.6 TB/s fp32).
 constexpr int kColBulkStages = 3;
-constexpr unsigned kColBulkStageBytes = 49152;
+constexpr unsigned kColBulkStageBytes = 49152;      // stage size for most m
+constexpr unsigned kColBulkBigStageBytes = 73728;   // 3 x 72 KB: 2 columns of fp32 m <= 9215,
+                                                    // or one of m <= 18424
 constexpr int kColBulkMaxTc = 12; // columns per stage: m >= 1024 fits <= 11 fp32 columns
 
-template <typename T, int RPT>
+template <typename T, int RPT, unsigned SB>
 __global__ void __launch_bounds__(kBulkThreads, 1)
     gemv_cm_colbulk_kernel(const T* __restrict__ A, const T* __restrict__ x, uint64_t m, uint64_t n,
                            uint64_t mp, int tc, T* __restrict__ partials) {
     pdl_enter();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* stages = reinterpret_cast<T*>(smem_raw);
-    constexpr uint64_t kStageElems = kColBulkStageBytes / sizeof(T);
+    constexpr uint64_t kStageElems = SB / sizeof(T);
     constexpr uint64_t q = 16 / sizeof(T); // elements per 16-byte unit
     constexpr unsigned ns = kColBulkStages;
     __shared__ __align__(8) uint64_t full[kColBulkStages];
@@ -1459,16 +1461,26 @@ inline int colbulk_forced() {
     }();
     return v;
 }
+// A stage size for m (0: none fits well): stages must hold >= 2 columns, or
+// one column filling >= 3/4 of the stage (fp32: 4/5) — a single column of
+// 50-75% of a stage leaves the ring short of bytes in flight (fp32 m = 8193
+// in 48 KB stages: 68 us against 58 on the realigning split; in 72 KB stages,
+// two per stage: 51.1), and fp32 14001 (76% of 72 KB) lost 56.1 -> 58.5
+// while fp64 7001 (76%) won 91.4 -> 85.2 (profiles/r02_cm_colbulk_big.jsonl).
+template <typename T> unsigned colbulk_stage(uint64_t m) {
+    constexpr uint64_t q = 16 / sizeof(T);
+    constexpr uint64_t fill_num = sizeof(T) == 4 ? 5 : 4, fill_den = sizeof(T) == 4 ? 4 : 3;
+    for (unsigned sb : {kColBulkStageBytes, kColBulkBigStageBytes}) {
+        if (m + 2 * q > sb / sizeof(T)) continue;
+        const uint64_t tcols = (sb / sizeof(T) - 2 * q) / m;
+        if (tcols >= 2 || m * sizeof(T) * fill_num >= uint64_t(sb) * fill_den) return sb;
+    }
+    return 0;
+}
 template <typename T> bool colbulk_ok(const T* A, uint64_t m) {
     if (colbulk_forced() == 0) return false;
     if (reinterpret_cast<uintptr_t>(A) % sizeof(T) != 0) return false;
-    constexpr uint64_t q = 16 / sizeof(T);
-    if (m < kBulkScalarMaxRows || m > (kColBulkStageBytes - 32) / sizeof(T) - q) return false;
-    // stages hold >= 2 columns, or one column fills >= 3/4 of its stage: a
-    // single column of 50-75% of a stage leaves the ring short of bytes in
-    // flight (fp32 m = 8193: 68 us against 58 on the realigning split)
-    const uint64_t tcols = (kColBulkStageBytes / sizeof(T) - 2 * q) / m;
-    return tcols >= 2 || m * sizeof(T) * 4 >= uint64_t(kColBulkStageBytes) * 3;
+    return m >= kBulkScalarMaxRows && colbulk_stage<T>(m) != 0;
 }
 
 // Full-column sweep for aligned m with m/V <= 1024 row vectors (at most one per
@@ -1611,29 +1623,39 @@ void combine16_launch(T* partials, const SplitGeom& g, uint64_t m, T* c, cudaStr
            static_cast<const T*>(partials), g.grid, m, uint64_t(g.mt), c);
 }
 
-template <typename T, int RPT>
+template <typename T, int RPT, unsigned SB>
 void colbulk_launch(const T* A, const T* x, uint64_t m, uint64_t n, const SplitGeom& g, T* partials,
                     cudaStream_t s) {
     static bool configured = [] {
-        cudaFuncSetAttribute(gemv_cm_colbulk_kernel<T, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kColBulkStages * kColBulkStageBytes));
+        cudaFuncSetAttribute(gemv_cm_colbulk_kernel<T, RPT, SB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(kColBulkStages * SB));
         return true;
     }();
     (void)configured;
-    launch(gemv_cm_colbulk_kernel<T, RPT>, g.grid, unsigned(kBulkThreads), g.smem, s, A, x, m, n,
-           uint64_t(g.mt), g.col_lanes, partials);
+    launch(gemv_cm_colbulk_kernel<T, RPT, SB>, g.grid, unsigned(kBulkThreads), g.smem, s, A, x, m,
+           n, uint64_t(g.mt), g.col_lanes, partials);
+}
+template <typename T, unsigned SB>
+void colbulk_rpt(const T* A, const T* x, uint64_t m, uint64_t n, const SplitGeom& g, T* partials,
+                 cudaStream_t s) {
+    const int rpt = g.rpt;
+    if (rpt <= 2) colbulk_launch<T, 2, SB>(A, x, m, n, g, partials, s);
+    else if (rpt <= 4) colbulk_launch<T, 4, SB>(A, x, m, n, g, partials, s);
+    else if (rpt <= 8) colbulk_launch<T, 8, SB>(A, x, m, n, g, partials, s);
+    else if (rpt <= 12) colbulk_launch<T, 12, SB>(A, x, m, n, g, partials, s);
+    else if (rpt <= 16) colbulk_launch<T, 16, SB>(A, x, m, n, g, partials, s);
+    else if (rpt <= 20) colbulk_launch<T, 20, SB>(A, x, m, n, g, partials, s);
+    else if (rpt <= 24) colbulk_launch<T, 24, SB>(A, x, m, n, g, partials, s);
+    else if (rpt <= 30) colbulk_launch<T, 30, SB>(A, x, m, n, g, partials, s);
+    else colbulk_launch<T, 36, SB>(A, x, m, n, g, partials, s);
 }
 template <typename T>
 void colbulk_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const SplitGeom& g, T* partials,
                 cudaStream_t s) {
-    const int rpt = g.rpt;
-    if (rpt <= 2) colbulk_launch<T, 2>(A, x, m, n, g, partials, s);
-    else if (rpt <= 4) colbulk_launch<T, 4>(A, x, m, n, g, partials, s);
-    else if (rpt <= 8) colbulk_launch<T, 8>(A, x, m, n, g, partials, s);
-    else if (rpt <= 12) colbulk_launch<T, 12>(A, x, m, n, g, partials, s);
-    else if (rpt <= 16) colbulk_launch<T, 16>(A, x, m, n, g, partials, s);
-    else if (rpt <= 20) colbulk_launch<T, 20>(A, x, m, n, g, partials, s);
-    else colbulk_launch<T, 24>(A, x, m, n, g, partials, s);
+    if (g.smem == size_t(kColBulkStages) * kColBulkStageBytes)
+        colbulk_rpt<T, kColBulkStageBytes>(A, x, m, n, g, partials, s);
+    else
+        colbulk_rpt<T, kColBulkBigStageBytes>(A, x, m, n, g, partials, s);
     combine16_launch<T>(partials, g, m, c, s);
 }
 
@@ -1659,10 +1681,11 @@ template <typename T> SplitGeom cm_split_geom(CmPath p, const T* A, uint64_t m, 
         g.row_lanes = kBulkConsumers;
         g.rpt = int((m + kBulkConsumers - 1) / kBulkConsumers);
         // columns per stage: as many whole columns as fit with the 16-byte lead-in
-        uint64_t tcols = (kColBulkStageBytes / sizeof(T) - 2 * q) / m;
+        const unsigned sb = colbulk_stage<T>(m);
+        uint64_t tcols = (sb / sizeof(T) - 2 * q) / m;
         if (tcols > uint64_t(kColBulkMaxTc)) tcols = kColBulkMaxTc;
         g.col_lanes = int(tcols < 1 ? 1 : tcols); // (carries tc to the launch)
-        g.smem = size_t(kColBulkStages) * kColBulkStageBytes;
+        g.smem = size_t(kColBulkStages) * sb;        // (and the stage size)
         const uint64_t tiles = (n + uint64_t(g.col_lanes) - 1) / uint64_t(g.col_lanes);
         const uint64_t sms = uint64_t(sm_count());
         g.grid = unsigned(tiles < sms ? tiles : sms);
