@@ -179,11 +179,15 @@ def one_case(cb, rng, kind, seed, dev):
 
 
 def main():
+    global MAX_ELEMS
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300.0)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--kinds", default="dot,gemv-row,gemv-col,gemv-col,ger-row,ger-col")
+    ap.add_argument("--max-elems", type=int, default=MAX_ELEMS,
+                    help="largest operand in elements (the CPU oracle's time per case grows with it)")
     args = ap.parse_args()
+    MAX_ELEMS = args.max_elems
     import paper_2108_02025_b200 as cb
     dev = torch.device("cuda:0")
     kinds = args.kinds.split(",")
@@ -205,7 +209,8 @@ def main():
         done += 1
         case += 1
     print(json.dumps({"summary": True, "cases": done, "failures": fails, "per_kind": per,
-                      "seconds": round(time.time() - t0, 1), "seed": args.seed}), flush=True)
+                      "seconds": round(time.time() - t0, 1), "seed": args.seed,
+                      "max_elems": MAX_ELEMS}), flush=True)
     return 1 if fails else 0
 
 
