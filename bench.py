@@ -188,7 +188,7 @@ def workload_config(w) -> dict:
     """The line's ``config``: workload-defining fields only, identical for our
     arm and the reference arm (so the driver can match the two lines).  How a
     run was executed (GPUs, machine, L2 policy details) goes under ``run``."""
-    step = w.alg_bytes(1)
+    step = w.footprint_bytes()
     return {"workload": f"{w.id}: {w.desc}", "m_per_gpu": w.m, "n": w.n,
             "layout": {"gemv-row": "row-major", "gemv-col": "col-major", "ger": "row-major",
                        "dot": "vector"}[w.op],
@@ -298,8 +298,9 @@ L2_BYTES = 126 << 20
 
 
 def l2_mode(step_bytes: int) -> str:
-    """'stream' when a step's inputs exceed the L2: the front-to-back sweep of
-    step k+1 misses on everything step k left behind.  Checked with ncu
+    """'stream' when the DISTINCT bytes a step touches (Workload.footprint_bytes:
+    GER's in-place C counts once, not as read + write) exceed the L2: the
+    front-to-back sweep of step k+1 misses on everything step k left behind.  Checked with ncu
     (--cache-control none) on back-to-back launches of the two smallest
     configs: every G1 launch (268.5 MB alg.) reads 268.5 MB from DRAM; a D1
     launch (134.2 MB) reads 131.2 MB, i.e. ~2% of it still hits in L2
@@ -480,8 +481,9 @@ def run_ours(args, ctx):
     ins = make_inputs(w, rows, ctx.dev)
     fn, launches_per_step = step_fn(w, ins, policy, ctx, sharded_dot=False)
     sampler = ClockSampler(ctx.local)
-    mode = args.l2 if args.l2 != "auto" else l2_mode(w.alg_bytes(1))
-    times, wall = time_steps(fn, args.steps, args.warmup, ctx, flush, sampler, mode=mode)
+    mode = args.l2 if args.l2 != "auto" else l2_mode(w.footprint_bytes())
+    times, wall = time_steps(fn, args.steps, args.warmup, ctx, flush, sampler, mode=mode,
+                             charge_writeback=(mode == "flush" and w.op == "ger"))
     t_rank = sum(times) / 1000.0
     t_max = ctx.max(t_rank)
     bytes_rank = w.alg_bytes(1)
@@ -754,8 +756,13 @@ def run_suite(args, ctx, flush, policy, peak):
             if fused:
                 peer_probe(fn, ctx)
             alg = w.alg_bytes(ctx.world)
-            mode = l2_mode(wl.alg_bytes(1))
-            times, _ = time_steps(fn, steps, args.warmup, ctx, flush, mode=mode)
+            # the shard's footprint decides (an R1 shard at N >= 4 fits in L2 and
+            # would run out of it back to back: 64 MiB of C at 9.8 TB/s,
+            # profiles/r02_shard_share.jsonl); a flushed GER is charged the
+            # write-back of the lines it leaves dirty in L2
+            mode = l2_mode(wl.footprint_bytes())
+            times, _ = time_steps(fn, steps, args.warmup, ctx, flush, mode=mode,
+                                  charge_writeback=(mode == "flush" and w.op == "ger"))
             t_max = ctx.max(sum(times) / 1000.0)
             gbs = alg * steps / t_max / 1e9
             desc = w.desc + ((", partials exchanged inside the kernel over peer memory "

@@ -49,6 +49,15 @@ class Workload:
             return m * n * s + gpus * n * s + 2 * m * s
         return 2 * m * n * s + m * s + gpus * n * s
 
+    def footprint_bytes(self) -> int:
+        """Distinct bytes one step touches on one GPU (what has to fit in L2 for a
+        back-to-back step to run out of L2): GER's C is read and written in place,
+        so it counts once here and twice in alg_bytes."""
+        s, m, n = self.s, self.m, self.n
+        if self.op == "dot":
+            return 2 * n * s
+        return m * n * s + m * s + n * s
+
     def flops(self) -> int:
         return 2 * self.n if self.op == "dot" else 2 * self.m * self.n
 

@@ -101,3 +101,25 @@ def test_both_arms_share_the_workload_config():
                        cwd=ROOT)
     d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
     assert d["config"] == bench.workload_config(WL.WORKLOADS["G1"])
+
+
+def test_l2_policy_follows_the_footprint_not_the_algorithmic_bytes():
+    """A GER shard whose in-place C fits in L2 must be flushed between steps even
+    though its read + write bytes exceed the L2 (R1 over 4 GPUs: 64 MiB of C, 134 MB
+    algorithmic; back to back it runs out of L2 at 9.8 TB/s,
+    profiles/r02_shard_share.jsonl)."""
+    import dataclasses
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_2108_02025_b200 import workloads as WL
+    r1 = WL.WORKLOADS["R1"]
+    assert r1.footprint_bytes() == 8192 * 8192 * 4 + 2 * 8192 * 4
+    assert r1.alg_bytes(1) == 2 * 8192 * 8192 * 4 + 2 * 8192 * 4
+    assert bench.l2_mode(r1.footprint_bytes()) == "stream"
+    quarter = dataclasses.replace(r1, m=r1.m // 4)
+    assert quarter.alg_bytes(1) > bench.L2_BYTES > quarter.footprint_bytes()
+    assert bench.l2_mode(quarter.footprint_bytes()) == "flush"
+    for wid in ("D1", "G1", "G2", "G3", "G4", "D2"):  # read-only inputs: footprint ~ alg bytes
+        w = WL.WORKLOADS[wid]
+        assert bench.l2_mode(w.footprint_bytes()) == "stream"
+        assert 0 <= w.alg_bytes(1) - w.footprint_bytes() <= w.m * w.s
