@@ -378,6 +378,45 @@ def time_steps(fn, steps, warmup, ctx, flush, sampler=None, mode="flush", charge
     return [s.elapsed_time(e) - sub for s, e in zip(starts, ends)], wall
 
 
+def rotating_copies(footprint: int) -> int:
+    """Independent copies of a step's operands so that their combined footprint
+    exceeds 2x the L2 (at least 3, at most 24)."""
+    return max(3, min(24, -(-2 * L2_BYTES // max(1, footprint)) + 1))
+
+
+def time_rotating(fns, steps, warmup, ctx, flush, charge_writeback=False):
+    """Steps back to back over len(fns) independent copies of the step's operands,
+    taken in turn: a step whose footprint fits in L2 (an R1 shard at N >= 4) still
+    reads its operands from HBM, because the copies used since its last turn pushed
+    them out — "inputs larger than L2" by rotation instead of a flush before every
+    launch, so launch latency and the write-back of dirty lines overlap the next
+    step as they do for the large configs in 'stream' mode.  One event pair around
+    all K steps; with charge_writeback the pair also encloses a final eviction pass
+    (minus its clean-L2 time), so the lines the last steps left dirty are charged
+    too.  Returns per-step ms (total / K)."""
+    import torch
+    R = len(fns)
+    sub = flush.evict_ms() if charge_writeback else 0.0
+    for k in range(max(warmup, R)):
+        fns[k % R]()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.barrier()
+    torch.cuda.synchronize()
+    prime = getattr(torch.cuda, "_sleep", None)  # private torch API: optional
+    if prime is not None:
+        prime(PRIME_CYCLES)
+    a.record()
+    for k in range(steps):
+        fns[k % R]()
+    if charge_writeback:
+        flush.evict_()
+    b.record()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    return [(a.elapsed_time(b) - sub) / steps] * steps
+
+
 # ------------------------------------------------------------ CPU baseline
 _CPU_INPUTS: dict = {}
 
@@ -761,9 +800,23 @@ def run_suite(args, ctx, flush, policy, peak):
             # profiles/r02_shard_share.jsonl); a flushed GER is charged the
             # write-back of the lines it leaves dirty in L2
             mode = l2_mode(wl.footprint_bytes())
-            times, _ = time_steps(fn, steps, args.warmup, ctx, flush, mode=mode,
-                                  charge_writeback=(mode == "flush" and w.op == "ger"))
-            t_max = ctx.max(sum(times) / 1000.0)
+            nsteps = steps
+            if mode == "flush" and not fused:
+                # footprint <= L2: back to back over rotating copies of the operands
+                # (time_rotating), the steady-state analogue of 'stream'; the
+                # flushed-per-launch time stays as the conservative column
+                mode = "rotate"
+                R = rotating_copies(wl.footprint_bytes())
+                rot = [fn] + [step_fn(wl, make_inputs(w, (b, e), ctx.dev), policy, ctx,
+                                      sharded_dot=True)[0] for _ in range(R - 1)]
+                nsteps = max(steps, 3 * R)
+                times = time_rotating(rot, nsteps, args.warmup, ctx, flush,
+                                      charge_writeback=w.op == "ger")
+                del rot
+            else:
+                times, _ = time_steps(fn, steps, args.warmup, ctx, flush, mode=mode,
+                                      charge_writeback=(mode == "flush" and w.op == "ger"))
+            t_max = ctx.max(sum(times) / 1000.0) * steps / nsteps  # seconds for `steps` steps
             gbs = alg * steps / t_max / 1e9
             desc = w.desc + ((", partials exchanged inside the kernel over peer memory "
                               "(cabl_cuda_dot_peer)" if w.op == "dot" else
@@ -775,7 +828,9 @@ def run_suite(args, ctx, flush, policy, peak):
                      "gflops": round(w.flops() * steps / t_max / 1e9, 2),
                      "alg_bytes": alg, "launches_per_step": lps, "l2": mode,
                      "scaling": "strong" if ctx.world > 1 else None}
-            if mode == "stream":  # also the conservative flushed number
+            if mode == "rotate":
+                entry["rotating_copies"] = R
+            if mode in ("stream", "rotate"):  # also the conservative flushed number
                 tf, _ = time_steps(fn, steps, args.warmup, ctx, flush, mode="flush",
                                    charge_writeback=w.op == "ger")
                 tfm = ctx.max(sum(tf) / 1000.0)
