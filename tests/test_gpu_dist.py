@@ -79,3 +79,45 @@ def test_bench_under_torchrun_world1(cuda):
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 1 and d["value"] > 1000 and d["gpu_launches"] == 20
+
+
+def test_rotating_copies_time_an_l2_sized_shard_from_hbm(cuda):
+    """bench.time_rotating on the R1 shard of an 8-GPU run (1024 x 8192 fp32, 32 MiB of
+    C): back to back over rotating copies it must be slower than the same steps on one
+    buffer (which never leave L2) — the copies really push each other out — and the
+    GER results must still be bitwise ger_ref on every copy."""
+    import dataclasses
+
+    import numpy as np
+    import torch
+    sys.path.insert(0, str(ROOT))
+    import bench
+    import paper_2108_02025_b200 as cb
+    from oracle import oracle as O
+    from paper_2108_02025_b200 import workloads as WL
+    dev = torch.device("cuda:0")
+    ctx = bench.Ctx(1, 0, 0, dev)
+    pol = cb.default_policy(1)
+    flush = bench.L2Flush(dev)
+    w = WL.WORKLOADS["R1"]
+    b, e = w.shard_rows(0, 8)
+    wl = dataclasses.replace(w, m=e - b)
+    assert bench.l2_mode(wl.footprint_bytes()) == "flush"
+    R = bench.rotating_copies(wl.footprint_bytes())
+    assert R * wl.footprint_bytes() > 2 * bench.L2_BYTES
+    ins = [bench.make_inputs(w, (b, e), dev) for _ in range(R)]
+    C0 = ins[0]["C"].data.cpu().numpy().copy()
+    fns = [bench.step_fn(wl, i, pol, ctx, sharded_dot=False)[0] for i in ins]
+    steps = 3 * R
+    rot = bench.time_rotating(fns, steps, 0, ctx, flush, charge_writeback=True)
+    one, _ = bench.time_steps(fns[0], steps, 3, ctx, flush, mode="stream")
+    assert len(rot) == steps and rot[0] > 0
+    assert rot[0] > 1.15 * one[0], (rot[0], one[0])
+    # copy 1 took 1 warm-up turn (R calls over R copies) + steps / R = 3 timed ones
+    x = ins[1]["x"].cpu().numpy()
+    y = ins[1]["y"].cpu().numpy()
+    want = np.ascontiguousarray(C0)
+    for _ in range(4):
+        O.ger_ref(x, y, want, 0)  # in place, row-major
+    got = ins[1]["C"].data.cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
