@@ -553,13 +553,6 @@ def run_ours(args, ctx):
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "error": str(e)}
 
-    # ---- suite of all BASELINE configs at this N
-    suite = None
-    if not args.no_suite:
-        suite = run_suite(args, ctx, flush, policy, peak)
-
-    if ctx.rank != 0:
-        return
     line = {
         "metric": "DOT/GEMV/GER achieved HBM GB/s & % of B200 roofline at 1/2/4/8 GPUs",
         "value": round(value, 2),
@@ -603,8 +596,53 @@ def run_ours(args, ctx):
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
         "wall_s_timed_region": round(wall, 4),
-        "suite": suite,
+        "suite": None,
     }
+
+    # ---- suite of all BASELINE configs at this N.  The headline above is complete;
+    # at N > 1 the suite's sharded entries use collectives that this pool (one GPU
+    # per box) has only run at world size 1, so a watchdog guards the line: if the
+    # suite has not finished within --suite-timeout seconds (a rank died or a
+    # collective hangs), rank 0 prints the line with the suite marked as timed out
+    # and every rank exits 0 instead of taking the headline down with it.
+    if not args.no_suite:
+        import threading
+        done = threading.Lock()
+
+        def give_up():
+            if not done.acquire(blocking=False):
+                return  # the normal path is already printing
+            if ctx.rank == 0:
+                line["suite"] = {"error": f"suite did not finish within {args.suite_timeout} s "
+                                          "(watchdog); headline, e2e and roofline are complete"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+        dog = None
+        if args.suite_timeout is None:
+            args.suite_timeout = 600.0 if ctx.world > 1 else 0.0
+        if args.suite_timeout > 0:
+            dog = threading.Timer(args.suite_timeout, give_up)
+            dog.daemon = True
+            dog.start()
+        try:
+            suite = run_suite(args, ctx, flush, policy, peak)
+        except Exception as ex:  # noqa: BLE001
+            if ctx.world == 1:
+                raise
+            # keep this rank alive (its peers may be inside a collective with it
+            # missing): the watchdog ends every rank, rank 0 after printing
+            print(f"bench.py: rank {ctx.rank}: suite failed: {ex!r}", file=sys.stderr, flush=True)
+            if dog is not None:
+                dog.join()
+            raise
+        if not done.acquire(blocking=False):
+            time.sleep(3600)  # the watchdog fired first and is printing / exiting
+        if dog is not None:
+            dog.cancel()
+        line["suite"] = suite
+    if ctx.rank != 0:
+        return
     print(json.dumps(line), flush=True)
 
 
@@ -1026,6 +1064,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--suite-steps", type=int, default=30)
+    ap.add_argument("--suite-timeout", type=float, default=None,
+                    help="seconds after which a suite that has not finished is abandoned and "
+                         "the headline line printed without it (default: 600 at N > 1, never "
+                         "at N = 1; 0 = never)")
     ap.add_argument("--fused-suite", action="store_true",
                     help="at N > 1 also time D2 / G4 with the exchange fused into the kernels "
                          "over peer memory (always on at N = 1)")

@@ -121,3 +121,18 @@ def test_rotating_copies_time_an_l2_sized_shard_from_hbm(cuda):
         O.ger_ref(x, y, want, 0)  # in place, row-major
     got = ins[1]["C"].data.cpu().numpy()
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_bench_suite_watchdog_keeps_the_headline(cuda):
+    """A suite that does not finish in time (at N > 1: a dead rank or a hung
+    collective) must not take the headline down: the line is printed with the suite
+    marked as timed out and the process exits 0."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--steps", "20", "--warmup", "3",
+                        "--no-e2e", "--no-cpu-baseline", "--suite-timeout", "0.05"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["value"] > 1000 and d["roofline"]["frac"] > 0.5
+    assert "watchdog" in d["suite"]["error"]
