@@ -282,9 +282,11 @@ def step_fn(w, ins, policy, ctx, sharded_dot: bool, fused: bool = False):
         return (lambda: ctx.gather_gemv(ins["A"], ins["x"], ins["c"], row_off)), 1
     if w.op == "gemv-row" and sharded_dot and ctx.world > 1 and w.id == "G4":
         # BASELINE config 5: "c slices all-gathered" (NCCL) after the row blocks
+        import torch
         m_total = WL.WORKLOADS["G4"].m
+        full_c = torch.empty(m_total, dtype=w.dtype, device=ctx.dev)
         return (lambda: shard.sharded_gemv_rows(ins["A"], ins["x"], ins["c"], policy,
-                                                gather=True, m_total=m_total)), 1
+                                                gather=True, m_total=m_total, out=full_c)), 1
     if w.op == "gemv-row":
         return (lambda: cb.gemv_row_major(ins["A"], ins["x"], ins["c"], policy)), 1
     if w.op == "gemv-col":

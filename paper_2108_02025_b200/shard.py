@@ -80,8 +80,13 @@ def sharded_dot(x_local: torch.Tensor, y_local: torch.Tensor, alpha0: float, out
 
 def sharded_gemv_rows(A_local: "cabl.DenseMatrix", x: torch.Tensor, c_local: torch.Tensor,
                       policy: "cabl.ExecPolicy", *, gather: bool = False, m_total: int = 0,
-                      group=None, local_fn: Callable | None = None) -> torch.Tensor | None:
-    """c_local += A_local x on this rank's row block; optionally all-gather c."""
+                      group=None, local_fn: Callable | None = None,
+                      out: torch.Tensor | None = None) -> torch.Tensor | None:
+    """c_local += A_local x on this rank's row block; optionally all-gather c
+    (into ``out``, m_total values, when given: no allocation per call).  Equal
+    slices (m_total % world == 0, e.g. G4 over 2/4/8 GPUs) are gathered straight
+    from c_local into the result, one collective and nothing else; ragged ones are
+    padded to the widest slice and cut again."""
     if local_fn is None:
         local_fn = (cabl.gemv_row_major if A_local.layout() == cabl.Layout.RowMajor
                     else cabl.gemv_col_major)
@@ -89,6 +94,15 @@ def sharded_gemv_rows(A_local: "cabl.DenseMatrix", x: torch.Tensor, c_local: tor
     if not gather:
         return None
     world = dist.get_world_size(group)
+    if out is not None:
+        cabl._require(out.numel() == m_total and out.dtype == c_local.dtype
+                      and out.device == c_local.device and out.is_contiguous(),
+                      "sharded_gemv_rows: out must hold m_total values of c's dtype on c's device")
+    if m_total % world == 0 and c_local.numel() * world == m_total and c_local.is_contiguous():
+        full = out if out is not None else torch.empty(m_total, dtype=c_local.dtype,
+                                                       device=c_local.device)
+        dist.all_gather_into_tensor(full, c_local, group=group)
+        return full
     widest = partition(m_total, world, 0)
     width = widest[1] - widest[0]
     padded = torch.zeros(width, dtype=c_local.dtype, device=c_local.device)
@@ -99,7 +113,7 @@ def sharded_gemv_rows(A_local: "cabl.DenseMatrix", x: torch.Tensor, c_local: tor
     for r in range(world):
         b, e = partition(m_total, world, r)
         pieces.append(slab[r * width: r * width + (e - b)])
-    return torch.cat(pieces)
+    return torch.cat(pieces, out=out) if out is not None else torch.cat(pieces)
 
 
 def _device_combine_rows(parts: torch.Tensor, world: int, c: torch.Tensor) -> None:

@@ -99,6 +99,24 @@ def _worker(rank, world, port, results):
         full = shard.sharded_gemv_rows(Aloc, torch.from_numpy(xv), cloc, pol, gather=True,
                                        m_total=m, local_fn=_oracle_gemv_rows)
         results[f"gemv_{rank}"] = full.numpy().copy()
+        # equal slices gathered straight into a caller-owned result (m = 1002 = 2 * 3 * 167)
+        me = 1002
+        Ae = O.gen_uniform(me * k, np.float64, 42, 3).reshape(me, k)
+        ce = O.gen_uniform(me, np.float64, 42, 4)
+        b2, e2 = shard.partition(me, world, rank)
+        Ae_loc = cb.DenseMatrix.wrap(torch.from_numpy(Ae[b2:e2].reshape(-1).copy()), e2 - b2, k,
+                                     cb.Layout.RowMajor)
+        dest = torch.full((me,), float("nan"), dtype=torch.float64)
+        got = shard.sharded_gemv_rows(Ae_loc, torch.from_numpy(xv), torch.from_numpy(ce[b2:e2].copy()),
+                                      pol, gather=True, m_total=me, local_fn=_oracle_gemv_rows,
+                                      out=dest)
+        assert got is dest
+        results[f"gemv_even_{rank}"] = dest.numpy().copy()
+        # ragged slices into a caller-owned result too
+        dest2 = torch.full((m,), float("nan"), dtype=torch.float64)
+        shard.sharded_gemv_rows(Aloc, torch.from_numpy(xv), torch.from_numpy(c0[b:e].copy()), pol,
+                                gather=True, m_total=m, local_fn=_oracle_gemv_rows, out=dest2)
+        results[f"gemv_out_{rank}"] = dest2.numpy().copy()
         # ---- GER row blocks, no communication
         gx = O.gen_uniform(m, np.float32, 42, 1)
         gy = O.gen_uniform(k, np.float32, 42, 2)
@@ -186,6 +204,13 @@ def test_sharded_paths_over_gloo(world):
     O.gemv_ref(A, 0, xv, c)
     for r in range(world):
         np.testing.assert_array_equal(results[f"gemv_{r}"], c)
+        np.testing.assert_array_equal(results[f"gemv_out_{r}"], c)
+    me = 1002
+    Ae = O.gen_uniform(me * k, np.float64, 42, 3)
+    ce = O.gen_uniform(me, np.float64, 42, 4)
+    O.gemv_ref(Ae, 0, xv, ce)
+    for r in range(world):
+        np.testing.assert_array_equal(results[f"gemv_even_{r}"], ce)
 
     # GER: the row blocks tile C and match the oracle bitwise
     gx, gy = O.gen_uniform(m, np.float32, 42, 1), O.gen_uniform(k, np.float32, 42, 2)
