@@ -78,6 +78,76 @@ def sharded_dot(x_local: torch.Tensor, y_local: torch.Tensor, alpha0: float, out
     return out
 
 
+# --------------------------------------------------------------------------
+# DOT whose bits do not depend on the GPU count ("optional
+# G-invariant result: fixed-size global segments with per-segment partials
+# gathered and summed in index order" — the reference's own block decomposition,
+# kernels.hpp:145-163, with the block a fixed number of elements instead of a
+# share of n / threads)
+
+INVARIANT_SEGMENT = 1 << 26  # elements per global segment (256 MiB of fp32 per vector)
+
+
+def invariant_segments(n_total: int, segment: int, world: int, rank: int) -> tuple[int, int]:
+    """The global segments [kb, ke) rank owns: whole segments, balanced, in rank order."""
+    return partition(-(-n_total // segment), world, rank)
+
+
+def invariant_range(n_total: int, segment: int, world: int, rank: int) -> tuple[int, int]:
+    """The element range of x and y rank must hold for sharded_dot_invariant."""
+    kb, ke = invariant_segments(n_total, segment, world, rank)
+    return min(kb * segment, n_total), min(ke * segment, n_total)
+
+
+def invariant_partials(x_local: torch.Tensor, y_local: torch.Tensor, segment: int,
+                       policy: "cabl.ExecPolicy", *, width: int | None = None,
+                       partial_fn: Callable = _device_partial) -> torch.Tensor:
+    """One partial per global segment of this rank's range, each from its own launch of
+    the single-GPU kernel (alpha0 = 0): a segment's partial is a function of its data
+    and length only, whoever computes it.  Returns `width` values (>= the segment
+    count; the rest zero)."""
+    n = x_local.numel()
+    count = -(-n // segment)
+    out = torch.zeros(max(count, width or 0, 1), dtype=x_local.dtype, device=x_local.device)
+    for k in range(count):
+        lo, hi = k * segment, min((k + 1) * segment, n)
+        partial_fn(x_local[lo:hi], y_local[lo:hi], out[k:k + 1], policy)
+    return out
+
+
+def sharded_dot_invariant(x_local: torch.Tensor, y_local: torch.Tensor, alpha0: float,
+                          out: torch.Tensor, policy: "cabl.ExecPolicy", *, n_total: int,
+                          segment: int = INVARIANT_SEGMENT, group=None,
+                          partial_fn: Callable = _device_partial,
+                          combine_fn: Callable = _device_combine) -> torch.Tensor:
+    """out[0] = alpha0 + the global segments' partials summed in index order: the same
+    bits on every rank AND for every GPU count (1 GPU included), as long as the
+    vectors' base addresses share their 32-byte alignment class.  Rank r holds
+    elements invariant_range(n_total, segment, world, r) of x and y.  One all-gather
+    of ceil(K / world) values per rank; with the default 2^26-element segments D2 is
+    64 launches in all (8 per GPU at N = 8)."""
+    grouped = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size(group) if grouped else 1
+    rank = dist.get_rank(group) if grouped else 0
+    b, e = invariant_range(n_total, segment, world, rank)
+    cabl._require(x_local.numel() == e - b and y_local.numel() == e - b,
+                  f"sharded_dot_invariant: rank {rank} must hold elements [{b}, {e}) of x and y")
+    counts = [(lambda kk: kk[1] - kk[0])(invariant_segments(n_total, segment, world, r))
+              for r in range(world)]
+    width = max(1, max(counts))
+    mine = invariant_partials(x_local, y_local, segment, policy, width=width,
+                              partial_fn=partial_fn)
+    if world == 1:
+        ordered = mine[:counts[0]]
+    else:
+        slab = torch.empty(world * width, dtype=mine.dtype, device=mine.device)
+        dist.all_gather_into_tensor(slab, mine[:width].contiguous(), group=group)
+        ordered = slab if all(c == width for c in counts) else torch.cat(
+            [slab[r * width: r * width + counts[r]] for r in range(world)])
+    combine_fn(ordered, alpha0, out)
+    return out
+
+
 def sharded_gemv_rows(A_local: "cabl.DenseMatrix", x: torch.Tensor, c_local: torch.Tensor,
                       policy: "cabl.ExecPolicy", *, gather: bool = False, m_total: int = 0,
                       group=None, local_fn: Callable | None = None,

@@ -136,3 +136,45 @@ def test_bench_suite_watchdog_keeps_the_headline(cuda):
     d = json.loads(lines[0])
     assert d["value"] > 1000 and d["roofline"]["frac"] > 0.5
     assert "watchdog" in d["suite"]["error"]
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_invariant_dot_gives_the_same_bits_for_every_gpu_count(cuda, dtype):
+    """shard.sharded_dot_invariant: fixed global segments, one partial per segment,
+    summed in index order.  The per-rank work of 1, 2, 3, 4 and 8 GPUs is run here in
+    turn on one device (each rank's launches are independent of the others: nothing
+    waits on a peer) and combined as the all-gather would deliver it: every GPU count
+    gives the same bits, equal to the real call at world size 1, and within the
+    contract bound of dot_ref."""
+    import numpy as np
+    import torch
+    sys.path.insert(0, str(ROOT))
+    import paper_2108_02025_b200 as cb
+    from oracle import oracle as O
+    from paper_2108_02025_b200 import shard
+    from tests import tolerances as T
+    dt = getattr(torch, dtype)
+    seg = 1 << 20
+    n = 11 * seg + 12_345  # 12 segments, the last one ragged
+    dev = torch.device("cuda:0")
+    x = cb.fill_uniform(torch.empty(n, dtype=dt, device=dev), 42, 1)
+    y = cb.fill_uniform(torch.empty(n, dtype=dt, device=dev), 42, 2)
+    pol = cb.default_policy(1)
+    real = torch.zeros(1, dtype=dt, device=dev)
+    shard.sharded_dot_invariant(x, y, 0.75, real, pol, n_total=n, segment=seg)
+    for G in (1, 2, 3, 4, 8):
+        pieces = []
+        for g in range(G):
+            b, e = shard.invariant_range(n, seg, G, g)
+            kb, ke = shard.invariant_segments(n, seg, G, g)
+            # a rank's shard is its own allocation (as on its own GPU), 256-byte aligned
+            xs, ys = x[b:e].clone(), y[b:e].clone()
+            pieces.append(shard.invariant_partials(xs, ys, seg, pol)[:ke - kb])
+        out = torch.zeros(1, dtype=dt, device=dev)
+        shard._device_combine(torch.cat(pieces), 0.75, out)
+        assert torch.equal(out, real), G
+    xn, yn = x.cpu().numpy(), y.cpu().numpy()
+    truth, sumabs = O.dot_truth(xn, yn, 0.75)
+    got = float(real.item())
+    assert abs(got - O.dot_ref(xn, yn, 0.75)) <= T.contract_tol(n, sumabs, 0.75, xn.dtype.type)
+    assert abs(got - truth) <= 4 * n * np.finfo(xn.dtype).eps * (sumabs + 0.75)

@@ -628,6 +628,18 @@ def test_gemv_65536_square_fp32_sampled_rows(cuda):
     err = (c.double() - ref).abs()
     bound = (T.gemv_rm_chain(n, np.float32) + 4) * T.EPS[np.dtype(np.float32)] * (absA + c0.double().abs())
     assert bool((err <= bound).all())
+    # the row-block shards of 2 / 4 / 8 GPUs (BASELINE config 5's partition), each run
+    # as its own call: bit for bit the rows of the single-GPU result, so the sharded
+    # G4 gives the same c at every GPU count (a row's order depends on n and on the
+    # sweep shape, which these shards share with the whole matrix)
+    from paper_2108_02025_b200 import shard
+    for G in (2, 4, 8):
+        for g in range(G):
+            b, e = shard.partition(m, G, g)
+            cs = c0[b:e].clone()
+            cb.gemv_row_major(cb.DenseMatrix.wrap(A[b * n:e * n], e - b, n, cb.Layout.RowMajor),
+                              x, cs, policy())
+            assert torch.equal(cs, c[b:e]), (G, g)
 
 
 def test_concurrent_host_threads_share_a_stream_safely(cuda):

@@ -87,6 +87,18 @@ def _worker(rank, world, port, results):
                               0.75, out, pol, partial_fn=_oracle_partial,
                               combine_fn=_ordered_combine)
             results[f"dot_{np.dtype(dt).name}_{rank}"] = float(out[0])
+        # ---- DOT with a GPU-count-invariant result: fixed global segments
+        ni, seg = 100_003, 4096  # 25 segments, the last one ragged
+        for dt in (np.float32, np.float64):
+            x = O.gen_uniform(ni, dt, 42, 1)
+            y = O.gen_uniform(ni, dt, 42, 2)
+            b, e = shard.invariant_range(ni, seg, world, rank)
+            out = torch.zeros(1, dtype=torch.from_numpy(x).dtype)
+            shard.sharded_dot_invariant(torch.from_numpy(x[b:e].copy()),
+                                        torch.from_numpy(y[b:e].copy()), 0.75, out, pol,
+                                        n_total=ni, segment=seg, partial_fn=_oracle_partial,
+                                        combine_fn=_ordered_combine)
+            results[f"doti_{np.dtype(dt).name}_{rank}"] = float(out[0])
         # ---- GEMV row blocks + gather
         m, k = 1001, 257
         A = O.gen_uniform(m * k, np.float64, 42, 3).reshape(m, k)
@@ -195,6 +207,24 @@ def test_sharded_paths_over_gloo(world):
         # and it agrees with the single-process oracle within the contract bound
         truth, sumabs = O.dot_truth(x, y, 0.75)
         assert abs(want - truth) <= 4 * n * np.finfo(dt).eps * (sumabs + 0.75)
+
+    # invariant DOT: the segment partials summed in index order — the same value for
+    # every world size (computed here with no process group at all, i.e. one rank)
+    ni, seg = 100_003, 4096
+    for dt in (np.float32, np.float64):
+        x, y = O.gen_uniform(ni, dt, 42, 1), O.gen_uniform(ni, dt, 42, 2)
+        total = dt(0)
+        for k in range(0, ni, seg):
+            total = dt(total + O.dot_ref(x[k:k + seg], y[k:k + seg], 0.0))
+        want = float(dt(total + dt(0.75)))
+        got = {results[f"doti_{np.dtype(dt).name}_{r}"] for r in range(world)}
+        assert got == {want}
+        import paper_2108_02025_b200 as cb
+        one = torch.zeros(1, dtype=torch.from_numpy(x).dtype)
+        shard.sharded_dot_invariant(torch.from_numpy(x), torch.from_numpy(y), 0.75, one,
+                                    cb.default_policy(1), n_total=ni, segment=seg,
+                                    partial_fn=_oracle_partial, combine_fn=_ordered_combine)
+        assert float(one[0]) == want
 
     # GEMV: gathered c equals the single-process oracle bitwise on every rank
     m, k = 1001, 257
