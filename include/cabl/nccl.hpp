@@ -92,6 +92,16 @@ inline int mdot(cabl_mgpu* c, const double* const* x, const double* const* y,
                 const std::uint64_t* n, double a, std::uint64_t cut, int ex, double* out) {
     return cabl_mgpu_dot_f64(c, x, y, n, a, cut, ex, out);
 }
+inline int mdot_seg(cabl_mgpu* c, const float* const* x, const float* const* y,
+                    const std::uint64_t* n, std::uint64_t seg, float a, std::uint64_t cut,
+                    float* out) {
+    return cabl_mgpu_dot_segmented_f32(c, x, y, n, seg, a, cut, out);
+}
+inline int mdot_seg(cabl_mgpu* c, const double* const* x, const double* const* y,
+                    const std::uint64_t* n, std::uint64_t seg, double a, std::uint64_t cut,
+                    double* out) {
+    return cabl_mgpu_dot_segmented_f64(c, x, y, n, seg, a, cut, out);
+}
 inline int mgemv_rm(cabl_mgpu* c, const float* const* A, const std::uint64_t* m, std::uint64_t n,
                     const float* const* x, float* const* cs, std::uint64_t cut, int ex,
                     float* const* full) {
@@ -217,6 +227,30 @@ template <typename T>
 T sharded_dot(Group& g, const std::vector<const DeviceVector<T>*>& x,
               const std::vector<const DeviceVector<T>*>& y, T alpha0, const ExecPolicy& policy) {
     return detail::dot_common(g, x, y, alpha0, policy, CABL_MGPU_NCCL, "sharded_dot");
+}
+
+// DOT over fixed global segments of `segment` elements (the shards, concatenated
+// in device order, cut every `segment` elements; every shard before the last
+// non-empty one a whole number of segments): one partial per segment, summed in
+// index order.  The result is bit for bit the same for any number of devices.
+template <typename T>
+T sharded_dot_segmented(Group& g, const std::vector<const DeviceVector<T>*>& x,
+                        const std::vector<const DeviceVector<T>*>& y, T alpha0,
+                        std::uint64_t segment, const ExecPolicy& policy) {
+    detail::one_per_device(g, x.size(), "sharded_dot_segmented");
+    detail::one_per_device(g, y.size(), "sharded_dot_segmented");
+    std::vector<const T*> xp, yp;
+    std::vector<std::uint64_t> n;
+    for (int r = 0; r < g.size(); ++r) {
+        detail::need(x[r]->len() == y[r]->len(), "dot: x and y lengths differ");
+        xp.push_back(x[r]->data());
+        yp.push_back(y[r]->data());
+        n.push_back(x[r]->len());
+    }
+    T out{};
+    mgpu_check(detail::mdot_seg(g.handle(), xp.data(), yp.data(), n.data(), segment,
+                                        alpha0, policy.plan.dot_cutoff, &out));
+    return out;
 }
 
 // sharded_dot with the exchange fused into the DOT kernel (peer memory, no

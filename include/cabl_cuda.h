@@ -377,6 +377,24 @@ CABL_API int cabl_mgpu_dot_f32(cabl_mgpu* ctx, const float* const* x, const floa
 CABL_API int cabl_mgpu_dot_f64(cabl_mgpu* ctx, const double* const* x, const double* const* y,
                                const uint64_t* n, double alpha0, uint64_t small_cutoff,
                                int exchange, double* result);
+/* The same sum over FIXED GLOBAL SEGMENTS, for a result that does not depend on
+ * the GPU count: the shards, concatenated in rank order, are cut every
+ * `segment` elements; each segment's partial is the single-GPU kernel's bits
+ * for that segment (alpha0 = 0), and *result = alpha0 + the K partials summed in
+ * index order.  Every shard before the last non-empty one must be a whole
+ * number of segments (CABL_EINVAL otherwise).  One device or eight: the same
+ * bits, provided the vectors' base addresses share their 32-byte alignment.
+ * (The reference's dot depends on its thread count the same way the plain
+ * cabl_mgpu_dot depends on the device count, kernels.hpp:145-163; this is its
+ * block decomposition with a fixed block length.)  NCCL all-gather exchange. */
+CABL_API int cabl_mgpu_dot_segmented_f32(cabl_mgpu* ctx, const float* const* x,
+                                         const float* const* y, const uint64_t* n,
+                                         uint64_t segment, float alpha0, uint64_t small_cutoff,
+                                         float* result);
+CABL_API int cabl_mgpu_dot_segmented_f64(cabl_mgpu* ctx, const double* const* x,
+                                         const double* const* y, const uint64_t* n,
+                                         uint64_t segment, double alpha0, uint64_t small_cutoff,
+                                         double* result);
 /* Row blocks: c[r] (m[r]) += A[r] (m[r] x n, row-major) x[r] (x replicated).
  * c_full: NULL, or one device buffer of sum(m) elements per rank that
  * receives every rank's updated slice at its row offset (the all-gather of

@@ -105,6 +105,8 @@ SIGNATURES: dict[str, list] = {
     "cabl_mgpu_last_call_ms": [vp, i32, C.POINTER(f32)],
     "cabl_mgpu_dot_f32": [vp, vp, vp, vp, f32, u64, i32, C.POINTER(f32)],
     "cabl_mgpu_dot_f64": [vp, vp, vp, vp, f64, u64, i32, C.POINTER(f64)],
+    "cabl_mgpu_dot_segmented_f32": [vp, vp, vp, vp, u64, f32, u64, C.POINTER(f32)],
+    "cabl_mgpu_dot_segmented_f64": [vp, vp, vp, vp, u64, f64, u64, C.POINTER(f64)],
     "cabl_mgpu_gemv_rm_f32": [vp, vp, vp, u64, vp, vp, u64, i32, vp],
     "cabl_mgpu_gemv_rm_f64": [vp, vp, vp, u64, vp, vp, u64, i32, vp],
     "cabl_mgpu_gemv_cm_cols_f32": [vp, vp, u64, vp, vp, vp, u64, i32],

@@ -487,6 +487,89 @@ int mgpu_dot(cabl_mgpu* c, const T* const* x, const T* const* y, const uint64_t*
     return CABL_OK;
 }
 
+// DOT over fixed global segments (a GPU-count-invariant result; SURVEY.md
+// §8(e)'s optional item, the reference's block decomposition of kernels.hpp:
+// 145-163 with a fixed block length): the shards, concatenated in rank order,
+// are cut every `segment` elements; each segment's partial comes from its own
+// launch of the single-GPU kernel (alpha0 = 0) on the device that holds it, so
+// it depends on the segment's data and length only; the K partials are
+// all-gathered (padded to the widest rank) and summed in index order + alpha0
+// on every device.  Every shard except the last non-empty one must therefore be a
+// whole number of segments.
+template <typename T>
+int mgpu_dot_segmented(cabl_mgpu* c, const T* const* x, const T* const* y, const uint64_t* n,
+                       uint64_t segment, T alpha0, uint64_t cutoff, T* result) {
+    if (!c) return mfail(CABL_EINVAL, "cabl_mgpu: null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    MG_RC(usable(c));
+    const int G = int(c->devs.size());
+    if (!x || !y || !n || !result)
+        return mfail(CABL_EINVAL, "cabl_mgpu_dot_segmented: null argument");
+    if (segment == 0) return mfail(CABL_EINVAL, "cabl_mgpu_dot_segmented: segment must be > 0");
+    int last = -1;
+    for (int r = 0; r < G; ++r) {
+        if (n[r] > 0 && (!x[r] || !y[r]))
+            return mfail(CABL_EINVAL, "cabl_mgpu_dot_segmented: x and y must not be null");
+        if (n[r] > 0) last = r;
+    }
+    std::vector<uint64_t> cnt(size_t(G), 0);
+    uint64_t K = 0, widest = 1;
+    for (int r = 0; r < G; ++r) {
+        if (r < last && n[r] % segment != 0)
+            return mfail(CABL_EINVAL, "cabl_mgpu_dot_segmented: every shard before the last "
+                                      "non-empty one must be a whole number of segments");
+        cnt[r] = (n[r] + segment - 1) / segment;
+        K += cnt[r];
+        if (cnt[r] > widest) widest = cnt[r];
+    }
+    if (K > 0xffffffffull) return mfail(CABL_EINVAL, "cabl_mgpu_dot_segmented: too many segments");
+    // scratch per device: own partials [widest], gathered [G * widest],
+    // partials in index order [K], result [1]
+    const size_t own = 0, gat = size_t(widest), ord = gat + size_t(G) * widest,
+                 res = ord + size_t(K ? K : 1), total = res + 1;
+    std::vector<T*> sc(size_t(G), nullptr);
+    for (int r = 0; r < G; ++r) {
+        void* p = nullptr;
+        MG_RC(scratch(c, r, total * sizeof(T), &p));
+        sc[r] = static_cast<T*>(p);
+    }
+    MG_RC(mark_start(c));
+    for (int r = 0; r < G; ++r) {
+        MG_RC(set_dev(c, r));
+        MG_CUDA(cudaMemsetAsync(sc[r] + own, 0, widest * sizeof(T), c->streams[r]), "partials memset");
+        for (uint64_t k = 0; k < cnt[r]; ++k) {
+            const uint64_t lo = k * segment, len = n[r] - lo < segment ? n[r] - lo : segment;
+            MG_RC(dot1(x[r] + lo, y[r] + lo, len, T(0), sc[r] + own + k, cutoff, c->streams[r]));
+        }
+    }
+    if (G > 1) {
+        const NcclApi& N = nccl();
+        MG_NCCL(c, N.GroupStart(), "ncclGroupStart");
+        for (int r = 0; r < G; ++r)
+            MG_NCCL(c, N.AllGather(sc[r] + own, sc[r] + gat, size_t(widest), nccl_type<T>(),
+                                   c->comms[r], c->streams[r]),
+                    "ncclAllGather");
+        MG_NCCL(c, N.GroupEnd(), "ncclGroupEnd");
+    }
+    for (int r = 0; r < G; ++r) {
+        MG_RC(set_dev(c, r));
+        const T* src = G > 1 ? sc[r] + gat : sc[r] + own;
+        uint64_t at = 0;
+        for (int q = 0; q < G; ++q) { // drop each rank's padding: index order, K values
+            if (cnt[q])
+                MG_CUDA(cudaMemcpyAsync(sc[r] + ord + at, src + size_t(q) * widest, cnt[q] * sizeof(T),
+                                        cudaMemcpyDeviceToDevice, c->streams[r]),
+                        "partials compaction");
+            at += cnt[q];
+        }
+        MG_RC(combine1(sc[r] + ord, uint32_t(K), alpha0, sc[r] + res, c->streams[r]));
+    }
+    MG_RC(wait_all(c, G > 1, "dot (segmented, NCCL all-gather)"));
+    MG_RC(set_dev(c, 0));
+    MG_CUDA(cudaMemcpy(result, sc[0] + res, sizeof(T), cudaMemcpyDeviceToHost), "result D2H");
+    return CABL_OK;
+}
+
 // ------------------------------------------------------- GEMV row blocks
 template <typename T>
 int mgpu_gemv_rm(cabl_mgpu* c, const T* const* A, const uint64_t* m, uint64_t n,
@@ -766,6 +849,17 @@ CABL_API int cabl_mgpu_dot_f64(cabl_mgpu* c, const double* const* x, const doubl
                                const uint64_t* n, double alpha0, uint64_t small_cutoff,
                                int exchange, double* result) {
     return mgpu_dot<double>(c, x, y, n, alpha0, small_cutoff, exchange, result);
+}
+CABL_API int cabl_mgpu_dot_segmented_f32(cabl_mgpu* c, const float* const* x, const float* const* y,
+                                         const uint64_t* n, uint64_t segment, float alpha0,
+                                         uint64_t small_cutoff, float* result) {
+    return mgpu_dot_segmented<float>(c, x, y, n, segment, alpha0, small_cutoff, result);
+}
+CABL_API int cabl_mgpu_dot_segmented_f64(cabl_mgpu* c, const double* const* x,
+                                         const double* const* y, const uint64_t* n,
+                                         uint64_t segment, double alpha0, uint64_t small_cutoff,
+                                         double* result) {
+    return mgpu_dot_segmented<double>(c, x, y, n, segment, alpha0, small_cutoff, result);
 }
 CABL_API int cabl_mgpu_gemv_rm_f32(cabl_mgpu* c, const float* const* A, const uint64_t* m,
                                    uint64_t n, const float* const* x, float* const* cs,

@@ -124,6 +124,21 @@ class MultiGpu:
                   C.byref(out))
         return out.value
 
+    def dot_segmented(self, xs, ys, alpha0: float, segment: int, policy=None) -> float:
+        """alpha0 + the partials of the fixed global segments (every `segment` elements of
+        the concatenated shards) summed in index order: the same bits for every device
+        count.  Every shard before the last non-empty one must be whole segments."""
+        sfx = self._shards("dot", xs, ys)
+        for x, y in zip(xs, ys):
+            cabl._require(x.numel() == y.numel(), "dot: x and y lengths differ")
+        pol = policy or cabl.default_policy(1)
+        out = C.c_float() if sfx == "f32" else C.c_double()
+        val = C.c_float(alpha0) if sfx == "f32" else C.c_double(alpha0)
+        _lib.call(f"cabl_mgpu_dot_segmented_{sfx}", self._ctx, _ptrs(xs), _ptrs(ys),
+                  _u64s([x.numel() for x in xs]), C.c_uint64(segment), val, pol.plan.dot_cutoff,
+                  C.byref(out))
+        return out.value
+
     def gemv_rm(self, As, xs, cs, policy=None, exchange: str = "nccl", c_full=None) -> None:
         """c[r] += A[r] x[r] (row blocks, A[r] a row-major DenseMatrix); with
         c_full every device also receives the whole updated c."""

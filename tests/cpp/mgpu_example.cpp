@@ -65,6 +65,40 @@ int main() {
                     double(fused), fused == expect ? "ok" : "MISMATCH");
     }
 
+    { // DOT over fixed global segments: the same bits for any device count
+        const std::size_t seg = std::size_t(1) << 20, K = (n + seg - 1) / seg;
+        float want = 0.f;
+        cudaSetDevice(0);
+        for (std::size_t k = 0; k < K; ++k) { // one single-GPU partial per segment, index order
+            const std::size_t lo = k * seg, hi = std::min(n, lo + seg);
+            Vector<float> xc(hi - lo), yc(hi - lo);
+            std::copy(x.begin() + lo, x.begin() + hi, xc.begin());
+            std::copy(y.begin() + lo, y.begin() + hi, yc.begin());
+            want = want + dot(DeviceVector<float>(xc), DeviceVector<float>(yc), 0.0f, pol);
+        }
+        want = want + 0.75f;
+        std::vector<DeviceVector<float>> sx, sy;
+        for (int r = 0; r < G; ++r) { // device r owns a balanced run of whole segments
+            const nccl::Range kr = nccl::partition(K, G, r);
+            const std::size_t lo = std::min(n, kr.begin * seg), hi = std::min(n, kr.end * seg);
+            Vector<float> xc(hi - lo), yc(hi - lo);
+            std::copy(x.begin() + lo, x.begin() + hi, xc.begin());
+            std::copy(y.begin() + lo, y.begin() + hi, yc.begin());
+            cudaSetDevice(g.device(r));
+            sx.emplace_back(xc);
+            sy.emplace_back(yc);
+        }
+        std::vector<const DeviceVector<float>*> sxp, syp;
+        for (int r = 0; r < G; ++r) {
+            sxp.push_back(&sx[r]);
+            syp.push_back(&sy[r]);
+        }
+        const float segd = nccl::sharded_dot_segmented(g, sxp, syp, 0.75f, seg, pol);
+        ok &= segd == want;
+        std::printf("segmented (device-count-invariant) dot over %d GPU(s): %.9g (expected %.9g) %s\n",
+                    G, double(segd), double(want), segd == want ? "ok" : "MISMATCH");
+    }
+
     // ---- GEMV (row blocks) and GER (row blocks)
     const std::size_t m = 8192, k = 4096;
     DenseMatrix<float> A(m, k, Layout::RowMajor), C(m, k, Layout::RowMajor);

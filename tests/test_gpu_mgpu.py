@@ -141,6 +141,43 @@ def test_mgpu_ger_rows_equal_per_shard_calls(mg, dtype):
         assert torch.equal(Cs[r].data, want[r].data)
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_mgpu_dot_segmented_is_gpu_count_invariant(mg, dtype):
+    """cabl_mgpu_dot_segmented: one partial per fixed global segment, summed in index
+    order.  On this box's devices it must give the bits of shard.sharded_dot_invariant
+    run on the whole vectors by one rank (which tests/test_gpu_dist.py shows equal to
+    the per-rank work of 1, 2, 3, 4 and 8 GPUs combined), and reject shards that are not
+    whole segments."""
+    import paper_2108_02025_b200 as cb
+    from paper_2108_02025_b200 import shard
+    G = mg.size
+    pol = cb.default_policy(1)
+    seg = 1 << 20
+    n = 9 * seg + 4321  # 10 segments, ragged last
+    xs, ys = [], []
+    for r in range(G):
+        b, e = shard.invariant_range(n, seg, G, r)
+        xs.append(_fill(e - b, dtype, 1, f"cuda:{r}", b))
+        ys.append(_fill(e - b, dtype, 2, f"cuda:{r}", b))
+    got = mg.dot_segmented(xs, ys, 0.75, seg, pol)
+    x_all = _fill(n, dtype, 1, "cuda:0")
+    y_all = _fill(n, dtype, 2, "cuda:0")
+    want = torch.zeros(1, dtype=dtype, device="cuda:0")
+    with torch.cuda.device(0):
+        shard.sharded_dot_invariant(x_all, y_all, 0.75, want, pol, n_total=n, segment=seg)
+    assert got == float(want.item())
+    assert mg.dot_segmented(xs, ys, 0.75, seg, pol) == got  # and run to run
+    # empty input: alpha0
+    empty = [_fill(0, dtype, 1, f"cuda:{r}") for r in range(G)]
+    assert mg.dot_segmented(empty, empty, 0.75, seg, pol) == 0.75
+    with pytest.raises(ValueError, match="segment must be > 0"):
+        mg.dot_segmented(xs, ys, 0.0, 0, pol)
+    if G > 1:  # a first shard that is not whole segments
+        bad = [_fill(seg + 1, dtype, 1, f"cuda:{r}") for r in range(G)]
+        with pytest.raises(ValueError, match="whole number of segments"):
+            mg.dot_segmented(bad, bad, 0.0, seg, pol)
+
+
 def test_mgpu_validates_every_shard_before_launching(mg):
     import paper_2108_02025_b200 as cb
     G = mg.size
