@@ -1047,7 +1047,7 @@ extern "C" int cabl_describe_device(int device, cabl_gpu_machine* out) {
 extern "C" {
 
 const char* cabl_last_error(void) { return g_err.c_str(); }
-int cabl_abi_version(void) { return 104; } // 1.04: + rank-ordered row combine over peer memory
+int cabl_abi_version(void) { return 106; } // 1.05: + cabl_mgpu_*; 1.06: + cabl_mgpu_dot_segmented_*
 int cabl_device_count(void) {
     int c = 0;
     if (cudaGetDeviceCount(&c) != cudaSuccess) {
