@@ -381,8 +381,9 @@ CABL_API int cabl_mgpu_dot_f64(cabl_mgpu* ctx, const double* const* x, const dou
  * the GPU count: the shards, concatenated in rank order, are cut every
  * `segment` elements; each segment's partial is the single-GPU kernel's bits
  * for that segment (alpha0 = 0), and *result = alpha0 + the K partials summed in
- * index order.  Every shard before the last non-empty one must be a whole
- * number of segments (CABL_EINVAL otherwise).  One device or eight: the same
+ * index order.  `segment` must be a multiple of 64 elements, and every shard
+ * before the last non-empty one a whole number of segments (CABL_EINVAL
+ * otherwise).  One device or eight: the same
  * bits, provided the vectors' base addresses share their 32-byte alignment.
  * (The reference's dot depends on its thread count the same way the plain
  * cabl_mgpu_dot depends on the device count, kernels.hpp:145-163; this is its

@@ -506,6 +506,11 @@ int mgpu_dot_segmented(cabl_mgpu* c, const T* const* x, const T* const* y, const
     if (!x || !y || !n || !result)
         return mfail(CABL_EINVAL, "cabl_mgpu_dot_segmented: null argument");
     if (segment == 0) return mfail(CABL_EINVAL, "cabl_mgpu_dot_segmented: segment must be > 0");
+    // a segment keeps the alignment class of its shard's base whichever device
+    // holds it (the kernel's vector path depends on it), so the cut points must
+    // not move it: whole 64-element (256 / 512-byte) units
+    if (segment % 64 != 0)
+        return mfail(CABL_EINVAL, "cabl_mgpu_dot_segmented: segment must be a multiple of 64 elements");
     int last = -1;
     for (int r = 0; r < G; ++r) {
         if (n[r] > 0 && (!x[r] || !y[r]))

@@ -129,6 +129,10 @@ def sharded_dot_invariant(x_local: torch.Tensor, y_local: torch.Tensor, alpha0: 
     grouped = dist.is_available() and dist.is_initialized()
     world = dist.get_world_size(group) if grouped else 1
     rank = dist.get_rank(group) if grouped else 0
+    # cut points must not move a segment's alignment class relative to its shard's
+    # base (the kernel's vector path depends on it): whole 64-element units
+    cabl._require(segment > 0 and segment % 64 == 0,
+                  "sharded_dot_invariant: segment must be a positive multiple of 64 elements")
     b, e = invariant_range(n_total, segment, world, rank)
     cabl._require(x_local.numel() == e - b and y_local.numel() == e - b,
                   f"sharded_dot_invariant: rank {rank} must hold elements [{b}, {e}) of x and y")

@@ -172,6 +172,8 @@ def test_mgpu_dot_segmented_is_gpu_count_invariant(mg, dtype):
     assert mg.dot_segmented(empty, empty, 0.75, seg, pol) == 0.75
     with pytest.raises(ValueError, match="segment must be > 0"):
         mg.dot_segmented(xs, ys, 0.0, 0, pol)
+    with pytest.raises(ValueError, match="multiple of 64"):
+        mg.dot_segmented(xs, ys, 0.0, 1000, pol)
     if G > 1:  # a first shard that is not whole segments
         bad = [_fill(seg + 1, dtype, 1, f"cuda:{r}") for r in range(G)]
         with pytest.raises(ValueError, match="whole number of segments"):
