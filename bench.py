@@ -5,7 +5,9 @@
                     [--workload G1] [--no-suite] [--no-cpu-baseline]
 
 Multi-GPU runs are launched one process per GPU by torchrun (RANK /
-LOCAL_RANK / WORLD_SIZE from the environment, NCCL over NVLink).
+LOCAL_RANK / WORLD_SIZE from the environment, NCCL over NVLink); without
+torchrun, ``--gpus N`` re-executes itself under torch.distributed.run after
+checking that N GPUs are visible, and a WORLD_SIZE other than N is refused.
 
 Headline workload (``--workload``, default G1 = BASELINE.json configs[1],
 GEMV fp32 row-major 8192 x 8192): a STEP is one pass of the hot path over one
@@ -16,7 +18,7 @@ owns its own 8192-row block of an (8192 N) x 8192 matrix with x replicated
 * ``value``     whole-job GB/s = algorithmic bytes of all ranks x K / the
                 max over ranks of the device time of the K steps, inputs
                 resident in HBM.  L2 policy (``--l2``, reported in config.l2):
-                a step whose inputs exceed the 126 MB L2 (every BASELINE
+                a step whose footprint exceeds the 126 MB L2 (every BASELINE
                 config: D1 134 MB ... D2 34 GB) runs back to back under one
                 event pair — ncu shows every back-to-back launch still reads
                 its full algorithmic bytes from DRAM; steps that fit in L2
@@ -31,7 +33,12 @@ owns its own 8192-row block of an (8192 N) x 8192 matrix with x replicated
 * ``cpu_baseline`` the compiled, UNMODIFIED reference (oracle/_ref,
                 kind "reference") — its threaded gemv_row_major with every
                 host core — on a bounded sample of the same workload.
-* ``suite``     every BASELINE config at this N (device GB/s, % of peak).
+* ``suite``     every BASELINE config at this N (device GB/s, % of peak): back
+                to back when the step's footprint exceeds L2, else back to back
+                over rotating copies of the operands (time_rotating); the
+                one-flushed-launch-at-a-time figure rides along.  At N > 1 a
+                watchdog (--suite-timeout) prints the finished headline line
+                if a suite collective hangs.
 
 ``--impl reference`` times the reference's own CPU implementation of the
 path on this box's host cores (rank 0 only) and prints the same line shape.
