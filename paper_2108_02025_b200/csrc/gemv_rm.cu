@@ -472,6 +472,95 @@ __global__ void __launch_bounds__(kRmBlock)
     }
 }
 
+// Rows of 9 .. 128 32-byte vectors (256 B .. 4 KiB) as a SWEEP: the CTA's 256
+// threads are RP = 256 / SL row slots of SL lanes (SL = 16, 32, 64 or 128: the
+// power of two >= the row's vectors), a pass loads one vector per thread of RP
+// consecutive rows, a group is R passes (R * RP consecutive rows = one
+// contiguous run of up to 64 KB, all its loads in flight before the first FMA),
+// and groups go to CTAs grid-stride, so the whole GPU reads A front to back as
+// the long-row sweeps do.  x's vector stays in registers for the CTA's lifetime
+// (the G-lanes kernel re-reads x from L1 for every row), c is loaded when the
+// group starts.  Per row: the thread's dot_vec, a butterfly over the slot's
+// lanes (within a warp), then for slots of 2 / 4 warps the warp partials in warp
+// order — fixed by n alone.  256 MiB fp32 flushed / back to back
+// (profiles/r02_rm_subsweep.jsonl): n = 1024 50.9 / 45.9 -> 44.2 / 39.8 us, 512
+// 51.0 / 46.0 -> 44.5 / 40.2, 256 51.1 / 46.7 -> 44.9 / 40.7, 400 71.8 -> 45.5.
+template <typename T, int R, int SL>
+__global__ void __launch_bounds__(kRmBlock, 2)
+    gemv_rm_subsweep_kernel(const T* __restrict__ A, const T* __restrict__ x, T* __restrict__ c,
+                            uint64_t m, uint64_t n) {
+    pdl_enter();
+    constexpr int RP = kRmBlock / SL, GR = R * RP;    // row slots per pass, rows per group
+    constexpr int PARTS = SL > 32 ? SL / 32 : 1;      // warp partials per row
+    __shared__ T red[2][R][RP * PARTS];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int slot = tid / SL, lr = tid % SL; // row slot, vector in the row
+    const uint64_t nv = n / Vec<T>::N;
+    const bool live = uint64_t(lr) < nv;
+    Vec<T> xv;
+    if (live) xv = ld_reuse(reinterpret_cast<const Vec<T>*>(x) + lr);
+    else
+#pragma unroll
+        for (int e = 0; e < Vec<T>::N; ++e) xv.v[e] = T(0);
+    const uint64_t groups = (m + GR - 1) / GR;
+    int parity = 0;
+    for (uint64_t g = blockIdx.x; g < groups; g += gridDim.x) {
+        const uint64_t row0 = g * GR;
+        // finishing thread t < GR owns row row0 + t (pass t / RP, slot t % RP)
+        const bool fin = tid < GR && row0 + tid < m;
+        const T c_row = fin ? c[row0 + tid] : T(0);
+        Vec<T> av[R];
+#pragma unroll
+        for (int p = 0; p < R; ++p) {
+            const uint64_t row = row0 + uint64_t(p) * RP + slot;
+            if (live && row < m) av[p] = ld_stream(reinterpret_cast<const Vec<T>*>(A + row * n) + lr);
+            else
+#pragma unroll
+                for (int e = 0; e < Vec<T>::N; ++e) av[p].v[e] = T(0);
+        }
+#pragma unroll
+        for (int p = 0; p < R; ++p) {
+            T v = dot_vec(av[p], xv, T(0));
+            if constexpr (SL >= 32) {
+                v = warp_sum(v);
+                if (lane == 0) red[parity][p][wid] = v; // wid = slot * PARTS + warp in the slot
+            } else {
+#pragma unroll
+                for (int o = SL / 2; o > 0; o >>= 1) v = add_rn(v, __shfl_xor_sync(0xffffffffu, v, o, SL));
+                if (lr == 0) red[parity][p][slot] = v;
+            }
+        }
+        __syncthreads();
+        if (fin) {
+            const int p = tid / RP, sl = tid % RP;
+            T sum = red[parity][p][sl * PARTS];
+#pragma unroll
+            for (int w = 1; w < PARTS; ++w) sum = add_rn(sum, red[parity][p][sl * PARTS + w]);
+            c[row0 + tid] = add_rn(c_row, sum);
+        }
+        parity ^= 1; // the next group's partials go to the other buffer: one barrier per group
+    }
+}
+
+// Slot lanes for the sub-CTA sweep (the power of two >= the row's vectors), or 0
+// when the G-lanes kernel keeps the row: fp32 rows always take the sweep (a slot
+// is always more than half full: n = 520, 65 of 128 lanes, 56.0 -> 53.4 us; 72, 9
+// of 16, 57.6 -> 52.0), fp64 rows from 55% (36: 9 of 16 lanes 117.5 -> 102.6 us,
+// but 260 / 132 / 68 at 51-53% lost 90 -> 105, 93 -> 111, 96 -> 109).
+// CABL_RM_SUBSWEEP=0 (tuning only) turns it off, CABL_RM_SUBSWEEP=<percent> sets
+// the least share of a slot's lanes a row must fill.
+inline int rm_subsweep_lanes(uint64_t nv, size_t elem) {
+    static const int knob = [] {
+        const char* e = tuning_env("CABL_RM_SUBSWEEP");
+        return e ? atoi(e) : -1;
+    }();
+    if (knob == 0) return 0;
+    const uint64_t min_pct = knob > 0 ? uint64_t(knob) : (elem == 4 ? 50 : 55);
+    for (int sl : {16, 32, 64, 128})
+        if (nv <= uint64_t(sl)) return nv * 100 >= uint64_t(sl) * min_pct ? sl : 0;
+    return 0;
+}
+
 template <typename T> bool rm_vec_ok(const T* A, const T* x, uint64_t n) {
     return aligned32(A) && aligned32(x) && (n % Vec<T>::N == 0);
 }
@@ -726,7 +815,23 @@ cudaError_t rm_launch_impl(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
     if (info) info->ctas = 0;
     if (m == 0 || n == 0) return cudaSuccess; // c += 0
     const int mode = rm_mode<T>(A, x, m, n);
-    if (mode == 7) {
+    if (mode == 7 && rm_subsweep_lanes(n / Vec<T>::N, sizeof(T)) != 0) {
+        constexpr int R = 8;
+        const int sl = rm_subsweep_lanes(n / Vec<T>::N, sizeof(T));
+        const uint64_t gr = uint64_t(R) * (kRmBlock / sl);
+        const uint64_t groups = (m + gr - 1) / gr;
+        const uint64_t cap = uint64_t(sm_count()) * 2;
+        const unsigned grid = unsigned(groups < cap ? groups : cap);
+        if (sl == 16)
+            launch(gemv_rm_subsweep_kernel<T, R, 16>, grid, kRmBlock, 0, s, A, x, c, m, n);
+        else if (sl == 32)
+            launch(gemv_rm_subsweep_kernel<T, R, 32>, grid, kRmBlock, 0, s, A, x, c, m, n);
+        else if (sl == 64)
+            launch(gemv_rm_subsweep_kernel<T, R, 64>, grid, kRmBlock, 0, s, A, x, c, m, n);
+        else
+            launch(gemv_rm_subsweep_kernel<T, R, 128>, grid, kRmBlock, 0, s, A, x, c, m, n);
+        if (info) info->ctas = grid;
+    } else if (mode == 7) {
         const uint64_t nv = n / Vec<T>::N;
         const int G = nv > 96 ? 32 : (nv > 48 ? 16 : (nv > 24 ? 8 : 4));
         const uint64_t max_groups = uint64_t(sm_count()) * 8 * (kRmBlock / G);

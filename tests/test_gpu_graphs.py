@@ -87,7 +87,8 @@ def test_dot_in_a_graph(cuda, dtype, n):
     (torch.float32, 4, 1 << 20),     # few long rows: chunk queue + per-row tickets
     (torch.float32, 100_000, 40),    # one thread per row
     (torch.float64, 3000, 1024),     # 8 x 1 sweep, fp64
-    (torch.float32, 50_000, 256),    # G lanes per row (1 KB rows)
+    (torch.float32, 50_000, 256),    # sub-CTA sweep, one warp per row (1 KB rows)
+    (torch.float64, 20_000, 264),    # G lanes per row (66 of 128 lanes: below fp64's fill rule)
     (torch.float32, 1000, 4097),     # few long scalar rows: one CTA per row
     (torch.float32, 20_000, 129),    # many scalar rows: G lanes per row, scalar loads
     (torch.float64, 7, 5),           # small (single CTA, reference order)

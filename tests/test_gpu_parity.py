@@ -124,6 +124,11 @@ RM_SHAPES = [(1, 777), (3, 3), (8, 8), (40, 200), (257, 259), (1000, 1000), (200
              # short rows: one thread per row (bitwise), vector and scalar loads
              (9472, 64), (100_000, 16), (20_001, 5), (9472, 256), (30_000, 255), (1 << 18, 1),
              (9472, 1024), (12_000, 999),
+             # rows of 1 / 2 / 4 warps of 32-byte vectors: the sub-CTA sweep (full and
+             # partly filled row slots, ragged last group), and the G-lanes kernel
+             # where a slot would be < 3/4 full
+             (9473, 512), (9600, 200), (9999, 776), (12_345, 1000), (9472, 96), (9500, 384),
+             (9473, 264), (10_000, 520),
              # rows of whole 16-byte (not 32-byte) vectors: the scalar-load kernel
              (20_000, 2052), (3000, 20_002), (1800, 65_540),
              # odd rows, long and short: the G-lanes scalar kernel
