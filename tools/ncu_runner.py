@@ -68,6 +68,16 @@ def main():
 
         class w:  # noqa: N801
             id = "CM4096"
+    elif args.config == "RM1024":  # row-major GEMV fp32 65536 x 1024: the sub-CTA sweep
+        m, n = 65536, 1024
+        A = cb.DenseMatrix.wrap(cb.fill_uniform(torch.empty(m * n, device=dev), WL.SEED,
+                                                WL.STREAM_A), m, n, cb.Layout.RowMajor)
+        x = cb.fill_uniform(torch.empty(n, device=dev), WL.SEED, WL.STREAM_X)
+        c = cb.fill_uniform(torch.empty(m, device=dev), WL.SEED, WL.STREAM_C)
+        fn = lambda: cb.gemv_row_major(A, x, c, pol)  # noqa: E731
+
+        class w:  # noqa: N801
+            id = "RM1024"
     elif args.config == "G1g":  # G1 through the gathering GEMV at world 1 (gemv_rm_gather_kernel)
         from paper_2108_02025_b200 import shard
         w = WL.WORKLOADS["G1"]

@@ -87,6 +87,8 @@ def main():
             alg = (2 * 8192 * 8193 + 8192 + 8193) * 4
         elif cfg == "CM4096":  # col-major GEMV fp32 4096 x 16384
             alg = (4096 * 16384 + 16384 + 2 * 4096) * 4
+        elif cfg == "RM1024":  # row-major GEMV fp32 65536 x 1024 (the sub-CTA sweep)
+            alg = (65536 * 1024 + 1024 + 2 * 65536) * 4
         else:  # D1f / G1g: D1 / G1 through the fused peer-memory paths
             alg = WL.WORKLOADS[cfg[:2]].alg_bytes(1)
         el = num(d, "sm__cycles_elapsed.max")
