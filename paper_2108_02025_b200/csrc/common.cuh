@@ -8,12 +8,28 @@
 // float4/double2.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
 #include <utility>
 
 namespace cabl_dev {
+
+// Opt a kernel in to more than 48 KB of dynamic shared memory.  The attribute
+// belongs to the kernel ON THE CURRENT DEVICE, so a process that drives several
+// devices (cabl_mgpu_*, cabl::nccl::Group) must set it on each of them: `done`
+// (one static per call site) keeps a bit per device ordinal.
+template <typename K>
+inline void ensure_dyn_smem(K kernel, int bytes, std::atomic<unsigned long long>& done) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    const unsigned long long bit = 1ull << (unsigned(dev) & 63u);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.fetch_or(bit, std::memory_order_release);
+}
+
 
 // Tuning / A-B switches (CABL_DOT_CFG, CABL_GEMV_RM_ORDER, CABL_CM_TILE, ...;
 // DESIGN.md §4 "Environment knobs") pick other launch shapes or kernels, and

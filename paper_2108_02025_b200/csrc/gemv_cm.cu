@@ -1352,12 +1352,8 @@ SplitGeom split_bulk_geom(uint64_t m, uint64_t n, int* tc, BulkCfg bc = bulk_cfg
 template <typename T, int NS, unsigned SB>
 void bulk_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const SplitGeom& g, int tc,
              T* partials, unsigned* ticket, cudaStream_t s) {
-    static bool configured = [] {
-        cudaFuncSetAttribute(gemv_cm_split_bulk_kernel<T, NS, SB>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(bulk_smem(NS, SB)));
-        return true;
-    }();
-    (void)configured;
+    static std::atomic<unsigned long long> configured{0};
+    ensure_dyn_smem(gemv_cm_split_bulk_kernel<T, NS, SB>, int(bulk_smem(NS, SB)), configured);
     // The per-row sum of the G CTA partials in a one-wave combine kernel
     // instead of by the last CTA alone (256 MiB flushed / back to back,
     // tools/ab_shapes.py: fp32 m = 256 51.4 / 46.5 -> 48.2 / 43.8 us, m = 504
@@ -1405,12 +1401,9 @@ void bulk_scalar_go(const T* A, const T* x, T* c, uint64_t m, uint64_t n, const 
     const int a_off = int((reinterpret_cast<uintptr_t>(A) & 15u) / sizeof(T));
     const uint64_t q = 16 / sizeof(T);
     const uint64_t x_off = a_off ? (uint64_t(tc) * m + a_off + q - 1) / q * q : uint64_t(tc) * m;
-    static bool configured = [] {
-        cudaFuncSetAttribute(gemv_cm_split_bulk_scalar_kernel<T, 3, 49152, RPT>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(bulk_smem(3, 49152)));
-        return true;
-    }();
-    (void)configured;
+    static std::atomic<unsigned long long> configured{0};
+    ensure_dyn_smem(gemv_cm_split_bulk_scalar_kernel<T, 3, 49152, RPT>, int(bulk_smem(3, 49152)),
+                    configured);
     // the G CTA partials of each row summed by the (scalar-load) one-wave
     // combine kernel, as in bulk_go (CABL_CM_BULK_COMB16=0: in-kernel, A/B)
     static const int comb = [] {
@@ -1626,12 +1619,8 @@ void combine16_launch(T* partials, const SplitGeom& g, uint64_t m, T* c, cudaStr
 template <typename T, int RPT, unsigned SB>
 void colbulk_launch(const T* A, const T* x, uint64_t m, uint64_t n, const SplitGeom& g, T* partials,
                     cudaStream_t s) {
-    static bool configured = [] {
-        cudaFuncSetAttribute(gemv_cm_colbulk_kernel<T, RPT, SB>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(kColBulkStages * SB));
-        return true;
-    }();
-    (void)configured;
+    static std::atomic<unsigned long long> configured{0};
+    ensure_dyn_smem(gemv_cm_colbulk_kernel<T, RPT, SB>, int(kColBulkStages * SB), configured);
     launch(gemv_cm_colbulk_kernel<T, RPT, SB>, g.grid, unsigned(kBulkThreads), g.smem, s, A, x, m,
            n, uint64_t(g.mt), g.col_lanes, partials);
 }
@@ -1803,13 +1792,9 @@ cudaError_t gemv_cm_launch(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
             else
                 bulk_scalar_go<T, 4>(A, x, c, m, n, g, tc, x_bulk, partials, ws.counters, s);
         } else if (path == kPathSplitRealign) {
-            static bool configured = [] {
-                cudaFuncSetAttribute(gemv_cm_split_realign_kernel<T>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(16 * 31 * Vec<T>::N * sizeof(T)));
-                return true;
-            }();
-            (void)configured;
+            static std::atomic<unsigned long long> configured{0};
+            ensure_dyn_smem(gemv_cm_split_realign_kernel<T>, int(16 * 31 * Vec<T>::N * sizeof(T)),
+                            configured);
             const bool ext = split_external_combine<T>(g, m);
             launch(gemv_cm_split_realign_kernel<T>, grid, kRealignBlock, g.smem, s, A, x, c, m, n,
                    g.mt, g.row_lanes, partials, ws.counters, int(ext));

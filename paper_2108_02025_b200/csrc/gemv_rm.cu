@@ -422,6 +422,12 @@ __global__ void __launch_bounds__(kRmBlock)
     }
 }
 
+// (Measured, not kept: the same chains fed by fully coalesced loads and a
+// shared-memory transpose — 256 consecutive rows per CTA, row pitch n + 1 — took
+// fp32 n = 64 / 32 57.0 / 64.1 us flushed against 53.1 / 51.0 for this kernel, fp64
+// n = 32 / 16 100.4 / 116.0 against 98.3 / 102.0: the two barriers per 64 KB block
+// and the scalar shared-memory traffic cost more than the 32-sector gathers they
+// replace; profiles/r02_rm_lane_t_lost.jsonl.)
 // Row bytes up to which one thread per row beats the CTA-wide sweeps
 // (CABL_RM_LANE_MAX overrides, tuning only).  gemv_rm_is_lane (kernels.cuh)
 // adds the row-count condition.

@@ -280,12 +280,8 @@ void ordered_launch_cfg(const T* A, uint64_t m, uint64_t n, const T* x, T* c, cu
                         unsigned grid) {
 
     using G = OrdGeom<T, SEG, NS>;
-    static bool configured = [] {
-        cudaFuncSetAttribute(gemv_rm_ordered_kernel<T, SEG, NS, PW>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::kSmem));
-        return true;
-    }();
-    (void)configured;
+    static std::atomic<unsigned long long> configured{0};
+    ensure_dyn_smem(gemv_rm_ordered_kernel<T, SEG, NS, PW>, int(G::kSmem), configured);
     launch(gemv_rm_ordered_kernel<T, SEG, NS, PW>, grid, kOrdRows + 32 * PW, G::kSmem, s, A, x, c,
            m, n);
 }
@@ -352,12 +348,8 @@ cudaError_t ordered_launch_tma(const T* A, uint64_t m, uint64_t n, const T* x, T
         last_n = n;
         last_s = sizeof(T);
     }
-    static bool configured = [] {
-        cudaFuncSetAttribute(gemv_rm_ordered_tma_kernel<T>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTmaSmem));
-        return true;
-    }();
-    (void)configured;
+    static std::atomic<unsigned long long> configured{0};
+    ensure_dyn_smem(gemv_rm_ordered_tma_kernel<T>, int(kTmaSmem), configured);
     launch(gemv_rm_ordered_tma_kernel<T>, grid, kOrdRows + 32, kTmaSmem, s, maps, x, c, m, n);
     return cudaSuccess;
 }

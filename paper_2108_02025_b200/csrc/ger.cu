@@ -474,12 +474,8 @@ void ger_any_go(unsigned per_sm, const T* u, const T* v, T* C, uint64_t outer, u
     const uint64_t stepv = uint64_t(kGerBlock) * V; // elements between a thread's vectors
     const size_t ysz = YS ? size_t(inner) * sizeof(T) : 0;
     if (YS && ysz > 48 * 1024) {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(ger_flat_any_kernel<T, YS, U, EARLY>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGerYsMax));
-            attr = true;
-        }
+        static std::atomic<unsigned long long> attr{0};
+        ensure_dyn_smem(ger_flat_any_kernel<T, YS, U, EARLY>, int(kGerYsMax), attr);
     }
     launch(ger_flat_any_kernel<T, YS, U, EARLY>, grid, kGerBlock, ysz, s, u, v, C, outer, inner,
            head, nvec, stepv / inner, stepv % inner);
