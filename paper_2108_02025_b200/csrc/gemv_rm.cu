@@ -25,7 +25,9 @@
 // Kernels by shape (rm_mode):
 //   * rows <= 256 B, many of them: one thread per row in the reference's
 //     order and rounding — bitwise gemv_ref (gemv_rm_lane_kernel, mode 3/4);
-//   * rows of 256 B .. 4 KiB: G lanes per row, 32-byte vectors (mode 7);
+//   * rows of 256 B .. 4 KiB: the sub-CTA sweep (row slots of 16 - 128 lanes,
+//     gemv_rm_subsweep_kernel), or G lanes per row for fp64 rows that fill
+//     barely half of a slot (gemv_rm_gvec_kernel) — both mode 7;
 //   * longer rows, enough of them: the CTA-wide SWEEP (modes 1, 2; a row
 //     shape with mostly empty last passes switches to 8 x 1 groups);
 //   * few rows: the unit kernel described above (mode 0);
