@@ -564,7 +564,7 @@ inline int rm_subsweep_lanes(uint64_t nv, size_t elem) {
     }();
     if (knob == 0) return 0;
     const uint64_t min_pct = knob > 0 ? uint64_t(knob) : (elem == 4 ? 50 : 55);
-    for (int sl : {16, 32, 64, 128})
+    for (int sl : {16, 32, 64, 128, 256})
         if (nv <= uint64_t(sl)) return nv * 100 >= uint64_t(sl) * min_pct ? sl : 0;
     return 0;
 }
@@ -609,6 +609,21 @@ template <typename T> int rm_mode(const T* A, const T* x, uint64_t m, uint64_t n
         (forced < 0 && n * sizeof(T) <= kGVecMaxBytes && m >= uint64_t(sm_count()) * 64)) {
         if (vec) return 7;
     }
+    // fp32 rows of 4 .. 8 KiB in one-row (256-lane) slots of the sub-CTA sweep: x in
+    // registers instead of an L1 load per group (256 MiB flushed / back to back,
+    // profiles/r02_rm_subsweep256.jsonl: n = 2048 45.0 / 40.3 -> 43.8 / 39.6 us, 1280
+    // 47.9 / 42.8 -> 45.5 / 41.5, 1032 55.0 / 50.0 -> 51.1 / 47.1); fp64 stays on the
+    // 8 x 1 sweep (n = 1024 81.0 / 76.3 against 82.4 / 77.9).  CABL_RM_SUBSWEEP_MAXB
+    // (tuning only) sets the byte limit for both types.
+    static const long long sub_maxb_knob = [] {
+        const char* e = tuning_env("CABL_RM_SUBSWEEP_MAXB");
+        return e ? atoll(e) : -1ll;
+    }();
+    const uint64_t sub_maxb = sub_maxb_knob >= 0 ? uint64_t(sub_maxb_knob)
+                                                 : (sizeof(T) == 4 ? uint64_t(8192) : uint64_t(0));
+    if (forced < 0 && vec && n * sizeof(T) > kGVecMaxBytes && n * sizeof(T) <= sub_maxb &&
+        m >= uint64_t(sm_count()) * 64 && rm_subsweep_lanes(n / Vec<T>::N, sizeof(T)) != 0)
+        return 7;
     if (!vec) return -1;
     if (forced >= 0 && forced <= 2) return forced;
     if (forced == 9 || (forced < 0 && rm_few_rows(m, n, sizeof(T)))) return 9;
@@ -836,6 +851,8 @@ cudaError_t rm_launch_impl(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
             launch(gemv_rm_subsweep_kernel<T, R, 32>, grid, kRmBlock, 0, s, A, x, c, m, n);
         else if (sl == 64)
             launch(gemv_rm_subsweep_kernel<T, R, 64>, grid, kRmBlock, 0, s, A, x, c, m, n);
+        else if (sl == 256)
+            launch(gemv_rm_subsweep_kernel<T, R, 256>, grid, kRmBlock, 0, s, A, x, c, m, n);
         else
             launch(gemv_rm_subsweep_kernel<T, R, 128>, grid, kRmBlock, 0, s, A, x, c, m, n);
         if (info) info->ctas = grid;

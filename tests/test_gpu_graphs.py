@@ -88,6 +88,7 @@ def test_dot_in_a_graph(cuda, dtype, n):
     (torch.float32, 100_000, 40),    # one thread per row
     (torch.float64, 3000, 1024),     # 8 x 1 sweep, fp64
     (torch.float32, 50_000, 256),    # sub-CTA sweep, one warp per row (1 KB rows)
+    (torch.float32, 10_000, 1536),   # sub-CTA sweep, one row per pass (6 KB rows)
     (torch.float64, 20_000, 264),    # G lanes per row (66 of 128 lanes: below fp64's fill rule)
     (torch.float32, 1000, 4097),     # few long scalar rows: one CTA per row
     (torch.float32, 20_000, 129),    # many scalar rows: G lanes per row, scalar loads

@@ -129,6 +129,8 @@ RM_SHAPES = [(1, 777), (3, 3), (8, 8), (40, 200), (257, 259), (1000, 1000), (200
              # where a slot would be < 3/4 full
              (9473, 512), (9600, 200), (9999, 776), (12_345, 1000), (9472, 96), (9500, 384),
              (9473, 264), (10_000, 520),
+             # 4 - 8 KiB rows: fp32 one-row slots of the sub-CTA sweep, fp64 the 8 x 1 sweep
+             (9473, 2048), (9600, 1280), (10_001, 1032),
              # rows of whole 16-byte (not 32-byte) vectors: the scalar-load kernel
              (20_000, 2052), (3000, 20_002), (1800, 65_540),
              # odd rows, long and short: the G-lanes scalar kernel
