@@ -31,8 +31,9 @@
 //   * longer rows, enough of them: the CTA-wide SWEEP (modes 1, 2; a row
 //     shape with mostly empty last passes switches to 8 x 1 groups);
 //   * few rows: the unit kernel described above (mode 0);
-//   * unaligned operands or n % (32/sizeof(T)) != 0: G lanes per row with
-//     scalar loads (mode -1).
+//   * unaligned operands or n % (32/sizeof(T)) != 0 (mode -1): the scalar
+//     sub-CTA sweep for rows of 65 .. 2048 elements and m >= 148 * 64, one CTA
+//     per row for few long rows, else G lanes per row with scalar loads.
 // CABL_GEMV_RM_ORDER=reference routes to gemv_rm_ordered.cu instead where it
 // applies.  Every kernel is bitwise reproducible run to run.
 //
@@ -550,6 +551,99 @@ __global__ void __launch_bounds__(kRmBlock, 2)
     }
 }
 
+// The same sweep for rows that are not whole aligned 32-byte vectors (odd n, or A / x
+// off a 32-byte boundary): scalar loads, thread lr of a slot takes elements lr, lr +
+// SL, ... (NE of them, so a warp's load is one contiguous 128-byte run), x's NE
+// elements stay in registers, FMA per element, then the slot butterfly and warp
+// partials as above.  Rows of up to NE * SL elements.
+// 256 MiB fp32 flushed (profiles/r02_rm_subsweep_scalar*.jsonl), G-lanes scalar kernel
+// -> this: n = 1001 75.9 -> 46.8 us, 255 65.8 -> 46.1, 129 90.2 -> 53.5, 65 89.3 ->
+// 53.4, 2047 64.0 -> 47.8; fp64 n = 1001 133.1 -> 82.0, 301 105.4 -> 86.2.
+template <typename T, int R, int SL, int NE>
+__global__ void __launch_bounds__(kRmBlock, 2)
+    gemv_rm_subsweep_scalar_kernel(const T* __restrict__ A, const T* __restrict__ x,
+                                   T* __restrict__ c, uint64_t m, uint64_t n) {
+    pdl_enter();
+    constexpr int RP = kRmBlock / SL, GR = R * RP;
+    constexpr int PARTS = SL > 32 ? SL / 32 : 1;
+    __shared__ T red[2][R][RP * PARTS];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int slot = tid / SL, lr = tid % SL;
+    T xr[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+        const uint64_t j = uint64_t(lr) + uint64_t(e) * SL;
+        xr[e] = j < n ? __ldg(x + j) : T(0);
+    }
+    const uint64_t groups = (m + GR - 1) / GR;
+    int parity = 0;
+    for (uint64_t g = blockIdx.x; g < groups; g += gridDim.x) {
+        const uint64_t row0 = g * GR;
+        const bool fin = tid < GR && row0 + tid < m;
+        const T c_row = fin ? c[row0 + tid] : T(0);
+        T av[R][NE];
+#pragma unroll
+        for (int p = 0; p < R; ++p) {
+            const uint64_t row = row0 + uint64_t(p) * RP + slot;
+            const T* rp = A + row * n;
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                const uint64_t j = uint64_t(lr) + uint64_t(e) * SL;
+                av[p][e] = (row < m && j < n) ? __ldcs(rp + j) : T(0);
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < R; ++p) {
+            T v = T(0);
+#pragma unroll
+            for (int e = 0; e < NE; ++e) v = fma_rn(av[p][e], xr[e], v);
+            if constexpr (SL >= 32) {
+                v = warp_sum(v);
+                if (lane == 0) red[parity][p][wid] = v;
+            } else {
+#pragma unroll
+                for (int o = SL / 2; o > 0; o >>= 1) v = add_rn(v, __shfl_xor_sync(0xffffffffu, v, o, SL));
+                if (lr == 0) red[parity][p][slot] = v;
+            }
+        }
+        __syncthreads();
+        if (fin) {
+            const int p = tid / RP, sl = tid % RP;
+            T sum = red[parity][p][sl * PARTS];
+#pragma unroll
+            for (int w = 1; w < PARTS; ++w) sum = add_rn(sum, red[parity][p][sl * PARTS + w]);
+            c[row0 + tid] = add_rn(c_row, sum);
+        }
+        parity ^= 1;
+    }
+}
+
+// Slot shape for the scalar sub-CTA sweep: rows of 65 .. 2048 elements take the
+// (SL lanes, NE elements per lane) pair with the smallest capacity SL * NE >= n, NE in
+// {5, 6, 8}, so a slot is always >= 75% full (a half-full slot lost: fp32 n = 513 in
+// 128 x 8 57.4 -> 63.5 us).  CABL_RM_SUBSWEEP_SCALAR=0|1 (tuning only) turns it
+// off / on.
+struct SubScalarShape {
+    int sl = 0, ne = 0;
+};
+inline SubScalarShape rm_subsweep_scalar_shape(uint64_t n) {
+    static const int knob = [] {
+        const char* e = tuning_env("CABL_RM_SUBSWEEP_SCALAR");
+        return e ? atoi(e) : -1;
+    }();
+    SubScalarShape best;
+    if (knob == 0 || n <= 64) return best;
+    uint64_t cap = ~uint64_t(0);
+    for (int sl : {16, 32, 64, 128, 256})
+        for (int ne : {5, 6, 8})
+            if (uint64_t(sl) * ne >= n && uint64_t(sl) * ne < cap) {
+                cap = uint64_t(sl) * ne;
+                best.sl = sl;
+                best.ne = ne;
+            }
+    return best;
+}
+
 // Slot lanes for the sub-CTA sweep (the power of two >= the row's vectors), or 0
 // when the G-lanes kernel keeps the row: fp32 rows always take the sweep (a slot
 // is always more than half full: n = 520, 65 of 128 lanes, 56.0 -> 53.4 us; 72, 9
@@ -926,6 +1020,30 @@ cudaError_t rm_launch_impl(const T* A, uint64_t m, uint64_t n, const T* x, T* c,
         launch(gemv_rm_scalar_cta_kernel<T>, grid, kRmBlock, 0, s, A, x, c, m, n);
         if (info) info->ctas = grid;
     } else {
+        const SubScalarShape sh =
+            m >= uint64_t(sm_count()) * 64 ? rm_subsweep_scalar_shape(n) : SubScalarShape{};
+        // fp64 rows of 513 .. 640 elements (128 lanes x 5) keep the G-lanes kernel: 513 /
+        // 601 flushed 93.9 / 96.3 -> 104.5 / 98.7 us, the one shape that lost
+        if (sh.sl != 0 && !(sizeof(T) == 8 && sh.sl == 128 && sh.ne == 5)) {
+            constexpr int R = sizeof(T) == 4 ? 8 : 4;
+            const uint64_t gr = uint64_t(R) * (kRmBlock / sh.sl);
+            const uint64_t groups = (m + gr - 1) / gr;
+            const uint64_t cap = uint64_t(sm_count()) * 2;
+            const unsigned grid = unsigned(groups < cap ? groups : cap);
+#define CABL_SUBSCALAR(SL_, NE_)                                                                 \
+    if (sh.sl == SL_ && sh.ne == NE_)                                                            \
+        launch(gemv_rm_subsweep_scalar_kernel<T, R, SL_, NE_>, grid, kRmBlock, 0, s, A, x, c, m, n);
+#define CABL_SUBSCALAR_SL(SL_) CABL_SUBSCALAR(SL_, 5) CABL_SUBSCALAR(SL_, 6) CABL_SUBSCALAR(SL_, 8)
+            CABL_SUBSCALAR_SL(16)
+            CABL_SUBSCALAR_SL(32)
+            CABL_SUBSCALAR_SL(64)
+            CABL_SUBSCALAR_SL(128)
+            CABL_SUBSCALAR_SL(256)
+#undef CABL_SUBSCALAR_SL
+#undef CABL_SUBSCALAR
+            if (info) info->ctas = grid;
+            return cudaGetLastError();
+        }
         // lanes per row: about 8 elements per lane, 4..32 lanes
         const int G = n > 128 ? 32 : (n > 64 ? 16 : (n > 32 ? 8 : 4));
         const uint64_t max_groups = uint64_t(sm_count()) * 8 * (kRmBlock / G);

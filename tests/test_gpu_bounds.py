@@ -66,7 +66,9 @@ RM = [(3, 5), (40, 1024), (2, 65536), (7200, 256), (3000, 999), (5000, 1028), (4
       (20_000, 16), (20_000, 256), (20_000, 33), (9000, 8200), (1, 1 << 18), (5, 40_000),
       (700, 5003),
       # the sub-CTA sweep: partly filled 128- / 16- / 32-lane row slots, ragged last group
-      (9473, 520), (10_001, 72), (9999, 1000), (9601, 144), (9473, 1288), (9500, 2048)]
+      (9473, 520), (10_001, 72), (9999, 1000), (9601, 144), (9473, 1288), (9500, 2048),
+      # the scalar sub-CTA sweep (odd rows; with an offset every shape here is scalar too)
+      (9473, 65), (9601, 1001), (9500, 2047), (10_000, 130)]
 CM = [(3, 5), (256, 4096), (4096, 300), (2008, 77), (1001, 300), (148 * 256 * 8, 4),
       (148 * 1024 + 1, 3), (1, 100_000), (257, 20_000), (74 * 256 * 8, 20), (8193, 300),
       (1025, 777), (3001, 129), (4096, 100), (8192, 301), (512, 5000), (1000, 3)]

@@ -91,7 +91,8 @@ def test_dot_in_a_graph(cuda, dtype, n):
     (torch.float32, 10_000, 1536),   # sub-CTA sweep, one row per pass (6 KB rows)
     (torch.float64, 20_000, 264),    # G lanes per row (66 of 128 lanes: below fp64's fill rule)
     (torch.float32, 1000, 4097),     # few long scalar rows: one CTA per row
-    (torch.float32, 20_000, 129),    # many scalar rows: G lanes per row, scalar loads
+    (torch.float32, 20_000, 129),    # many scalar rows: the scalar sub-CTA sweep
+    (torch.float32, 5000, 129),      # fewer scalar rows: G lanes per row, scalar loads
     (torch.float64, 7, 5),           # small (single CTA, reference order)
 ])
 def test_gemv_row_major_in_a_graph(cuda, dtype, m, n):

@@ -129,6 +129,8 @@ RM_SHAPES = [(1, 777), (3, 3), (8, 8), (40, 200), (257, 259), (1000, 1000), (200
              # where a slot would be < 3/4 full
              (9473, 512), (9600, 200), (9999, 776), (12_345, 1000), (9472, 96), (9500, 384),
              (9473, 264), (10_000, 520),
+             # odd rows of 65 .. 2048 elements: the scalar sub-CTA sweep (every slot width)
+             (9473, 65), (10_000, 129), (9600, 1001), (9500, 2047), (20_000, 300), (9999, 513),
              # 4 - 8 KiB rows: fp32 one-row slots of the sub-CTA sweep, fp64 the 8 x 1 sweep
              (9473, 2048), (9600, 1280), (10_001, 1032),
              # rows of whole 16-byte (not 32-byte) vectors: the scalar-load kernel
