@@ -12,7 +12,7 @@ CMD="python bench.py --steps 20 --warmup 3 --no-suite --no-e2e --no-cpu-baseline
 $CMD > gpurun_out/plain_launches.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 python tools/ncu_runner.py --config G1 --reps 6 --no-flush > gpurun_out/plain_b2b.log 2>&1 && timeout 600 ncu --cache-control none --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:gemv_rm -c 6 --csv --log-file gpurun_out/ncu_b2b_G1.csv python tools/ncu_runner.py --config G1 --reps 6 --no-flush > gpurun_out/ncu_b2b.log 2>&1
 python tools/ncu_runner.py --config D1 --reps 6 --no-flush > gpurun_out/plain_b2b_D1.log 2>&1 && timeout 600 ncu --cache-control none --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:dot_kernel -c 6 --csv --log-file gpurun_out/ncu_b2b_D1.csv python tools/ncu_runner.py --config D1 --reps 6 --no-flush > gpurun_out/ncu_b2b_D1.log 2>&1
-for cfg in "G1 gemv_rm_sweep" "D1 dot_kernel" "R1 ger_tile" "G2 gemv_cm_tall" "G3 gemv_cm_split" "D2 dot_chunk" "G4 gemv_rm_sweep" "D1f dot_peer" "R1x ger_flat_any" "G1g gemv_rm_gather" "CM4096 gemv_cm_fullcol_kernel" "RM1024 gemv_rm_subsweep"; do
+for cfg in "G1 gemv_rm_sweep" "D1 dot_kernel" "R1 ger_tile" "G2 gemv_cm_tall" "G3 gemv_cm_split" "D2 dot_chunk" "G4 gemv_rm_sweep" "D1f dot_peer" "R1x ger_flat_any" "G1g gemv_rm_gather" "CM4096 gemv_cm_fullcol_kernel" "RM1024 gemv_rm_subsweep_kernel" "RM1001 gemv_rm_subsweep_scalar"; do
   set -- $cfg
   python tools/ncu_runner.py --config $1 --reps 2 > gpurun_out/plain_$1.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$2 -s 1 -c 1 -o gpurun_out/prof_$1 -f python tools/ncu_runner.py --config $1 --reps 2 > gpurun_out/ncu_$1.log 2>&1

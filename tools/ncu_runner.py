@@ -68,8 +68,9 @@ def main():
 
         class w:  # noqa: N801
             id = "CM4096"
-    elif args.config == "RM1024":  # row-major GEMV fp32 65536 x 1024: the sub-CTA sweep
-        m, n = 65536, 1024
+    elif args.config in ("RM1024", "RM1001"):  # row-major GEMV fp32, 4 KiB rows: the sub-CTA
+        # sweep (65536 x 1024) and its scalar variant for odd rows (67041 x 1001)
+        m, n = (65536, 1024) if args.config == "RM1024" else (67041, 1001)
         A = cb.DenseMatrix.wrap(cb.fill_uniform(torch.empty(m * n, device=dev), WL.SEED,
                                                 WL.STREAM_A), m, n, cb.Layout.RowMajor)
         x = cb.fill_uniform(torch.empty(n, device=dev), WL.SEED, WL.STREAM_X)
@@ -77,7 +78,7 @@ def main():
         fn = lambda: cb.gemv_row_major(A, x, c, pol)  # noqa: E731
 
         class w:  # noqa: N801
-            id = "RM1024"
+            id = args.config
     elif args.config == "G1g":  # G1 through the gathering GEMV at world 1 (gemv_rm_gather_kernel)
         from paper_2108_02025_b200 import shard
         w = WL.WORKLOADS["G1"]

@@ -89,6 +89,8 @@ def main():
             alg = (4096 * 16384 + 16384 + 2 * 4096) * 4
         elif cfg == "RM1024":  # row-major GEMV fp32 65536 x 1024 (the sub-CTA sweep)
             alg = (65536 * 1024 + 1024 + 2 * 65536) * 4
+        elif cfg == "RM1001":  # row-major GEMV fp32 67041 x 1001 (the scalar sub-CTA sweep)
+            alg = (67041 * 1001 + 1001 + 2 * 67041) * 4
         else:  # D1f / G1g: D1 / G1 through the fused peer-memory paths
             alg = WL.WORKLOADS[cfg[:2]].alg_bytes(1)
         el = num(d, "sm__cycles_elapsed.max")
